@@ -1,0 +1,174 @@
+/*
+ * patchserve.h — C ABI of the B200-native PatchedServe patch-execution path.
+ *
+ * One shared library (libpatchserve.so, sm_100a) exports these entry points.
+ * They take plain device/host pointers, sizes and a CUDA stream (as void*);
+ * no framework types cross the boundary.  Each entry cites the reference
+ * interface it replaces (paths relative to /root/reference/pkg/src/mixserve/).
+ * The Python facade (paper_2501_09253_b200/) binds them with ctypes and keeps
+ * the reference's `mixserve` API drop-in; INTEGRATION.md shows the binding.
+ *
+ * Layouts:
+ *   NCHW patch array  (P, C, ps, ps)            — CSPBatch.data / block I/O (csp.py:71)
+ *   CL tokens         (P*ps*ps, Cp) bf16         — channels-last, Cp = C rounded up to 64
+ *   CL frames         (P, ps+2, ps+2, Cp) bf16   — halo frames (patched.py:57-89), channels-last
+ *   NCHW frames       (P, C, ps+2, ps+2)         — reference layout of exchange_halos
+ * Integer metadata is int32; neighbour table (P, 8) in N,NE,E,SE,S,SW,W,NW order
+ * (csp.py:20-23), -1 where absent.
+ *
+ * Errors: every entry returns PS_OK or an error code; ps_last_error() gives the
+ * message.  PS_ERR_INPUT maps to mixserve.errors.InputError (errors.py:4-5),
+ * PS_ERR_INTEGRITY to IntegrityError (errors.py:8-9).  Launch failures are
+ * PS_ERR_CUDA.  No entry falls back to the CPU.
+ */
+#ifndef PATCHSERVE_H
+#define PATCHSERVE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PS_OK 0
+#define PS_ERR_INPUT 1
+#define PS_ERR_INTEGRITY 2
+#define PS_ERR_CUDA 3
+
+#define PS_DTYPE_F32 0
+#define PS_DTYPE_BF16 1
+
+/* ------------------------------------------------------------ library */
+int ps_abi_version(void);
+const char* ps_last_error(void);
+/* Number of kernels this library has launched (process lifetime). */
+uint64_t ps_launch_count(void);
+/* Device properties check: returns PS_OK on an sm_100 device. */
+int ps_device_check(int device);
+
+/* ------------------------------------------------- CSP format (csp.py) */
+/* Patch count / resolution count of a split: csp.py:117-140 validation. */
+int ps_csp_count(int n_req, const int32_t* dims, int32_t patch_size, int32_t* n_patches, int32_t* n_res);
+/* Integer half of split(): csp.py:142-179 (stable resolution-major order,
+ * request/resolution offsets, per-patch request_index/ordinal/row/col,
+ * 8-neighbour table).  Host arrays, sized from ps_csp_count. */
+int ps_csp_build(int n_req, const int32_t* dims, int32_t patch_size, int32_t* order, int32_t* request_offset,
+                 int32_t* resolution_dims, int32_t* resolution_offset, int32_t* request_index, int32_t* ordinal,
+                 int32_t* row, int32_t* col, int32_t* neighbors);
+/* Pixel half of split(): csp.py:161-167.  src_ptrs: DEVICE array [n_req] of
+ * latent pointers (C, L, L) in storage-slot order; sides: DEVICE [n_req]. */
+int ps_csp_split(void* stream, const uint64_t* src_ptrs, const int32_t* request_offset, const int32_t* sides,
+                 int n_req, int C, int ps, int dtype, void* dst, int n_patches);
+/* reassemble(): csp.py:196-214, the inverse copy into per-request latents. */
+int ps_csp_reassemble(void* stream, const void* src, const uint64_t* dst_ptrs, const int32_t* request_offset,
+                      const int32_t* sides, int n_req, int C, int ps, int dtype, int n_patches);
+
+/* ----------------------------------------- patched operators (patched.py) */
+/* exchange_halos(): patched.py:57-89, NCHW frames (P, C, ps+2, ps+2). */
+int ps_halo_frames_nchw(void* stream, const void* src, int dtype, const int32_t* neighbors, int P, int C, int ps,
+                        void* dst);
+/* Per-(patch, group) partial moments of an NCHW bf16 array (first half of
+ * stitched_group_norm, patched.py:132-137).  partials: fp32 [P, G, 2] (mean, M2). */
+int ps_gn_partials(void* stream, const void* x, int P, int C, int ps, int G, float* partials);
+/* Pool partials per request into mean / rstd (patched.py:135-140, eps).
+ * stats: fp32 [R, G, 2] (mean, rstd). */
+int ps_gn_finalize(void* stream, const float* partials, const int32_t* request_offset, int R, int G, int cg_hw,
+                   float eps, float* stats);
+/* NCHW (bf16) -> CL tokens, with optional per-image GroupNorm affine or
+ * LayerNorm (kernels.py:209-227).  mode: 0 copy, 1 group_norm, 2 layer_norm. */
+int ps_to_cl(void* stream, const void* x, int P, int C, int ps, int Cp, int mode, const float* stats,
+             const int32_t* request_index, int G, const float* gamma, const float* beta, float eps, void* out);
+/* NCHW (bf16) -> CL halo frames (P, ps+2, ps+2, Cp), optionally GroupNorm-ed on
+ * the fly: the fused "stitcher" of stitched_group_norm(emit_halos=True),
+ * patched.py:141-144 / PAPER.md:371-373.  mode: 0 copy, 1 group_norm. */
+int ps_frames_cl(void* stream, const void* x, int P, int C, int ps, int Cp, int mode, const float* stats,
+                 const int32_t* request_index, const int32_t* neighbors, int G, const float* gamma,
+                 const float* beta, void* out);
+/* CL tokens -> NCHW bf16, optionally adding an NCHW bf16 residual (patched.py:215-217). */
+int ps_from_cl(void* stream, const void* x_cl, int P, int C, int ps, int Cp, const void* resid, void* out);
+
+/* Dense contraction on tcgen05: D[M,N] = A[M,K] B[N,K]^T (+bias), bf16 in, fp32 accumulate.
+ * a: CL tokens [M, lda] (a_mode 0) or CL frames (a_mode 1: implicit conv3, K = 9*Cp,
+ *    B laid out [N, 9*Cp] with K index tap*Cp + c, tap = ky*3 + kx).
+ * epi: 0 -> out CL [M, ldo]; 1 -> GELU then out CL; 2 -> out NCHW (P, c_real, ps, ps)
+ *      with optional NCHW residual `resid`; 3 -> columns < n_split to out [M, ldo],
+ *      the rest transposed to out2 [N - n_split, ldo2].
+ * Replaces _channel_matmul / _conv_valid / attend_tokens projections
+ * (kernels.py:99-111, 148-161, 264-267) behind patched_conv / feed_forward. */
+typedef struct ps_gemm_args {
+  const void* a; int lda; int M;
+  int a_mode; int P; int ps; int Cp;      /* a_mode 1 geometry */
+  const void* b; int N; int K;           /* B [N, K] bf16, row-major */
+  const float* bias;
+  int epi; void* out; int ldo; void* out2; int ldo2; int n_split;
+  const void* resid; int c_real;
+  int bn;                                 /* tile N: 64,128,160,192,256,320 (0 = auto) */
+} ps_gemm_args;
+int ps_gemm(void* stream, const ps_gemm_args* args);
+
+/* Per-image attention over the CSP token order (patched_self_attention,
+ * patched.py:154-176 -> attend_tokens/_attend_single, kernels.py:230-267).
+ * qk: [T, 2*Dp] bf16 (Q then K per token), vt: [Dp, ldv] bf16 (V transposed, ldv % 8 == 0),
+ * img_tok0: DEVICE [n_img+1] token offsets; tiles: DEVICE [n_tiles] (q0, img).
+ * out: [T, Dp] bf16 = softmax(Q K^T / sqrt(D)) V per image. */
+int ps_attention(void* stream, const void* qk, const void* vt, int ldv, int T, int Dp, int D, const int32_t* img_tok0,
+                 const int32_t* tile_q0, const int32_t* tile_img, int n_tiles, void* out);
+
+/* ------------------------------------------------------ patch cache (cache.py) */
+/* Pairwise-summation plan of numpy's add-reduce for n elements (cache.py:54-55
+ * via np.mean).  Sizes first (plan == NULL), then fill:
+ *   leaves: int32 [2*n_leaves] (start, len); nodes: int32 [2*n_internal] child ids
+ *   (ids < n_leaves are leaves), level_off: int32 [n_levels+1]. */
+int ps_pairwise_plan(int64_t n, int32_t* n_leaves, int32_t* n_internal, int32_t* n_levels, int32_t* leaves,
+                     int32_t* nodes, int32_t* level_off);
+/* predict_reuse(): cache.py:107-122 with _mse_predictor (cache.py:87-88):
+ * mask[p] = exists[slot] && mse(x[p], snap_in[slot]) < sigma && streak[slot] < max_streak,
+ * mse bit-exact to numpy (fp64, same pairwise tree).  x: (P, n) bf16 NCHW;
+ * slots: DEVICE int32 [P] (-1 = no entry); scratch: fp64 [P, n_leaves + n_internal];
+ * counters: int64 [2] += (reused, fresh). */
+int ps_cache_predict(void* stream, const void* x, int P, int64_t n, const int32_t* slots, const void* snap_in,
+                     const uint8_t* exists, const int32_t* streak, double sigma, int max_streak,
+                     const int32_t* leaves, int n_leaves, const int32_t* nodes, int n_internal,
+                     const int32_t* level_off, int n_levels, double* scratch, uint8_t* mask, int64_t* counters);
+/* Active-patch compaction (np.flatnonzero(~mask), ascending) + count. */
+int ps_compact(void* stream, const uint8_t* mask, int P, int32_t* active, int32_t* n_active, int32_t* reused,
+               int32_t* n_reused);
+/* gather(): cache.py:124-137 — cached (inputs, outputs) at masked rows, zeros elsewhere.
+ * error_flag: int32, set to 1 when a masked patch has no entry (IntegrityError). */
+int ps_cache_gather(void* stream, const uint8_t* mask, const int32_t* slots, const uint8_t* exists, int P,
+                    int64_t n, const void* snap_in, const void* snap_out, void* ins, void* outs, int32_t* error_flag);
+/* batched_fill(): cache.py:139-151 — streak += 1 at masked rows; optional out copy. */
+int ps_cache_fill(void* stream, const uint8_t* mask, const int32_t* slots, const uint8_t* exists, int32_t* streak,
+                  int P, int64_t n, const void* snap_out, void* out, int32_t* error_flag);
+/* batched_update(): cache.py:153-169 — fresh snapshots, streak 0 at unmasked rows;
+ * counters: int64 [2] += (refreshed, inserted). */
+int ps_cache_update(void* stream, const uint8_t* mask, const int32_t* slots, uint8_t* exists, int32_t* streak,
+                    int P, int64_t n, const void* x, const void* y, void* snap_in, void* snap_out,
+                    int64_t* counters);
+/* evict_expired(): cache.py:171-181 — clear `exists` for listed slots. */
+int ps_cache_evict(void* stream, uint8_t* exists, int32_t* streak, const int32_t* slots, int n_slots);
+/* Block-level fusion of the engine's cache sequence (engine.py:137-142):
+ * substitute: x_sub = mask ? snap_in[slot] : x   (patched.py:243-244)
+ * finish:     masked -> y = snap_out[slot], streak++ (patched.py:246, cache.py:150)
+ *             unmasked -> snap_in/out[slot] = x/y, streak = 0, exists = 1 (cache.py:165-169) */
+int ps_cache_substitute(void* stream, const uint8_t* mask, const int32_t* slots, int P, int64_t n, const void* x,
+                        const void* snap_in, void* x_sub);
+int ps_cache_finish(void* stream, const uint8_t* mask, const int32_t* slots, uint8_t* exists, int32_t* streak,
+                    int P, int64_t n, const void* x, void* y, void* snap_in, void* snap_out, int64_t* counters);
+/* masked selection used by masked_block_forward (patched.py:241-246): out = mask ? a : b. */
+int ps_select_patches(void* stream, const uint8_t* mask, int P, int64_t n, const void* a, const void* b, void* out);
+
+/* ------------------------------------------------ step wrapper (model.py) */
+/* h = bf16(latent + prompt[request_index[p]])  (model.py:163, engine.py:131-132). */
+int ps_prompt_bias(void* stream, const float* latent, const float* prompts, const int32_t* request_index, int P,
+                   int C, int ps, void* h);
+/* blend(): model.py:129-131 with per-request rate (model.py:156-166):
+ * out = (1 - r) * latent + r * tanh(h), fp32 master latents. */
+int ps_blend(void* stream, const float* latent, const void* h, const float* rates, const int32_t* request_index,
+             int P, int C, int ps, float* out);
+/* Dtype conversion helpers for the facade (f32 <-> bf16). */
+int ps_convert(void* stream, const void* src, int src_dtype, void* dst, int dst_dtype, int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PATCHSERVE_H */

@@ -1,0 +1,50 @@
+"""Small torch plumbing shared by the facade: device checks, streams, pointers."""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .errors import InputError
+
+
+def stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2501_09253_b200 needs a CUDA device (B200); there is no CPU path")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def to_device(x, dtype=None) -> torch.Tensor:
+    """CUDA tensor view/copy of x (torch tensor or numpy array)."""
+    dev = require_cuda()
+    if isinstance(x, torch.Tensor):
+        t = x
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(x))
+    if t.device.type != "cuda":
+        t = t.to(dev, non_blocking=True)
+    if dtype is not None and t.dtype != dtype:
+        t = t.to(dtype)
+    return t.contiguous()
+
+
+def check_finite(t: torch.Tensor) -> None:
+    # kernels.py:20-24 rejects non-finite inputs
+    if not bool(torch.isfinite(t).all()):
+        raise InputError("non-finite values in input")
+
+
+def round_up(x: int, m: int) -> int:
+    return (x + m - 1) // m * m
+
+
+def i32(a, dev=None) -> torch.Tensor:
+    return torch.as_tensor(np.asarray(a, dtype=np.int32), device=dev or require_cuda())

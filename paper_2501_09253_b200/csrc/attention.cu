@@ -1,0 +1,299 @@
+// Per-image self-attention over the heterogeneous CSP patch batch (K7).
+//
+// Reference: patched_self_attention (patched.py:154-176) stitches every image
+// and calls attend_tokens / _attend_single (kernels.py:230-267): single head,
+// D = C, softmax(q k^T / sqrt(D)) v in 256-row chunks.  Attention is
+// permutation-equivariant in the tokens of one image, so this kernel works
+// directly in CSP (patch-major) token order — no stitching — and restricts
+// keys to the query tile's image via `img_tok0`.
+//
+// One CTA = one (image, 128-query) tile; keys stream in 64-token blocks.
+//   S_j = Q K_j^T   : tcgen05, M=128 N=64 K=Dp  -> TMEM (double-buffered, 2x64 cols)
+//   P_j = exp2(S_j*scale_log2 - m)  (softmax warps, fp32, written to smem as bf16)
+//   O  += P_j V_j   : tcgen05, M=128 N=Dp K=64  -> TMEM (Dp cols)
+// Online-softmax rescaling of O is done lazily (only when the running max grows
+// by more than 2^8), so the TMEM round trip is rare.
+// Warp roles: w0 TMA producer, w1 MMA issuer, w2 TMEM allocator, w4..w7 softmax
+// and epilogue (thread = query row = TMEM lane).
+#include "common.cuh"
+#include "ps_internal.h"
+
+namespace ps {
+
+constexpr int AT_BM = 128;
+constexpr int AT_BN = 64;
+constexpr int AT_THREADS = 256;
+
+template <int DP>
+struct AttnCfg {
+  static constexpr int KB = DP / 64;                  // 64-wide chunks of the head dim
+  static constexpr int Q_BYTES = KB * AT_BM * 128;    // Q tile, KB swizzle columns
+  static constexpr int SLOT_BYTES = DP * 128;         // K tile (64 x DP) or V^T tile (DP x 64)
+  static constexpr int P_BYTES = AT_BM * 128;         // P tile 128 x 64 bf16
+  static constexpr int BUDGET = 224 * 1024 - Q_BYTES - P_BYTES - 1024 - 512;
+  static constexpr int NS = BUDGET / SLOT_BYTES > 6 ? 6 : BUDGET / SLOT_BYTES;
+  static constexpr int PV_N = DP <= 256 ? DP : DP / 2;  // MMA N for O += P V
+  static constexpr int PV_MMAS = DP / PV_N;
+  static constexpr int S_COL = 0;                     // S buffers at cols [0,64) and [64,128)
+  static constexpr int O_COL = 128;
+  static constexpr int TMEM_COLS = (O_COL + DP) <= 256 ? 256 : 512;
+  static constexpr int SMEM = Q_BYTES + NS * SLOT_BYTES + P_BYTES + 1024 + 512;
+  static_assert(NS >= 2, "not enough shared memory for the K/V ring");
+  static_assert(PV_N % 16 == 0 && PV_N <= 256, "bad PV N");
+};
+
+template <int DP>
+__global__ void __launch_bounds__(AT_THREADS, 1)
+    attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
+  using Cfg = AttnCfg<DP>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sSlots = sQ + Cfg::Q_BYTES;
+  uint8_t* sP = sSlots + Cfg::NS * Cfg::SLOT_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + Cfg::P_BYTES);
+  uint64_t* q_full = bars;
+  uint64_t* slot_full = bars + 1;
+  uint64_t* slot_empty = slot_full + Cfg::NS;
+  uint64_t* s_full = slot_empty + Cfg::NS;  // [2]
+  uint64_t* s_free = s_full + 2;            // [2]
+  uint64_t* p_full = s_free + 2;
+  uint64_t* p_free = p_full + 1;
+  uint64_t* o_full = p_free + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x;
+  const int q0 = p.tile_q0[tile];
+  const int img = p.tile_img[tile];
+  const int k_begin = p.img_tok0[img], k_end = p.img_tok0[img + 1];
+  const int n_kb = (k_end - k_begin + AT_BN - 1) / AT_BN;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < Cfg::NS; ++s) {
+      mbar_init(&slot_full[s], 1);
+      mbar_init(&slot_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_free[b], 128);
+    }
+    mbar_init(p_full, 128);
+    mbar_init(p_free, 1);
+    mbar_init(o_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, Cfg::Q_BYTES);
+      for (int kc = 0; kc < Cfg::KB; ++kc) tma_load_2d(sQ + kc * AT_BM * 128, &tmQ, q_full, kc * 64, q0);
+      // consumption order: K0, then (K_{j+1}, V_j) for j = 0.., then V_last
+      int slot = 0;
+      uint32_t phase = 0;
+      auto load_k = [&](int j) {
+        mbar_wait(&slot_empty[slot], phase ^ 1);
+        uint8_t* dst = sSlots + slot * Cfg::SLOT_BYTES;
+        mbar_arrive_expect_tx(&slot_full[slot], Cfg::SLOT_BYTES);
+        for (int kc = 0; kc < Cfg::KB; ++kc)
+          tma_load_2d(dst + kc * AT_BN * 128, &tmK, &slot_full[slot], kc * 64, k_begin + j * AT_BN);
+        if (++slot == Cfg::NS) { slot = 0; phase ^= 1; }
+      };
+      auto load_v = [&](int j) {
+        mbar_wait(&slot_empty[slot], phase ^ 1);
+        uint8_t* dst = sSlots + slot * Cfg::SLOT_BYTES;
+        mbar_arrive_expect_tx(&slot_full[slot], Cfg::SLOT_BYTES);
+        for (int dc = 0; dc < Cfg::KB; ++dc)
+          tma_load_2d(dst + dc * 64 * 128, &tmV, &slot_full[slot], k_begin + j * AT_BN, dc * 64);
+        if (++slot == Cfg::NS) { slot = 0; phase ^= 1; }
+      };
+      load_k(0);
+      for (int j = 0; j < n_kb; ++j) {
+        if (j + 1 < n_kb) load_k(j + 1);
+        load_v(j);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc_s = idesc_bf16_f32(AT_BM, AT_BN);
+    constexpr uint32_t idesc_o = idesc_bf16_f32(AT_BM, Cfg::PV_N);
+    int slot = 0;
+    uint32_t phase = 0;
+    auto issue_s = [&](int j) {
+      const int buf = j & 1;
+      if (j >= 2) mbar_wait(&s_free[buf], ((j - 2) >> 1) & 1);
+      mbar_wait(&slot_full[slot], phase);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint8_t* kt = sSlots + slot * Cfg::SLOT_BYTES;
+        for (int kc = 0; kc < Cfg::KB; ++kc)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            mma_bf16_ss(tmem + Cfg::S_COL + buf * AT_BN, sdesc_sw128(sQ + kc * AT_BM * 128 + k * 32),
+                        sdesc_sw128(kt + kc * AT_BN * 128 + k * 32), idesc_s, (kc | k) != 0);
+        mma_commit(&slot_empty[slot]);
+        mma_commit(&s_full[buf]);
+      }
+      __syncwarp();
+      if (++slot == Cfg::NS) { slot = 0; phase ^= 1; }
+    };
+    auto issue_pv = [&](int j) {
+      mbar_wait(p_full, j & 1);
+      mbar_wait(&slot_full[slot], phase);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint8_t* vt = sSlots + slot * Cfg::SLOT_BYTES;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int n = 0; n < Cfg::PV_MMAS; ++n)
+            mma_bf16_ss(tmem + Cfg::O_COL + n * Cfg::PV_N, sdesc_sw128(sP + k * 32),
+                        sdesc_sw128(vt + n * Cfg::PV_N * 128 + k * 32), idesc_o, (j | k) != 0);
+        mma_commit(&slot_empty[slot]);
+        mma_commit(p_free);
+        if (j == n_kb - 1) mma_commit(o_full);
+      }
+      __syncwarp();
+      if (++slot == Cfg::NS) { slot = 0; phase ^= 1; }
+    };
+    mbar_wait(q_full, 0);
+    issue_s(0);
+    for (int j = 0; j < n_kb; ++j) {
+      if (j + 1 < n_kb) issue_s(j + 1);
+      issue_pv(j);
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ softmax + epilogue
+    const int wq = warp & 3;
+    const int row = wq * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int j = 0; j < n_kb; ++j) {
+      const int buf = j & 1;
+      mbar_wait(&s_full[buf], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t sr[64];
+      PS_TMEM_LD32(tmem + lane_base + Cfg::S_COL + buf * AT_BN, sr);
+      PS_TMEM_LD32(tmem + lane_base + Cfg::S_COL + buf * AT_BN + 32, (sr + 32));
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&s_free[buf]);
+      const int kvalid = k_end - (k_begin + j * AT_BN);  // keys valid in this block
+      float s[64];
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        s[i] = (i < kvalid) ? __uint_as_float(sr[i]) * p.scale_log2 : -INFINITY;
+        mx = fmaxf(mx, s[i]);
+      }
+      // lazy rescale: keep the stale max unless it grew by more than 8 (log2 units)
+      float m_use = m_run;
+      bool need = (m_run == -INFINITY) || (mx > m_run + 8.0f);
+      if (need) m_use = fmaxf(mx, m_run);
+      const float alpha = (m_run == -INFINITY) ? 0.f : exp2f(m_run - m_use);
+      float sum = 0.f;
+      uint32_t pk[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float a = exp2f(s[2 * i] - m_use), b = exp2f(s[2 * i + 1] - m_use);
+        sum += a + b;
+        pk[i] = pack_bf16(a, b);
+      }
+      l_run = l_run * alpha + sum;
+      // P buffer and O are owned by the MMA of block j-1 until it completes
+      if (j >= 1) mbar_wait(p_free, (j - 1) & 1);
+      tc_fence_after();
+      const bool warp_rescale = __any_sync(0xffffffffu, need && j >= 1 && alpha != 1.f);
+      if (warp_rescale) {
+        const float sc = (need && j >= 1) ? alpha : 1.f;
+#pragma unroll 1
+        for (int c = 0; c < DP; c += 16) {
+          uint32_t o[16];
+          PS_TMEM_LD16(tmem + lane_base + Cfg::O_COL + c, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * sc);
+          PS_TMEM_ST16(tmem + lane_base + Cfg::O_COL + c, o);
+        }
+        tmem_st_wait();
+      }
+      m_run = m_use;
+      // P row -> smem, K-major 128B-swizzled (16B chunk c of row r at c ^ (r & 7))
+      uint4* prow = reinterpret_cast<uint4*>(sP + row * 128);
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        prow[c ^ (row & 7)] = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(p_full);
+    }
+    // epilogue: O / l -> bf16 channels-last
+    mbar_wait(o_full, 0);
+    tc_fence_after();
+    const int q = q0 + row;
+    const bool ok = q < k_end;
+    const float inv = 1.f / l_run;
+    __nv_bfloat16* dst = p.out + (size_t)q * p.Dp;
+#pragma unroll 1
+    for (int c = 0; c < DP; c += 32) {
+      uint32_t o[32];
+      PS_TMEM_LD32(tmem + lane_base + Cfg::O_COL + c, o);
+      tmem_ld_wait();
+      if (ok) {
+        uint4* d4 = reinterpret_cast<uint4*>(dst + c);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(o[8 * v + 0]) * inv, __uint_as_float(o[8 * v + 1]) * inv);
+          w.y = pack_bf16(__uint_as_float(o[8 * v + 2]) * inv, __uint_as_float(o[8 * v + 3]) * inv);
+          w.z = pack_bf16(__uint_as_float(o[8 * v + 4]) * inv, __uint_as_float(o[8 * v + 5]) * inv);
+          w.w = pack_bf16(__uint_as_float(o[8 * v + 6]) * inv, __uint_as_float(o[8 * v + 7]) * inv);
+          d4[v] = w;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem, Cfg::TMEM_COLS);
+}
+
+template <int DP>
+static int launch_dp(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const AttnParams& p,
+                     cudaStream_t st) {
+  using Cfg = AttnCfg<DP>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    attr = true;
+  }
+  attn_kernel<DP><<<p.n_tiles, AT_THREADS, Cfg::SMEM, st>>>(q, k, v, p);
+  count_launch();
+  return check_launch("attention");
+}
+
+int attention_launch(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& vt, const AttnParams& p, int dp,
+                     cudaStream_t st) {
+  switch (dp) {
+    case 64: return launch_dp<64>(q, k, vt, p, st);
+    case 128: return launch_dp<128>(q, k, vt, p, st);
+    case 192: return launch_dp<192>(q, k, vt, p, st);
+    case 256: return launch_dp<256>(q, k, vt, p, st);
+    case 320: return launch_dp<320>(q, k, vt, p, st);
+    default: return set_error(PS_ERR_INPUT, "attention: unsupported head dim %d", dp);
+  }
+}
+
+}  // namespace ps

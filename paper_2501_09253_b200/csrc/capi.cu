@@ -1,0 +1,302 @@
+// C-ABI layer: error state, launch counting, TMA descriptor encoding, host-side
+// metadata builders (CSP split plan, numpy pairwise-summation plan) and the GEMM /
+// attention entry points.
+#include <cudaTypedefs.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <functional>
+#include <mutex>
+#include <numeric>
+#include <vector>
+
+#include "ps_internal.h"
+
+namespace ps {
+
+static thread_local char g_err[512] = "";
+static std::atomic<uint64_t> g_launches{0};
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(PS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return PS_OK;
+}
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// --------------------------------------------------------- tensor maps
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// bf16 tensor map with 128B swizzle; dims/strides innermost first (strides in bytes, rank-1 of them).
+int make_tmap(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+              const uint32_t* box) {
+  auto fn = encode_fn();
+  if (!fn) return set_error(PS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (reinterpret_cast<uintptr_t>(base) % 16) return set_error(PS_ERR_INPUT, "TMA base not 16B aligned");
+  for (int i = 0; i < rank - 1; ++i)
+    if (strides_bytes[i] % 16) return set_error(PS_ERR_INPUT, "TMA stride %d not a multiple of 16B", i);
+  uint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims, strides_bytes, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(PS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return PS_OK;
+}
+
+int make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld_elems,
+                 uint32_t box_rows) {
+  uint64_t dims[2] = {cols, rows};
+  uint64_t strides[1] = {ld_elems * 2};
+  uint32_t box[2] = {64, box_rows};
+  return make_tmap(m, base, 2, dims, strides, box);
+}
+
+}  // namespace ps
+
+using namespace ps;
+
+extern "C" {
+
+int ps_abi_version(void) { return 1; }
+const char* ps_last_error(void) { return g_err; }
+uint64_t ps_launch_count(void) { return g_launches.load(); }
+
+int ps_device_check(int device) {
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) return set_error(PS_ERR_CUDA, "cudaGetDeviceProperties: %s", cudaGetErrorString(e));
+  if (prop.major != 10 || prop.minor != 0)
+    return set_error(PS_ERR_CUDA, "device %d is sm_%d%d; this library is built for sm_100a", device, prop.major,
+                     prop.minor);
+  return PS_OK;
+}
+
+// ---------------------------------------------------------------- CSP plan
+static int csp_validate(int n_req, const int32_t* dims, int32_t ps) {
+  if (n_req < 1) return set_error(PS_ERR_INPUT, "empty batch");
+  if (ps < 1) return set_error(PS_ERR_INPUT, "patch size must be positive, got %d", ps);
+  for (int i = 0; i < n_req; ++i) {
+    if (dims[i] <= 0) return set_error(PS_ERR_INPUT, "latent dims must be positive, got %d", dims[i]);
+    if (dims[i] % ps) return set_error(PS_ERR_INPUT, "patch size %d does not tile latent dim %d", ps, dims[i]);
+  }
+  return PS_OK;
+}
+
+int ps_csp_count(int n_req, const int32_t* dims, int32_t ps, int32_t* n_patches, int32_t* n_res) {
+  int rc = csp_validate(n_req, dims, ps);
+  if (rc) return rc;
+  int64_t total = 0;
+  std::vector<int32_t> d(dims, dims + n_req);
+  for (int i = 0; i < n_req; ++i) total += (int64_t)(d[i] / ps) * (d[i] / ps);
+  if (total > INT32_MAX) return set_error(PS_ERR_INPUT, "too many patches");
+  std::sort(d.begin(), d.end());
+  *n_patches = (int32_t)total;
+  *n_res = (int32_t)(std::unique(d.begin(), d.end()) - d.begin());
+  return PS_OK;
+}
+
+// csp.py:142-179: stable sort by latent dim (ties keep arrival order), offsets,
+// per-patch row-major ordinals and the 8-neighbour table (N,NE,E,SE,S,SW,W,NW).
+int ps_csp_build(int n_req, const int32_t* dims, int32_t ps, int32_t* order, int32_t* request_offset,
+                 int32_t* resolution_dims, int32_t* resolution_offset, int32_t* request_index, int32_t* ordinal,
+                 int32_t* row, int32_t* col, int32_t* neighbors) {
+  int rc = csp_validate(n_req, dims, ps);
+  if (rc) return rc;
+  static const int dr[8] = {-1, -1, 0, 1, 1, 1, 0, -1};
+  static const int dc[8] = {0, 1, 1, 1, 0, -1, -1, -1};
+  std::vector<int32_t> ord(n_req);
+  std::iota(ord.begin(), ord.end(), 0);
+  std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return dims[a] < dims[b]; });
+  int32_t start = 0;
+  request_offset[0] = 0;
+  int n_res = 0;
+  for (int s = 0; s < n_req; ++s) {
+    const int src = ord[s];
+    order[s] = src;
+    const int side = dims[src] / ps;
+    for (int r = 0; r < side; ++r)
+      for (int c = 0; c < side; ++c) {
+        const int p = start + r * side + c;
+        request_index[p] = s;
+        ordinal[p] = r * side + c;
+        row[p] = r;
+        col[p] = c;
+        for (int d = 0; d < 8; ++d) {
+          const int rr = r + dr[d], cc = c + dc[d];
+          neighbors[p * 8 + d] = (rr >= 0 && rr < side && cc >= 0 && cc < side) ? start + rr * side + cc : -1;
+        }
+      }
+    start += side * side;
+    request_offset[s + 1] = start;
+    if (n_res == 0 || resolution_dims[n_res - 1] != dims[src]) {
+      resolution_dims[n_res] = dims[src];
+      resolution_offset[n_res] = request_offset[s];
+      ++n_res;
+    }
+  }
+  resolution_offset[n_res] = start;
+  return PS_OK;
+}
+
+// ------------------------------------------------------- pairwise plan
+// numpy pairwise_sum (loops_utils.h.src, PW_BLOCKSIZE 128): n <= 128 is a leaf
+// (sequential below 8, 8 strided accumulators otherwise); larger n splits at
+// n2 = n/2 - (n/2 % 8).  Nodes are numbered leaves first (in order), then
+// internal nodes grouped by height so a level can be evaluated in parallel.
+int ps_pairwise_plan(int64_t n, int32_t* n_leaves, int32_t* n_internal, int32_t* n_levels, int32_t* leaves,
+                     int32_t* nodes, int32_t* level_off) {
+  if (n < 1 || n > (int64_t)1 << 30) return set_error(PS_ERR_INPUT, "pairwise plan: bad n %lld", (long long)n);
+  struct Node { int64_t lo, len; int left, right, height; };
+  std::vector<Node> tree;
+  std::vector<std::pair<int64_t, int64_t>> lv;
+  // recursive build (depth <= 30)
+  std::function<int(int64_t, int64_t)> rec = [&](int64_t lo, int64_t len) -> int {
+    if (len <= 128) {
+      lv.push_back({lo, len});
+      tree.push_back({lo, len, -1 - (int)(lv.size() - 1), -1, 0});
+      return (int)tree.size() - 1;
+    }
+    int64_t n2 = len / 2;
+    n2 -= n2 % 8;
+    int l = rec(lo, n2);
+    int r = rec(lo + n2, len - n2);
+    tree.push_back({lo, len, l, r, std::max(tree[l].height, tree[r].height) + 1});
+    return (int)tree.size() - 1;
+  };
+  rec(0, n);
+  const int L = (int)lv.size();
+  int H = 0;
+  for (auto& t : tree) H = std::max(H, t.height);
+  const int I = (int)tree.size() - L;
+  *n_leaves = L;
+  *n_internal = I;
+  *n_levels = H;
+  if (leaves == nullptr) return PS_OK;
+  // final ids: leaf k -> k; internal nodes ordered by (height, post-order)
+  std::vector<int> id(tree.size());
+  int next = L;
+  for (int h = 1; h <= H; ++h) {
+    level_off[h - 1] = next - L;
+    for (size_t i = 0; i < tree.size(); ++i)
+      if (tree[i].height == h && tree[i].right >= 0) id[i] = next++;
+  }
+  level_off[H] = next - L;
+  for (size_t i = 0; i < tree.size(); ++i)
+    if (tree[i].right < 0) id[i] = -1 - tree[i].left;
+  for (int k = 0; k < L; ++k) {
+    leaves[2 * k] = (int32_t)lv[k].first;
+    leaves[2 * k + 1] = (int32_t)lv[k].second;
+  }
+  for (size_t i = 0; i < tree.size(); ++i)
+    if (tree[i].right >= 0) {
+      const int j = id[i] - L;
+      nodes[2 * j] = id[tree[i].left];
+      nodes[2 * j + 1] = id[tree[i].right];
+    }
+  return PS_OK;
+}
+
+// ---------------------------------------------------------------- GEMM
+int ps_gemm(void* stream, const ps_gemm_args* a) {
+  if (!a || !a->a || !a->b || !a->out) return set_error(PS_ERR_INPUT, "gemm: null pointer");
+  if (a->K % 64) return set_error(PS_ERR_INPUT, "gemm: K (%d) must be a multiple of 64", a->K);
+  if (a->M < 1 || a->N < 1) return set_error(PS_ERR_INPUT, "gemm: empty problem");
+  int bn = a->bn;
+  if (bn == 0) bn = a->N <= 64 ? 64 : a->N <= 128 ? 128 : a->N <= 160 ? 160 : a->N <= 256 ? 256 : a->N <= 320 ? 320 : 256;
+  const int mma_n = bn <= 256 ? bn : bn / 2;
+  CUtensorMap ta, tb;
+  GemmParams p{};
+  p.M = a->M;
+  p.N = a->N;
+  p.K = a->K;
+  p.a_mode = a->a_mode;
+  int rc;
+  if (a->a_mode == A_CONV3) {
+    const int ps_ = a->ps, hw = ps_ * ps_;
+    if (a->K != 9 * a->Cp || a->Cp % 64) return set_error(PS_ERR_INPUT, "conv3 gemm: K must be 9*Cp, Cp %% 64 == 0");
+    if ((ps_ & (ps_ - 1)) || ps_ > 128)
+      return set_error(PS_ERR_INPUT, "conv3 gemm: patch size %d must be a power of two <= 128", ps_);
+    p.conv_cp = a->Cp;
+    if (hw >= 128) {
+      p.conv_rows = 128 / ps_;
+      p.conv_np = 1;
+      p.conv_tpp = hw / 128;
+    } else {
+      p.conv_rows = ps_;
+      p.conv_np = 128 / hw;
+      p.conv_tpp = 1;
+    }
+    if (a->M != a->P * hw) return set_error(PS_ERR_INPUT, "conv3 gemm: M must be P*ps*ps");
+    const uint64_t f = ps_ + 2;
+    uint64_t dims[4] = {(uint64_t)a->Cp, f, f, (uint64_t)a->P};
+    uint64_t strides[3] = {(uint64_t)a->Cp * 2, (uint64_t)a->Cp * 2 * f, (uint64_t)a->Cp * 2 * f * f};
+    uint32_t box[4] = {64, (uint32_t)ps_, (uint32_t)p.conv_rows, (uint32_t)p.conv_np};
+    rc = make_tmap(&ta, a->a, 4, dims, strides, box);
+  } else {
+    rc = make_tmap_2d(&ta, a->a, a->M, a->K, a->lda, 128);
+  }
+  if (rc) return rc;
+  rc = make_tmap_2d(&tb, a->b, a->N, a->K, a->K, mma_n);
+  if (rc) return rc;
+  p.epi = a->epi;
+  p.bias = a->bias;
+  p.out = (__nv_bfloat16*)a->out;
+  p.ldo = a->ldo;
+  p.out2 = (__nv_bfloat16*)a->out2;
+  p.ldo2 = a->ldo2;
+  p.n_split = a->n_split;
+  p.resid = (const __nv_bfloat16*)a->resid;
+  p.c_real = a->c_real;
+  p.hw = a->ps * a->ps;
+  if (a->epi == EPI_RESID_NCHW && (a->ps < 1 || a->c_real < 1 || a->c_real > a->N))
+    return set_error(PS_ERR_INPUT, "gemm: NCHW epilogue needs ps and 1 <= c_real <= N");
+  if ((a->epi == EPI_STORE_CL || a->epi == EPI_GELU_CL) && (a->ldo < a->N || a->ldo % 8))
+    return set_error(PS_ERR_INPUT, "gemm: ldo must be >= N and a multiple of 8");
+  return gemm_launch(ta, tb, p, bn, (cudaStream_t)stream);
+}
+
+// ----------------------------------------------------------- attention
+int ps_attention(void* stream, const void* qk, const void* vt, int ldv, int T, int Dp, int D, const int32_t* img_tok0,
+                 const int32_t* tile_q0, const int32_t* tile_img, int n_tiles, void* out) {
+  if (Dp % 64 || Dp < 64 || Dp > 320) return set_error(PS_ERR_INPUT, "attention: Dp %d unsupported", Dp);
+  if (D < 1 || D > Dp) return set_error(PS_ERR_INPUT, "attention: bad D");
+  if (n_tiles < 1) return PS_OK;
+  CUtensorMap tq, tk, tv;
+  int rc = make_tmap_2d(&tq, qk, T, Dp, 2 * (uint64_t)Dp, 128);
+  if (!rc) rc = make_tmap_2d(&tk, (const __nv_bfloat16*)qk + Dp, T, Dp, 2 * (uint64_t)Dp, 64);
+  if (!rc) rc = make_tmap_2d(&tv, vt, Dp, T, ldv, 64);
+  if (rc) return rc;
+  AttnParams p{};
+  p.T_total = T;
+  p.Dp = Dp;
+  p.n_tiles = n_tiles;
+  p.tile_q0 = tile_q0;
+  p.tile_img = tile_img;
+  p.img_tok0 = img_tok0;
+  p.scale_log2 = 1.4426950408889634f / sqrtf((float)D);
+  p.out = (__nv_bfloat16*)out;
+  return attention_launch(tq, tk, tv, p, Dp, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,237 @@
+// CSP split / reassemble (K2), NCHW halo frames (K3, API layout), step wrapper
+// (K10: prompt bias, blend) and dtype conversion.  All HBM-bound: 16-byte
+// vector accesses along the contiguous pixel axis, grid-stride over the
+// 148 SMs.
+#include "common.cuh"
+#include "ps_internal.h"
+
+namespace ps {
+
+static inline int grid_for(int64_t work, int threads) {
+  int64_t b = (work + threads - 1) / threads;
+  const int64_t cap = 148 * 16;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+// Copy one patch row segment (ps elements) between an image (C, L, L) and the
+// patch array (P, C, ps, ps).  VEC elements per thread-step (16 bytes).
+template <typename T, int VEC, bool TO_PATCHES>
+__global__ void csp_copy_kernel(const uint64_t* __restrict__ img_ptrs, const int32_t* __restrict__ req_off,
+                                const int32_t* __restrict__ sides, int n_req, int C, int ps, T* __restrict__ patches,
+                                int64_t total_vec) {
+  const int vps = ps / VEC;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < total_vec;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    // v -> (patch, c, y, xv)
+    int64_t t = v;
+    const int xv = (int)(t % vps);
+    t /= vps;
+    const int y = (int)(t % ps);
+    t /= ps;
+    const int c = (int)(t % C);
+    const int p = (int)(t / C);
+    // owning request: binary search over request offsets (n_req is small)
+    int lo = 0, hi = n_req - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (__ldg(req_off + mid) <= p) lo = mid; else hi = mid - 1;
+    }
+    const int side = __ldg(sides + lo);
+    const int k = p - __ldg(req_off + lo);
+    const int r = k / side, cc = k % side;
+    const int L = side * ps;
+    T* img = reinterpret_cast<T*>(img_ptrs[lo]);
+    const int64_t io = ((int64_t)c * L + (int64_t)r * ps + y) * L + (int64_t)cc * ps + xv * VEC;
+    const int64_t po = (((int64_t)p * C + c) * ps + y) * ps + xv * VEC;
+    if constexpr (VEC * sizeof(T) == 16) {
+      if (TO_PATCHES)
+        *reinterpret_cast<uint4*>(patches + po) = __ldg(reinterpret_cast<const uint4*>(img + io));
+      else
+        *reinterpret_cast<uint4*>(img + io) = __ldg(reinterpret_cast<const uint4*>(patches + po));
+    } else {
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) {
+        if (TO_PATCHES) patches[po + i] = img[io + i];
+        else img[io + i] = patches[po + i];
+      }
+    }
+  }
+}
+
+template <bool TO_PATCHES>
+static int csp_copy(cudaStream_t st, const uint64_t* ptrs, const int32_t* off, const int32_t* sides, int n_req,
+                    int C, int ps, int dtype, void* patches, int P) {
+  const int64_t elems = (int64_t)P * C * ps * ps;
+  if (elems == 0) return PS_OK;
+  const int th = 256;
+  if (dtype == PS_DTYPE_F32) {
+    if (ps % 4 == 0)
+      csp_copy_kernel<float, 4, TO_PATCHES><<<grid_for(elems / 4, th), th, 0, st>>>(ptrs, off, sides, n_req, C, ps,
+                                                                                 (float*)patches, elems / 4);
+    else
+      csp_copy_kernel<float, 1, TO_PATCHES><<<grid_for(elems, th), th, 0, st>>>(ptrs, off, sides, n_req, C, ps,
+                                                                             (float*)patches, elems);
+  } else if (dtype == PS_DTYPE_BF16) {
+    if (ps % 8 == 0)
+      csp_copy_kernel<__nv_bfloat16, 8, TO_PATCHES><<<grid_for(elems / 8, th), th, 0, st>>>(
+          ptrs, off, sides, n_req, C, ps, (__nv_bfloat16*)patches, elems / 8);
+    else
+      csp_copy_kernel<__nv_bfloat16, 1, TO_PATCHES><<<grid_for(elems, th), th, 0, st>>>(
+          ptrs, off, sides, n_req, C, ps, (__nv_bfloat16*)patches, elems);
+  } else {
+    return set_error(PS_ERR_INPUT, "csp copy: unsupported dtype %d", dtype);
+  }
+  count_launch();
+  return check_launch(TO_PATCHES ? "csp_split" : "csp_reassemble");
+}
+
+// NCHW halo frames: frame (fy, fx) of patch p reads its own patch for the
+// interior, else the neighbour in that direction (patched.py:64-88), else 0.
+template <typename T>
+__global__ void halo_nchw_kernel(const T* __restrict__ src, const int32_t* __restrict__ nbr, int P, int C, int ps,
+                                 T* __restrict__ dst) {
+  const int f = ps + 2;
+  const int64_t total = (int64_t)P * C * f * f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int fx = (int)(i % f);
+    const int fy = (int)((i / f) % f);
+    const int c = (int)((i / ((int64_t)f * f)) % C);
+    const int p = (int)(i / ((int64_t)f * f * C));
+    const int ry = fy == 0 ? -1 : (fy == f - 1 ? 1 : 0);
+    const int rx = fx == 0 ? -1 : (fx == f - 1 ? 1 : 0);
+    // direction index N,NE,E,SE,S,SW,W,NW
+    int q = p, sy = fy - 1, sx = fx - 1;
+    if (ry != 0 || rx != 0) {
+      int d;
+      if (ry < 0) d = rx < 0 ? 7 : (rx > 0 ? 1 : 0);
+      else if (ry > 0) d = rx < 0 ? 5 : (rx > 0 ? 3 : 4);
+      else d = rx < 0 ? 6 : 2;
+      q = __ldg(nbr + (int64_t)p * 8 + d);
+      sy = ry < 0 ? ps - 1 : (ry > 0 ? 0 : fy - 1);
+      sx = rx < 0 ? ps - 1 : (rx > 0 ? 0 : fx - 1);
+    }
+    T v = T(0.f);
+    if (q >= 0) v = src[(((int64_t)q * C + c) * ps + sy) * ps + sx];
+    dst[i] = v;
+  }
+}
+
+__global__ void prompt_bias_kernel(const float* __restrict__ lat, const float* __restrict__ prompts,
+                                   const int32_t* __restrict__ ri, int P, int C, int hw,
+                                   __nv_bfloat16* __restrict__ h) {
+  const int64_t total4 = (int64_t)P * C * hw / 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total4; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i * 4;
+    const int c = (int)((e / hw) % C);
+    const int p = (int)(e / ((int64_t)hw * C));
+    const float b = __ldg(prompts + (int64_t)__ldg(ri + p) * C + c);
+    const float4 x = __ldg(reinterpret_cast<const float4*>(lat) + i);
+    uint2 o;
+    o.x = pack_bf16(x.x + b, x.y + b);
+    o.y = pack_bf16(x.z + b, x.w + b);
+    reinterpret_cast<uint2*>(h)[i] = o;
+  }
+}
+
+__global__ void blend_kernel(const float* __restrict__ lat, const __nv_bfloat16* __restrict__ h,
+                             const float* __restrict__ rates, const int32_t* __restrict__ ri, int P, int C, int hw,
+                             float* __restrict__ out) {
+  const int64_t total4 = (int64_t)P * C * hw / 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total4; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i * 4;
+    const int p = (int)(e / ((int64_t)hw * C));
+    const float r = __ldg(rates + __ldg(ri + p));
+    const float4 x = __ldg(reinterpret_cast<const float4*>(lat) + i);
+    const uint2 hv = __ldg(reinterpret_cast<const uint2*>(h) + i);
+    const __nv_bfloat162 h01 = *reinterpret_cast<const __nv_bfloat162*>(&hv.x);
+    const __nv_bfloat162 h23 = *reinterpret_cast<const __nv_bfloat162*>(&hv.y);
+    float4 o;
+    o.x = (1.f - r) * x.x + r * tanhf(__low2float(h01));
+    o.y = (1.f - r) * x.y + r * tanhf(__high2float(h01));
+    o.z = (1.f - r) * x.z + r * tanhf(__low2float(h23));
+    o.w = (1.f - r) * x.w + r * tanhf(__high2float(h23));
+    reinterpret_cast<float4*>(out)[i] = o;
+  }
+}
+
+template <typename S, typename D>
+__global__ void convert_kernel(const S* __restrict__ src, D* __restrict__ dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = D(float(src[i]));
+}
+
+}  // namespace ps
+
+using namespace ps;
+
+extern "C" {
+
+int ps_csp_split(void* stream, const uint64_t* src_ptrs, const int32_t* request_offset, const int32_t* sides,
+                 int n_req, int C, int ps_, int dtype, void* dst, int n_patches) {
+  if (n_req < 1 || C < 1 || ps_ < 1) return set_error(PS_ERR_INPUT, "csp_split: bad sizes");
+  return csp_copy<true>((cudaStream_t)stream, src_ptrs, request_offset, sides, n_req, C, ps_, dtype, dst, n_patches);
+}
+
+int ps_csp_reassemble(void* stream, const void* src, const uint64_t* dst_ptrs, const int32_t* request_offset,
+                      const int32_t* sides, int n_req, int C, int ps_, int dtype, int n_patches) {
+  if (n_req < 1 || C < 1 || ps_ < 1) return set_error(PS_ERR_INPUT, "csp_reassemble: bad sizes");
+  return csp_copy<false>((cudaStream_t)stream, dst_ptrs, request_offset, sides, n_req, C, ps_, dtype,
+                         const_cast<void*>(src), n_patches);
+}
+
+int ps_halo_frames_nchw(void* stream, const void* src, int dtype, const int32_t* neighbors, int P, int C, int ps_,
+                        void* dst) {
+  const int64_t total = (int64_t)P * C * (ps_ + 2) * (ps_ + 2);
+  if (total == 0) return PS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == PS_DTYPE_F32)
+    halo_nchw_kernel<float><<<grid_for(total, 256), 256, 0, st>>>((const float*)src, neighbors, P, C, ps_,
+                                                                  (float*)dst);
+  else if (dtype == PS_DTYPE_BF16)
+    halo_nchw_kernel<__nv_bfloat16><<<grid_for(total, 256), 256, 0, st>>>((const __nv_bfloat16*)src, neighbors, P, C,
+                                                                          ps_, (__nv_bfloat16*)dst);
+  else
+    return set_error(PS_ERR_INPUT, "halo: unsupported dtype");
+  count_launch();
+  return check_launch("halo_frames_nchw");
+}
+
+int ps_prompt_bias(void* stream, const float* latent, const float* prompts, const int32_t* request_index, int P,
+                   int C, int ps_, void* h) {
+  const int hw = ps_ * ps_;
+  if (hw % 4) return set_error(PS_ERR_INPUT, "prompt_bias: ps*ps must be a multiple of 4");
+  const int64_t n4 = (int64_t)P * C * hw / 4;
+  if (n4 == 0) return PS_OK;
+  prompt_bias_kernel<<<grid_for(n4, 256), 256, 0, (cudaStream_t)stream>>>(latent, prompts, request_index, P, C, hw,
+                                                                          (__nv_bfloat16*)h);
+  count_launch();
+  return check_launch("prompt_bias");
+}
+
+int ps_blend(void* stream, const float* latent, const void* h, const float* rates, const int32_t* request_index,
+             int P, int C, int ps_, float* out) {
+  const int hw = ps_ * ps_;
+  if (hw % 4) return set_error(PS_ERR_INPUT, "blend: ps*ps must be a multiple of 4");
+  const int64_t n4 = (int64_t)P * C * hw / 4;
+  if (n4 == 0) return PS_OK;
+  blend_kernel<<<grid_for(n4, 256), 256, 0, (cudaStream_t)stream>>>(latent, (const __nv_bfloat16*)h, rates,
+                                                                    request_index, P, C, hw, out);
+  count_launch();
+  return check_launch("blend");
+}
+
+int ps_convert(void* stream, const void* src, int sd, void* dst, int dd, int64_t n) {
+  if (n == 0) return PS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int g = grid_for(n, 256);
+  if (sd == PS_DTYPE_F32 && dd == PS_DTYPE_BF16)
+    convert_kernel<float, __nv_bfloat16><<<g, 256, 0, st>>>((const float*)src, (__nv_bfloat16*)dst, n);
+  else if (sd == PS_DTYPE_BF16 && dd == PS_DTYPE_F32)
+    convert_kernel<__nv_bfloat16, float><<<g, 256, 0, st>>>((const __nv_bfloat16*)src, (float*)dst, n);
+  else
+    return set_error(PS_ERR_INPUT, "convert: unsupported dtype pair");
+  count_launch();
+  return check_launch("convert");
+}
+
+}  // extern "C"

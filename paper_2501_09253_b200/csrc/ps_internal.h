@@ -1,0 +1,48 @@
+// Internal declarations shared by the CUDA translation units and the C-ABI layer.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/patchserve.h"
+
+namespace ps {
+
+enum AMode { A_PLAIN = 0, A_CONV3 = 1 };
+enum Epi { EPI_STORE_CL = 0, EPI_GELU_CL = 1, EPI_RESID_NCHW = 2, EPI_SPLIT_VT = 3 };
+
+struct GemmParams {
+  int M, N, K;  // K is a multiple of 64 (channel padding)
+  int a_mode;
+  // conv3 geometry (A_CONV3): Cp, tiles per patch, patches per tile, frame rows per tile
+  int conv_cp, conv_tpp, conv_np, conv_rows;
+  int epi;
+  const float* bias;  // [N] or null
+  __nv_bfloat16* out;
+  int ldo;
+  __nv_bfloat16* out2;  // EPI_SPLIT_VT: transposed tail [N - n_split, ldo2]
+  int ldo2, n_split;
+  const __nv_bfloat16* resid;  // EPI_RESID_NCHW: block input (P, c_real, hw) or null
+  int c_real, hw;
+};
+
+int set_error(int code, const char* fmt, ...);
+int check_launch(const char* what);
+void count_launch();
+int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p, int bn, cudaStream_t st);
+
+struct AttnParams {
+  int T_total;   // tokens in the batch (rows of qk / columns of vt)
+  int Dp;        // padded head dim (multiple of 64)
+  int n_tiles;   // number of (image, 128-query) tiles
+  const int* tile_q0;    // [n_tiles] first query token of the tile
+  const int* tile_img;   // [n_tiles] image index
+  const int* img_tok0;   // [n_img + 1] token offsets of images
+  float scale_log2;      // log2(e) / sqrt(D_real)
+  __nv_bfloat16* out;    // [T_total, Dp] channels-last
+};
+int attention_launch(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& vt, const AttnParams& p,
+                     int dp, cudaStream_t st);
+
+}  // namespace ps

@@ -1,0 +1,405 @@
+"""Patched operators over CSP batches — drop-in for mixserve/patched.py.
+
+Every stage runs on the sm_100a library through the C ABI.  Inside a block the
+activations live channels-last ("CL": tokens x Cp, bf16, Cp = C rounded up to
+64) so every contraction is a K-major tcgen05 GEMM; block inputs/outputs (the
+residual stream) are NCHW (P, C, ps, ps) bf16, the reference's logical layout.
+
+Fusions (each still counts one stage launch, as the reference does,
+patched.py:33-45):
+* group_norm followed by a k=3 conv emits channels-last halo frames directly
+  (the stitcher, patched.py:191-201);
+* a GEMM stage followed by `residual` writes the NCHW block output with the
+  residual added in its epilogue (patched.py:215-217);
+* attention = QKV GEMM (V written transposed) -> per-image flash attention ->
+  output projection (patched.py:154-176, kernels.py:257-267).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from collections import Counter
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._dev import require_cuda, round_up, stream, to_device
+from .csp import CSPBatch
+from .errors import InputError
+from .params import device_params
+
+_launches: Counter = Counter()
+BF16 = torch.bfloat16
+
+
+def reset_launch_counters() -> None:
+    _launches.clear()
+
+
+def launch_counters() -> dict:
+    return dict(_launches)
+
+
+def _launch(kind: str) -> None:
+    _launches[kind] += 1
+
+
+# ---------------------------------------------------------------- helpers
+
+
+def _check_data(batch: CSPBatch, data) -> torch.Tensor:
+    t = to_device(data)
+    if t.dim() != 4 or t.shape[0] != batch.n_patches or tuple(t.shape[2:]) != (batch.patch_size,) * 2:
+        raise InputError(
+            f"patch data must be ({batch.n_patches},C,{batch.patch_size},{batch.patch_size}), got {tuple(t.shape)}")
+    return t
+
+
+def _bf16_nchw(t: torch.Tensor) -> torch.Tensor:
+    if t.dtype == BF16:
+        return t.contiguous()
+    if t.dtype != torch.float32:
+        t = t.to(torch.float32)
+    out = torch.empty(t.shape, dtype=BF16, device=t.device)
+    _lib.call("ps_convert", stream(), t.contiguous().data_ptr(), _lib.DTYPE_F32, out.data_ptr(), _lib.DTYPE_BF16,
+              t.numel())
+    return out
+
+
+class Act:
+    """An activation: NCHW bf16 (P, C, ps, ps) or CL bf16 (T, Cp)."""
+
+    __slots__ = ("layout", "t", "C")
+
+    def __init__(self, layout: str, t: torch.Tensor, c: int):
+        self.layout, self.t, self.C = layout, t, c
+
+    @property
+    def Cp(self) -> int:
+        return round_up(self.C, 64)
+
+
+class Ctx:
+    """Per-call geometry and device metadata for one batch."""
+
+    def __init__(self, batch: CSPBatch):
+        self.b = batch
+        self.ps = batch.patch_size
+        self.P = batch.n_patches
+        self.hw = self.ps * self.ps
+        self.T = self.P * self.hw
+        self.dev = batch.device()
+        self.device = require_cuda()
+
+    def empty_cl(self, cp: int) -> torch.Tensor:
+        return torch.empty((self.T, cp), dtype=BF16, device=self.device)
+
+    def empty_nchw(self, c: int) -> torch.Tensor:
+        return torch.empty((self.P, c, self.ps, self.ps), dtype=BF16, device=self.device)
+
+    # layout conversions --------------------------------------------------
+    def as_cl(self, a: Act) -> torch.Tensor:
+        if a.layout == "cl":
+            return a.t
+        out = self.empty_cl(a.Cp)
+        _lib.call("ps_to_cl", stream(), a.t.data_ptr(), self.P, a.C, self.ps, a.Cp, 0, None, None, 0, None, None,
+                  C.c_float(0.0), out.data_ptr())
+        return out
+
+    def as_nchw(self, a: Act, resid: torch.Tensor | None = None) -> torch.Tensor:
+        if a.layout == "nchw" and resid is None:
+            return a.t
+        src = self.as_cl(a) if a.layout == "nchw" else a.t
+        out = self.empty_nchw(a.C)
+        _lib.call("ps_from_cl", stream(), src.data_ptr(), self.P, a.C, self.ps, a.Cp,
+                  None if resid is None else resid.data_ptr(), out.data_ptr())
+        return out
+
+    # GEMM ------------------------------------------------------------------
+    def gemm(self, a, lda, b, n, k, bias, epi, out, ldo=0, out2=None, ldo2=0, n_split=0, resid=None, c_real=0,
+             conv=False, cp_in=0):
+        g = _lib.GemmArgs()
+        g.a, g.lda, g.M = a.data_ptr(), lda, self.T
+        g.a_mode, g.P, g.ps, g.Cp = (1 if conv else 0), self.P, self.ps, cp_in
+        g.b, g.N, g.K = b.data_ptr(), n, k
+        g.bias = None if bias is None else bias.data_ptr()
+        g.epi, g.out, g.ldo = epi, out.data_ptr(), ldo
+        g.out2, g.ldo2, g.n_split = (None if out2 is None else out2.data_ptr()), ldo2, n_split
+        g.resid, g.c_real = (None if resid is None else resid.data_ptr()), c_real
+        g.bn = _pick_bn(n)
+        _lib.check(_lib.load().ps_gemm(stream(), C.byref(g)))
+
+    def gemm_out(self, a_cl, lda, w, n, k, bias, c_out, resid_nchw, gelu=False):
+        """Plain GEMM; NCHW output with residual when `resid_nchw` is given."""
+        if resid_nchw is not None:
+            out = self.empty_nchw(c_out)
+            self.gemm(a_cl, lda, w, n, k, bias, 2, out, resid=resid_nchw, c_real=c_out)
+            return Act("nchw", out, c_out)
+        out = self.empty_cl(n)
+        self.gemm(a_cl, lda, w, n, k, bias, 1 if gelu else 0, out, ldo=n)
+        return Act("cl", out, c_out)
+
+    # stages ---------------------------------------------------------------
+    def gn_stats(self, x_nchw: torch.Tensor, c: int, dp: dict) -> torch.Tensor:
+        g = dp["groups"]
+        part = torch.empty((self.P, g, 2), dtype=torch.float32, device=self.device)
+        _lib.call("ps_gn_partials", stream(), x_nchw.data_ptr(), self.P, c, self.ps, g, part.data_ptr())
+        stats = torch.empty((self.b.n_requests, g, 2), dtype=torch.float32, device=self.device)
+        _lib.call("ps_gn_finalize", stream(), part.data_ptr(), self.dev["request_offset"].data_ptr(),
+                  self.b.n_requests, g, (c // g) * self.hw, C.c_float(dp["eps"]), stats.data_ptr())
+        return stats
+
+    def group_norm(self, a: Act, prm, frames: bool):
+        dp = device_params(prm, a.C)
+        x = self.as_nchw(a)
+        stats = self.gn_stats(x, a.C, dp)
+        if frames:
+            fr = torch.empty((self.P, self.ps + 2, self.ps + 2, a.Cp), dtype=BF16, device=self.device)
+            _lib.call("ps_frames_cl", stream(), x.data_ptr(), self.P, a.C, self.ps, a.Cp, 1, stats.data_ptr(),
+                      self.dev["request_index"].data_ptr(), self.dev["neighbors"].data_ptr(), dp["groups"],
+                      dp["gamma"].data_ptr(), dp["beta"].data_ptr(), fr.data_ptr())
+            return None, fr
+        out = self.empty_cl(a.Cp)
+        _lib.call("ps_to_cl", stream(), x.data_ptr(), self.P, a.C, self.ps, a.Cp, 1, stats.data_ptr(),
+                  self.dev["request_index"].data_ptr(), dp["groups"], dp["gamma"].data_ptr(), dp["beta"].data_ptr(),
+                  C.c_float(dp["eps"]), out.data_ptr())
+        return Act("cl", out, a.C), None
+
+    def frames_of(self, a: Act) -> torch.Tensor:
+        x = self.as_nchw(a)
+        fr = torch.empty((self.P, self.ps + 2, self.ps + 2, a.Cp), dtype=BF16, device=self.device)
+        _lib.call("ps_frames_cl", stream(), x.data_ptr(), self.P, a.C, self.ps, a.Cp, 0, None,
+                  self.dev["request_index"].data_ptr(), self.dev["neighbors"].data_ptr(), 1, None, None,
+                  fr.data_ptr())
+        return fr
+
+    def conv(self, a: Act, prm, frames, resid):
+        dp = device_params(prm, a.C)
+        if dp["k"] == 3:
+            if frames is None:
+                frames = self.frames_of(a)
+                _launch("halo_exchange")
+            if resid is not None:
+                out = self.empty_nchw(dp["c_out"])
+                self.gemm(frames, 0, dp["w"], dp["cp_out"], 9 * dp["cp_in"], dp["b"], 2, out, resid=resid,
+                          c_real=dp["c_out"], conv=True, cp_in=dp["cp_in"])
+                return Act("nchw", out, dp["c_out"])
+            out = self.empty_cl(dp["cp_out"])
+            self.gemm(frames, 0, dp["w"], dp["cp_out"], 9 * dp["cp_in"], dp["b"], 0, out, ldo=dp["cp_out"],
+                      conv=True, cp_in=dp["cp_in"])
+            return Act("cl", out, dp["c_out"])
+        x = self.as_cl(a)
+        return self.gemm_out(x, a.Cp, dp["w"], dp["cp_out"], dp["cp_in"], dp["b"], dp["c_out"], resid)
+
+    def linear(self, a: Act, prm, resid):
+        dp = device_params(prm, a.C)
+        x = self.as_cl(a)
+        return self.gemm_out(x, a.Cp, dp["w"], dp["cp_out"], dp["cp_in"], dp["b"], dp["c_out"], resid)
+
+    def feed_forward(self, a: Act, prm, resid):
+        dp = device_params(prm, a.C)
+        x = self.as_cl(a)
+        h = self.empty_cl(dp["hp"])
+        self.gemm(x, a.Cp, dp["w1"], dp["hp"], dp["cp"], dp["b1"], 1, h, ldo=dp["hp"])
+        return self.gemm_out(h, dp["hp"], dp["w2"], dp["cp"], dp["hp"], dp["b2"], dp["c_out"], resid)
+
+    def layer_norm(self, a: Act, prm):
+        dp = device_params(prm, a.C)
+        x = self.as_nchw(a)
+        out = self.empty_cl(a.Cp)
+        _lib.call("ps_to_cl", stream(), x.data_ptr(), self.P, a.C, self.ps, a.Cp, 2, None, None, 0,
+                  dp["gamma"].data_ptr(), dp["beta"].data_ptr(), C.c_float(dp["eps"]), out.data_ptr())
+        return Act("cl", out, a.C)
+
+    def attention(self, a: Act, prm, resid):
+        dp = device_params(prm, a.C)
+        x = self.as_cl(a)
+        d, dpp = dp["d"], dp["dp"]
+        qk = torch.empty((self.T, 2 * dpp), dtype=BF16, device=self.device)
+        ldv = round_up(self.T, 64)
+        vt = torch.empty((dpp, ldv), dtype=BF16, device=self.device)
+        self.gemm(x, a.Cp, dp["wqkv"], 3 * dpp, dpp, None, 3, qk, ldo=2 * dpp, out2=vt, ldo2=ldv, n_split=2 * dpp)
+        o = self.empty_cl(dpp)
+        _lib.call("ps_attention", stream(), qk.data_ptr(), vt.data_ptr(), ldv, self.T, dpp, d,
+                  self.dev["img_tok0"].data_ptr(), self.dev["tile_q0"].data_ptr(), self.dev["tile_img"].data_ptr(),
+                  self.dev["n_tiles"], o.data_ptr())
+        return self.gemm_out(o, dpp, dp["wo"], dpp, dpp, None, d, resid)
+
+
+_BN_CHOICES = (320, 256, 192, 160, 128, 64)
+
+
+def _pick_bn(n: int) -> int:
+    best = None
+    for bn in _BN_CHOICES:
+        cost = -(-n // bn) * bn
+        if best is None or cost < best[0]:
+            best = (cost, bn)
+    return best[1]
+
+
+# ------------------------------------------------------- public operators
+
+
+def exchange_halos(batch: CSPBatch, data) -> torch.Tensor:
+    """(P, C, ps+2, ps+2) frames: patch pixels plus a 1-pixel neighbour ring (patched.py:57-89)."""
+    data = _check_data(batch, data)
+    if data.dtype not in (torch.float32, BF16):
+        data = data.to(torch.float32)
+    p_n, c, ps = data.shape[0], data.shape[1], batch.patch_size
+    out = torch.empty((p_n, c, ps + 2, ps + 2), dtype=data.dtype, device=data.device)
+    _lib.call("ps_halo_frames_nchw", stream(), data.data_ptr(),
+              _lib.DTYPE_F32 if data.dtype == torch.float32 else _lib.DTYPE_BF16,
+              batch.device()["neighbors"].data_ptr(), p_n, c, ps, out.data_ptr())
+    return out
+
+
+def _frames_nchw_to_cl(ctx: Ctx, frames: torch.Tensor, c: int) -> torch.Tensor:
+    f = _bf16_nchw(frames)
+    cp = round_up(c, 64)
+    out = torch.empty((ctx.P, ctx.ps + 2, ctx.ps + 2, cp), dtype=BF16, device=ctx.device)
+    _lib.call("ps_to_cl", stream(), f.data_ptr(), ctx.P, c, ctx.ps + 2, cp, 0, None, None, 0, None, None,
+              C.c_float(0.0), out.data_ptr())
+    return out
+
+
+def patched_conv(batch: CSPBatch, data, p, frames=None) -> torch.Tensor:
+    """Convolution over patches; k=3 reads context from halo frames (patched.py:92-113)."""
+    data = _check_data(batch, data)
+    c = data.shape[1]
+    k = int(np.asarray(p.weights).shape[2])
+    ctx = Ctx(batch)
+    a = Act("nchw", _bf16_nchw(data), c)
+    fr = None
+    if k == 3 and frames is not None:
+        frames = to_device(frames)
+        if tuple(frames.shape) != (batch.n_patches, c, batch.patch_size + 2, batch.patch_size + 2):
+            raise InputError(f"bad halo frame shape {tuple(frames.shape)}")
+        fr = _frames_nchw_to_cl(ctx, frames, c)
+    out = ctx.conv(a, p, fr, None)
+    _launch("conv")
+    return ctx.as_nchw(out)
+
+
+def stitched_group_norm(batch: CSPBatch, data, p, emit_halos: bool = False):
+    """Group norm pooled over each request's patches (patched.py:116-144)."""
+    data = _check_data(batch, data)
+    c = data.shape[1]
+    if c % p.groups != 0:
+        raise InputError(f"groups={p.groups} does not divide channels={c}")
+    ctx = Ctx(batch)
+    out_cl, _ = ctx.group_norm(Act("nchw", _bf16_nchw(data), c), p, frames=False)
+    out = ctx.as_nchw(out_cl)
+    _launch("group_norm")
+    if emit_halos:
+        return out, exchange_halos(batch, out)
+    return out
+
+
+def patched_layer_norm(batch: CSPBatch, data, p) -> torch.Tensor:
+    """Per-position layer norm (patched.py:147-151)."""
+    data = _check_data(batch, data)
+    ctx = Ctx(batch)
+    out = ctx.as_nchw(ctx.layer_norm(Act("nchw", _bf16_nchw(data), data.shape[1]), p))
+    _launch("layer_norm")
+    return out
+
+
+def patched_self_attention(batch: CSPBatch, data, p) -> torch.Tensor:
+    """Global self-attention per image (patched.py:154-176)."""
+    data = _check_data(batch, data)
+    ctx = Ctx(batch)
+    out = ctx.as_nchw(ctx.attention(Act("nchw", _bf16_nchw(data), data.shape[1]), p, None))
+    _launch("attention")
+    return out
+
+
+def feed_forward(batch: CSPBatch, data, p) -> torch.Tensor:
+    """Pixel-wise MLP (kernels.py:124-127) over the patch array."""
+    data = _check_data(batch, data)
+    ctx = Ctx(batch)
+    return ctx.as_nchw(ctx.feed_forward(Act("nchw", _bf16_nchw(data), data.shape[1]), p, None))
+
+
+_GEMM_STAGES = ("conv", "feed_forward", "linear", "attention")
+
+
+def run_block(batch: CSPBatch, x, ops) -> torch.Tensor:
+    """Execute one block of (kind, params) stages (patched.py:179-221); returns NCHW bf16."""
+    x = _check_data(batch, x)
+    for kind, _ in ops:
+        if kind not in ("group_norm", "layer_norm", "conv", "attention", "feed_forward", "linear", "residual"):
+            raise InputError(f"unknown block stage {kind!r}")
+    ctx = Ctx(batch)
+    block_in = _bf16_nchw(x)
+    cur = Act("nchw", block_in, x.shape[1])
+    frames = None
+    fused_residual = False
+    for i, (kind, prm) in enumerate(ops):
+        nxt = ops[i + 1][0] if i + 1 < len(ops) else None
+        resid = block_in if (nxt == "residual" and kind in _GEMM_STAGES) else None
+        if kind == "group_norm":
+            fuse = (nxt == "conv" and int(np.asarray(ops[i + 1][1].weights).shape[2]) == 3)
+            a, fr = ctx.group_norm(cur, prm, frames=fuse)
+            _launch("group_norm")
+            if fuse:
+                # the normalised activation only exists as halo frames for the conv
+                frames, cur = fr, Act("frames", None, cur.C)
+            else:
+                cur, frames = a, None
+            continue
+        if kind == "conv":
+            cur = ctx.conv(cur, prm, frames, resid)
+        elif kind == "layer_norm":
+            cur = ctx.layer_norm(cur, prm)
+        elif kind == "attention":
+            cur = ctx.attention(cur, prm, resid)
+        elif kind == "feed_forward":
+            cur = ctx.feed_forward(cur, prm, resid)
+        elif kind == "linear":
+            cur = ctx.linear(cur, prm, resid)
+        elif kind == "residual":
+            if not fused_residual:
+                if cur.C != block_in.shape[1]:
+                    raise InputError(f"residual shape mismatch: {cur.C} vs {block_in.shape[1]} channels")
+                cur = Act("nchw", ctx.as_nchw(cur, resid=block_in), cur.C)
+        _launch(kind)
+        fused_residual = resid is not None
+        frames = None
+    return ctx.as_nchw(cur)
+
+
+def _mask_tensor(batch: CSPBatch, mask) -> torch.Tensor:
+    if isinstance(mask, torch.Tensor):
+        if mask.dtype != torch.bool or tuple(mask.shape) != (batch.n_patches,):
+            raise InputError(f"mask must be ({batch.n_patches},) bool, got {tuple(mask.shape)} {mask.dtype}")
+        return mask.to(require_cuda()).contiguous()
+    m = np.asarray(mask)
+    if m.shape != (batch.n_patches,) or m.dtype != np.bool_:
+        raise InputError(f"mask must be ({batch.n_patches},) bool, got {m.shape} {m.dtype}")
+    return torch.as_tensor(m, device=require_cuda())
+
+
+def select_patches(mask: torch.Tensor, a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """out[p] = a[p] if mask[p] else b[p] (bf16 patch arrays)."""
+    out = torch.empty_like(b)
+    n = b[0].numel() if b.shape[0] else 0
+    _lib.call("ps_select_patches", stream(), mask.view(torch.uint8).data_ptr(), b.shape[0], n, a.data_ptr(),
+              b.data_ptr(), out.data_ptr())
+    return out
+
+
+def masked_block_forward(batch: CSPBatch, x, mask, ops, cached_inputs, cached_outputs) -> torch.Tensor:
+    """Run a block reusing cached results for masked patches (patched.py:224-246)."""
+    x = _check_data(batch, x)
+    m = _mask_tensor(batch, mask)
+    n_masked = int(m.sum())
+    if n_masked == batch.n_patches:
+        return _bf16_nchw(_check_data(batch, cached_outputs)).clone()
+    if n_masked == 0:
+        return run_block(batch, x, ops)
+    ci = _bf16_nchw(_check_data(batch, cached_inputs))
+    co = _bf16_nchw(_check_data(batch, cached_outputs))
+    y = run_block(batch, select_patches(m, ci, _bf16_nchw(x)), ops)
+    return select_patches(m, co, y)

@@ -1,0 +1,143 @@
+"""Kernel-level parity on the B200: tcgen05 GEMM / implicit conv / attention against
+plain fp32 torch references (floating point, stated tolerances), copy kernels
+bit-exact."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2501_09253_b200 import _lib  # noqa: E402
+from paper_2501_09253_b200._dev import stream  # noqa: E402
+
+
+def _gemm(a, b, bias=None, epi=0, bn=0, out=None, ldo=None):
+    M, K = a.shape
+    N = b.shape[0]
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+    g = _lib.GemmArgs()
+    g.a, g.lda, g.M = a.data_ptr(), a.stride(0), M
+    g.a_mode = 0
+    g.b, g.N, g.K = b.data_ptr(), N, K
+    g.bias = None if bias is None else bias.data_ptr()
+    g.epi, g.out, g.ldo = epi, out.data_ptr(), ldo or N
+    g.bn = bn
+    _lib.check(_lib.load().ps_gemm(stream(), C.byref(g)))
+    return out
+
+
+@pytest.mark.parametrize("M,N,K,bn", [(128, 64, 64, 64), (256, 128, 128, 128), (1000, 320, 320, 320),
+                                      (384, 160, 192, 160), (512, 256, 640, 256), (200, 1280, 320, 320),
+                                      (130, 192, 64, 192)])
+def test_gemm_matches_fp32(M, N, K, bn):
+    torch.manual_seed(M + N + K)
+    a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    b = (torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
+    bias = torch.randn(N, device="cuda")
+    got = _gemm(a, b, bias, bn=bn).float()
+    want = a.float() @ b.float().T + bias
+    err = (got - want).abs().max().item()
+    # bf16 output rounding of O(1..4) values: <= 2^-7 relative
+    assert err <= 2e-2 * max(1.0, want.abs().max().item()), err
+
+
+def test_gemm_gelu_epilogue():
+    torch.manual_seed(0)
+    a = torch.randn(256, 128, device="cuda").to(torch.bfloat16)
+    b = (torch.randn(256, 128, device="cuda") / 11).to(torch.bfloat16)
+    bias = torch.randn(256, device="cuda") * 0.1
+    got = _gemm(a, b, bias, epi=1).float()
+    x = a.float() @ b.float().T + bias
+    want = 0.5 * x * (1 + torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
+    assert (got - want).abs().max().item() <= 2e-2
+
+
+def test_split_reassemble_bit_exact():
+    import paper_2501_09253_b200 as ps
+    rng = np.random.default_rng(0)
+    lats = [(f"r{i}", torch.tensor(rng.normal(size=(3, d, d)), dtype=torch.float32))
+            for i, d in enumerate((64, 96, 64, 128))]
+    b = ps.split(lats, patch_size=32)
+    back = ps.reassemble(b)
+    for rid, lat in lats:
+        assert torch.equal(back[rid].cpu(), lat)
+    # patch 0 of the first 64-latent is its top-left tile (csp.py:167)
+    sl = b.patches_of_request("r0")
+    assert torch.equal(b.data[sl.start].cpu(), lats[0][1][:, :32, :32])
+
+
+# ------------------------------------------------ SDXL-shaped (C=320) stages
+# fp32 torch references of the same operators on the stitched images.
+
+def _sdxl_batch(dims=(64, 96, 64), c=320, seed=0):
+    import paper_2501_09253_b200 as ps
+    g = torch.Generator().manual_seed(seed)
+    lats = [(f"r{i}", torch.randn(c, d, d, generator=g).to(torch.bfloat16).float()) for i, d in enumerate(dims)]
+    return lats, ps.split(lats, patch_size=32)
+
+
+def _rel_close(got, want, atol, rtol):
+    excess = ((got - want).abs() - (atol + rtol * want.abs())).max().item()
+    assert excess <= 0, f"excess {excess:.3e}, max |d| {(got - want).abs().max().item():.3e}"
+
+
+def test_conv3_sdxl_vs_torch():
+    import paper_2501_09253_b200 as ps
+    lats, b = _sdxl_batch()
+    g = torch.Generator().manual_seed(1)
+    w = (torch.randn(320, 320, 3, 3, generator=g) * (0.8 / (9 * 320) ** 0.5)).to(torch.bfloat16).float()
+    bias = torch.randn(320, generator=g) * 0.01
+    prm = ps.ConvParams(weights=w.double().numpy(), bias=bias.double().numpy())
+    got = ps.reassemble(b, ps.patched_conv(b, b.data, prm))
+    for rid, lat in lats:
+        want = torch.nn.functional.conv2d(lat[None].cuda(), w.cuda(), bias.cuda(), padding=1)[0]
+        _rel_close(got[rid].float(), want, 2e-2, 1e-2)
+
+
+def test_group_norm_sdxl_vs_torch():
+    import paper_2501_09253_b200 as ps
+    lats, b = _sdxl_batch(seed=2)
+    g = torch.Generator().manual_seed(3)
+    gamma, beta = 1 + 0.05 * torch.randn(320, generator=g), 0.05 * torch.randn(320, generator=g)
+    prm = ps.GroupNormParams(groups=32, gamma=gamma.double().numpy(), beta=beta.double().numpy())
+    got = ps.reassemble(b, ps.stitched_group_norm(b, b.data, prm))
+    for rid, lat in lats:
+        want = torch.nn.functional.group_norm(lat[None].cuda(), 32, gamma.cuda(), beta.cuda(), eps=1e-5)[0]
+        _rel_close(got[rid].float(), want, 2e-2, 1e-2)
+
+
+def test_attention_sdxl_vs_torch():
+    import paper_2501_09253_b200 as ps
+    lats, b = _sdxl_batch(dims=(64, 96), seed=4)
+    g = torch.Generator().manual_seed(5)
+    ws = [(torch.randn(320, 320, generator=g) * (0.8 / 320 ** 0.5)).to(torch.bfloat16).float() for _ in range(4)]
+    prm = ps.AttentionParams(*(x.double().numpy() for x in ws))
+    got = ps.reassemble(b, ps.patched_self_attention(b, b.data, prm))
+    for rid, lat in lats:
+        t = lat.cuda().reshape(320, -1).T  # (T, C) row-major tokens, kernels.py:270-273
+        q, k, v = t @ ws[0].cuda(), t @ ws[1].cuda(), t @ ws[2].cuda()
+        s = torch.softmax((q @ k.T) / 320 ** 0.5, dim=1)
+        o = (s @ v) @ ws[3].cuda()
+        want = o.T.reshape(320, lat.shape[1], lat.shape[2])
+        _rel_close(got[rid].float(), want, 5e-2, 2e-2)
+
+
+def test_feed_forward_residual_sdxl_vs_torch():
+    import paper_2501_09253_b200 as ps
+    lats, b = _sdxl_batch(dims=(64,), seed=6)
+    g = torch.Generator().manual_seed(7)
+    w1 = (torch.randn(1280, 320, generator=g) * (0.8 / 320 ** 0.5)).to(torch.bfloat16).float()
+    w2 = (torch.randn(320, 1280, generator=g) * (0.8 / 1280 ** 0.5)).to(torch.bfloat16).float()
+    b1, b2 = 0.01 * torch.randn(1280, generator=g), 0.01 * torch.randn(320, generator=g)
+    prm = ps.FeedForwardParams(w1.double().numpy(), b1.double().numpy(), w2.double().numpy(), b2.double().numpy())
+    got = ps.reassemble(b, ps.run_block(b, b.data, [("feed_forward", prm), ("residual", None)]))
+    lat = lats[0][1].cuda()
+    t = lat.reshape(320, -1).T
+    h = t @ w1.cuda().T + b1.cuda()
+    h = 0.5 * h * (1 + torch.tanh(0.7978845608028654 * (h + 0.044715 * h ** 3)))
+    want = (h @ w2.cuda().T + b2.cuda()).T.reshape(lat.shape) + lat
+    _rel_close(got["r0"].float(), want, 5e-2, 2e-2)

@@ -1,0 +1,127 @@
+"""Pin the CPU oracle (oracle/) against golden vectors recorded from the reference.
+
+Integer / copy results must match bit for bit; float results match bit for bit
+where the reference's arithmetic is order-deterministic (channel loops) and to
+1e-12 where it goes through BLAS (attention) or pooled numpy reductions.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import mixref as R
+from tests.golden.cases import (
+    CSP_CASES, MSE_CASES, cache_trace_inputs, cfg1_requests, mse_inputs, ops_small_inputs,
+)
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _load_json(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("case", range(len(CSP_CASES)))
+def test_csp_metadata_matches_reference(case):
+    g = _load_json("csp_kats.json")[case]
+    dims, ps = CSP_CASES[case]
+    rng = np.random.default_rng(0)
+    reqs = [(f"r{i}", rng.normal(size=(1, d, d))) for i, d in enumerate(dims)]
+    b = R.split(reqs, patch_size=ps)
+    assert b.patch_size == g["patch_size"]
+    assert [e.request_id for e in b.requests] == g["order"]
+    for k in ("request_offset", "resolution_offset", "request_index", "ordinal", "row", "col", "neighbors"):
+        assert getattr(b, k).tolist() == g[k], k
+    assert b.resolution_dims == g["resolution_dims"]
+    # split/reassemble are pure copies (csp.py:167, 212)
+    back = R.reassemble(b)
+    for rid, lat in reqs:
+        np.testing.assert_array_equal(back[rid], lat)
+
+
+def _ops_small():
+    reqs, prm, extra = ops_small_inputs()
+    b = R.split(reqs, patch_size=4)
+    P = dict(gn=R.GroupNormParams(**prm["gn"]), ln=R.LayerNormParams(**prm["ln"]),
+             c3=R.ConvParams(**prm["c3"]), c1=R.ConvParams(**prm["c1"]),
+             at=R.AttentionParams(**prm["at"]), ff=R.FeedForwardParams(**prm["ff"]))
+    return reqs, b, P, extra
+
+
+def test_patched_ops_match_reference():
+    g = np.load(os.path.join(GOLD, "ops_small.npz"))
+    reqs, b, P, extra = _ops_small()
+    np.testing.assert_array_equal(b.data, g["data"])
+    np.testing.assert_array_equal(R.exchange_halos(b, b.data), g["halos"])
+    gno, fr = R.stitched_group_norm(b, b.data, P["gn"], emit_halos=True)
+    np.testing.assert_array_equal(gno, g["gn"])
+    np.testing.assert_array_equal(fr, g["gn_frames"])
+    np.testing.assert_array_equal(R.patched_conv(b, b.data, P["c3"]), g["conv3"])
+    np.testing.assert_array_equal(R.patched_conv(b, b.data, P["c1"]), g["conv1"])
+    np.testing.assert_allclose(R.patched_self_attention(b, b.data, P["at"]), g["attn"], atol=1e-12, rtol=0)
+    np.testing.assert_array_equal(R.patched_layer_norm(b, b.data, P["ln"]), g["ln"])
+    np.testing.assert_array_equal(R.feed_forward(b.data, P["ff"]), g["ff"])
+    unet = [("group_norm", P["gn"]), ("conv", P["c3"]), ("attention", P["at"]),
+            ("feed_forward", P["ff"]), ("residual", None)]
+    dit = [("layer_norm", P["ln"]), ("attention", P["at"]), ("feed_forward", P["ff"]), ("residual", None)]
+    y = R.run_block(b, b.data, unet)
+    np.testing.assert_allclose(y, g["block_unet"], atol=1e-12, rtol=0)
+    np.testing.assert_allclose(R.run_block(b, b.data, dit), g["block_dit"], atol=1e-12, rtol=0)
+    np.testing.assert_array_equal(g["mask"], extra["mask"])
+    got = R.masked_block_forward(b, g["x_cur"], g["mask"], unet, b.data, g["block_unet"])
+    np.testing.assert_allclose(got, g["masked_unet"], atol=1e-12, rtol=0)
+
+
+def test_launch_counter_semantics():
+    # pkg/tests/test_patched.py:316-340 — one count per stage, fused halos
+    reqs, b, P, _ = _ops_small()
+    R.LAUNCHES.clear()
+    R.run_block(b, b.data, [("group_norm", P["gn"]), ("conv", P["c3"])])
+    assert R.LAUNCHES == {"group_norm": 1, "conv": 1}
+    R.LAUNCHES.clear()
+    R.run_block(b, b.data, [("conv", P["c3"])])
+    assert R.LAUNCHES == {"halo_exchange": 1, "conv": 1}
+
+
+def test_config1_denoise_steps_match_reference():
+    g = np.load(os.path.join(GOLD, "cfg1_steps.npz"))
+    cfg = R.ModelConfig(arch="unet_like", channels=4, hidden=8, n_blocks=2, groups=2, seed=0)
+    w = R.init_weights(cfg)
+    wflat = np.concatenate([np.ravel(getattr(p, f)) for ops in w for _, p in ops if p is not None
+                            for f in p.__dataclass_fields__ if f not in ("groups", "eps")])
+    np.testing.assert_array_equal(wflat, g["weights_flat"])
+    reqs = cfg1_requests()
+    prompts = {rid: R.make_prompt(cfg, rid) for rid, _ in reqs}
+    np.testing.assert_array_equal(np.stack([prompts[r] for r, _ in reqs]), g["prompts"])
+    b = R.split(reqs, patch_size=16)
+    data = b.data
+    for s in range(2):  # two steps keep the CPU suite fast; fixtures hold four
+        b.data = data
+        data = R.denoise_batch(cfg, w, b, prompts, {r: s for r, _ in reqs}, {r: 4 for r, _ in reqs})
+        np.testing.assert_allclose(data, g[f"step{s}"], atol=1e-12, rtol=0)
+
+
+def test_cache_traces_match_reference():
+    for t in _load_json("cache_traces.json"):
+        c = R.Cache(2, 0.1, 3)
+        for (keys, x, live), rec in zip(cache_trace_inputs(t["seed"]), t["steps"]):
+            keys = [tuple(k) for k in keys]
+            for blk in range(2):
+                m = c.predict_reuse(blk, keys, x)
+                assert m.astype(int).tolist() == rec["masks"][blk]
+                c.batched_fill(blk, keys, m, np.zeros_like(x))
+                c.batched_update(blk, keys, m, x, np.tanh(x + blk))
+            if live is not None:
+                assert c.evict_expired([tuple(k) for k in live]) == rec["evicted"]
+        final = [sorted([[list(k), e.reuse_streak] for k, e in c.stores[bk].items()]) for bk in range(2)]
+        assert final == t["final"]
+        assert c.stats.__dict__ == t["stats"]
+
+
+def test_mse_bits_match_reference():
+    for g in _load_json("mse_bits.json"):
+        a, b = mse_inputs(tuple(g["shape"]), g["seed"], g["kind"])
+        assert R.mse(a, b).hex() == g["mse_hex"], g
