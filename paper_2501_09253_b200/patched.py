@@ -31,6 +31,9 @@ from .params import device_params
 
 _launches: Counter = Counter()
 BF16 = torch.bfloat16
+# bench hook: when a list, (start, end) CUDA events are recorded around every
+# attention-kernel launch on the launching stream
+ATTN_TIMER = None
 
 
 def reset_launch_counters() -> None:
@@ -221,9 +224,16 @@ class Ctx:
         vt = torch.empty((dpp, ldv), dtype=BF16, device=self.device)
         self.gemm(x, a.Cp, dp["wqkv"], 3 * dpp, dpp, None, 3, qk, ldo=2 * dpp, out2=vt, ldo2=ldv, n_split=2 * dpp)
         o = self.empty_cl(dpp)
+        timer = ATTN_TIMER
+        if timer is not None:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
         _lib.call("ps_attention", stream(), qk.data_ptr(), vt.data_ptr(), ldv, self.T, dpp, d,
                   self.dev["img_tok0"].data_ptr(), self.dev["tile_q0"].data_ptr(), self.dev["tile_img"].data_ptr(),
                   self.dev["n_tiles"], o.data_ptr())
+        if timer is not None:
+            ev[1].record()
+            timer.append(ev)
         return self.gemm_out(o, dpp, dp["wo"], dpp, dpp, None, d, resid)
 
 
