@@ -87,8 +87,9 @@ int ps_frames_cl(void* stream, const void* x, int P, int C, int ps, int Cp, int 
 int ps_from_cl(void* stream, const void* x_cl, int P, int C, int ps, int Cp, const void* resid, void* out);
 
 /* Dense contraction on tcgen05: D[M,N] = A[M,K] B[N,K]^T (+bias), bf16 in, fp32 accumulate.
- * a: CL tokens [M, lda] (a_mode 0) or CL frames (a_mode 1: implicit conv3, K = 9*Cp,
- *    B laid out [N, 9*Cp] with K index tap*Cp + c, tap = ky*3 + kx).
+ * a: CL tokens [M, lda] (a_mode 0), CL frames (a_mode 1: implicit conv3, K = 9*Cp,
+ *    B laid out [N, 9*Cp] with K index tap*Cp + c, tap = ky*3 + kx), or tile-major
+ *    tokens (a_mode 2: [ceil(M/128)][K/64][128][64], as written with out_tiled = 1).
  * epi: 0 -> out CL [M, ldo]; 1 -> GELU then out CL; 2 -> out NCHW (P, c_real, ps, ps)
  *      with optional NCHW residual `resid`; 3 -> columns < n_split to out [M, ldo],
  *      the rest transposed to out2 [N - n_split, ldo2].
@@ -102,6 +103,7 @@ typedef struct ps_gemm_args {
   int epi; void* out; int ldo; void* out2; int ldo2; int n_split;
   const void* resid; int c_real;
   int bn;                                 /* tile N: 64,128,160,192,256,320 (0 = auto) */
+  int out_tiled;                          /* epi 0/1: write tile-major [ceil(M/128)][ldo/64][128][64] */
 } ps_gemm_args;
 int ps_gemm(void* stream, const ps_gemm_args* args);
 

@@ -190,27 +190,35 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       tc_fence_before();
       mbar_arrive(&s_free[buf]);
       const int kvalid = k_end - (k_begin + j * AT_BN);  // keys valid in this block
-      float s[64];
-      float mx = -INFINITY;
+      if (kvalid < AT_BN) {  // only the last block of an image can be ragged
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        s[i] = (i < kvalid) ? __uint_as_float(sr[i]) * p.scale_log2 : -INFINITY;
-        mx = fmaxf(mx, s[i]);
+        for (int i = 0; i < 64; ++i)
+          if (i >= kvalid) sr[i] = __float_as_uint(-INFINITY);
       }
+      float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 64; i += 4) {
+        mx0 = fmaxf(mx0, fmaxf(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])));
+        mx1 = fmaxf(mx1, fmaxf(__uint_as_float(sr[i + 2]), __uint_as_float(sr[i + 3])));
+      }
+      const float mx = fmaxf(mx0, mx1) * p.scale_log2;  // scale_log2 > 0
       // lazy rescale: keep the stale max unless it grew by more than 8 (log2 units)
       float m_use = m_run;
-      bool need = (m_run == -INFINITY) || (mx > m_run + 8.0f);
+      const bool need = (m_run == -INFINITY) || (mx > m_run + 8.0f);
       if (need) m_use = fmaxf(mx, m_run);
-      const float alpha = (m_run == -INFINITY) ? 0.f : exp2f(m_run - m_use);
-      float sum = 0.f;
+      const float alpha = (m_run == -INFINITY) ? 0.f : ex2_approx(m_run - m_use);
+      const float neg = -m_use;
+      float sum0 = 0.f, sum1 = 0.f;
       uint32_t pk[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        const float a = exp2f(s[2 * i] - m_use), b = exp2f(s[2 * i + 1] - m_use);
-        sum += a + b;
+        const float a = ex2_approx(fmaf(__uint_as_float(sr[2 * i]), p.scale_log2, neg));
+        const float b = ex2_approx(fmaf(__uint_as_float(sr[2 * i + 1]), p.scale_log2, neg));
+        sum0 += a;
+        sum1 += b;
         pk[i] = pack_bf16(a, b);
       }
-      l_run = l_run * alpha + sum;
+      l_run = l_run * alpha + (sum0 + sum1);
       // P buffer and O are owned by the MMA of block j-1 until it completes
       if (j >= 1) mbar_wait(p_free, (j - 1) & 1);
       tc_fence_after();

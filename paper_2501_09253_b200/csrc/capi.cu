@@ -222,8 +222,8 @@ int ps_gemm(void* stream, const ps_gemm_args* a) {
   if (!a || !a->a || !a->b || !a->out) return set_error(PS_ERR_INPUT, "gemm: null pointer");
   if (a->K % 64) return set_error(PS_ERR_INPUT, "gemm: K (%d) must be a multiple of 64", a->K);
   if (a->M < 1 || a->N < 1) return set_error(PS_ERR_INPUT, "gemm: empty problem");
-  int bn = a->bn;
-  if (bn == 0) bn = a->N <= 64 ? 64 : a->N <= 128 ? 128 : a->N <= 160 ? 160 : a->N <= 256 ? 256 : a->N <= 320 ? 320 : 256;
+  if (a->N % 16) return set_error(PS_ERR_INPUT, "gemm: N (%d) must be a multiple of 16", a->N);
+  const int bn = a->bn ? a->bn : gemm_pick_bn(a->N, a->K);
   const int mma_n = bn <= 256 ? bn : bn / 2;
   CUtensorMap ta, tb;
   GemmParams p{};
@@ -253,6 +253,9 @@ int ps_gemm(void* stream, const ps_gemm_args* a) {
     uint64_t strides[3] = {(uint64_t)a->Cp * 2, (uint64_t)a->Cp * 2 * f, (uint64_t)a->Cp * 2 * f * f};
     uint32_t box[4] = {64, (uint32_t)ps_, (uint32_t)p.conv_rows, (uint32_t)p.conv_np};
     rc = make_tmap(&ta, a->a, 4, dims, strides, box);
+  } else if (a->a_mode == A_TILED) {
+    const uint64_t rows = (uint64_t)((a->M + 127) / 128) * (a->K / 64) * 128;
+    rc = make_tmap_2d(&ta, a->a, rows, 64, 64, 128);
   } else {
     rc = make_tmap_2d(&ta, a->a, a->M, a->K, a->lda, 128);
   }
@@ -269,6 +272,9 @@ int ps_gemm(void* stream, const ps_gemm_args* a) {
   p.resid = (const __nv_bfloat16*)a->resid;
   p.c_real = a->c_real;
   p.hw = a->ps * a->ps;
+  p.out_tiled = a->out_tiled;
+  if (a->out_tiled && (a->epi > EPI_GELU_CL || a->ldo % 64))
+    return set_error(PS_ERR_INPUT, "gemm: tiled output needs a channels-last epilogue and ldo %% 64 == 0");
   if (a->epi == EPI_RESID_NCHW && (a->ps < 1 || a->c_real < 1 || a->c_real > a->N))
     return set_error(PS_ERR_INPUT, "gemm: NCHW epilogue needs ps and 1 <= c_real <= N");
   if ((a->epi == EPI_STORE_CL || a->epi == EPI_GELU_CL) && (a->ldo < a->N || a->ldo % 8))

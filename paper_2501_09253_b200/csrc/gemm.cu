@@ -12,8 +12,13 @@
 //     kernels.py:148-161; the frames reproduce zero padding at image borders).
 // B is the weight matrix, K-major, bf16.
 //
-// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer (one lane), w2 TMEM
-// allocator, w4..w7 epilogue (TMEM lanes 32*(w%4)..+31 = tile rows).
+// Persistent: one CTA per SM walks tiles t = blockIdx.x + i*gridDim.x in
+// n-fastest order (CTAs running together share A tiles in L2).  The TMEM
+// accumulator is double-buffered (2 x BN columns), so the epilogue of tile i
+// overlaps the MMAs of tile i+1.
+// Warp roles (384 threads): w0 TMA producer, w1 MMA issuer (one lane), w2 TMEM
+// allocator, w4..w11 epilogue (warp w reads TMEM lanes 32*(w%4)..+31, and half
+// of the tile's columns).
 // Epilogues: bias (+GELU) -> channels-last bf16; bias + residual -> NCHW bf16
 // (the block output / residual stream, reference patched.py:215-217); split
 // store with the trailing columns written transposed (V^T for attention).
@@ -24,20 +29,42 @@ namespace ps {
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
-constexpr int GEMM_THREADS = 256;
+constexpr int GEMM_THREADS = 384;
+constexpr int GEMM_EPI_THREADS = 256;
 
+// BN <= 256: double-buffered accumulators (2*BN TMEM columns), one MMA per k-step.
+// BN == 320: single accumulator (long-K GEMMs: conv3, FF2), two N=160 MMAs per k-step,
+// so A is read once per 128-token tile.
 template <int BN>
 struct GemmCfg {
+  static constexpr int NBUF = BN <= 256 ? 2 : 1;
   static constexpr int MMA_N = BN <= 256 ? BN : BN / 2;
   static constexpr int N_MMA = BN / MMA_N;
   static constexpr int A_BYTES = GEMM_BM * 128;
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 6 ? 6 : (200 * 1024) / STAGE_BYTES;
-  static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : BN <= 256 ? 256 : 512;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-  static_assert(MMA_N % 16 == 0 && MMA_N >= 16 && MMA_N <= 256, "invalid UMMA N");
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int TMEM_COLS = NBUF * BN <= 128 ? 128 : NBUF * BN <= 256 ? 256 : 512;
+  static constexpr int HALF = BN / 2;  // columns per epilogue warp
+  static constexpr int STAGE_EPI = 2 * 16 * GEMM_BM * 4;  // NCHW transpose staging, per column half
+  static constexpr int SMEM = STAGES * STAGE_BYTES + STAGE_EPI + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(MMA_N % 16 == 0 && MMA_N >= 64 && MMA_N <= 256, "invalid UMMA N");
+  static_assert(HALF % 16 == 0, "epilogue chunking");
 };
+
+__device__ __forceinline__ void store16_cl(__nv_bfloat16* dst, const float* v) {
+  uint4 w0, w1;
+  w0.x = pack_bf16(v[0], v[1]);
+  w0.y = pack_bf16(v[2], v[3]);
+  w0.z = pack_bf16(v[4], v[5]);
+  w0.w = pack_bf16(v[6], v[7]);
+  w1.x = pack_bf16(v[8], v[9]);
+  w1.y = pack_bf16(v[10], v[11]);
+  w1.z = pack_bf16(v[12], v[13]);
+  w1.w = pack_bf16(v[14], v[15]);
+  reinterpret_cast<uint4*>(dst)[0] = w0;
+  reinterpret_cast<uint4*>(dst)[1] = w1;
+}
 
 template <int BN>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
@@ -46,14 +73,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   using Cfg = GemmCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  float* epi_stage = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + Cfg::STAGE_EPI);
   uint64_t* empty = full + Cfg::STAGES;
-  uint64_t* acc_full = empty + Cfg::STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  uint64_t* acc_full = empty + Cfg::STAGES;  // [2]
+  uint64_t* acc_empty = acc_full + 2;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m_tile = blockIdx.x, n_tile = blockIdx.y;
-  const int n0 = n_tile * BN;
+  const int num_n = (p.N + BN - 1) / BN;
+  const int num_m = (p.M + GEMM_BM - 1) / GEMM_BM;
+  const int n_tiles = num_m * num_n;
   const int num_kb = p.K / GEMM_BK;
 
   if (warp == 0 && lane == 0) {
@@ -63,7 +93,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(acc_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], GEMM_EPI_THREADS);
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
@@ -77,27 +110,42 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      int p0 = 0, y0 = 0;
-      if (p.a_mode == A_CONV3) {
-        p0 = (m_tile / p.conv_tpp) * p.conv_np;
-        y0 = (m_tile % p.conv_tpp) * p.conv_rows;
-      }
       const int kcb = p.conv_cp / GEMM_BK;
-      for (int kb = 0; kb < num_kb; ++kb) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
-        uint8_t* sb = sa + Cfg::A_BYTES;
-        mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const int m_tile = t / num_n, n0 = (t % num_n) * BN;
+        int p0 = 0, y0 = 0;
         if (p.a_mode == A_CONV3) {
-          const int tap = kb / kcb, cb = kb % kcb;
-          tma_load_4d(sa, &tmA, &full[stage], cb * GEMM_BK, tap % 3, y0 + tap / 3, p0);
-        } else {
-          tma_load_2d(sa, &tmA, &full[stage], kb * GEMM_BK, m_tile * GEMM_BM);
+          p0 = (m_tile / p.conv_tpp) * p.conv_np;
+          y0 = (m_tile % p.conv_tpp) * p.conv_rows;
         }
+        // warm L2 with this tile's residual rows (NCHW, 128 contiguous pixels per channel)
+        const bool pf = p.epi == EPI_RESID_NCHW && p.resid != nullptr && p.hw >= GEMM_BM && n0 < p.c_real;
+        const int tok0 = m_tile * GEMM_BM;
+        const int cpk = (p.c_real + num_kb - 1) / num_kb;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          if (pf && tok0 + GEMM_BM <= p.M) {
+            const int pidx = tok0 / p.hw, pix0 = tok0 - pidx * p.hw;
+            for (int n = kb * cpk; n < min(p.c_real, (kb + 1) * cpk); ++n)
+              l2_prefetch(p.resid + ((size_t)pidx * p.c_real + n) * p.hw + pix0, GEMM_BM * 2);
+          }
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
+          uint8_t* sb = sa + Cfg::A_BYTES;
+          mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+          if (p.a_mode == A_CONV3) {
+            const int tap = kb / kcb, cb = kb % kcb;
+            tma_load_4d(sa, &tmA, &full[stage], cb * GEMM_BK, tap % 3, y0 + tap / 3, p0);
+          } else if (p.a_mode == A_TILED) {
+            // tile-major A: the (m_tile, kb) box is one contiguous 16 KB block
+            tma_load_2d(sa, &tmA, &full[stage], 0, (m_tile * num_kb + kb) * GEMM_BM);
+          } else {
+            tma_load_2d(sa, &tmA, &full[stage], kb * GEMM_BK, m_tile * GEMM_BM);
+          }
 #pragma unroll
-        for (int j = 0; j < Cfg::N_MMA; ++j)
-          tma_load_2d(sb + j * Cfg::MMA_N * 128, &tmB, &full[stage], kb * GEMM_BK, n0 + j * Cfg::MMA_N);
-        if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+          for (int j = 0; j < Cfg::N_MMA; ++j)
+            tma_load_2d(sb + j * Cfg::MMA_N * 128, &tmB, &full[stage], kb * GEMM_BK, n0 + j * Cfg::MMA_N);
+          if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+        }
       }
     }
   } else if (warp == 1) {
@@ -105,98 +153,163 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     constexpr uint32_t idesc = idesc_bf16_f32(GEMM_BM, Cfg::MMA_N);
     int stage = 0;
     uint32_t phase = 0;
-    for (int kb = 0; kb < num_kb; ++kb) {
-      mbar_wait(&full[stage], phase);
+    int li = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++li) {
+      const int buf = li % Cfg::NBUF;
+      const int use = li / Cfg::NBUF;
+      mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
       tc_fence_after();
-      if (lane == 0) {
-        const uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
-        const uint8_t* sb = sa + Cfg::A_BYTES;
+      const uint32_t d = tmem + buf * BN;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
+          const uint8_t* sb = sa + Cfg::A_BYTES;
 #pragma unroll
-        for (int k = 0; k < GEMM_BK / 16; ++k) {
-          const uint64_t ad = sdesc_sw128(sa + k * 32);
+          for (int k = 0; k < GEMM_BK / 16; ++k)
 #pragma unroll
-          for (int j = 0; j < Cfg::N_MMA; ++j) {
-            const uint64_t bd = sdesc_sw128(sb + j * Cfg::MMA_N * 128 + k * 32);
-            mma_bf16_ss(tmem + j * Cfg::MMA_N, ad, bd, idesc, (kb | k) != 0);
-          }
+            for (int j = 0; j < Cfg::N_MMA; ++j)
+              mma_bf16_ss(d + j * Cfg::MMA_N, sdesc_sw128(sa + k * 32),
+                          sdesc_sw128(sb + j * Cfg::MMA_N * 128 + k * 32), idesc, (kb | k) != 0);
+          mma_commit(&empty[stage]);
+          if (kb == num_kb - 1) mma_commit(&acc_full[buf]);
         }
-        mma_commit(&empty[stage]);
-        if (kb == num_kb - 1) mma_commit(acc_full);
+        __syncwarp();
+        if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
       }
-      __syncwarp();
-      if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
     }
   } else if (warp >= 4) {
     // ---------------------------------------------------------------- epilogue
     const int wq = warp & 3;
+    const int half = (warp - 4) >> 2;
     const int row = wq * 32 + lane;
-    const int m = m_tile * GEMM_BM + row;
-    const bool row_ok = m < p.M;
-    mbar_wait(acc_full, 0);
-    tc_fence_after();
-    const uint32_t tbase = tmem + ((uint32_t)(wq * 32) << 16);
-    // NCHW addressing for this token row
-    const int pidx = p.hw > 0 ? m / p.hw : 0;
-    const int pix = p.hw > 0 ? m - pidx * p.hw : 0;
+    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    int li = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++li) {
+      const int buf = li % Cfg::NBUF;
+      const int use = li / Cfg::NBUF;
+      const int m_tile = t / num_n, n_tile = t % num_n;
+      const int m = m_tile * GEMM_BM + row;
+      const bool row_ok = m < p.M;
+      const int pidx = p.hw > 0 ? m / p.hw : 0;
+      const int pix = p.hw > 0 ? m - pidx * p.hw : 0;
+      mbar_wait(&acc_full[buf], use & 1);
+      tc_fence_after();
+      // NCHW epilogue through a smem transpose: thread (channel, 16-pixel run) moves
+      // 32 contiguous bytes of residual in and of output out
+      const bool vec_nchw = p.epi == EPI_RESID_NCHW && (p.hw % 16) == 0 && (m_tile + 1) * GEMM_BM <= p.M;
+      float* st = epi_stage + half * 16 * GEMM_BM;
+      const int tq = wq * 32 + lane;  // thread index within this column half
+      const int ci = tq >> 3, seg = tq & 7;
+      const int tok_v = m_tile * GEMM_BM + seg * 16;
+      const int pidx_v = p.hw > 0 ? tok_v / p.hw : 0;
+      const int pix_v = p.hw > 0 ? tok_v - pidx_v * p.hw : 0;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      uint32_t r[32];
-      PS_TMEM_LD32(tbase + c0, r);
-      tmem_ld_wait();
-      const int nb = n0 + c0;
-      if (nb >= p.N) break;
-      float v[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int n = nb + i;
-        float x = __uint_as_float(r[i]);
-        if (p.bias != nullptr && n < p.N) x += __ldg(p.bias + n);
-        if (p.epi == EPI_GELU_CL) x = gelu_tanh(x);
-        v[i] = x;
-      }
-      if (!row_ok) continue;
-      if (p.epi == EPI_STORE_CL || p.epi == EPI_GELU_CL ||
-          (p.epi == EPI_SPLIT_VT && nb + 32 <= p.n_split)) {
-        __nv_bfloat16* dst = p.out + (size_t)m * p.ldo + nb;
-        if (nb + 32 <= p.N) {
-          uint4* d4 = reinterpret_cast<uint4*>(dst);
+      for (int c = half * Cfg::HALF; c < (half + 1) * Cfg::HALF; c += 16) {
+        uint32_t r[16];
+        PS_TMEM_LD16(tmem + lane_base + buf * BN + c, r);
+        const int nb = n_tile * BN + c;
+        uint4 rs0 = make_uint4(0, 0, 0, 0), rs1 = rs0;
+        const int nv = nb + ci;
+        const size_t off_v = ((size_t)pidx_v * p.c_real + nv) * p.hw + pix_v;
+        if (vec_nchw && p.resid != nullptr && nv < p.c_real) {
+          rs0 = __ldg(reinterpret_cast<const uint4*>(p.resid + off_v));
+          rs1 = __ldg(reinterpret_cast<const uint4*>(p.resid + off_v) + 1);
+        }
+        // bias: four 16-byte broadcast loads while the TMEM load is in flight
+        float bv[16];
+        if (p.bias != nullptr && nb < p.N) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            uint4 w;
-            w.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
-            w.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
-            w.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
-            w.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
-            d4[q] = w;
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + nb) + q);
+            bv[4 * q] = b4.x; bv[4 * q + 1] = b4.y; bv[4 * q + 2] = b4.z; bv[4 * q + 3] = b4.w;
           }
         } else {
-          for (int i = 0; i < 32 && nb + i < p.N; ++i) dst[i] = __float2bfloat16_rn(v[i]);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) bv[i] = 0.f;
         }
-      } else if (p.epi == EPI_SPLIT_VT) {
-        for (int i = 0; i < 32; ++i) {
-          const int n = nb + i;
-          if (n >= p.N) break;
-          if (n < p.n_split)
-            p.out[(size_t)m * p.ldo + n] = __float2bfloat16_rn(v[i]);
+        tmem_ld_wait();
+        if (nb >= p.N) continue;
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float x = __uint_as_float(r[i]) + bv[i];
+          if (p.epi == EPI_GELU_CL) {
+            const float u = 0.7978845608028654f * fmaf(0.044715f * x, x * x, x);
+            const float hx = 0.5f * x;
+            x = fmaf(hx, tanh_fast(u), hx);
+          }
+          v[i] = x;
+        }
+        if (vec_nchw) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) st[i * GEMM_BM + row] = v[i];
+          named_bar_sync(1 + half, 128);
+          if (nv < p.c_real) {
+            const float4* src = reinterpret_cast<const float4*>(st + ci * GEMM_BM + seg * 16);
+            float o[16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 f = src[q];
+              o[4 * q] = f.x; o[4 * q + 1] = f.y; o[4 * q + 2] = f.z; o[4 * q + 3] = f.w;
+            }
+            const __nv_bfloat162* h0 = reinterpret_cast<const __nv_bfloat162*>(&rs0);
+            const __nv_bfloat162* h1 = reinterpret_cast<const __nv_bfloat162*>(&rs1);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              o[2 * q] += __low2float(h0[q]);
+              o[2 * q + 1] += __high2float(h0[q]);
+              o[8 + 2 * q] += __low2float(h1[q]);
+              o[8 + 2 * q + 1] += __high2float(h1[q]);
+            }
+            store16_cl(p.out + off_v, o);
+          }
+          named_bar_sync(1 + half, 128);
+          continue;
+        }
+        if (!row_ok) continue;
+        if (p.epi == EPI_STORE_CL || p.epi == EPI_GELU_CL || (p.epi == EPI_SPLIT_VT && nb < p.n_split)) {
+          if (p.out_tiled)
+            store16_cl(p.out + (((size_t)m_tile * (p.ldo / 64) + nb / 64) * GEMM_BM + row) * 64 + (nb & 63), v);
           else
-            p.out2[(size_t)(n - p.n_split) * p.ldo2 + m] = __float2bfloat16_rn(v[i]);
-        }
-      } else {  // EPI_RESID_NCHW: block output, (P, C, ps, ps)
-        for (int i = 0; i < 32; ++i) {
-          const int n = nb + i;
-          if (n >= p.c_real) break;
-          const size_t off = ((size_t)pidx * p.c_real + n) * p.hw + pix;
-          float x = v[i];
-          if (p.resid != nullptr) x += bf(p.resid[off]);
-          p.out[off] = __float2bfloat16_rn(x);
+            store16_cl(p.out + (size_t)m * p.ldo + nb, v);
+        } else if (p.epi == EPI_SPLIT_VT) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            p.out2[(size_t)(nb + i - p.n_split) * p.ldo2 + m] = __float2bfloat16_rn(v[i]);
+        } else {  // EPI_RESID_NCHW, ragged tile: scalar path
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int n = nb + i;
+            if (n < p.c_real) {
+              const size_t off = ((size_t)pidx * p.c_real + n) * p.hw + pix;
+              float x = v[i];
+              if (p.resid != nullptr) x += bf(p.resid[off]);
+              p.out[off] = __float2bfloat16_rn(x);
+            }
+          }
         }
       }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[buf]);
     }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc(tmem, Cfg::TMEM_COLS);
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
 }
 
 template <int BN>
@@ -207,7 +320,8 @@ static int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const GemmParam
     cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr = true;
   }
-  dim3 grid((p.M + GEMM_BM - 1) / GEMM_BM, (p.N + BN - 1) / BN);
+  const int tiles = ((p.M + GEMM_BM - 1) / GEMM_BM) * ((p.N + BN - 1) / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
   gemm_tc_kernel<BN><<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(a, b, p);
   count_launch();
   return check_launch("gemm_tc");
@@ -223,6 +337,18 @@ int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p,
     case 320: return launch_bn<320>(a, b, p, st);
     default: return set_error(PS_ERR_INPUT, "unsupported GEMM tile N %d", bn);
   }
+}
+
+int gemm_pick_bn(int n, int k) {
+  // long reductions amortise a single accumulator: one 320-wide tile reads A once
+  if (n == 320 && k >= 1024) return 320;
+  static const int choices[] = {256, 192, 160, 128, 64};
+  int best = 64, best_cost = 1 << 30;
+  for (int bn : choices) {
+    const int cost = (n + bn - 1) / bn * bn;
+    if (cost < best_cost) { best_cost = cost; best = bn; }
+  }
+  return best;
 }
 
 }  // namespace ps

@@ -160,58 +160,137 @@ __global__ void __launch_bounds__(256) to_cl_kernel(const __nv_bfloat16* __restr
   }
 }
 
-// CL frames (P, ps+2, ps+2, Cp), one CTA per (patch, 64-channel chunk).
-__global__ void __launch_bounds__(256) frames_cl_kernel(const __nv_bfloat16* __restrict__ x, int C, int ps, int Cp,
-                                                        int mode, const float* __restrict__ stats,
-                                                        const int32_t* __restrict__ ri,
-                                                        const int32_t* __restrict__ nbr, int G,
-                                                        const float* __restrict__ gamma,
-                                                        const float* __restrict__ beta,
-                                                        __nv_bfloat16* __restrict__ out) {
-  extern __shared__ float fr[];  // [64][ps+3]
+// Vectorised NCHW -> CL transpose with optional GroupNorm, R frame rows per CTA.
+// FRAMES: output (P, ps+2, ps+2, Cp) with the 1-pixel neighbour ring (zero
+// outside the image); else output (P*ps*ps, Cp) tokens.  smem tile
+// [R][W][64] bf16 with the channel index XOR-swizzled by the pixel so both the
+// scattered stores (phase 1) and the 16-byte channel-run reads (phase 2) are
+// bank-conflict free.
+template <bool FRAMES, int VEC>
+__global__ void __launch_bounds__(256) frames_vec_kernel(const __nv_bfloat16* __restrict__ x, int C, int ps, int Cp,
+                                                         int mode, const float* __restrict__ stats,
+                                                         const int32_t* __restrict__ ri,
+                                                         const int32_t* __restrict__ nbr, int G,
+                                                         const float* __restrict__ gamma,
+                                                         const float* __restrict__ beta, int R,
+                                                         __nv_bfloat16* __restrict__ out) {
+  extern __shared__ __align__(16) __nv_bfloat16 tile[];
   const int p = blockIdx.x, c0 = blockIdx.y * 64;
-  const int f = ps + 2, hw = ps * ps;
-  const int ld = f + 1;
+  const int F = FRAMES ? ps + 2 : ps;    // output side
+  const int off = FRAMES ? 1 : 0;        // interior offset in the output row
+  const int r0 = blockIdx.z * R;
+  const int rows = min(R, F - r0);
+  const int hw = ps * ps;
   const int cg = mode == 1 ? C / G : 1;
-  const int req = __ldg(ri + p);
-  int nb[8];
+  const int req = mode == 1 ? __ldg(ri + p) : 0;
+  auto sw = [](int fx) { return (fx & 7) << 3; };
+  auto norm = [&](float v, int c) {
+    if (mode == 1) {
+      const int g = c / cg;
+      v = (v - __ldg(stats + ((int64_t)req * G + g) * 2)) * __ldg(stats + ((int64_t)req * G + g) * 2 + 1) *
+              __ldg(gamma + c) + __ldg(beta + c);
+    }
+    return v;
+  };
+  // phase 1: interior columns, VEC pixels per load
+  const int nvec = ps / VEC;
+  const int work = rows * 64 * nvec;
+  for (int k = threadIdx.x; k < work; k += blockDim.x) {
+    const int j = k % nvec;
+    const int c = (k / nvec) % 64 + c0;
+    const int r = k / (nvec * 64);
+    const int fy = r0 + r;
+    int q = p, sy = fy - off;
+    if (FRAMES) {
+      if (fy == 0) { q = __ldg(nbr + (int64_t)p * 8 + 0); sy = ps - 1; }
+      else if (fy == F - 1) { q = __ldg(nbr + (int64_t)p * 8 + 4); sy = 0; }
+    }
+    float v[VEC];
+    if (q >= 0 && c < C) {
+      const __nv_bfloat16* src = x + ((int64_t)q * C + c) * hw + sy * ps + j * VEC;
+      if constexpr (VEC == 8) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(src));
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
-  for (int d = 0; d < 8; ++d) nb[d] = __ldg(nbr + (int64_t)p * 8 + d);
-  for (int fy = 0; fy < f; ++fy) {
-    const int ry = fy == 0 ? -1 : (fy == f - 1 ? 1 : 0);
-    for (int k = threadIdx.x; k < 64 * f; k += blockDim.x) {
-      const int cc = k / f, fx = k - cc * f;
-      const int c = c0 + cc;
-      const int rx = fx == 0 ? -1 : (fx == f - 1 ? 1 : 0);
-      int q = p, sy = fy - 1, sx = fx - 1;
-      if (ry != 0 || rx != 0) {
-        int d;
-        if (ry < 0) d = rx < 0 ? 7 : (rx > 0 ? 1 : 0);
-        else if (ry > 0) d = rx < 0 ? 5 : (rx > 0 ? 3 : 4);
-        else d = rx < 0 ? 6 : 2;
-        q = nb[d];
-        sy = ry < 0 ? ps - 1 : (ry > 0 ? 0 : fy - 1);
-        sx = rx < 0 ? ps - 1 : (rx > 0 ? 0 : fx - 1);
+        for (int i = 0; i < 4; ++i) { v[2 * i] = __low2float(h[i]); v[2 * i + 1] = __high2float(h[i]); }
+      } else if constexpr (VEC == 4) {
+        const uint2 u = __ldg(reinterpret_cast<const uint2*>(src));
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) { v[2 * i] = __low2float(h[i]); v[2 * i + 1] = __high2float(h[i]); }
+      } else {
+        v[0] = bf(src[0]);
       }
-      float v = 0.f;
-      if (q >= 0 && c < C) {
-        v = bf(x[((int64_t)q * C + c) * hw + sy * ps + sx]);
-        if (mode == 1) {
-          const int g = c / cg;
-          v = (v - stats[((int64_t)req * G + g) * 2]) * stats[((int64_t)req * G + g) * 2 + 1] * gamma[c] + beta[c];
-        }
-      }
-      fr[cc * ld + fx] = v;
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) v[i] = norm(v[i], c);
+    } else {
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) v[i] = 0.f;
     }
-    __syncthreads();
-    __nv_bfloat16* orow = out + (((int64_t)p * f + fy) * f) * Cp + c0;
-    for (int k = threadIdx.x; k < f * 32; k += blockDim.x) {
-      const int fx = k >> 5, cpair = k & 31;
-      reinterpret_cast<uint32_t*>(orow + (int64_t)fx * Cp)[cpair] =
-          pack_bf16(fr[(2 * cpair) * ld + fx], fr[(2 * cpair + 1) * ld + fx]);
+    const int cc = c - c0;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      const int fx = off + j * VEC + i;
+      tile[((r * F) + fx) * 64 + (cc ^ sw(fx))] = __float2bfloat16_rn(v[i]);
     }
-    __syncthreads();
   }
+  // phase 1b: ring columns (frames only)
+  if (FRAMES) {
+    for (int k = threadIdx.x; k < rows * 64 * 2; k += blockDim.x) {
+      const int side = k & 1;  // 0 = west, 1 = east
+      const int c = (k >> 1) % 64 + c0;
+      const int r = k / 128;
+      const int fy = r0 + r;
+      const int ry = fy == 0 ? -1 : (fy == F - 1 ? 1 : 0);
+      const int d = side == 0 ? (ry < 0 ? 7 : (ry > 0 ? 5 : 6)) : (ry < 0 ? 1 : (ry > 0 ? 3 : 2));
+      const int q = __ldg(nbr + (int64_t)p * 8 + d);
+      const int sy = ry < 0 ? ps - 1 : (ry > 0 ? 0 : fy - 1);
+      const int sx = side == 0 ? ps - 1 : 0;
+      float v = 0.f;
+      if (q >= 0 && c < C) v = norm(bf(x[((int64_t)q * C + c) * hw + sy * ps + sx]), c);
+      const int fx = side == 0 ? 0 : F - 1;
+      tile[((r * F) + fx) * 64 + ((c - c0) ^ sw(fx))] = __float2bfloat16_rn(v);
+    }
+  }
+  __syncthreads();
+  // phase 2: 16-byte channel runs, consecutive threads -> consecutive 16B of one pixel row
+  const int nout = rows * F * 8;
+  for (int k = threadIdx.x; k < nout; k += blockDim.x) {
+    const int g8 = k & 7;
+    const int fx = (k >> 3) % F;
+    const int r = (k >> 3) / F;
+    const uint4 u = *reinterpret_cast<const uint4*>(tile + ((r * F) + fx) * 64 + ((g8 * 8) ^ sw(fx)));
+    const int64_t pixel = ((int64_t)p * F + r0 + r) * F + fx;
+    *reinterpret_cast<uint4*>(out + pixel * Cp + c0 + g8 * 8) = u;
+  }
+}
+
+template <bool FRAMES>
+static int launch_frames_vec(cudaStream_t st, const void* x, int P, int C, int ps, int Cp, int mode,
+                             const float* stats, const int32_t* ri, const int32_t* nbr, int G, const float* gamma,
+                             const float* beta, void* out) {
+  const int F = FRAMES ? ps + 2 : ps;
+  int R = 8;
+  while (R > 1 && R * F * 64 * 2 > 96 * 1024) R >>= 1;
+  const int smem = R * F * 64 * 2;
+  dim3 grid(P, Cp / 64, (F + R - 1) / R);
+  auto xb = (const __nv_bfloat16*)x;
+  auto ob = (__nv_bfloat16*)out;
+#define PS_FRAMES_LAUNCH(V)                                                                                      \
+  {                                                                                                              \
+    static bool attr = false;                                                                                    \
+    if (!attr) {                                                                                                 \
+      cudaFuncSetAttribute(frames_vec_kernel<FRAMES, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024); \
+      attr = true;                                                                                               \
+    }                                                                                                            \
+    frames_vec_kernel<FRAMES, V><<<grid, 256, smem, st>>>(xb, C, ps, Cp, mode, stats, ri, nbr, G, gamma, beta, R, ob); \
+  }
+  if (ps % 8 == 0) PS_FRAMES_LAUNCH(8)
+  else if (ps % 4 == 0) PS_FRAMES_LAUNCH(4)
+  else PS_FRAMES_LAUNCH(1)
+#undef PS_FRAMES_LAUNCH
+  count_launch();
+  return check_launch(FRAMES ? "frames_cl" : "to_cl");
 }
 
 // CL [T, Cp] -> NCHW (P, C, hw), optional + resid (NCHW).
@@ -280,6 +359,9 @@ int ps_to_cl(void* stream, const void* x, int P, int C, int ps_, int Cp, int mod
   if (mode == 1 && (G < 1 || C % G)) return set_error(PS_ERR_INPUT, "groups=%d does not divide channels=%d", G, C);
   const int64_t T = (int64_t)P * ps_ * ps_;
   if (T == 0) return PS_OK;
+  if (mode != 2)
+    return launch_frames_vec<false>((cudaStream_t)stream, x, P, C, ps_, Cp, mode, stats, request_index, nullptr, G,
+                                    gamma, beta, out);
   to_cl_kernel<<<(unsigned)((T + TC_TOK - 1) / TC_TOK), 256, 0, (cudaStream_t)stream>>>(
       (const __nv_bfloat16*)x, P, C, ps_ * ps_, Cp, mode, stats, request_index, G, gamma, beta, eps,
       (__nv_bfloat16*)out);
@@ -293,18 +375,8 @@ int ps_frames_cl(void* stream, const void* x, int P, int C, int ps_, int Cp, int
   if (Cp % 64 || Cp < C) return set_error(PS_ERR_INPUT, "frames_cl: Cp must be >= C and a multiple of 64");
   if (mode == 1 && (G < 1 || C % G)) return set_error(PS_ERR_INPUT, "groups=%d does not divide channels=%d", G, C);
   if (P == 0) return PS_OK;
-  const int smem = 64 * (ps_ + 3) * 4;
-  if (smem > 200 * 1024) return set_error(PS_ERR_INPUT, "frames_cl: patch too large");
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(frames_cl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
-  frames_cl_kernel<<<dim3(P, Cp / 64), 256, smem, (cudaStream_t)stream>>>(
-      (const __nv_bfloat16*)x, C, ps_, Cp, mode, stats, request_index, neighbors, G, gamma, beta,
-      (__nv_bfloat16*)out);
-  count_launch();
-  return check_launch("frames_cl");
+  return launch_frames_vec<true>((cudaStream_t)stream, x, P, C, ps_, Cp, mode, stats, request_index, neighbors, G,
+                                 gamma, beta, out);
 }
 
 int ps_from_cl(void* stream, const void* x_cl, int P, int C, int ps_, int Cp, const void* resid, void* out) {

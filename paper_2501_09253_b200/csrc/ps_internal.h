@@ -9,7 +9,7 @@
 
 namespace ps {
 
-enum AMode { A_PLAIN = 0, A_CONV3 = 1 };
+enum AMode { A_PLAIN = 0, A_CONV3 = 1, A_TILED = 2 };
 enum Epi { EPI_STORE_CL = 0, EPI_GELU_CL = 1, EPI_RESID_NCHW = 2, EPI_SPLIT_VT = 3 };
 
 struct GemmParams {
@@ -25,12 +25,14 @@ struct GemmParams {
   int ldo2, n_split;
   const __nv_bfloat16* resid;  // EPI_RESID_NCHW: block input (P, c_real, hw) or null
   int c_real, hw;
+  int out_tiled;  // CL stores in 128x64 tile-major order ([M/128][ldo/64][128][64])
 };
 
 int set_error(int code, const char* fmt, ...);
 int check_launch(const char* what);
 void count_launch();
 int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p, int bn, cudaStream_t st);
+int gemm_pick_bn(int n, int k);
 
 struct AttnParams {
   int T_total;   // tokens in the batch (rows of qk / columns of vt)

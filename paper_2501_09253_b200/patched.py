@@ -121,26 +121,27 @@ class Ctx:
 
     # GEMM ------------------------------------------------------------------
     def gemm(self, a, lda, b, n, k, bias, epi, out, ldo=0, out2=None, ldo2=0, n_split=0, resid=None, c_real=0,
-             conv=False, cp_in=0):
+             conv=False, cp_in=0, a_tiled=False, out_tiled=False):
         g = _lib.GemmArgs()
         g.a, g.lda, g.M = a.data_ptr(), lda, self.T
-        g.a_mode, g.P, g.ps, g.Cp = (1 if conv else 0), self.P, self.ps, cp_in
+        g.a_mode, g.P, g.ps, g.Cp = (1 if conv else 2 if a_tiled else 0), self.P, self.ps, cp_in
+        g.out_tiled = 1 if out_tiled else 0
         g.b, g.N, g.K = b.data_ptr(), n, k
         g.bias = None if bias is None else bias.data_ptr()
         g.epi, g.out, g.ldo = epi, out.data_ptr(), ldo
         g.out2, g.ldo2, g.n_split = (None if out2 is None else out2.data_ptr()), ldo2, n_split
         g.resid, g.c_real = (None if resid is None else resid.data_ptr()), c_real
-        g.bn = _pick_bn(n)
+        g.bn = 0  # library picks the tile width (gemm_pick_bn)
         _lib.check(_lib.load().ps_gemm(stream(), C.byref(g)))
 
-    def gemm_out(self, a_cl, lda, w, n, k, bias, c_out, resid_nchw, gelu=False):
+    def gemm_out(self, a_cl, lda, w, n, k, bias, c_out, resid_nchw, gelu=False, a_tiled=False):
         """Plain GEMM; NCHW output with residual when `resid_nchw` is given."""
         if resid_nchw is not None:
             out = self.empty_nchw(c_out)
-            self.gemm(a_cl, lda, w, n, k, bias, 2, out, resid=resid_nchw, c_real=c_out)
+            self.gemm(a_cl, lda, w, n, k, bias, 2, out, resid=resid_nchw, c_real=c_out, a_tiled=a_tiled)
             return Act("nchw", out, c_out)
         out = self.empty_cl(n)
-        self.gemm(a_cl, lda, w, n, k, bias, 1 if gelu else 0, out, ldo=n)
+        self.gemm(a_cl, lda, w, n, k, bias, 1 if gelu else 0, out, ldo=n, a_tiled=a_tiled)
         return Act("cl", out, c_out)
 
     # stages ---------------------------------------------------------------
@@ -203,9 +204,11 @@ class Ctx:
     def feed_forward(self, a: Act, prm, resid):
         dp = device_params(prm, a.C)
         x = self.as_cl(a)
-        h = self.empty_cl(dp["hp"])
-        self.gemm(x, a.Cp, dp["w1"], dp["hp"], dp["cp"], dp["b1"], 1, h, ldo=dp["hp"])
-        return self.gemm_out(h, dp["hp"], dp["w2"], dp["cp"], dp["hp"], dp["b2"], dp["c_out"], resid)
+        # hidden activations in 128x64 tile-major order: the second GEMM streams
+        # each of its A boxes as one contiguous 16 KB block from HBM
+        h = torch.empty((round_up(self.T, 128), dp["hp"]), dtype=BF16, device=self.device)
+        self.gemm(x, a.Cp, dp["w1"], dp["hp"], dp["cp"], dp["b1"], 1, h, ldo=dp["hp"], out_tiled=True)
+        return self.gemm_out(h, dp["hp"], dp["w2"], dp["cp"], dp["hp"], dp["b2"], dp["c_out"], resid, a_tiled=True)
 
     def layer_norm(self, a: Act, prm):
         dp = device_params(prm, a.C)
@@ -235,18 +238,6 @@ class Ctx:
             ev[1].record()
             timer.append(ev)
         return self.gemm_out(o, dpp, dp["wo"], dpp, dpp, None, d, resid)
-
-
-_BN_CHOICES = (320, 256, 192, 160, 128, 64)
-
-
-def _pick_bn(n: int) -> int:
-    best = None
-    for bn in _BN_CHOICES:
-        cost = -(-n // bn) * bn
-        if best is None or cost < best[0]:
-            best = (cost, bn)
-    return best[1]
 
 
 # ------------------------------------------------------- public operators

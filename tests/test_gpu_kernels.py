@@ -30,9 +30,9 @@ def _gemm(a, b, bias=None, epi=0, bn=0, out=None, ldo=None):
     return out
 
 
-@pytest.mark.parametrize("M,N,K,bn", [(128, 64, 64, 64), (256, 128, 128, 128), (1000, 320, 320, 320),
-                                      (384, 160, 192, 160), (512, 256, 640, 256), (200, 1280, 320, 320),
-                                      (130, 192, 64, 192)])
+@pytest.mark.parametrize("M,N,K,bn", [(128, 64, 64, 64), (256, 128, 128, 128), (1000, 320, 320, 160),
+                                      (384, 160, 192, 160), (512, 256, 640, 256), (200, 1280, 320, 256),
+                                      (130, 192, 64, 192), (1000, 320, 1280, 320), (256, 320, 2880, 0)])
 def test_gemm_matches_fp32(M, N, K, bn):
     torch.manual_seed(M + N + K)
     a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
