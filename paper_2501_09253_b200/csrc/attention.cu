@@ -7,40 +7,59 @@
 // directly in CSP (patch-major) token order — no stitching — and restricts
 // keys to the query tile's image via `img_tok0`.
 //
-// One CTA = one (image, 128-query) tile; keys stream in 64-token blocks.
-//   S_j = Q K_j^T   : tcgen05, M=128 N=64 K=Dp  -> TMEM (double-buffered, 2x64 cols)
-//   P_j = exp2(S_j*scale_log2 - m)  (softmax warps, fp32, written to smem as bf16)
-//   O  += P_j V_j   : tcgen05, M=128 N=Dp K=64  -> TMEM (Dp cols)
-// Online-softmax rescaling of O is done lazily (only when the running max grows
-// by more than 2^8), so the TMEM round trip is rare.
-// Warp roles: w0 TMA producer, w1 MMA issuer, w2 TMEM allocator, w4..w7 softmax
-// and epilogue (thread = query row = TMEM lane).
+// One CTA = one (image, 128-query) tile; keys stream in 128-token blocks.
+//   S_j = Q K_j^T   : tcgen05 SS, M=128 N=128 K=Dp -> TMEM cols [S_COL, +128)
+//   P_j = exp2(S_j*scale_log2 - m)   (softmax warps, fp32) -> bf16 into TMEM
+//                                      cols [P_COL, +64) with tcgen05.st
+//   O  += P_j V_j   : tcgen05 TS (A = P from TMEM), M=128 N=Dp K=128 -> O cols
+// TMEM: O (Dp) + S (128) + P (64) <= 512 columns.  Keeping P in TMEM removes
+// the P round trip through shared memory, and 128-key blocks halve the Q
+// re-reads of the S MMAs: shared-memory bandwidth, not the tensor pipe, was the
+// limit of the 64-key SS design.
+// K streams in 16 KB (128 keys x 64 dims) chunks through one ring, V^T in
+// (Dp x 64 keys) pieces through another.
+// Online-softmax rescaling of O is lazy (only when the running max grows by
+// more than 2^8).  Warp roles: w0 TMA producer, w1 MMA issuer, w2 TMEM
+// allocator, w4..w7 softmax + epilogue (thread = query row = TMEM lane).
 #include "common.cuh"
 #include "ps_internal.h"
 
 namespace ps {
 
 constexpr int AT_BM = 128;
-constexpr int AT_BN = 64;
+constexpr int AT_BN = 128;
 constexpr int AT_THREADS = 256;
 
 template <int DP>
 struct AttnCfg {
-  static constexpr int KB = DP / 64;                  // 64-wide chunks of the head dim
-  static constexpr int Q_BYTES = KB * AT_BM * 128;    // Q tile, KB swizzle columns
-  static constexpr int SLOT_BYTES = DP * 128;         // K tile (64 x DP) or V^T tile (DP x 64)
-  static constexpr int P_BYTES = AT_BM * 128;         // P tile 128 x 64 bf16
-  static constexpr int BUDGET = 224 * 1024 - Q_BYTES - P_BYTES - 1024 - 512;
-  static constexpr int NS = BUDGET / SLOT_BYTES > 6 ? 6 : BUDGET / SLOT_BYTES;
+  static constexpr int KB = DP / 64;                 // 64-wide chunks of the head dim
+  static constexpr int Q_BYTES = KB * AT_BM * 128;   // Q tile: KB swizzle columns of 128 rows
+  static constexpr int K_SLOT = AT_BN * 128;         // 128 keys x 64 dims
+  static constexpr int V_SLOT = DP * 128;            // DP dims x 64 keys (V^T piece)
+  static constexpr int NV = 2;
+  static constexpr int BUDGET = 227 * 1024 - Q_BYTES - NV * V_SLOT - 1024 - 512;
+  static constexpr int NK = BUDGET / K_SLOT > 6 ? 6 : BUDGET / K_SLOT;
   static constexpr int PV_N = DP <= 256 ? DP : DP / 2;  // MMA N for O += P V
   static constexpr int PV_MMAS = DP / PV_N;
-  static constexpr int S_COL = 0;                     // S buffers at cols [0,64) and [64,128)
-  static constexpr int O_COL = 128;
-  static constexpr int TMEM_COLS = (O_COL + DP) <= 256 ? 256 : 512;
-  static constexpr int SMEM = Q_BYTES + NS * SLOT_BYTES + P_BYTES + 1024 + 512;
-  static_assert(NS >= 2, "not enough shared memory for the K/V ring");
+  static constexpr int O_COL = 0;
+  static constexpr int S_COL = DP;                   // 128 fp32 columns
+  static constexpr int P_COL = DP + 128;             // 64 columns of packed bf16 pairs
+  static constexpr int TMEM_COLS = (P_COL + 64) <= 256 ? 256 : 512;
+  static constexpr int SMEM = Q_BYTES + NK * K_SLOT + NV * V_SLOT + 1024 + 512;
+  static_assert(NK >= 2, "not enough shared memory for the K ring");
+  static_assert(P_COL + 64 <= 512, "TMEM budget");
   static_assert(PV_N % 16 == 0 && PV_N <= 256, "bad PV N");
 };
+
+// D[tmem] (+)= A[tmem] * B[smem]^T (A = P, bf16 packed in TMEM).
+PS_DEV void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 
 template <int DP>
 __global__ void __launch_bounds__(AT_THREADS, 1)
@@ -50,15 +69,17 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
-  uint8_t* sSlots = sQ + Cfg::Q_BYTES;
-  uint8_t* sP = sSlots + Cfg::NS * Cfg::SLOT_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + Cfg::P_BYTES);
+  uint8_t* sK = sQ + Cfg::Q_BYTES;
+  uint8_t* sV = sK + Cfg::NK * Cfg::K_SLOT;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + Cfg::NV * Cfg::V_SLOT);
   uint64_t* q_full = bars;
-  uint64_t* slot_full = bars + 1;
-  uint64_t* slot_empty = slot_full + Cfg::NS;
-  uint64_t* s_full = slot_empty + Cfg::NS;  // [2]
-  uint64_t* s_free = s_full + 2;            // [2]
-  uint64_t* p_full = s_free + 2;
+  uint64_t* k_full = bars + 1;
+  uint64_t* k_empty = k_full + Cfg::NK;
+  uint64_t* v_full = k_empty + Cfg::NK;
+  uint64_t* v_empty = v_full + Cfg::NV;
+  uint64_t* s_full = v_empty + Cfg::NV;
+  uint64_t* s_free = s_full + 1;
+  uint64_t* p_full = s_free + 1;
   uint64_t* p_free = p_full + 1;
   uint64_t* o_full = p_free + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
@@ -75,14 +96,16 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
     mbar_init(q_full, 1);
-    for (int s = 0; s < Cfg::NS; ++s) {
-      mbar_init(&slot_full[s], 1);
-      mbar_init(&slot_empty[s], 1);
+    for (int s = 0; s < Cfg::NK; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&s_full[b], 1);
-      mbar_init(&s_free[b], 128);
+    for (int s = 0; s < Cfg::NV; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
     }
+    mbar_init(s_full, 1);
+    mbar_init(s_free, 128);
     mbar_init(p_full, 128);
     mbar_init(p_free, 1);
     mbar_init(o_full, 1);
@@ -99,25 +122,27 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     if (lane == 0) {
       mbar_arrive_expect_tx(q_full, Cfg::Q_BYTES);
       for (int kc = 0; kc < Cfg::KB; ++kc) tma_load_2d(sQ + kc * AT_BM * 128, &tmQ, q_full, kc * 64, q0);
-      // consumption order: K0, then (K_{j+1}, V_j) for j = 0.., then V_last
-      int slot = 0;
-      uint32_t phase = 0;
+      int ks = 0, vs = 0;
+      uint32_t kph = 0, vph = 0;
       auto load_k = [&](int j) {
-        mbar_wait(&slot_empty[slot], phase ^ 1);
-        uint8_t* dst = sSlots + slot * Cfg::SLOT_BYTES;
-        mbar_arrive_expect_tx(&slot_full[slot], Cfg::SLOT_BYTES);
-        for (int kc = 0; kc < Cfg::KB; ++kc)
-          tma_load_2d(dst + kc * AT_BN * 128, &tmK, &slot_full[slot], kc * 64, k_begin + j * AT_BN);
-        if (++slot == Cfg::NS) { slot = 0; phase ^= 1; }
+        for (int kc = 0; kc < Cfg::KB; ++kc) {
+          mbar_wait(&k_empty[ks], kph ^ 1);
+          mbar_arrive_expect_tx(&k_full[ks], Cfg::K_SLOT);
+          tma_load_2d(sK + ks * Cfg::K_SLOT, &tmK, &k_full[ks], kc * 64, k_begin + j * AT_BN);
+          if (++ks == Cfg::NK) { ks = 0; kph ^= 1; }
+        }
       };
       auto load_v = [&](int j) {
-        mbar_wait(&slot_empty[slot], phase ^ 1);
-        uint8_t* dst = sSlots + slot * Cfg::SLOT_BYTES;
-        mbar_arrive_expect_tx(&slot_full[slot], Cfg::SLOT_BYTES);
-        for (int dc = 0; dc < Cfg::KB; ++dc)
-          tma_load_2d(dst + dc * 64 * 128, &tmV, &slot_full[slot], k_begin + j * AT_BN, dc * 64);
-        if (++slot == Cfg::NS) { slot = 0; phase ^= 1; }
+        for (int ka = 0; ka < 2; ++ka) {
+          mbar_wait(&v_empty[vs], vph ^ 1);
+          mbar_arrive_expect_tx(&v_full[vs], Cfg::V_SLOT);
+          uint8_t* dst = sV + vs * Cfg::V_SLOT;
+          for (int dc = 0; dc < Cfg::KB; ++dc)
+            tma_load_2d(dst + dc * 64 * 128, &tmV, &v_full[vs], k_begin + j * AT_BN + ka * 64, dc * 64);
+          if (++vs == Cfg::NV) { vs = 0; vph ^= 1; }
+        }
       };
+      // consumption order of the MMA warp: S0, then (S_{j+1}, PV_j) per block
       load_k(0);
       for (int j = 0; j < n_kb; ++j) {
         if (j + 1 < n_kb) load_k(j + 1);
@@ -128,44 +153,51 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     // ---------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc_s = idesc_bf16_f32(AT_BM, AT_BN);
     constexpr uint32_t idesc_o = idesc_bf16_f32(AT_BM, Cfg::PV_N);
-    int slot = 0;
-    uint32_t phase = 0;
+    int ks = 0, vs = 0;
+    uint32_t kph = 0, vph = 0;
     auto issue_s = [&](int j) {
-      const int buf = j & 1;
-      if (j >= 2) mbar_wait(&s_free[buf], ((j - 2) >> 1) & 1);
-      mbar_wait(&slot_full[slot], phase);
+      // S buffer is free once the softmax warps loaded S_{j-1}
+      if (j >= 1) mbar_wait(s_free, (j - 1) & 1);
       tc_fence_after();
-      if (lane == 0) {
-        const uint8_t* kt = sSlots + slot * Cfg::SLOT_BYTES;
-        for (int kc = 0; kc < Cfg::KB; ++kc)
+      for (int kc = 0; kc < Cfg::KB; ++kc) {
+        mbar_wait(&k_full[ks], kph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint8_t* kt = sK + ks * Cfg::K_SLOT;
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            mma_bf16_ss(tmem + Cfg::S_COL + buf * AT_BN, sdesc_sw128(sQ + kc * AT_BM * 128 + k * 32),
-                        sdesc_sw128(kt + kc * AT_BN * 128 + k * 32), idesc_s, (kc | k) != 0);
-        mma_commit(&slot_empty[slot]);
-        mma_commit(&s_full[buf]);
+            mma_bf16_ss(tmem + Cfg::S_COL, sdesc_sw128(sQ + kc * AT_BM * 128 + k * 32), sdesc_sw128(kt + k * 32),
+                        idesc_s, (kc | k) != 0);
+          mma_commit(&k_empty[ks]);
+          if (kc == Cfg::KB - 1) mma_commit(s_full);
+        }
+        __syncwarp();
+        if (++ks == Cfg::NK) { ks = 0; kph ^= 1; }
       }
-      __syncwarp();
-      if (++slot == Cfg::NS) { slot = 0; phase ^= 1; }
     };
     auto issue_pv = [&](int j) {
       mbar_wait(p_full, j & 1);
-      mbar_wait(&slot_full[slot], phase);
       tc_fence_after();
-      if (lane == 0) {
-        const uint8_t* vt = sSlots + slot * Cfg::SLOT_BYTES;
+      for (int ka = 0; ka < 2; ++ka) {
+        mbar_wait(&v_full[vs], vph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint8_t* vt = sV + vs * Cfg::V_SLOT;
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+          for (int k = 0; k < 4; ++k)
 #pragma unroll
-          for (int n = 0; n < Cfg::PV_MMAS; ++n)
-            mma_bf16_ss(tmem + Cfg::O_COL + n * Cfg::PV_N, sdesc_sw128(sP + k * 32),
-                        sdesc_sw128(vt + n * Cfg::PV_N * 128 + k * 32), idesc_o, (j | k) != 0);
-        mma_commit(&slot_empty[slot]);
-        mma_commit(p_free);
-        if (j == n_kb - 1) mma_commit(o_full);
+            for (int n = 0; n < Cfg::PV_MMAS; ++n)
+              mma_bf16_ts(tmem + Cfg::O_COL + n * Cfg::PV_N, tmem + Cfg::P_COL + ka * 32 + k * 8,
+                          sdesc_sw128(vt + n * Cfg::PV_N * 128 + k * 32), idesc_o, (j | ka | k) != 0);
+          mma_commit(&v_empty[vs]);
+          if (ka == 1) {
+            mma_commit(p_free);
+            if (j == n_kb - 1) mma_commit(o_full);
+          }
+        }
+        __syncwarp();
+        if (++vs == Cfg::NV) { vs = 0; vph ^= 1; }
       }
-      __syncwarp();
-      if (++slot == Cfg::NS) { slot = 0; phase ^= 1; }
     };
     mbar_wait(q_full, 0);
     issue_s(0);
@@ -180,24 +212,23 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     float m_run = -INFINITY, l_run = 0.f;
     for (int j = 0; j < n_kb; ++j) {
-      const int buf = j & 1;
-      mbar_wait(&s_full[buf], (j >> 1) & 1);
+      mbar_wait(s_full, j & 1);
       tc_fence_after();
-      uint32_t sr[64];
-      PS_TMEM_LD32(tmem + lane_base + Cfg::S_COL + buf * AT_BN, sr);
-      PS_TMEM_LD32(tmem + lane_base + Cfg::S_COL + buf * AT_BN + 32, (sr + 32));
+      uint32_t sr[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) PS_TMEM_LD32(tmem + lane_base + Cfg::S_COL + 32 * c, (sr + 32 * c));
       tmem_ld_wait();
       tc_fence_before();
-      mbar_arrive(&s_free[buf]);
+      mbar_arrive(s_free);
       const int kvalid = k_end - (k_begin + j * AT_BN);  // keys valid in this block
       if (kvalid < AT_BN) {  // only the last block of an image can be ragged
 #pragma unroll
-        for (int i = 0; i < 64; ++i)
+        for (int i = 0; i < 128; ++i)
           if (i >= kvalid) sr[i] = __float_as_uint(-INFINITY);
       }
       float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < 64; i += 4) {
+      for (int i = 0; i < 128; i += 4) {
         mx0 = fmaxf(mx0, fmaxf(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])));
         mx1 = fmaxf(mx1, fmaxf(__uint_as_float(sr[i + 2]), __uint_as_float(sr[i + 3])));
       }
@@ -209,17 +240,16 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       const float alpha = (m_run == -INFINITY) ? 0.f : ex2_approx(m_run - m_use);
       const float neg = -m_use;
       float sum0 = 0.f, sum1 = 0.f;
-      uint32_t pk[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
+      for (int i = 0; i < 64; ++i) {
         const float a = ex2_approx(fmaf(__uint_as_float(sr[2 * i]), p.scale_log2, neg));
         const float b = ex2_approx(fmaf(__uint_as_float(sr[2 * i + 1]), p.scale_log2, neg));
         sum0 += a;
         sum1 += b;
-        pk[i] = pack_bf16(a, b);
+        sr[i] = pack_bf16(a, b);  // packed P overwrites the consumed half of sr
       }
       l_run = l_run * alpha + (sum0 + sum1);
-      // P buffer and O are owned by the MMA of block j-1 until it completes
+      // P columns and O are owned by the MMAs of block j-1 until they complete
       if (j >= 1) mbar_wait(p_free, (j - 1) & 1);
       tc_fence_after();
       const bool warp_rescale = __any_sync(0xffffffffu, need && j >= 1 && alpha != 1.f);
@@ -234,15 +264,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * sc);
           PS_TMEM_ST16(tmem + lane_base + Cfg::O_COL + c, o);
         }
-        tmem_st_wait();
       }
       m_run = m_use;
-      // P row -> smem, K-major 128B-swizzled (16B chunk c of row r at c ^ (r & 7))
-      uint4* prow = reinterpret_cast<uint4*>(sP + row * 128);
 #pragma unroll
-      for (int c = 0; c < 8; ++c)
-        prow[c ^ (row & 7)] = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-      fence_proxy_async();
+      for (int c = 0; c < 4; ++c) PS_TMEM_ST16(tmem + lane_base + Cfg::P_COL + 16 * c, (sr + 16 * c));
+      tmem_st_wait();
       tc_fence_before();
       mbar_arrive(p_full);
     }

@@ -290,7 +290,7 @@ int ps_attention(void* stream, const void* qk, const void* vt, int ldv, int T, i
   if (n_tiles < 1) return PS_OK;
   CUtensorMap tq, tk, tv;
   int rc = make_tmap_2d(&tq, qk, T, Dp, 2 * (uint64_t)Dp, 128);
-  if (!rc) rc = make_tmap_2d(&tk, (const __nv_bfloat16*)qk + Dp, T, Dp, 2 * (uint64_t)Dp, 64);
+  if (!rc) rc = make_tmap_2d(&tk, (const __nv_bfloat16*)qk + Dp, T, Dp, 2 * (uint64_t)Dp, 128);
   if (!rc) rc = make_tmap_2d(&tv, vt, Dp, T, ldv, 64);
   if (rc) return rc;
   AttnParams p{};
