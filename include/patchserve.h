@@ -104,6 +104,7 @@ typedef struct ps_gemm_args {
   const void* resid; int c_real;
   int bn;                                 /* tile N: 64,128,160,192,256,320 (0 = auto) */
   int out_tiled;                          /* epi 0/1: write tile-major [ceil(M/128)][ldo/64][128][64] */
+  unsigned long long* dbg;                /* optional device counters [8] of per-role wait cycles, or NULL */
 } ps_gemm_args;
 int ps_gemm(void* stream, const ps_gemm_args* args);
 

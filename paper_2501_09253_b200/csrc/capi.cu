@@ -273,7 +273,8 @@ int ps_gemm(void* stream, const ps_gemm_args* a) {
   p.c_real = a->c_real;
   p.hw = a->ps * a->ps;
   p.out_tiled = a->out_tiled;
-  if (a->out_tiled && (a->epi > EPI_GELU_CL || a->ldo % 64))
+  p.dbg = a->dbg;
+  if (a->out_tiled && (a->epi > EPI_GELU_CL || a->ldo % 64 || bn % 64))
     return set_error(PS_ERR_INPUT, "gemm: tiled output needs a channels-last epilogue and ldo %% 64 == 0");
   if (a->epi == EPI_RESID_NCHW && (a->ps < 1 || a->c_real < 1 || a->c_real > a->N))
     return set_error(PS_ERR_INPUT, "gemm: NCHW epilogue needs ps and 1 <= c_real <= N");

@@ -105,6 +105,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // profiling: cycles each role spends blocked on its barriers (p.dbg != null)
+  unsigned long long t_wait = 0, t_wait2 = 0;
+  const long long t_start = clock64();
+  auto timed_wait = [&](uint64_t* bar, uint32_t par, unsigned long long& acc) {
+    if (p.dbg) {
+      const long long t0 = clock64();
+      mbar_wait(bar, par);
+      acc += clock64() - t0;
+    } else {
+      mbar_wait(bar, par);
+    }
+  };
   if (warp == 0) {
     // ---------------------------------------------------------------- producer
     if (lane == 0) {
@@ -128,7 +140,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             for (int n = kb * cpk; n < min(p.c_real, (kb + 1) * cpk); ++n)
               l2_prefetch(p.resid + ((size_t)pidx * p.c_real + n) * p.hw + pix0, GEMM_BM * 2);
           }
-          mbar_wait(&empty[stage], phase ^ 1);
+          timed_wait(&empty[stage], phase ^ 1, t_wait);
           uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
           uint8_t* sb = sa + Cfg::A_BYTES;
           mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
@@ -157,11 +169,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++li) {
       const int buf = li % Cfg::NBUF;
       const int use = li / Cfg::NBUF;
-      mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
+      timed_wait(&acc_empty[buf], (use & 1) ^ 1, t_wait2);
       tc_fence_after();
       const uint32_t d = tmem + buf * BN;
       for (int kb = 0; kb < num_kb; ++kb) {
-        mbar_wait(&full[stage], phase);
+        timed_wait(&full[stage], phase, t_wait);
         tc_fence_after();
         if (lane == 0) {
           const uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
@@ -194,7 +206,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const bool row_ok = m < p.M;
       const int pidx = p.hw > 0 ? m / p.hw : 0;
       const int pix = p.hw > 0 ? m - pidx * p.hw : 0;
-      mbar_wait(&acc_full[buf], use & 1);
+      timed_wait(&acc_full[buf], use & 1, t_wait);
       tc_fence_after();
       // NCHW epilogue through a smem transpose: thread (channel, 16-pixel run) moves
       // 32 contiguous bytes of residual in and of output out
@@ -294,6 +306,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tc_fence_before();
       mbar_arrive(&acc_empty[buf]);
     }
+  }
+  if (p.dbg && lane == 0) {
+    const unsigned long long tot = clock64() - t_start;
+    if (warp == 0) { atomicAdd(p.dbg + 0, t_wait); atomicAdd(p.dbg + 1, tot); }
+    if (warp == 1) { atomicAdd(p.dbg + 2, t_wait); atomicAdd(p.dbg + 3, t_wait2); atomicAdd(p.dbg + 4, tot); }
+    if (warp == 4) { atomicAdd(p.dbg + 5, t_wait); atomicAdd(p.dbg + 6, tot); }
   }
   tc_fence_before();
   __syncthreads();

@@ -26,6 +26,7 @@ struct GemmParams {
   const __nv_bfloat16* resid;  // EPI_RESID_NCHW: block input (P, c_real, hw) or null
   int c_real, hw;
   int out_tiled;  // CL stores in 128x64 tile-major order ([M/128][ldo/64][128][64])
+  unsigned long long* dbg;  // optional per-role wait-cycle counters (profiling)
 };
 
 int set_error(int code, const char* fmt, ...);

@@ -1,0 +1,48 @@
+"""Per-role barrier wait fractions of the config-2 GEMMs (GemmArgs.dbg counters)."""
+import ctypes as C, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2501_09253_b200 import _lib
+from paper_2501_09253_b200._dev import stream
+
+T = 118784
+def run(name, M, N, K, epi, bn=0, out_tiled=0, a_tiled=0, resid=False):
+    a = torch.randn(M if not a_tiled else ((M + 127) // 128 * 128), K, device="cuda").to(torch.bfloat16)
+    b = (torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
+    bias = torch.zeros(N, device="cuda")
+    dbg = torch.zeros(8, dtype=torch.int64, device="cuda")
+    out = torch.empty(max(M * N, (M + 127) // 128 * 128 * N) + 1024, dtype=torch.bfloat16, device="cuda")
+    out2 = torch.empty(N * ((M + 63) // 64 * 64), dtype=torch.bfloat16, device="cuda")
+    res = torch.randn(M * N, device="cuda").to(torch.bfloat16) if resid else None
+    g = _lib.GemmArgs()
+    g.a, g.lda, g.M, g.a_mode = a.data_ptr(), K, M, 2 if a_tiled else 0
+    g.b, g.N, g.K, g.bias = b.data_ptr(), N, K, bias.data_ptr()
+    g.epi, g.out, g.ldo, g.bn, g.out_tiled = epi, out.data_ptr(), N, bn, out_tiled
+    g.P, g.ps = M // 1024, 32
+    if epi == 3:
+        g.out2, g.ldo2, g.n_split, g.ldo = out2.data_ptr(), (M + 63) // 64 * 64, 2 * N // 3, 2 * N // 3
+    if epi == 2:
+        g.resid, g.c_real = res.data_ptr(), N
+    for i in range(3):
+        _lib.check(_lib.load().ps_gemm(stream(), C.byref(g)))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(5):
+        _lib.check(_lib.load().ps_gemm(stream(), C.byref(g)))
+    e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    g.dbg = dbg.data_ptr()
+    _lib.check(_lib.load().ps_gemm(stream(), C.byref(g)))
+    torch.cuda.synchronize()
+    d = dbg.tolist()
+    f = lambda a, b: a / b if b else 0
+    print(f"{name:8s} {ms*1e3:7.1f} us {2*M*N*K/ms/1e9:7.1f} TF | prod wait {f(d[0],d[1]):.2f} | mma wait-full {f(d[2],d[4]):.2f} wait-acc {f(d[3],d[4]):.2f} | epi wait-acc {f(d[5],d[6]):.2f}")
+
+run("conv-ish", T, 320, 2880, 0)
+run("qkv", T, 960, 320, 3)
+run("oproj", T, 320, 320, 0)
+run("ff1", T, 1280, 320, 1, out_tiled=1)
+run("ff2", T, 320, 1280, 2, a_tiled=1, resid=True)
+run("ff2-cl", T, 320, 1280, 0, a_tiled=1)
+run("plain256", T, 256, 1024, 0)
