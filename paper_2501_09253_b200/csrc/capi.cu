@@ -50,7 +50,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // bf16 tensor map with 128B swizzle; dims/strides innermost first (strides in bytes, rank-1 of them).
 int make_tmap(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
-              const uint32_t* box) {
+              const uint32_t* box, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto fn = encode_fn();
   if (!fn) return set_error(PS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   if (reinterpret_cast<uintptr_t>(base) % 16) return set_error(PS_ERR_INPUT, "TMA base not 16B aligned");
@@ -58,7 +58,7 @@ int make_tmap(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, 
     if (strides_bytes[i] % 16) return set_error(PS_ERR_INPUT, "TMA stride %d not a multiple of 16B", i);
   uint32_t es[5] = {1, 1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims, strides_bytes, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(PS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return PS_OK;
@@ -274,13 +274,33 @@ int ps_gemm(void* stream, const ps_gemm_args* a) {
   p.hw = a->ps * a->ps;
   p.out_tiled = a->out_tiled;
   p.dbg = a->dbg;
+  // channels-last outputs leave through TMA stores (32 rows x 16 columns per warp box)
+  CUtensorMap tc;
+  memset(&tc, 0, sizeof(tc));
+  p.store_tma = 0;
+  if ((a->epi == EPI_STORE_CL || a->epi == EPI_GELU_CL || a->epi == EPI_SPLIT_VT) && a->ldo % 8 == 0) {
+    uint64_t dims[2], strides[1];
+    if (a->out_tiled) {
+      dims[0] = 64;
+      dims[1] = (uint64_t)((a->M + 127) / 128) * (a->ldo / 64) * 128;
+      strides[0] = 128;
+    } else {
+      dims[0] = (uint64_t)(a->epi == EPI_SPLIT_VT ? a->n_split : a->N);
+      dims[1] = (uint64_t)a->M;
+      strides[0] = (uint64_t)a->ldo * 2;
+    }
+    uint32_t box[2] = {32, 128};
+    rc = make_tmap(&tc, a->out, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (rc) return rc;
+    p.store_tma = 1;
+  }
   if (a->out_tiled && (a->epi > EPI_GELU_CL || a->ldo % 64 || bn % 64))
     return set_error(PS_ERR_INPUT, "gemm: tiled output needs a channels-last epilogue and ldo %% 64 == 0");
   if (a->epi == EPI_RESID_NCHW && (a->ps < 1 || a->c_real < 1 || a->c_real > a->N))
     return set_error(PS_ERR_INPUT, "gemm: NCHW epilogue needs ps and 1 <= c_real <= N");
   if ((a->epi == EPI_STORE_CL || a->epi == EPI_GELU_CL) && (a->ldo < a->N || a->ldo % 8))
     return set_error(PS_ERR_INPUT, "gemm: ldo must be >= N and a multiple of 8");
-  return gemm_launch(ta, tb, p, bn, (cudaStream_t)stream);
+  return gemm_launch(ta, tb, tc, p, bn, (cudaStream_t)stream);
 }
 
 // ----------------------------------------------------------- attention

@@ -54,6 +54,17 @@ PS_DEV void tma_load_4d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, 
       : "memory");
 }
 
+PS_DEV void tma_store_2d(const CUtensorMap* m, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+PS_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+PS_DEV void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+template <int N>
+PS_DEV void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory"); }
 PS_DEV void l2_prefetch(const void* ptr, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(ptr)), "r"(bytes)
                : "memory");
@@ -157,5 +168,21 @@ PS_DEV float gelu_tanh(float x) {
   return 0.5f * x * (1.0f + tanhf(0.7978845608028654f * (x + 0.044715f * x * x * x)));
 }
 PS_DEV float bf(__nv_bfloat16 v) { return __bfloat162float(v); }
+// GELU (tanh form, kernels.py:118-121) on two packed bf16 values:
+// 0.5 x (1 + tanh(x (c0 + c1 x^2))), c0 = sqrt(2/pi), c1 = 0.044715 c0.
+// Five bf16x2 FMA-pipe ops + one MUFU per pair; max error ~1.3 bf16 ulps.
+PS_DEV uint32_t gelu_bf16x2(uint32_t hx) {
+  uint32_t x2, t, u, th, h, y;
+  const uint32_t c0 = 0x3F4C3F4Cu;   // bf16x2(0.7978845608) = 0x3F4C
+  const uint32_t c1 = 0x3D123D12u;   // bf16x2(0.0356774081) = 0x3D12
+  const uint32_t half = 0x3F003F00u; // bf16x2(0.5)
+  asm("mul.rn.bf16x2 %0, %1, %1;" : "=r"(x2) : "r"(hx));
+  asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(t) : "r"(x2), "r"(c1), "r"(c0));
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(u) : "r"(t), "r"(hx));
+  asm("tanh.approx.bf16x2 %0, %1;" : "=r"(th) : "r"(u));
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(h) : "r"(hx), "r"(half));
+  asm("fma.rn.bf16x2 %0, %1, %2, %1;" : "=r"(y) : "r"(h), "r"(th));
+  return y;
+}
 
 }  // namespace ps

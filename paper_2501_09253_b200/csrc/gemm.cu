@@ -43,13 +43,14 @@ struct GemmCfg {
   static constexpr int A_BYTES = GEMM_BM * 128;
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = (176 * 1024) / STAGE_BYTES > 8 ? 8 : (176 * 1024) / STAGE_BYTES;
   static constexpr int TMEM_COLS = NBUF * BN <= 128 ? 128 : NBUF * BN <= 256 ? 256 : 512;
   static constexpr int HALF = BN / 2;  // columns per epilogue warp
-  static constexpr int STAGE_EPI = 2 * 16 * GEMM_BM * 4;  // NCHW transpose staging, per column half
-  static constexpr int SMEM = STAGES * STAGE_BYTES + STAGE_EPI + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int STAGE_EPI = 2 * 16 * GEMM_BM * 4;  // transposed-store staging, per epilogue warpgroup
+  static constexpr int STAGE_TMA = 2 * 2 * GEMM_BM * 64;  // per warpgroup: two 128x32 bf16 store boxes
+  static constexpr int SMEM = STAGES * STAGE_BYTES + STAGE_EPI + STAGE_TMA + 1024 /*align*/ + 256 /*barriers*/;
   static_assert(MMA_N % 16 == 0 && MMA_N >= 64 && MMA_N <= 256, "invalid UMMA N");
-  static_assert(HALF % 16 == 0, "epilogue chunking");
+  static_assert(BN % 32 == 0 && (BN / 2) % 32 == 0 || BN <= 256, "epilogue chunking");
 };
 
 __device__ __forceinline__ void store16_cl(__nv_bfloat16* dst, const float* v) {
@@ -69,12 +70,13 @@ __device__ __forceinline__ void store16_cl(__nv_bfloat16* dst, const float* v) {
 template <int BN>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const GemmParams p) {
+                   const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
   using Cfg = GemmCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* epi_stage = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + Cfg::STAGE_EPI);
+  uint8_t* tma_stage = smem + Cfg::STAGES * Cfg::STAGE_BYTES + Cfg::STAGE_EPI;
+  uint64_t* full = reinterpret_cast<uint64_t*>(tma_stage + Cfg::STAGE_TMA);
   uint64_t* empty = full + Cfg::STAGES;
   uint64_t* acc_full = empty + Cfg::STAGES;  // [2]
   uint64_t* acc_empty = acc_full + 2;        // [2]
@@ -89,13 +91,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    if (p.store_tma) tma_prefetch(&tmC);
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], GEMM_EPI_THREADS);
+      mbar_init(&acc_empty[b], Cfg::NBUF == 2 ? GEMM_EPI_THREADS / 2 : GEMM_EPI_THREADS);
     }
     fence_mbar_init();
   }
@@ -193,120 +196,181 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp >= 4) {
     // ---------------------------------------------------------------- epilogue
-    const int wq = warp & 3;
-    const int half = (warp - 4) >> 2;
-    const int row = wq * 32 + lane;
+    // Two warpgroups.  With double-buffered accumulators (NBUF = 2) warpgroup g
+    // owns the tiles whose accumulator is buffer g, so each has two MMA-tile
+    // durations for its epilogue; with NBUF = 1 they split the columns.
+    //  * channels-last outputs: 32-column chunks staged in a 64B-swizzled
+    //    [128 rows x 64 B] smem box, written by one TMA store per chunk;
+    //  * NCHW (residual) / V^T outputs: 16-column pieces transposed through smem,
+    //    each thread moving 32 contiguous bytes along the token axis.
+    const int wg = (warp - 4) >> 2;  // epilogue warpgroup
+    const int wq = warp & 3;         // TMEM lane quadrant
+    const int row = wq * 32 + lane;  // tile row = TMEM lane
+    const int bar_id = 1 + wg;
+    const bool leader = (warp & 3) == 0 && lane == 0;
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    uint8_t* box_base = tma_stage + wg * 2 * (GEMM_BM * 64);  // two 8 KB boxes per warpgroup
+    float* st = epi_stage + wg * 16 * GEMM_BM;                 // [16][128] fp32 transpose tile
+    const int ci = row >> 3, seg = row & 7;                    // transposed role
+    const int c_lo = Cfg::NBUF == 1 ? wg * (BN / 2) : 0;
+    const int c_hi = Cfg::NBUF == 1 ? c_lo + BN / 2 : BN;
+    int n_store = 0;
     int li = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++li) {
       const int buf = li % Cfg::NBUF;
       const int use = li / Cfg::NBUF;
+      if (Cfg::NBUF == 2 && buf != wg) continue;
       const int m_tile = t / num_n, n_tile = t % num_n;
       const int m = m_tile * GEMM_BM + row;
       const bool row_ok = m < p.M;
+      const bool tile_full = (m_tile + 1) * GEMM_BM <= p.M;
       const int pidx = p.hw > 0 ? m / p.hw : 0;
       const int pix = p.hw > 0 ? m - pidx * p.hw : 0;
-      timed_wait(&acc_full[buf], use & 1, t_wait);
-      tc_fence_after();
-      // NCHW epilogue through a smem transpose: thread (channel, 16-pixel run) moves
-      // 32 contiguous bytes of residual in and of output out
-      const bool vec_nchw = p.epi == EPI_RESID_NCHW && (p.hw % 16) == 0 && (m_tile + 1) * GEMM_BM <= p.M;
-      float* st = epi_stage + half * 16 * GEMM_BM;
-      const int tq = wq * 32 + lane;  // thread index within this column half
-      const int ci = tq >> 3, seg = tq & 7;
       const int tok_v = m_tile * GEMM_BM + seg * 16;
       const int pidx_v = p.hw > 0 ? tok_v / p.hw : 0;
       const int pix_v = p.hw > 0 ? tok_v - pidx_v * p.hw : 0;
+      const bool vec_nchw = p.epi == EPI_RESID_NCHW && (p.hw % 16) == 0 && tile_full;
+      const bool vec_vt = p.epi == EPI_SPLIT_VT && (p.ldo2 % 8) == 0 && tile_full;
+      timed_wait(&acc_full[buf], use & 1, t_wait);
+      tc_fence_after();
+      if (n_tile * BN + c_lo >= p.N) {  // no columns of this tile for this warpgroup
+        tc_fence_before();
+        mbar_arrive(&acc_empty[buf]);
+        continue;
+      }
 #pragma unroll 1
-      for (int c = half * Cfg::HALF; c < (half + 1) * Cfg::HALF; c += 16) {
-        uint32_t r[16];
-        PS_TMEM_LD16(tmem + lane_base + buf * BN + c, r);
+      for (int c = c_lo; c < c_hi; c += 32) {
         const int nb = n_tile * BN + c;
-        uint4 rs0 = make_uint4(0, 0, 0, 0), rs1 = rs0;
-        const int nv = nb + ci;
-        const size_t off_v = ((size_t)pidx_v * p.c_real + nv) * p.hw + pix_v;
-        if (vec_nchw && p.resid != nullptr && nv < p.c_real) {
-          rs0 = __ldg(reinterpret_cast<const uint4*>(p.resid + off_v));
-          rs1 = __ldg(reinterpret_cast<const uint4*>(p.resid + off_v) + 1);
-        }
-        // bias: four 16-byte broadcast loads while the TMEM load is in flight
-        float bv[16];
-        if (p.bias != nullptr && nb < p.N) {
+        if (nb >= p.N) break;  // uniform across the warpgroup
+        uint32_t r[32];
+        PS_TMEM_LD32(tmem + lane_base + buf * BN + c, r);
+        float bv[32];
+        if (p.bias != nullptr) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < 8; ++q) {
             const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + nb) + q);
             bv[4 * q] = b4.x; bv[4 * q + 1] = b4.y; bv[4 * q + 2] = b4.z; bv[4 * q + 3] = b4.w;
           }
         } else {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) bv[i] = 0.f;
+          for (int i = 0; i < 32; ++i) bv[i] = 0.f;
         }
         tmem_ld_wait();
-        if (nb >= p.N) continue;
-        float v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          float x = __uint_as_float(r[i]) + bv[i];
-          if (p.epi == EPI_GELU_CL) {
-            const float u = 0.7978845608028654f * fmaf(0.044715f * x, x * x, x);
-            const float hx = 0.5f * x;
-            x = fmaf(hx, tanh_fast(u), hx);
-          }
-          v[i] = x;
+        if (c + 32 >= c_hi || nb + 32 >= p.N) {
+          // last chunk of this tile for this warpgroup: hand the accumulator back early
+          tc_fence_before();
+          mbar_arrive(&acc_empty[buf]);
         }
-        if (vec_nchw) {
+        float v[32];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) st[i * GEMM_BM + row] = v[i];
-          named_bar_sync(1 + half, 128);
-          if (nv < p.c_real) {
-            const float4* src = reinterpret_cast<const float4*>(st + ci * GEMM_BM + seg * 16);
-            float o[16];
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) + bv[i];
+        const bool cl_tma = p.store_tma &&
+                            (p.epi == EPI_STORE_CL || p.epi == EPI_GELU_CL || (p.epi == EPI_SPLIT_VT && nb < p.n_split));
+        if (cl_tma) {
+          uint8_t* box = box_base + (n_store & 1) * (GEMM_BM * 64);
+          if (leader) bulk_wait_read<1>();  // the TMA store that last used this box has read it
+          named_bar_sync(bar_id, 128);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float4 f = src[q];
-              o[4 * q] = f.x; o[4 * q + 1] = f.y; o[4 * q + 2] = f.z; o[4 * q + 3] = f.w;
+          for (int q = 0; q < 4; ++q) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              pk[e] = pack_bf16(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
+              if (p.epi == EPI_GELU_CL) pk[e] = gelu_bf16x2(pk[e]);
             }
-            const __nv_bfloat162* h0 = reinterpret_cast<const __nv_bfloat162*>(&rs0);
-            const __nv_bfloat162* h1 = reinterpret_cast<const __nv_bfloat162*>(&rs1);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              o[2 * q] += __low2float(h0[q]);
-              o[2 * q + 1] += __high2float(h0[q]);
-              o[8 + 2 * q] += __low2float(h1[q]);
-              o[8 + 2 * q + 1] += __high2float(h1[q]);
-            }
-            store16_cl(p.out + off_v, o);
+            *reinterpret_cast<uint4*>(box + row * 64 + ((q ^ ((row >> 1) & 3)) << 4)) =
+                make_uint4(pk[0], pk[1], pk[2], pk[3]);
           }
-          named_bar_sync(1 + half, 128);
+          fence_proxy_async();
+          named_bar_sync(bar_id, 128);
+          if (leader) {
+            if (p.out_tiled)
+              tma_store_2d(&tmC, box, nb & 63, (m_tile * (p.ldo / 64) + nb / 64) * GEMM_BM);
+            else
+              tma_store_2d(&tmC, box, nb, m_tile * GEMM_BM);
+            bulk_commit();
+          }
+          ++n_store;
           continue;
         }
-        if (!row_ok) continue;
-        if (p.epi == EPI_STORE_CL || p.epi == EPI_GELU_CL || (p.epi == EPI_SPLIT_VT && nb < p.n_split)) {
-          if (p.out_tiled)
-            store16_cl(p.out + (((size_t)m_tile * (p.ldo / 64) + nb / 64) * GEMM_BM + row) * 64 + (nb & 63), v);
-          else
-            store16_cl(p.out + (size_t)m * p.ldo + nb, v);
-        } else if (p.epi == EPI_SPLIT_VT) {
+        if (p.epi == EPI_GELU_CL) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            p.out2[(size_t)(nb + i - p.n_split) * p.ldo2 + m] = __float2bfloat16_rn(v[i]);
-        } else {  // EPI_RESID_NCHW, ragged tile: scalar path
+          for (int i = 0; i < 32; ++i) {
+            const float x = v[i];
+            const float u = 0.7978845608028654f * fmaf(0.044715f * x, x * x, x);
+            const float hx = 0.5f * x;
+            v[i] = fmaf(hx, tanh_fast(u), hx);
+          }
+        }
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int n = nb + i;
-            if (n < p.c_real) {
-              const size_t off = ((size_t)pidx * p.c_real + n) * p.hw + pix;
-              float x = v[i];
-              if (p.resid != nullptr) x += bf(p.resid[off]);
-              p.out[off] = __float2bfloat16_rn(x);
+        for (int s16 = 0; s16 < 32; s16 += 16) {
+          const int n0 = nb + s16;
+          if (n0 >= p.N) break;
+          const bool tr_vt = vec_vt && n0 >= p.n_split;
+          if (vec_nchw || tr_vt) {
+            // transposed store: thread (column n0 + ci, tokens tok_v .. +15)
+            const int nv = n0 + ci;
+            const size_t off_v = tr_vt ? (size_t)(nv - p.n_split) * p.ldo2 + tok_v
+                                       : ((size_t)pidx_v * p.c_real + nv) * p.hw + pix_v;
+            uint4 rs0 = make_uint4(0, 0, 0, 0), rs1 = rs0;
+            if (vec_nchw && p.resid != nullptr && nv < p.c_real) {
+              rs0 = __ldg(reinterpret_cast<const uint4*>(p.resid + off_v));
+              rs1 = __ldg(reinterpret_cast<const uint4*>(p.resid + off_v) + 1);
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) st[i * GEMM_BM + row] = v[s16 + i];
+            named_bar_sync(bar_id, 128);
+            if (tr_vt || nv < p.c_real) {
+              const float4* src = reinterpret_cast<const float4*>(st + ci * GEMM_BM + seg * 16);
+              float o[16];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float4 f = src[q];
+                o[4 * q] = f.x; o[4 * q + 1] = f.y; o[4 * q + 2] = f.z; o[4 * q + 3] = f.w;
+              }
+              const __nv_bfloat162* h0 = reinterpret_cast<const __nv_bfloat162*>(&rs0);
+              const __nv_bfloat162* h1 = reinterpret_cast<const __nv_bfloat162*>(&rs1);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                o[2 * q] += __low2float(h0[q]);
+                o[2 * q + 1] += __high2float(h0[q]);
+                o[8 + 2 * q] += __low2float(h1[q]);
+                o[8 + 2 * q + 1] += __high2float(h1[q]);
+              }
+              store16_cl((tr_vt ? p.out2 : p.out) + off_v, o);
+            }
+            named_bar_sync(bar_id, 128);
+            continue;
+          }
+          if (!row_ok) continue;
+          if (p.epi == EPI_STORE_CL || p.epi == EPI_GELU_CL || p.epi == EPI_SPLIT_VT) {
+            if (p.epi == EPI_SPLIT_VT && n0 >= p.n_split) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                p.out2[(size_t)(n0 + i - p.n_split) * p.ldo2 + m] = __float2bfloat16_rn(v[s16 + i]);
+            } else if (p.out_tiled) {
+              store16_cl(p.out + (((size_t)m_tile * (p.ldo / 64) + n0 / 64) * GEMM_BM + row) * 64 + (n0 & 63),
+                         v + s16);
+            } else {
+              store16_cl(p.out + (size_t)m * p.ldo + n0, v + s16);
+            }
+          } else {  // EPI_RESID_NCHW, ragged tile: scalar path
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int n = n0 + i;
+              if (n < p.c_real) {
+                const size_t off = ((size_t)pidx * p.c_real + n) * p.hw + pix;
+                float x = v[s16 + i];
+                if (p.resid != nullptr) x += bf(p.resid[off]);
+                p.out[off] = __float2bfloat16_rn(x);
+              }
             }
           }
         }
       }
-      tc_fence_before();
-      mbar_arrive(&acc_empty[buf]);
     }
   }
+  if (warp >= 4 && lane == 0 && p.store_tma) bulk_wait<0>();
   if (p.dbg && lane == 0) {
     const unsigned long long tot = clock64() - t_start;
     if (warp == 0) { atomicAdd(p.dbg + 0, t_wait); atomicAdd(p.dbg + 1, tot); }
@@ -331,7 +395,8 @@ static int num_sms() {
 }
 
 template <int BN>
-static int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p, cudaStream_t st) {
+static int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const GemmParams& p,
+                     cudaStream_t st) {
   using Cfg = GemmCfg<BN>;
   static bool attr = false;
   if (!attr) {
@@ -340,19 +405,20 @@ static int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const GemmParam
   }
   const int tiles = ((p.M + GEMM_BM - 1) / GEMM_BM) * ((p.N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  gemm_tc_kernel<BN><<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(a, b, p);
+  gemm_tc_kernel<BN><<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(a, b, c, p);
   count_launch();
   return check_launch("gemm_tc");
 }
 
-int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p, int bn, cudaStream_t st) {
+int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const GemmParams& p, int bn,
+                cudaStream_t st) {
   switch (bn) {
-    case 64: return launch_bn<64>(a, b, p, st);
-    case 128: return launch_bn<128>(a, b, p, st);
-    case 160: return launch_bn<160>(a, b, p, st);
-    case 192: return launch_bn<192>(a, b, p, st);
-    case 256: return launch_bn<256>(a, b, p, st);
-    case 320: return launch_bn<320>(a, b, p, st);
+    case 64: return launch_bn<64>(a, b, c, p, st);
+    case 128: return launch_bn<128>(a, b, c, p, st);
+    case 160: return launch_bn<160>(a, b, c, p, st);
+    case 192: return launch_bn<192>(a, b, c, p, st);
+    case 256: return launch_bn<256>(a, b, c, p, st);
+    case 320: return launch_bn<320>(a, b, c, p, st);
     default: return set_error(PS_ERR_INPUT, "unsupported GEMM tile N %d", bn);
   }
 }

@@ -27,12 +27,14 @@ struct GemmParams {
   int c_real, hw;
   int out_tiled;  // CL stores in 128x64 tile-major order ([M/128][ldo/64][128][64])
   unsigned long long* dbg;  // optional per-role wait-cycle counters (profiling)
+  int store_tma;            // channels-last stores through the tmC tensor map (32x16 boxes)
 };
 
 int set_error(int code, const char* fmt, ...);
 int check_launch(const char* what);
 void count_launch();
-int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p, int bn, cudaStream_t st);
+int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const GemmParams& p, int bn,
+                cudaStream_t st);
 int gemm_pick_bn(int n, int k);
 
 struct AttnParams {
