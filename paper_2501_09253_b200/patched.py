@@ -229,7 +229,8 @@ class Ctx:
         o = self.empty_cl(dpp)
         timer = ATTN_TIMER
         if timer is not None:
-            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ext = torch.cuda.is_current_stream_capturing()  # event nodes inside a captured graph
+            ev = (torch.cuda.Event(enable_timing=True, external=ext), torch.cuda.Event(enable_timing=True, external=ext))
             ev[0].record()
         _lib.call("ps_attention", stream(), qk.data_ptr(), vt.data_ptr(), ldv, self.T, dpp, d,
                   self.dev["img_tok0"].data_ptr(), self.dev["tile_q0"].data_ptr(), self.dev["tile_img"].data_ptr(),

@@ -1,0 +1,173 @@
+"""Streaming denoise steps for a fixed batch composition.
+
+The serving loop of the reference re-splits, runs the blocks and reassembles
+every step (engine.py:126-160).  For a composition that stays fixed across
+steps (the common case between admissions), `DenoisePipeline` captures that
+whole step — CSP split (csp.py:117-193), prompt bias (model.py:163), the
+blocks (patched.py:179-221), blend (model.py:129-131) and reassemble
+(csp.py:196-214) — into one CUDA graph per buffer set, and overlaps each
+step's host->device input copy and device->host result copy with the compute
+of its neighbours on separate streams:
+
+    copy-in  stream:  H2D(i+1) .......
+    compute  stream:  graph(i)  graph(i+1) ...
+    copy-out stream:  ........ D2H(i-1)
+
+Two buffer sets alternate, so step i+1's inputs land while step i computes.
+Every device kernel is the library's (no host syncs inside a step, ~70 kernel
+launches replayed as one graph).
+"""
+
+from __future__ import annotations
+
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._dev import require_cuda
+from .csp import split
+from .model import ModelConfig, blend_batch, prompt_bias, rate_schedule
+from .patched import run_block
+
+
+class DenoisePipeline:
+    def __init__(self, cfg: ModelConfig, weights, dims: Sequence[int], patch_size: int,
+                 channels: int | None = None, n_sets: int = 2, use_graph: bool = True):
+        self.dev = require_cuda()
+        self.cfg, self.weights = cfg, weights
+        self.dims = [int(d) for d in dims]
+        self.C = channels or cfg.channels
+        self.ps = int(patch_size)
+        self.n_sets = n_sets
+        self.use_graph = use_graph
+        R = len(self.dims)
+        # static per-set buffers: per-request latents in/out, prompt bias, rates
+        self.lat_in = [[torch.empty((self.C, d, d), dtype=torch.float32, device=self.dev) for d in self.dims]
+                       for _ in range(n_sets)]
+        self.lat_out = [[torch.empty_like(x) for x in s] for s in self.lat_in]
+        self.bias = [torch.zeros((R, self.C), dtype=torch.float32, device=self.dev) for _ in range(n_sets)]
+        self.rates = [torch.zeros(R, dtype=torch.float32, device=self.dev) for _ in range(n_sets)]
+        self.bias_host = [torch.zeros((R, self.C), dtype=torch.float32).pin_memory() for _ in range(n_sets)]
+        # one CSP batch per set; its device metadata is built once and reused every step
+        self.batches = [split([(f"s{k}-r{i}", x) for i, x in enumerate(self.lat_in[k])], patch_size=self.ps)
+                        for k in range(n_sets)]
+        order = [int(e.request_id.split("-r")[1]) for e in self.batches[0].requests]
+        self.slot_of_req = {r: s for s, r in enumerate(order)}  # arrival index -> storage slot
+        self.s_in = torch.cuda.Stream(self.dev)
+        self.s_out = torch.cuda.Stream(self.dev)
+        self.graphs = [None] * n_sets
+        self._pool = None
+        self.ev_h2d = [torch.cuda.Event() for _ in range(n_sets)]
+        self.ev_comp = [torch.cuda.Event() for _ in range(n_sets)]
+        self.ev_d2h = [torch.cuda.Event() for _ in range(n_sets)]
+
+    # ------------------------------------------------------------ step body
+    def _step(self, k: int) -> None:
+        b = self.batches[k]
+        src_ptrs = b.device()
+        _lib.call("ps_csp_split", torch.cuda.current_stream().cuda_stream, self._in_ptrs[k].data_ptr(),
+                  src_ptrs["request_offset"].data_ptr(), src_ptrs["sides"].data_ptr(), b.n_requests, self.C,
+                  self.ps, _lib.DTYPE_F32, b.data.data_ptr(), b.n_patches)
+        h = prompt_bias(b, b.data, self.bias[k])
+        for ops in self.weights:
+            h = run_block(b, h, ops)
+        new = blend_batch(b, b.data, h, self.rates[k])
+        _lib.call("ps_csp_reassemble", torch.cuda.current_stream().cuda_stream, new.data_ptr(),
+                  self._out_ptrs[k].data_ptr(), src_ptrs["request_offset"].data_ptr(), src_ptrs["sides"].data_ptr(),
+                  b.n_requests, self.C, self.ps, _lib.DTYPE_F32, b.n_patches)
+
+    def prepare(self) -> None:
+        """Upload weights (eager warm-up) and capture one graph per buffer set."""
+        self._in_ptrs, self._out_ptrs = [], []
+        for k in range(self.n_sets):
+            order = [self.slot_of_req_inv(s) for s in range(len(self.dims))]
+            self._in_ptrs.append(torch.tensor([self.lat_in[k][r].data_ptr() for r in order], dtype=torch.int64,
+                                              device=self.dev))
+            self._out_ptrs.append(torch.tensor([self.lat_out[k][r].data_ptr() for r in order], dtype=torch.int64,
+                                               device=self.dev))
+        for k in range(self.n_sets):
+            self._step(k)  # eager: weights, metadata, tensor maps, kernel attributes
+        torch.cuda.synchronize()
+        l0 = _lib.launches()
+        self._step(0)
+        torch.cuda.synchronize()
+        self.kernels_per_step = _lib.launches() - l0
+        if not self.use_graph:
+            return
+        cap = torch.cuda.Stream(self.dev)
+        for k in range(self.n_sets):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, pool=self._pool, stream=cap):
+                self._step(k)
+            if self._pool is None:
+                self._pool = g.pool()
+            self.graphs[k] = g
+        torch.cuda.synchronize()
+
+    def slot_of_req_inv(self, slot: int) -> int:
+        for r, s in self.slot_of_req.items():
+            if s == slot:
+                return r
+        raise KeyError(slot)
+
+    # ---------------------------------------------------------------- run
+    def set_prompts(self, prompts: Sequence[np.ndarray]) -> None:
+        """Per-request prompt vectors in arrival order (model.py:97-103)."""
+        for k in range(self.n_sets):
+            for r, v in enumerate(prompts):
+                self.bias_host[k][self.slot_of_req[r]] = torch.as_tensor(np.asarray(v, dtype=np.float32))
+            self.bias[k].copy_(self.bias_host[k])
+
+    def run(self, host_inputs: Sequence[Sequence[torch.Tensor]], step_idx: Sequence[Sequence[int]],
+            total_steps: Sequence[int], host_outputs: Sequence[Sequence[torch.Tensor]]) -> None:
+        """Denoise len(host_inputs) independent steps.
+
+        host_inputs[i][r]: pinned (C, L_r, L_r) fp32 latents of request r for step i;
+        step_idx[i][r] / total_steps[r]: schedule position (model.py:56-63);
+        host_outputs[i][r]: pinned destination of the updated latents.
+        """
+        comp = torch.cuda.current_stream()
+        n = len(host_inputs)
+        # per-step rates for all steps, uploaded once (storage-slot order)
+        table = np.zeros((n, len(self.dims)), dtype=np.float32)
+        for i in range(n):
+            for r in range(len(self.dims)):
+                table[i, self.slot_of_req[r]] = rate_schedule(step_idx[i][r], total_steps[r])
+        rates_dev = torch.as_tensor(table, device=self.dev)
+        self.s_in.wait_stream(comp)  # rates_dev was written on the compute stream
+        for i in range(n):
+            k = i % self.n_sets
+            # copy-in: wait until the compute that last read set k is done
+            self.s_in.wait_event(self.ev_comp[k])
+            with torch.cuda.stream(self.s_in):
+                for r, x in enumerate(host_inputs[i]):
+                    self.lat_in[k][r].copy_(x, non_blocking=True)
+                self.rates[k].copy_(rates_dev[i], non_blocking=True)
+                self.ev_h2d[k].record(self.s_in)
+            # compute: inputs landed and the previous results of set k were copied out
+            comp.wait_event(self.ev_h2d[k])
+            comp.wait_event(self.ev_d2h[k])
+            if self.graphs[k] is not None:
+                self.graphs[k].replay()
+            else:
+                self._step(k)
+            self.ev_comp[k].record(comp)
+            # copy-out
+            self.s_out.wait_event(self.ev_comp[k])
+            with torch.cuda.stream(self.s_out):
+                for r, y in enumerate(host_outputs[i]):
+                    y.copy_(self.lat_out[k][r], non_blocking=True)
+                self.ev_d2h[k].record(self.s_out)
+        comp.wait_stream(self.s_out)
+        comp.wait_stream(self.s_in)
+
+    def run_resident(self, n_steps: int) -> None:
+        """Replay the step graph on device-resident inputs (no host copies)."""
+        for i in range(n_steps):
+            k = i % self.n_sets
+            if self.graphs[k] is not None:
+                self.graphs[k].replay()
+            else:
+                self._step(k)

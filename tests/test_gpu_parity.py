@@ -348,3 +348,29 @@ def test_dit_denoise_within_budget():
     for rid, lat in reqs:
         want = R.denoise_image(rcfg, rw, np.float32(lat).astype(np.float64), prompts[rid], si[rid], ts[rid])
         assert np.abs(np_(got[rid]) - want).max() <= 1e-2
+
+
+def test_pipeline_graph_matches_denoise_batch():
+    """DenoisePipeline (CUDA graph, overlapped copies) reproduces denoise_batch bit for bit."""
+    from paper_2501_09253_b200.pipeline import DenoisePipeline
+    cfg = ps.ModelConfig(arch="unet_like", channels=64, hidden=128, n_blocks=2, groups=8, seed=5)
+    w = ps.init_weights(cfg)
+    rng = np.random.default_rng(9)
+    dims = [64, 32, 64, 96]
+    lats = [rng.normal(size=(64, d, d)).astype(np.float32) for d in dims]
+    ids = [f"q{i}" for i in range(len(dims))]
+    prompts = [ps.make_prompt(cfg, r) for r in ids]
+    pipe = DenoisePipeline(cfg, w, dims, 32)
+    pipe.set_prompts(prompts)
+    pipe.prepare()
+    steps = 3
+    host_in = [[torch.tensor(x).pin_memory() for x in lats] for _ in range(steps)]
+    host_out = [[torch.empty_like(x).pin_memory() for x in host_in[0]] for _ in range(steps)]
+    pipe.run(host_in, [[s, s, s + 1, 0] for s in range(steps)], [5, 5, 5, 5], host_out)
+    torch.cuda.synchronize()
+    b = ps.split([(r, torch.tensor(x)) for r, x in zip(ids, lats)], patch_size=32)
+    for s in range(steps):
+        si = dict(zip(ids, [s, s, s + 1, 0]))
+        want = ps.reassemble(b, ps.denoise_batch(cfg, w, b, dict(zip(ids, prompts)), si, dict.fromkeys(ids, 5)))
+        for r, rid in enumerate(ids):
+            assert torch.equal(host_out[s][r], want[rid].cpu()), (s, rid)
