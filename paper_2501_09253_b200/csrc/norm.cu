@@ -26,39 +26,50 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return t;
 }
 
-// grid (P, G): partial mean / M2 over cg*hw contiguous elements.
-__global__ void gn_partials_kernel(const __nv_bfloat16* __restrict__ x, int C, int hw, int G,
-                                   float* __restrict__ partials) {
+// grid (P, G): partial mean / M2 over cg*hw contiguous elements.  The CTA's
+// slice is read once into registers (up to GN_REG 16-byte vectors per thread);
+// mean and then M2 are reduced from registers (two-pass numerics, one pass of HBM).
+constexpr int GN_REG = 8;
+__global__ void __launch_bounds__(256) gn_partials_kernel(const __nv_bfloat16* __restrict__ x, int C, int hw, int G,
+                                                          float* __restrict__ partials) {
   __shared__ float red[32];
   const int p = blockIdx.x, g = blockIdx.y;
   const int cg = C / G;
   const int64_t n = (int64_t)cg * hw;
   const __nv_bfloat16* base = x + ((int64_t)p * C + (int64_t)g * cg) * hw;
-  const bool vec = (n % 8 == 0) && (((uintptr_t)base & 15) == 0);
-  float s = 0.f;
+  const bool vec = (n % 8 == 0) && (((uintptr_t)base & 15) == 0) && (n / 8 <= (int64_t)GN_REG * blockDim.x);
+  float mean, m2 = 0.f;
   if (vec) {
-    for (int64_t i = threadIdx.x; i < n / 8; i += blockDim.x) {
-      uint4 u = __ldg(reinterpret_cast<const uint4*>(base) + i);
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+    uint4 reg[GN_REG];
+    const int nv = (int)(n / 8);
+#pragma unroll
+    for (int i = 0; i < GN_REG; ++i) {
+      const int k = threadIdx.x + i * blockDim.x;
+      reg[i] = k < nv ? __ldg(reinterpret_cast<const uint4*>(base) + k) : make_uint4(0, 0, 0, 0);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < GN_REG; ++i) {
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&reg[i]);
 #pragma unroll
       for (int k = 0; k < 4; ++k) s += __low2float(h[k]) + __high2float(h[k]);
     }
-  } else {
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += bf(base[i]);
-  }
-  const float mean = block_sum(s, red) / (float)n;
-  float m2 = 0.f;
-  if (vec) {
-    for (int64_t i = threadIdx.x; i < n / 8; i += blockDim.x) {
-      uint4 u = __ldg(reinterpret_cast<const uint4*>(base) + i);
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+    mean = block_sum(s, red) / (float)n;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float a = __low2float(h[k]) - mean, b = __high2float(h[k]) - mean;
-        m2 += a * a + b * b;
+    for (int i = 0; i < GN_REG; ++i) {
+      if (threadIdx.x + i * blockDim.x < nv) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&reg[i]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float a = __low2float(h[k]) - mean, b = __high2float(h[k]) - mean;
+          m2 += a * a + b * b;
+        }
       }
     }
   } else {
+    float s = 0.f;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += bf(base[i]);
+    mean = block_sum(s, red) / (float)n;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
       const float a = bf(base[i]) - mean;
       m2 += a * a;
@@ -181,57 +192,82 @@ __global__ void __launch_bounds__(256) frames_vec_kernel(const __nv_bfloat16* __
   const int r0 = blockIdx.z * R;
   const int rows = min(R, F - r0);
   const int hw = ps * ps;
-  const int cg = mode == 1 ? C / G : 1;
   const int req = mode == 1 ? __ldg(ri + p) : 0;
   auto sw = [](int fx) { return (fx & 7) << 3; };
-  auto norm = [&](float v, int c) {
-    if (mode == 1) {
-      const int g = c / cg;
-      v = (v - __ldg(stats + ((int64_t)req * G + g) * 2)) * __ldg(stats + ((int64_t)req * G + g) * 2 + 1) *
-              __ldg(gamma + c) + __ldg(beta + c);
+  // per-channel affine of this CTA's 64 channels: y = x * a + b (GroupNorm) or identity
+  __shared__ float ch_a[64], ch_b[64];
+  if (threadIdx.x < 64) {
+    const int c = c0 + threadIdx.x;
+    float a = 1.f, b = 0.f;
+    if (mode == 1 && c < C) {
+      const int g = c / (C / G);
+      const float mu = __ldg(stats + ((int64_t)req * G + g) * 2), rs = __ldg(stats + ((int64_t)req * G + g) * 2 + 1);
+      a = rs * __ldg(gamma + c);
+      b = __ldg(beta + c) - mu * a;
     }
-    return v;
-  };
-  // phase 1: interior columns, VEC pixels per load
+    ch_a[threadIdx.x] = a;
+    ch_b[threadIdx.x] = b;
+  }
+  __syncthreads();
+  auto norm = [&](float v, int cc) { return fmaf(v, ch_a[cc], ch_b[cc]); };
+  // phase 1: interior columns, VEC pixels per load, UNR independent loads in flight per thread
+  constexpr int UNR = VEC == 8 ? 4 : 2;
   const int nvec = ps / VEC;
   const int work = rows * 64 * nvec;
-  for (int k = threadIdx.x; k < work; k += blockDim.x) {
-    const int j = k % nvec;
-    const int c = (k / nvec) % 64 + c0;
-    const int r = k / (nvec * 64);
-    const int fy = r0 + r;
-    int q = p, sy = fy - off;
-    if (FRAMES) {
-      if (fy == 0) { q = __ldg(nbr + (int64_t)p * 8 + 0); sy = ps - 1; }
-      else if (fy == F - 1) { q = __ldg(nbr + (int64_t)p * 8 + 4); sy = 0; }
+  for (int base = threadIdx.x; base < work; base += blockDim.x * UNR) {
+    uint4 raw[UNR];
+    int kk[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int k = base + u * blockDim.x;
+      kk[u] = k;
+      raw[u] = make_uint4(0, 0, 0, 0);
+      if (k < work) {
+        const int j = k % nvec;
+        const int c = (k / nvec) % 64 + c0;
+        const int fy = r0 + k / (nvec * 64);
+        int q = p, sy = fy - off;
+        if (FRAMES) {
+          if (fy == 0) { q = __ldg(nbr + (int64_t)p * 8 + 0); sy = ps - 1; }
+          else if (fy == F - 1) { q = __ldg(nbr + (int64_t)p * 8 + 4); sy = 0; }
+        }
+        if (q >= 0 && c < C) {
+          const __nv_bfloat16* src = x + ((int64_t)q * C + c) * hw + sy * ps + j * VEC;
+          if constexpr (VEC == 8) {
+            raw[u] = __ldg(reinterpret_cast<const uint4*>(src));
+          } else if constexpr (VEC == 4) {
+            const uint2 t2 = __ldg(reinterpret_cast<const uint2*>(src));
+            raw[u].x = t2.x; raw[u].y = t2.y;
+          } else {
+            raw[u].x = (uint32_t)__bfloat16_as_ushort(src[0]);
+          }
+        } else {
+          kk[u] = -1 - k;  // zero halo / padding channel: write zeros
+        }
+      }
     }
-    float v[VEC];
-    if (q >= 0 && c < C) {
-      const __nv_bfloat16* src = x + ((int64_t)q * C + c) * hw + sy * ps + j * VEC;
-      if constexpr (VEC == 8) {
-        const uint4 u = __ldg(reinterpret_cast<const uint4*>(src));
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) { v[2 * i] = __low2float(h[i]); v[2 * i + 1] = __high2float(h[i]); }
-      } else if constexpr (VEC == 4) {
-        const uint2 u = __ldg(reinterpret_cast<const uint2*>(src));
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-        for (int i = 0; i < 2; ++i) { v[2 * i] = __low2float(h[i]); v[2 * i + 1] = __high2float(h[i]); }
+    for (int u = 0; u < UNR; ++u) {
+      int k = kk[u];
+      const bool zero = k < 0;
+      if (zero) k = -1 - k;
+      if (k >= work) continue;
+      const int j = k % nvec;
+      const int cc = (k / nvec) % 64;
+      const int r = k / (nvec * 64);
+      float v[VEC];
+      if constexpr (VEC == 1) {
+        v[0] = __uint_as_float(raw[u].x << 16);
       } else {
-        v[0] = bf(src[0]);
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[u]);
+#pragma unroll
+        for (int i = 0; i < VEC / 2; ++i) { v[2 * i] = __low2float(h[i]); v[2 * i + 1] = __high2float(h[i]); }
       }
 #pragma unroll
-      for (int i = 0; i < VEC; ++i) v[i] = norm(v[i], c);
-    } else {
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) v[i] = 0.f;
-    }
-    const int cc = c - c0;
-#pragma unroll
-    for (int i = 0; i < VEC; ++i) {
-      const int fx = off + j * VEC + i;
-      tile[((r * F) + fx) * 64 + (cc ^ sw(fx))] = __float2bfloat16_rn(v[i]);
+      for (int i = 0; i < VEC; ++i) {
+        const int fx = off + j * VEC + i;
+        tile[((r * F) + fx) * 64 + (cc ^ sw(fx))] = __float2bfloat16_rn(zero ? 0.f : norm(v[i], cc));
+      }
     }
   }
   // phase 1b: ring columns (frames only)
@@ -247,7 +283,7 @@ __global__ void __launch_bounds__(256) frames_vec_kernel(const __nv_bfloat16* __
       const int sy = ry < 0 ? ps - 1 : (ry > 0 ? 0 : fy - 1);
       const int sx = side == 0 ? ps - 1 : 0;
       float v = 0.f;
-      if (q >= 0 && c < C) v = norm(bf(x[((int64_t)q * C + c) * hw + sy * ps + sx]), c);
+      if (q >= 0 && c < C) v = norm(bf(x[((int64_t)q * C + c) * hw + sy * ps + sx]), c - c0);
       const int fx = side == 0 ? 0 : F - 1;
       tile[((r * F) + fx) * 64 + ((c - c0) ^ sw(fx))] = __float2bfloat16_rn(v);
     }
