@@ -105,6 +105,8 @@ typedef struct ps_gemm_args {
   int bn;                                 /* tile N: 64,128,160,192,256,320 (0 = auto) */
   int out_tiled;                          /* epi 0/1: write tile-major [ceil(M/128)][ldo/64][128][64] */
   unsigned long long* dbg;                /* optional device counters [8] of per-role wait cycles, or NULL */
+  const int32_t* m_map;                   /* optional DEVICE list of 128-row tiles to compute (compaction) */
+  int m_count;                            /* entries in m_map */
 } ps_gemm_args;
 int ps_gemm(void* stream, const ps_gemm_args* args);
 

@@ -274,6 +274,8 @@ int ps_gemm(void* stream, const ps_gemm_args* a) {
   p.hw = a->ps * a->ps;
   p.out_tiled = a->out_tiled;
   p.dbg = a->dbg;
+  p.m_map = a->m_map;
+  p.m_count = a->m_map ? a->m_count : 0;
   // channels-last outputs leave through TMA stores (32 rows x 16 columns per warp box)
   CUtensorMap tc;
   memset(&tc, 0, sizeof(tc));

@@ -84,8 +84,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_n = (p.N + BN - 1) / BN;
-  const int num_m = (p.M + GEMM_BM - 1) / GEMM_BM;
+  const int num_m = p.m_map ? p.m_count : (p.M + GEMM_BM - 1) / GEMM_BM;
   const int n_tiles = num_m * num_n;
+  // logical -> physical 128-row tile (active-patch compaction)
+  auto phys_m = [&](int lm) { return p.m_map ? __ldg(p.m_map + lm) : lm; };
   const int num_kb = p.K / GEMM_BK;
 
   if (warp == 0 && lane == 0) {
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       uint32_t phase = 0;
       const int kcb = p.conv_cp / GEMM_BK;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const int m_tile = t / num_n, n0 = (t % num_n) * BN;
+        const int m_tile = phys_m(t / num_n), n0 = (t % num_n) * BN;
         int p0 = 0, y0 = 0;
         if (p.a_mode == A_CONV3) {
           p0 = (m_tile / p.conv_tpp) * p.conv_np;
@@ -220,7 +222,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int buf = li % Cfg::NBUF;
       const int use = li / Cfg::NBUF;
       if (Cfg::NBUF == 2 && buf != wg) continue;
-      const int m_tile = t / num_n, n_tile = t % num_n;
+      const int m_tile = phys_m(t / num_n), n_tile = t % num_n;
       const int m = m_tile * GEMM_BM + row;
       const bool row_ok = m < p.M;
       const bool tile_full = (m_tile + 1) * GEMM_BM <= p.M;
@@ -403,7 +405,8 @@ static int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const CUtensorM
     cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr = true;
   }
-  const int tiles = ((p.M + GEMM_BM - 1) / GEMM_BM) * ((p.N + BN - 1) / BN);
+  const int tiles = (p.m_map ? p.m_count : (p.M + GEMM_BM - 1) / GEMM_BM) * ((p.N + BN - 1) / BN);
+  if (tiles == 0) return PS_OK;
   const int grid = tiles < num_sms() ? tiles : num_sms();
   gemm_tc_kernel<BN><<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(a, b, c, p);
   count_launch();

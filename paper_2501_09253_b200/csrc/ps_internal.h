@@ -27,7 +27,9 @@ struct GemmParams {
   int c_real, hw;
   int out_tiled;  // CL stores in 128x64 tile-major order ([M/128][ldo/64][128][64])
   unsigned long long* dbg;  // optional per-role wait-cycle counters (profiling)
-  int store_tma;            // channels-last stores through the tmC tensor map (32x16 boxes)
+  int store_tma;            // channels-last stores through the tmC tensor map
+  const int* m_map;         // optional: physical 128-row tile of each logical tile (compaction)
+  int m_count;              // number of mapped tiles when m_map != null
 };
 
 int set_error(int code, const char* fmt, ...);

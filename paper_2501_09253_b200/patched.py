@@ -94,6 +94,13 @@ class Ctx:
         self.T = self.P * self.hw
         self.dev = batch.device()
         self.device = require_cuda()
+        # active-patch compaction (None = every 128-row tile): (device tile map, count)
+        self.rows_live = None   # tiles of images with >= 1 patch to recompute (context for conv3/attention/GN)
+        self.rows_act = None    # tiles of the patches to recompute
+        self.attn_live = None   # attention query tiles (tile_q0, tile_img, n) of live images / active patches
+        self.attn_act = None
+        self.rows = None        # row set of the stage being run (set by _run_ops)
+        self.attn_tiles = None
 
     def empty_cl(self, cp: int) -> torch.Tensor:
         return torch.empty((self.T, cp), dtype=BF16, device=self.device)
@@ -121,8 +128,10 @@ class Ctx:
 
     # GEMM ------------------------------------------------------------------
     def gemm(self, a, lda, b, n, k, bias, epi, out, ldo=0, out2=None, ldo2=0, n_split=0, resid=None, c_real=0,
-             conv=False, cp_in=0, a_tiled=False, out_tiled=False):
+             conv=False, cp_in=0, a_tiled=False, out_tiled=False, rows=None):
         g = _lib.GemmArgs()
+        if rows is not None:
+            g.m_map, g.m_count = rows[0].data_ptr(), rows[1]
         g.a, g.lda, g.M = a.data_ptr(), lda, self.T
         g.a_mode, g.P, g.ps, g.Cp = (1 if conv else 2 if a_tiled else 0), self.P, self.ps, cp_in
         g.out_tiled = 1 if out_tiled else 0
@@ -134,14 +143,14 @@ class Ctx:
         g.bn = 0  # library picks the tile width (gemm_pick_bn)
         _lib.check(_lib.load().ps_gemm(stream(), C.byref(g)))
 
-    def gemm_out(self, a_cl, lda, w, n, k, bias, c_out, resid_nchw, gelu=False, a_tiled=False):
+    def gemm_out(self, a_cl, lda, w, n, k, bias, c_out, resid_nchw, gelu=False, a_tiled=False, rows=None):
         """Plain GEMM; NCHW output with residual when `resid_nchw` is given."""
         if resid_nchw is not None:
             out = self.empty_nchw(c_out)
-            self.gemm(a_cl, lda, w, n, k, bias, 2, out, resid=resid_nchw, c_real=c_out, a_tiled=a_tiled)
+            self.gemm(a_cl, lda, w, n, k, bias, 2, out, resid=resid_nchw, c_real=c_out, a_tiled=a_tiled, rows=rows)
             return Act("nchw", out, c_out)
         out = self.empty_cl(n)
-        self.gemm(a_cl, lda, w, n, k, bias, 1 if gelu else 0, out, ldo=n, a_tiled=a_tiled)
+        self.gemm(a_cl, lda, w, n, k, bias, 1 if gelu else 0, out, ldo=n, a_tiled=a_tiled, rows=rows)
         return Act("cl", out, c_out)
 
     # stages ---------------------------------------------------------------
@@ -187,19 +196,21 @@ class Ctx:
             if resid is not None:
                 out = self.empty_nchw(dp["c_out"])
                 self.gemm(frames, 0, dp["w"], dp["cp_out"], 9 * dp["cp_in"], dp["b"], 2, out, resid=resid,
-                          c_real=dp["c_out"], conv=True, cp_in=dp["cp_in"])
+                          c_real=dp["c_out"], conv=True, cp_in=dp["cp_in"], rows=self.rows)
                 return Act("nchw", out, dp["c_out"])
             out = self.empty_cl(dp["cp_out"])
             self.gemm(frames, 0, dp["w"], dp["cp_out"], 9 * dp["cp_in"], dp["b"], 0, out, ldo=dp["cp_out"],
-                      conv=True, cp_in=dp["cp_in"])
+                      conv=True, cp_in=dp["cp_in"], rows=self.rows)
             return Act("cl", out, dp["c_out"])
         x = self.as_cl(a)
-        return self.gemm_out(x, a.Cp, dp["w"], dp["cp_out"], dp["cp_in"], dp["b"], dp["c_out"], resid)
+        return self.gemm_out(x, a.Cp, dp["w"], dp["cp_out"], dp["cp_in"], dp["b"], dp["c_out"], resid,
+                             rows=self.rows)
 
     def linear(self, a: Act, prm, resid):
         dp = device_params(prm, a.C)
         x = self.as_cl(a)
-        return self.gemm_out(x, a.Cp, dp["w"], dp["cp_out"], dp["cp_in"], dp["b"], dp["c_out"], resid)
+        return self.gemm_out(x, a.Cp, dp["w"], dp["cp_out"], dp["cp_in"], dp["b"], dp["c_out"], resid,
+                             rows=self.rows)
 
     def feed_forward(self, a: Act, prm, resid):
         dp = device_params(prm, a.C)
@@ -207,8 +218,10 @@ class Ctx:
         # hidden activations in 128x64 tile-major order: the second GEMM streams
         # each of its A boxes as one contiguous 16 KB block from HBM
         h = torch.empty((round_up(self.T, 128), dp["hp"]), dtype=BF16, device=self.device)
-        self.gemm(x, a.Cp, dp["w1"], dp["hp"], dp["cp"], dp["b1"], 1, h, ldo=dp["hp"], out_tiled=True)
-        return self.gemm_out(h, dp["hp"], dp["w2"], dp["cp"], dp["hp"], dp["b2"], dp["c_out"], resid, a_tiled=True)
+        self.gemm(x, a.Cp, dp["w1"], dp["hp"], dp["cp"], dp["b1"], 1, h, ldo=dp["hp"], out_tiled=True,
+                  rows=self.rows)
+        return self.gemm_out(h, dp["hp"], dp["w2"], dp["cp"], dp["hp"], dp["b2"], dp["c_out"], resid, a_tiled=True,
+                             rows=self.rows)
 
     def layer_norm(self, a: Act, prm):
         dp = device_params(prm, a.C)
@@ -225,20 +238,21 @@ class Ctx:
         qk = torch.empty((self.T, 2 * dpp), dtype=BF16, device=self.device)
         ldv = round_up(self.T, 64)
         vt = torch.empty((dpp, ldv), dtype=BF16, device=self.device)
-        self.gemm(x, a.Cp, dp["wqkv"], 3 * dpp, dpp, None, 3, qk, ldo=2 * dpp, out2=vt, ldo2=ldv, n_split=2 * dpp)
+        self.gemm(x, a.Cp, dp["wqkv"], 3 * dpp, dpp, None, 3, qk, ldo=2 * dpp, out2=vt, ldo2=ldv, n_split=2 * dpp,
+                  rows=self.rows_live)
         o = self.empty_cl(dpp)
         timer = ATTN_TIMER
         if timer is not None:
             ext = torch.cuda.is_current_stream_capturing()  # event nodes inside a captured graph
             ev = (torch.cuda.Event(enable_timing=True, external=ext), torch.cuda.Event(enable_timing=True, external=ext))
             ev[0].record()
+        tq0, timg, nt = self.attn_tiles or (self.dev["tile_q0"], self.dev["tile_img"], self.dev["n_tiles"])
         _lib.call("ps_attention", stream(), qk.data_ptr(), vt.data_ptr(), ldv, self.T, dpp, d,
-                  self.dev["img_tok0"].data_ptr(), self.dev["tile_q0"].data_ptr(), self.dev["tile_img"].data_ptr(),
-                  self.dev["n_tiles"], o.data_ptr())
+                  self.dev["img_tok0"].data_ptr(), tq0.data_ptr(), timg.data_ptr(), nt, o.data_ptr())
         if timer is not None:
             ev[1].record()
             timer.append(ev)
-        return self.gemm_out(o, dpp, dp["wo"], dpp, dpp, None, d, resid)
+        return self.gemm_out(o, dpp, dp["wo"], dpp, dpp, None, d, resid, rows=self.rows)
 
 
 # ------------------------------------------------------- public operators
@@ -330,16 +344,66 @@ _GEMM_STAGES = ("conv", "feed_forward", "linear", "attention")
 def run_block(batch: CSPBatch, x, ops) -> torch.Tensor:
     """Execute one block of (kind, params) stages (patched.py:179-221); returns NCHW bf16."""
     x = _check_data(batch, x)
+    return _run_ops(Ctx(batch), x, ops)
+
+
+def run_block_active(batch: CSPBatch, x, ops, active) -> torch.Tensor:
+    """run_block whose outputs are only needed for the `active` patches.
+
+    Active-patch compaction: pixel-wise stages and attention query
+    rows run on the active patches only; the context stages (conv3 halo
+    neighbours, attention keys/values) run on every patch of an image that has at
+    least one active patch.  Rows of inactive patches in the result are
+    unspecified (the cache splices their cached outputs, patched.py:246).  The
+    active rows are bit-identical to run_block's.
+    """
+    x = _check_data(batch, x)
+    active = np.asarray(active, dtype=bool)
+    ctx = Ctx(batch)
+    if ctx.hw % 128 or active.all():
+        return _run_ops(ctx, x, ops)  # tiles would span patches: no compaction
+    act = np.flatnonzero(active)
+    live_img = np.unique(batch.request_index[act])
+    live = np.flatnonzero(np.isin(batch.request_index, live_img))
+    tpp = ctx.hw // 128
+
+    def tiles(pats):
+        m = (pats[:, None] * tpp + np.arange(tpp)[None, :]).ravel().astype(np.int32)
+        return torch.as_tensor(m, device=ctx.device), int(m.size)
+
+    ctx.rows_live, ctx.rows_act = tiles(live), tiles(act)
+    sizes = batch.request_offset[1:] - batch.request_offset[:-1]
+
+    def attn(pats):  # query tiles of these patches, longest images first
+        order = sorted(pats.tolist(), key=lambda p: -int(sizes[batch.request_index[p]]))
+        q0 = [p * ctx.hw + 128 * j for p in order for j in range(tpp)]
+        img = [int(batch.request_index[p]) for p in order for _ in range(tpp)]
+        return (torch.as_tensor(np.asarray(q0, np.int32), device=ctx.device),
+                torch.as_tensor(np.asarray(img, np.int32), device=ctx.device), len(q0))
+
+    ctx.attn_live, ctx.attn_act = attn(live), attn(act)
+    return _run_ops(ctx, x, ops)
+
+
+def _run_ops(ctx: "Ctx", x: torch.Tensor, ops) -> torch.Tensor:
     for kind, _ in ops:
         if kind not in ("group_norm", "layer_norm", "conv", "attention", "feed_forward", "linear", "residual"):
             raise InputError(f"unknown block stage {kind!r}")
-    ctx = Ctx(batch)
     block_in = _bf16_nchw(x)
     cur = Act("nchw", block_in, x.shape[1])
     frames = None
     fused_residual = False
+
+    def is_context(op):  # stages whose outputs depend on other patches of the image
+        k, prm = op
+        return k in ("group_norm", "attention") or (k == "conv" and int(np.asarray(prm.weights).shape[2]) == 3)
+
     for i, (kind, prm) in enumerate(ops):
         nxt = ops[i + 1][0] if i + 1 < len(ops) else None
+        # compaction: a stage feeding a later context stage must produce every live-image row
+        ctx_after = any(is_context(o) for o in ops[i + 1:])
+        ctx.rows = ctx.rows_live if ctx_after else ctx.rows_act
+        ctx.attn_tiles = ctx.attn_live if ctx_after else ctx.attn_act
         resid = block_in if (nxt == "residual" and kind in _GEMM_STAGES) else None
         if kind == "group_norm":
             fuse = (nxt == "conv" and int(np.asarray(ops[i + 1][1].weights).shape[2]) == 3)
