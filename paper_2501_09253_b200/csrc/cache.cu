@@ -35,14 +35,30 @@ __device__ __forceinline__ double leaf_sum(const __nv_bfloat16* a, const __nv_bf
     for (int i = 0; i < n; ++i) res = __dadd_rn(res, sq(i));
     return res;
   }
-  double r[8];
+  // 8 strided accumulators: element i goes to r[i % 8]; 16-byte smem loads deliver exactly one
+  // element per accumulator (leaf starts are multiples of 8 in numpy's tree)
+  auto sq8 = [&](int i, double* d8) {
+    const uint4 ua = *reinterpret_cast<const uint4*>(a + i);
+    const uint4 ub = *reinterpret_cast<const uint4*>(b + i);
+    const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&ua);
+    const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&ub);
 #pragma unroll
-  for (int j = 0; j < 8; ++j) r[j] = sq(j);
+    for (int k = 0; k < 4; ++k) {
+      const double d0 = __dsub_rn((double)__low2float(ha[k]), (double)__low2float(hb[k]));
+      const double d1 = __dsub_rn((double)__high2float(ha[k]), (double)__high2float(hb[k]));
+      d8[2 * k] = __dmul_rn(d0, d0);
+      d8[2 * k + 1] = __dmul_rn(d1, d1);
+    }
+  };
+  double r[8];
+  sq8(0, r);
   int i = 8;
   const int stop = n - (n % 8);
   for (; i < stop; i += 8) {
+    double d8[8];
+    sq8(i, d8);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], sq(i + j));
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], d8[j]);
   }
   double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                          __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
@@ -72,6 +88,7 @@ __global__ void __launch_bounds__(LEAVES_PER_CTA) mse_leaf_kernel(
   const bool vec = (n % 8 == 0) && v1 <= n;
   if (vec) {
     const int nv = (int)((v1 - v0) / 8);
+#pragma unroll 4
     for (int i = threadIdx.x; i < nv; i += blockDim.x) {
       reinterpret_cast<uint4*>(sa)[i] = __ldg(reinterpret_cast<const uint4*>(xa + v0) + i);
       reinterpret_cast<uint4*>(sb)[i] = __ldg(reinterpret_cast<const uint4*>(xb + v0) + i);
@@ -299,11 +316,13 @@ int ps_cache_predict(void* stream, const void* x, int P, int64_t n, const int32_
   if (n < 1 || n_leaves < 1) return set_error(PS_ERR_INPUT, "cache_predict: empty patches");
   cudaStream_t st = (cudaStream_t)stream;
   const int stride = n_leaves + n_internal;
-  // shared staging: up to 128 leaves of <= 128 elements, two operands, +16 slack
-  const int smem = 2 * (LEAVES_PER_CTA * 128 + 16) * 2;
+  // shared staging of two operands: the widest span of LEAVES_PER_CTA consecutive leaves of
+  // this n's tree (+16 elements of vector alignment slack); smaller staging -> more CTAs per SM
+  const int smem = 2 * (int)(pairwise_max_span(n, LEAVES_PER_CTA) + 16) * 2;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(mse_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(mse_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         2 * (LEAVES_PER_CTA * 128 + 16) * 2);
     attr = true;
   }
   mse_leaf_kernel<<<dim3(P, (n_leaves + LEAVES_PER_CTA - 1) / LEAVES_PER_CTA), LEAVES_PER_CTA, smem, st>>>(

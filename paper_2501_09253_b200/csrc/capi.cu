@@ -72,6 +72,35 @@ int make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
   return make_tmap(m, base, 2, dims, strides, box);
 }
 
+// leaves (start, length) of numpy's pairwise_sum tree over n elements, in order
+static void pairwise_leaves(int64_t lo, int64_t n, std::vector<std::pair<int64_t, int64_t>>& out) {
+  if (n <= 128) {
+    out.push_back({lo, n});
+    return;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  pairwise_leaves(lo, n2, out);
+  pairwise_leaves(lo + n2, n - n2, out);
+}
+
+int64_t pairwise_max_span(int64_t n, int group) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int64_t, int>, int64_t>> memo;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : memo)
+    if (e.first.first == n && e.first.second == group) return e.second;
+  std::vector<std::pair<int64_t, int64_t>> lv;
+  pairwise_leaves(0, n, lv);
+  int64_t best = 0;
+  for (size_t i = 0; i < lv.size(); i += group) {
+    const size_t j = std::min(lv.size(), i + group) - 1;
+    best = std::max(best, lv[j].first + lv[j].second - lv[i].first);
+  }
+  memo.push_back({{n, group}, best});
+  return best;
+}
+
 }  // namespace ps
 
 using namespace ps;

@@ -38,6 +38,8 @@ void count_launch();
 int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const GemmParams& p, int bn,
                 cudaStream_t st);
 int gemm_pick_bn(int n, int k);
+// widest element span of `group` consecutive leaves of numpy's pairwise tree over n elements
+int64_t pairwise_max_span(int64_t n, int group);
 
 struct AttnParams {
   int T_total;   // tokens in the batch (rows of qk / columns of vt)
