@@ -118,10 +118,23 @@ def run_ours(args):
     from paper_2501_09253_b200.pipeline import DenoisePipeline
 
     rank, world, local = _env_rank()
+    # one process per GPU; BENCH_DIST_BACKEND=gloo lets ranks share a GPU (code-path checks on a 1-GPU box)
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
     _lib.check(_lib.load().ps_device_check(local))
 
     cfg = ps.ModelConfig(arch="unet_like", channels=C, hidden=HIDDEN, groups=GROUPS, n_blocks=BLOCKS, seed=0)
@@ -162,10 +175,7 @@ def run_ours(args):
     launches = pipe.kernels_per_step * args.steps
     ms = start.elapsed_time(end)
     attn_ms = [a.elapsed_time(b) for a, b in graph_attn]  # from the last replay of each graph
-    t = torch.tensor([ms], device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = max_over_ranks(ms)
 
     # ---------------- timed region 2: e2e through the public API from pinned host memory
     host_in = [[torch.tensor(lat, dtype=torch.float32).pin_memory() for _, lat in reqs] for _ in range(2)]
@@ -186,10 +196,7 @@ def run_ours(args):
     e2e(args.steps)
     e1.record()
     barrier()
-    t2 = torch.tensor([e0.elapsed_time(e1)], device=dev)
-    if world > 1:
-        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-    e2e_ms = float(t2.item())
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
 
     if rank == 0:
         peaks = _peaks()
