@@ -117,6 +117,18 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // profiling (p.dbg): cycles blocked per barrier class
+  unsigned long long w_a = 0, w_b = 0, w_c = 0;
+  const long long t_start = clock64();
+  auto twait = [&](uint64_t* bar, uint32_t par, unsigned long long& acc) {
+    if (p.dbg) {
+      const long long t0 = clock64();
+      mbar_wait(bar, par);
+      acc += clock64() - t0;
+    } else {
+      mbar_wait(bar, par);
+    }
+  };
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
@@ -157,10 +169,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     uint32_t kph = 0, vph = 0;
     auto issue_s = [&](int j) {
       // S buffer is free once the softmax warps loaded S_{j-1}
-      if (j >= 1) mbar_wait(s_free, (j - 1) & 1);
+      if (j >= 1) twait(s_free, (j - 1) & 1, w_a);
       tc_fence_after();
       for (int kc = 0; kc < Cfg::KB; ++kc) {
-        mbar_wait(&k_full[ks], kph);
+        twait(&k_full[ks], kph, w_c);
         tc_fence_after();
         if (lane == 0) {
           const uint8_t* kt = sK + ks * Cfg::K_SLOT;
@@ -176,10 +188,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       }
     };
     auto issue_pv = [&](int j) {
-      mbar_wait(p_full, j & 1);
+      twait(p_full, j & 1, w_b);
       tc_fence_after();
       for (int ka = 0; ka < 2; ++ka) {
-        mbar_wait(&v_full[vs], vph);
+        twait(&v_full[vs], vph, w_c);
         tc_fence_after();
         if (lane == 0) {
           const uint8_t* vt = sV + vs * Cfg::V_SLOT;
@@ -212,7 +224,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     float m_run = -INFINITY, l_run = 0.f;
     for (int j = 0; j < n_kb; ++j) {
-      mbar_wait(s_full, j & 1);
+      twait(s_full, j & 1, w_a);
       tc_fence_after();
       uint32_t sr[128];
 #pragma unroll
@@ -250,7 +262,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       }
       l_run = l_run * alpha + (sum0 + sum1);
       // P columns and O are owned by the MMAs of block j-1 until they complete
-      if (j >= 1) mbar_wait(p_free, (j - 1) & 1);
+      if (j >= 1) twait(p_free, (j - 1) & 1, w_b);
       tc_fence_after();
       const bool warp_rescale = __any_sync(0xffffffffu, need && j >= 1 && alpha != 1.f);
       if (warp_rescale) {
@@ -297,6 +309,12 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         }
       }
     }
+  }
+  if (p.dbg && lane == 0) {
+    const unsigned long long tot = clock64() - t_start;
+    // [0] mma:s_free [1] mma:p_full [2] mma:k/v_full [3] mma total [4] softmax:s_full [5] softmax:p_free [6] sm total
+    if (warp == 1) { atomicAdd(p.dbg + 0, w_a); atomicAdd(p.dbg + 1, w_b); atomicAdd(p.dbg + 2, w_c); atomicAdd(p.dbg + 3, tot); }
+    if (warp == 4) { atomicAdd(p.dbg + 4, w_a); atomicAdd(p.dbg + 5, w_b); atomicAdd(p.dbg + 6, tot); }
   }
   tc_fence_before();
   __syncthreads();

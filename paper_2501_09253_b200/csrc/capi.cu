@@ -105,6 +105,8 @@ int64_t pairwise_max_span(int64_t n, int group) {
 
 using namespace ps;
 
+static unsigned long long* g_attn_dbg = nullptr;  // profiling hook (ps_attention_debug)
+
 extern "C" {
 
 int ps_abi_version(void) { return 1; }
@@ -193,6 +195,13 @@ int ps_csp_build(int n_req, const int32_t* dims, int32_t ps, int32_t* order, int
 // (sequential below 8, 8 strided accumulators otherwise); larger n splits at
 // n2 = n/2 - (n/2 % 8).  Nodes are numbered leaves first (in order), then
 // internal nodes grouped by height so a level can be evaluated in parallel.
+// Profiling only: device counters [8] that later attention launches accumulate
+// per-role barrier-wait cycles into (NULL disables).
+int ps_attention_debug(unsigned long long* counters) {
+  g_attn_dbg = counters;
+  return PS_OK;
+}
+
 int ps_pairwise_plan(int64_t n, int32_t* n_leaves, int32_t* n_internal, int32_t* n_levels, int32_t* leaves,
                      int32_t* nodes, int32_t* level_off) {
   if (n < 1 || n > (int64_t)1 << 30) return set_error(PS_ERR_INPUT, "pairwise plan: bad n %lld", (long long)n);
@@ -354,6 +363,7 @@ int ps_attention(void* stream, const void* qk, const void* vt, int ldv, int T, i
   p.img_tok0 = img_tok0;
   p.scale_log2 = 1.4426950408889634f / sqrtf((float)D);
   p.out = (__nv_bfloat16*)out;
+  p.dbg = g_attn_dbg;
   return attention_launch(tq, tk, tv, p, Dp, (cudaStream_t)stream);
 }
 

@@ -50,6 +50,7 @@ struct AttnParams {
   const int* img_tok0;   // [n_img + 1] token offsets of images
   float scale_log2;      // log2(e) / sqrt(D_real)
   __nv_bfloat16* out;    // [T_total, Dp] channels-last
+  unsigned long long* dbg;  // optional per-role wait counters (profiling)
 };
 int attention_launch(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& vt, const AttnParams& p,
                      int dp, cudaStream_t st);
