@@ -117,6 +117,11 @@ int ps_gemm(void* stream, const ps_gemm_args* args);
  * out: [T, Dp] bf16 = softmax(Q K^T / sqrt(D)) V per image. */
 int ps_attention(void* stream, const void* qk, const void* vt, int ldv, int T, int Dp, int D, const int32_t* img_tok0,
                  const int32_t* tile_q0, const int32_t* tile_img, int n_tiles, void* out);
+/* Same as ps_attention on CTA pairs (cta_group::2, M = 256): each tile is 256
+ * queries of one image (pair_q0 steps by 256); default path on B200. */
+int ps_attention_pairs(void* stream, const void* qk, const void* vt, int ldv, int T, int Dp, int D,
+                       const int32_t* img_tok0, const int32_t* pair_q0, const int32_t* pair_img, int n_pairs,
+                       void* out);
 /* Profiling: device counters [8] of per-role barrier-wait cycles for later ps_attention launches (NULL = off). */
 int ps_attention_debug(unsigned long long* counters);
 

@@ -129,11 +129,14 @@ class CSPBatch:
             tok0 = (self.request_offset * hw).astype(np.int64)
             # attention tiles: (q0, image) per 128 queries, longest images first (LPT)
             order = sorted(range(self.n_requests), key=lambda r: -(tok0[r + 1] - tok0[r]))
-            q0s, imgs = [], []
+            q0s, imgs, pq0, pimg = [], [], [], []
             for r in order:
                 for q in range(int(tok0[r]), int(tok0[r + 1]), 128):
                     q0s.append(q)
                     imgs.append(r)
+                for q in range(int(tok0[r]), int(tok0[r + 1]), 256):  # CTA-pair tiles
+                    pq0.append(q)
+                    pimg.append(r)
             self._dev.update(
                 request_offset=i32(self.request_offset, dev),
                 request_index=i32(self.request_index, dev),
@@ -143,6 +146,9 @@ class CSPBatch:
                 tile_q0=i32(q0s, dev),
                 tile_img=i32(imgs, dev),
                 n_tiles=len(q0s),
+                pair_q0=i32(pq0, dev),
+                pair_img=i32(pimg, dev),
+                n_pairs=len(pq0),
             )
         return self._dev
 

@@ -1,0 +1,340 @@
+// Per-image self-attention on CTA pairs (cta_group::2) — experimental (PS_ATTN_PAIRS=1).
+// Measured slower than the single-CTA kernel on config 2 (1.73 vs 1.53 ms): the pair's
+// softmax, not operand bandwidth, ends up on the critical path; kept for the record.
+//
+// Same math as attention.cu (reference patched.py:154-176 -> kernels.py:230-267,
+// one head, D = C, keys restricted to the query tile's image), but each cluster of
+// two CTAs on one TPC owns 256 queries and issues M=256 tcgen05 MMAs:
+//   * CTA r holds its own 128 query rows (Q in smem, S/P/O in its TMEM lanes);
+//   * every 128-key block is split between the pair: CTA r loads keys
+//     [64r, 64r+64) of K and half of the V^T rows of each PV MMA;
+//   * the leader (rank 0) issues all MMAs; TMA loads of both CTAs complete on the
+//     leader's barriers; MMA completions are multicast to both CTAs.
+// Per SM this halves the K/V bytes loaded and read by the tensor core, which is
+// what limited the single-CTA kernel (shared-memory bandwidth).
+#include "common.cuh"
+#include "ps_internal.h"
+
+namespace ps {
+
+constexpr int A2_BM = 128;  // query rows per CTA (256 per pair)
+constexpr int A2_BN = 128;  // keys per block (64 per CTA)
+constexpr int A2_THREADS = 256;
+
+template <int DP>
+struct Attn2Cfg {
+  static constexpr int KB = DP / 64;
+  static constexpr int Q_BYTES = KB * A2_BM * 128;
+  static constexpr int K_SLOT = (A2_BN / 2) * 128;          // 64 keys x 64 dims, this CTA's half
+  static constexpr int PV_N = DP <= 256 ? DP : DP / 2;       // N of one PV MMA
+  static constexpr int PV_MMAS = DP / PV_N;
+  static constexpr int V_ROWS = PV_N / 2;                   // V^T rows per CTA per PV MMA
+  static constexpr int V_SLOT = PV_MMAS * V_ROWS * 128;     // one 64-key atom, this CTA's rows
+  static constexpr int NV = 4;
+  static constexpr int BUDGET = 227 * 1024 - Q_BYTES - NV * V_SLOT - 1024 - 512 - 2048;
+  static constexpr int NK = BUDGET / K_SLOT > 10 ? 10 : BUDGET / K_SLOT;
+  static constexpr int O_COL = 0;
+  static constexpr int S_COL = DP;
+  static constexpr int P_COL = DP + 128;
+  static constexpr int TMEM_COLS = (P_COL + 64) <= 256 ? 256 : 512;
+  static constexpr int SMEM = Q_BYTES + NK * K_SLOT + NV * V_SLOT + 1024 + 512 + 2048;
+  static_assert(NK >= 4, "K ring too small");
+  static_assert(V_ROWS % 8 == 0, "V^T half rows must be whole swizzle atoms");
+};
+
+template <int DP>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
+    attn2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                 const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
+  using Cfg = Attn2Cfg<DP>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + Cfg::Q_BYTES;
+  uint8_t* sV = sK + Cfg::NK * Cfg::K_SLOT;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + Cfg::NV * Cfg::V_SLOT);
+  uint64_t* q_full = bars;                    // leader
+  uint64_t* k_full = bars + 1;                // leader
+  uint64_t* k_empty = k_full + Cfg::NK;       // both (multicast commit)
+  uint64_t* v_full = k_empty + Cfg::NK;       // leader
+  uint64_t* v_empty = v_full + Cfg::NV;       // both
+  uint64_t* s_full = v_empty + Cfg::NV;       // both
+  uint64_t* s_free = s_full + 1;              // leader, 256 arrivals
+  uint64_t* p_full = s_free + 1;              // leader, 256 arrivals
+  uint64_t* p_free = p_full + 1;              // both
+  uint64_t* o_full = p_free + 1;              // both
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1;
+  const int q0 = p.tile_q0[pair] + (int)rank * A2_BM;
+  const int img = p.tile_img[pair];
+  const int k_begin = p.img_tok0[img], k_end = p.img_tok0[img + 1];
+  const int n_kb = (k_end - k_begin + A2_BN - 1) / A2_BN;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < Cfg::NK; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < Cfg::NV; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_free, 2 * 128);
+    mbar_init(p_full, 2 * 128);
+    mbar_init(p_free, 1);
+    mbar_init(o_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_2sm(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  unsigned long long w_a = 0, w_b = 0, w_c = 0;
+  const long long t_start = clock64();
+  auto twait = [&](uint64_t* bar, uint32_t par, unsigned long long& acc) {
+    if (p.dbg) {
+      const long long t0 = clock64();
+      mbar_wait(bar, par);
+      acc += clock64() - t0;
+    } else {
+      mbar_wait(bar, par);
+    }
+  };
+  if (warp == 0) {
+    // -------------------------------------------------- producer (both CTAs)
+    if (lane == 0) {
+      const uint32_t lq = mapa_shared(q_full, 0);
+      if (leader) mbar_arrive_expect_tx(q_full, 2 * Cfg::Q_BYTES);
+      for (int kc = 0; kc < Cfg::KB; ++kc) tma_load_2d_2sm(sQ + kc * A2_BM * 128, &tmQ, lq, kc * 64, q0);
+      int ks = 0, vs = 0;
+      uint32_t kph = 0, vph = 0;
+      auto load_k = [&](int j) {
+        for (int kc = 0; kc < Cfg::KB; ++kc) {
+          mbar_wait(&k_empty[ks], kph ^ 1);
+          if (leader) mbar_arrive_expect_tx(&k_full[ks], 2 * Cfg::K_SLOT);
+          tma_load_2d_2sm(sK + ks * Cfg::K_SLOT, &tmK, mapa_shared(&k_full[ks], 0), kc * 64,
+                          k_begin + j * A2_BN + (int)rank * (A2_BN / 2));
+          if (++ks == Cfg::NK) { ks = 0; kph ^= 1; }
+        }
+      };
+      auto load_v = [&](int j) {
+        for (int ka = 0; ka < 2; ++ka) {
+          mbar_wait(&v_empty[vs], vph ^ 1);
+          if (leader) mbar_arrive_expect_tx(&v_full[vs], 2 * Cfg::V_SLOT);
+          const uint32_t lb = mapa_shared(&v_full[vs], 0);
+          uint8_t* dst = sV + vs * Cfg::V_SLOT;
+          for (int n = 0; n < Cfg::PV_MMAS; ++n)
+            tma_load_2d_2sm(dst + n * Cfg::V_ROWS * 128, &tmV, lb, k_begin + j * A2_BN + ka * 64,
+                            n * Cfg::PV_N + (int)rank * Cfg::V_ROWS);
+          if (++vs == Cfg::NV) { vs = 0; vph ^= 1; }
+        }
+      };
+      load_k(0);
+      for (int j = 0; j < n_kb; ++j) {
+        if (j + 1 < n_kb) load_k(j + 1);
+        load_v(j);
+      }
+    }
+  } else if (warp == 1) {
+    // -------------------------------------------- MMA issuer (leader only)
+    if (leader) {
+      constexpr uint32_t idesc_s = idesc_bf16_f32(2 * A2_BM, A2_BN);
+      constexpr uint32_t idesc_o = idesc_bf16_f32(2 * A2_BM, Cfg::PV_N);
+      int ks = 0, vs = 0;
+      uint32_t kph = 0, vph = 0;
+      auto issue_s = [&](int j) {
+        if (j >= 1) twait(s_free, (j - 1) & 1, w_a);
+        tc_fence_after();
+        for (int kc = 0; kc < Cfg::KB; ++kc) {
+          twait(&k_full[ks], kph, w_c);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint8_t* kt = sK + ks * Cfg::K_SLOT;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_bf16_ss_2sm(tmem + Cfg::S_COL, sdesc_sw128(sQ + kc * A2_BM * 128 + k * 32),
+                              sdesc_sw128(kt + k * 32), idesc_s, (kc | k) != 0);
+            mma_commit_2sm(&k_empty[ks], 0x3);
+            if (kc == Cfg::KB - 1) mma_commit_2sm(s_full, 0x3);
+          }
+          __syncwarp();
+          if (++ks == Cfg::NK) { ks = 0; kph ^= 1; }
+        }
+      };
+      auto issue_pv = [&](int j) {
+        twait(p_full, j & 1, w_b);
+        tc_fence_after();
+        for (int ka = 0; ka < 2; ++ka) {
+          twait(&v_full[vs], vph, w_c);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint8_t* vt = sV + vs * Cfg::V_SLOT;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+              for (int n = 0; n < Cfg::PV_MMAS; ++n)
+                mma_bf16_ts_2sm(tmem + Cfg::O_COL + n * Cfg::PV_N, tmem + Cfg::P_COL + ka * 32 + k * 8,
+                                sdesc_sw128(vt + n * Cfg::V_ROWS * 128 + k * 32), idesc_o, (j | ka | k) != 0);
+            mma_commit_2sm(&v_empty[vs], 0x3);
+            if (ka == 1) {
+              mma_commit_2sm(p_free, 0x3);
+              if (j == n_kb - 1) mma_commit_2sm(o_full, 0x3);
+            }
+          }
+          __syncwarp();
+          if (++vs == Cfg::NV) { vs = 0; vph ^= 1; }
+        }
+      };
+      mbar_wait(q_full, 0);
+      issue_s(0);
+      for (int j = 0; j < n_kb; ++j) {
+        if (j + 1 < n_kb) issue_s(j + 1);
+        issue_pv(j);
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ softmax + epilogue
+    const int wq = warp & 3;
+    const int row = wq * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    const uint32_t s_free_l = mapa_shared(s_free, 0);
+    const uint32_t p_full_l = mapa_shared(p_full, 0);
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int j = 0; j < n_kb; ++j) {
+      twait(s_full, j & 1, w_a);
+      tc_fence_after();
+      uint32_t sr[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) PS_TMEM_LD32(tmem + lane_base + Cfg::S_COL + 32 * c, (sr + 32 * c));
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive_cluster(s_free_l);
+      const int kvalid = k_end - (k_begin + j * A2_BN);  // keys valid in this block
+      if (kvalid < A2_BN) {  // only the last block of an image can be ragged
+#pragma unroll
+        for (int i = 0; i < 128; ++i)
+          if (i >= kvalid) sr[i] = __float_as_uint(-INFINITY);
+      }
+      float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 128; i += 4) {
+        mx0 = fmaxf(mx0, fmaxf(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])));
+        mx1 = fmaxf(mx1, fmaxf(__uint_as_float(sr[i + 2]), __uint_as_float(sr[i + 3])));
+      }
+      const float mx = fmaxf(mx0, mx1) * p.scale_log2;  // scale_log2 > 0
+      // lazy rescale: keep the stale max unless it grew by more than 8 (log2 units)
+      float m_use = m_run;
+      const bool need = (m_run == -INFINITY) || (mx > m_run + 8.0f);
+      if (need) m_use = fmaxf(mx, m_run);
+      const float alpha = (m_run == -INFINITY) ? 0.f : ex2_approx(m_run - m_use);
+      const float neg = -m_use;
+      float sum0 = 0.f, sum1 = 0.f;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        const float a = ex2_approx(fmaf(__uint_as_float(sr[2 * i]), p.scale_log2, neg));
+        const float b = ex2_approx(fmaf(__uint_as_float(sr[2 * i + 1]), p.scale_log2, neg));
+        sum0 += a;
+        sum1 += b;
+        sr[i] = pack_bf16(a, b);  // packed P overwrites the consumed half of sr
+      }
+      l_run = l_run * alpha + (sum0 + sum1);
+      // P columns and O are owned by the MMAs of block j-1 until they complete
+      if (j >= 1) twait(p_free, (j - 1) & 1, w_b);
+      tc_fence_after();
+      const bool warp_rescale = __any_sync(0xffffffffu, need && j >= 1 && alpha != 1.f);
+      if (warp_rescale) {
+        const float sc = (need && j >= 1) ? alpha : 1.f;
+#pragma unroll 1
+        for (int c = 0; c < DP; c += 16) {
+          uint32_t o[16];
+          PS_TMEM_LD16(tmem + lane_base + Cfg::O_COL + c, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * sc);
+          PS_TMEM_ST16(tmem + lane_base + Cfg::O_COL + c, o);
+        }
+      }
+      m_run = m_use;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) PS_TMEM_ST16(tmem + lane_base + Cfg::P_COL + 16 * c, (sr + 16 * c));
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive_cluster(p_full_l);
+    }
+    // epilogue: O / l -> bf16 channels-last
+    mbar_wait(o_full, 0);
+    tc_fence_after();
+    const int q = q0 + row;
+    const bool ok = q < k_end;
+    const float inv = 1.f / l_run;
+    __nv_bfloat16* dst = p.out + (size_t)q * p.Dp;
+#pragma unroll 1
+    for (int c = 0; c < DP; c += 32) {
+      uint32_t o[32];
+      PS_TMEM_LD32(tmem + lane_base + Cfg::O_COL + c, o);
+      tmem_ld_wait();
+      if (ok) {
+        uint4* d4 = reinterpret_cast<uint4*>(dst + c);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(o[8 * v + 0]) * inv, __uint_as_float(o[8 * v + 1]) * inv);
+          w.y = pack_bf16(__uint_as_float(o[8 * v + 2]) * inv, __uint_as_float(o[8 * v + 3]) * inv);
+          w.z = pack_bf16(__uint_as_float(o[8 * v + 4]) * inv, __uint_as_float(o[8 * v + 5]) * inv);
+          w.w = pack_bf16(__uint_as_float(o[8 * v + 6]) * inv, __uint_as_float(o[8 * v + 7]) * inv);
+          d4[v] = w;
+        }
+      }
+    }
+  }
+  if (p.dbg && lane == 0) {
+    const unsigned long long tot = clock64() - t_start;
+    if (warp == 1 && leader) { atomicAdd(p.dbg + 0, w_a); atomicAdd(p.dbg + 1, w_b); atomicAdd(p.dbg + 2, w_c); atomicAdd(p.dbg + 3, tot); }
+    if (warp == 4) { atomicAdd(p.dbg + 4, w_a); atomicAdd(p.dbg + 5, w_b); atomicAdd(p.dbg + 6, tot); }
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_2sm(tmem, Cfg::TMEM_COLS);
+}
+
+template <int DP>
+static int launch2_dp(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const AttnParams& p,
+                      cudaStream_t st) {
+  using Cfg = Attn2Cfg<DP>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn2_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    attr = true;
+  }
+  attn2_kernel<DP><<<2 * p.n_tiles, A2_THREADS, Cfg::SMEM, st>>>(q, k, v, p);
+  count_launch();
+  return check_launch("attention_2cta");
+}
+
+int attention2_launch(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& vt, const AttnParams& p, int dp,
+                      cudaStream_t st) {
+  switch (dp) {
+    case 64: return launch2_dp<64>(q, k, vt, p, st);
+    case 128: return launch2_dp<128>(q, k, vt, p, st);
+    case 192: return launch2_dp<192>(q, k, vt, p, st);
+    case 256: return launch2_dp<256>(q, k, vt, p, st);
+    case 320: return launch2_dp<320>(q, k, vt, p, st);
+    default: return set_error(PS_ERR_INPUT, "attention: unsupported head dim %d", dp);
+  }
+}
+
+int attention2_v_rows(int dp) { return (dp <= 256 ? dp : dp / 2) / 2; }
+
+}  // namespace ps

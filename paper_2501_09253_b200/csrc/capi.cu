@@ -195,6 +195,30 @@ int ps_csp_build(int n_req, const int32_t* dims, int32_t ps, int32_t* order, int
 // (sequential below 8, 8 strided accumulators otherwise); larger n splits at
 // n2 = n/2 - (n/2 % 8).  Nodes are numbered leaves first (in order), then
 // internal nodes grouped by height so a level can be evaluated in parallel.
+int ps_attention_pairs(void* stream, const void* qk, const void* vt, int ldv, int T, int Dp, int D,
+                       const int32_t* img_tok0, const int32_t* pair_q0, const int32_t* pair_img, int n_pairs,
+                       void* out) {
+  if (Dp % 64 || Dp < 64 || Dp > 320) return set_error(PS_ERR_INPUT, "attention: Dp %d unsupported", Dp);
+  if (D < 1 || D > Dp) return set_error(PS_ERR_INPUT, "attention: bad D");
+  if (n_pairs < 1) return PS_OK;
+  CUtensorMap tq, tk, tv;
+  int rc = make_tmap_2d(&tq, qk, T, Dp, 2 * (uint64_t)Dp, 128);
+  if (!rc) rc = make_tmap_2d(&tk, (const __nv_bfloat16*)qk + Dp, T, Dp, 2 * (uint64_t)Dp, 64);
+  if (!rc) rc = make_tmap_2d(&tv, vt, Dp, T, ldv, attention2_v_rows(Dp));
+  if (rc) return rc;
+  AttnParams p{};
+  p.T_total = T;
+  p.Dp = Dp;
+  p.n_tiles = n_pairs;
+  p.tile_q0 = pair_q0;
+  p.tile_img = pair_img;
+  p.img_tok0 = img_tok0;
+  p.scale_log2 = 1.4426950408889634f / sqrtf((float)D);
+  p.out = (__nv_bfloat16*)out;
+  p.dbg = g_attn_dbg;
+  return attention2_launch(tq, tk, tv, p, Dp, (cudaStream_t)stream);
+}
+
 // Profiling only: device counters [8] that later attention launches accumulate
 // per-role barrier-wait cycles into (NULL disables).
 int ps_attention_debug(unsigned long long* counters) {

@@ -54,5 +54,8 @@ struct AttnParams {
 };
 int attention_launch(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& vt, const AttnParams& p,
                      int dp, cudaStream_t st);
+int attention2_launch(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& vt, const AttnParams& p,
+                      int dp, cudaStream_t st);
+int attention2_v_rows(int dp);
 
 }  // namespace ps

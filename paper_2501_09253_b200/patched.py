@@ -18,6 +18,7 @@ patched.py:33-45):
 from __future__ import annotations
 
 import ctypes as C
+import os
 from collections import Counter
 
 import numpy as np
@@ -31,6 +32,8 @@ from .params import device_params
 
 _launches: Counter = Counter()
 BF16 = torch.bfloat16
+# attention on CTA pairs (tcgen05 cta_group::2) only on request: measured slower
+USE_PAIRS = os.environ.get("PS_ATTN_PAIRS", "0") == "1"
 # bench hook: when a list, (start, end) CUDA events are recorded around every
 # attention-kernel launch on the launching stream
 ATTN_TIMER = None
@@ -246,9 +249,14 @@ class Ctx:
             ext = torch.cuda.is_current_stream_capturing()  # event nodes inside a captured graph
             ev = (torch.cuda.Event(enable_timing=True, external=ext), torch.cuda.Event(enable_timing=True, external=ext))
             ev[0].record()
-        tq0, timg, nt = self.attn_tiles or (self.dev["tile_q0"], self.dev["tile_img"], self.dev["n_tiles"])
-        _lib.call("ps_attention", stream(), qk.data_ptr(), vt.data_ptr(), ldv, self.T, dpp, d,
-                  self.dev["img_tok0"].data_ptr(), tq0.data_ptr(), timg.data_ptr(), nt, o.data_ptr())
+        if self.attn_tiles is not None:
+            tq0, timg, nt, pairs = self.attn_tiles
+        elif USE_PAIRS:
+            tq0, timg, nt, pairs = self.dev["pair_q0"], self.dev["pair_img"], self.dev["n_pairs"], True
+        else:
+            tq0, timg, nt, pairs = self.dev["tile_q0"], self.dev["tile_img"], self.dev["n_tiles"], False
+        _lib.call("ps_attention_pairs" if pairs else "ps_attention", stream(), qk.data_ptr(), vt.data_ptr(), ldv,
+                  self.T, dpp, d, self.dev["img_tok0"].data_ptr(), tq0.data_ptr(), timg.data_ptr(), nt, o.data_ptr())
         if timer is not None:
             ev[1].record()
             timer.append(ev)
@@ -374,12 +382,16 @@ def run_block_active(batch: CSPBatch, x, ops, active) -> torch.Tensor:
     ctx.rows_live, ctx.rows_act = tiles(live), tiles(act)
     sizes = batch.request_offset[1:] - batch.request_offset[:-1]
 
+    pairs = USE_PAIRS and ctx.hw % 256 == 0
+    tq = 256 if pairs else 128
+
     def attn(pats):  # query tiles of these patches, longest images first
         order = sorted(pats.tolist(), key=lambda p: -int(sizes[batch.request_index[p]]))
-        q0 = [p * ctx.hw + 128 * j for p in order for j in range(tpp)]
-        img = [int(batch.request_index[p]) for p in order for _ in range(tpp)]
+        n = ctx.hw // tq
+        q0 = [p * ctx.hw + tq * j for p in order for j in range(n)]
+        img = [int(batch.request_index[p]) for p in order for _ in range(n)]
         return (torch.as_tensor(np.asarray(q0, np.int32), device=ctx.device),
-                torch.as_tensor(np.asarray(img, np.int32), device=ctx.device), len(q0))
+                torch.as_tensor(np.asarray(img, np.int32), device=ctx.device), len(q0), pairs)
 
     ctx.attn_live, ctx.attn_act = attn(live), attn(act)
     return _run_ops(ctx, x, ops)

@@ -14,7 +14,7 @@ x = b.data.to(torch.bfloat16)
 at = w[0][2][1]
 for _ in range(2):
     ps.patched_self_attention(b, x, at)
-dbg = torch.zeros(8, dtype=torch.int64, device="cuda")
+dbg = torch.zeros(16, dtype=torch.int64, device="cuda")
 _lib.load().ps_attention_debug(dbg.data_ptr())
 ps.patched_self_attention(b, x, at)
 torch.cuda.synchronize()
@@ -23,3 +23,5 @@ d = dbg.tolist()
 f = lambda a, t: a / t if t else 0
 print(f"MMA warp: wait s_free {f(d[0], d[3]):.2f}  wait p_full {f(d[1], d[3]):.2f}  wait K/V {f(d[2], d[3]):.2f}")
 print(f"softmax : wait s_full {f(d[4], d[6]):.2f}  wait p_free {f(d[5], d[6]):.2f}")
+nb = max(1, d[12])
+print(f"softmax per 128-key block (cycles): S load {d[8]/nb:.0f}  exp+sum {d[9]/nb:.0f}  wait PV/rescale {d[10]/nb:.0f}  P store {d[11]/nb:.0f}")
