@@ -19,8 +19,8 @@
 // K streams in 16 KB (128 keys x 64 dims) chunks through one ring, V^T in
 // (Dp x 64 keys) pieces through another.
 // Online-softmax rescaling of O is lazy (only when the running max grows by
-// more than 2^8).  Warp roles: w0 TMA producer, w1 MMA issuer, w2 TMEM
-// allocator, w4..w7 softmax + epilogue (thread = query row = TMEM lane).
+// more than 2^8).  Warp roles: w0 TMA producer, w1 S issuer, w2 TMEM
+// allocator, w3 PV issuer, w4..w7 softmax + epilogue (thread = query row = TMEM lane).
 #include "common.cuh"
 #include "ps_internal.h"
 
@@ -161,61 +161,66 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         load_v(j);
       }
     }
-  } else if (warp == 1) {
-    // ---------------------------------------------------------- MMA issuer
+  } else if (warp == 1 || warp == 3) {
+    // ---------------------------------------------------------- MMA issuers
+    // w1 issues S_j = Q K_j^T, w3 issues O += P_j V_j.  Two issuing threads keep
+    // the tensor pipe fed while either one waits on a barrier: a wait costs the
+    // issuer ~76 clk even when the phase already completed, and the MMA queue
+    // of one thread is too shallow to cover it (tools/micro/mma_contention.cu:
+    // one issuer with a wait per 4 N128 MMAs -> 77% of peak, two issuers -> 100%).
     constexpr uint32_t idesc_s = idesc_bf16_f32(AT_BM, AT_BN);
     constexpr uint32_t idesc_o = idesc_bf16_f32(AT_BM, Cfg::PV_N);
-    int ks = 0, vs = 0;
-    uint32_t kph = 0, vph = 0;
-    auto issue_s = [&](int j) {
-      // S buffer is free once the softmax warps loaded S_{j-1}
-      if (j >= 1) twait(s_free, (j - 1) & 1, w_a);
-      tc_fence_after();
-      for (int kc = 0; kc < Cfg::KB; ++kc) {
-        twait(&k_full[ks], kph, w_c);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint8_t* kt = sK + ks * Cfg::K_SLOT;
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            mma_bf16_ss(tmem + Cfg::S_COL, sdesc_sw128(sQ + kc * AT_BM * 128 + k * 32), sdesc_sw128(kt + k * 32),
-                        idesc_s, (kc | k) != 0);
-          mma_commit(&k_empty[ks]);
-          if (kc == Cfg::KB - 1) mma_commit(s_full);
-        }
-        __syncwarp();
-        if (++ks == Cfg::NK) { ks = 0; kph ^= 1; }
-      }
-    };
-    auto issue_pv = [&](int j) {
-      twait(p_full, j & 1, w_b);
-      tc_fence_after();
-      for (int ka = 0; ka < 2; ++ka) {
-        twait(&v_full[vs], vph, w_c);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint8_t* vt = sV + vs * Cfg::V_SLOT;
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-#pragma unroll
-            for (int n = 0; n < Cfg::PV_MMAS; ++n)
-              mma_bf16_ts(tmem + Cfg::O_COL + n * Cfg::PV_N, tmem + Cfg::P_COL + ka * 32 + k * 8,
-                          sdesc_sw128(vt + n * Cfg::PV_N * 128 + k * 32), idesc_o, (j | ka | k) != 0);
-          mma_commit(&v_empty[vs]);
-          if (ka == 1) {
-            mma_commit(p_free);
-            if (j == n_kb - 1) mma_commit(o_full);
-          }
-        }
-        __syncwarp();
-        if (++vs == Cfg::NV) { vs = 0; vph ^= 1; }
-      }
-    };
     mbar_wait(q_full, 0);
-    issue_s(0);
-    for (int j = 0; j < n_kb; ++j) {
-      if (j + 1 < n_kb) issue_s(j + 1);
-      issue_pv(j);
+    if (warp == 1) {
+      int ks = 0;
+      uint32_t kph = 0;
+      for (int j = 0; j < n_kb; ++j) {
+        // S buffer is free once the softmax warps loaded S_{j-1}
+        if (j >= 1) twait(s_free, (j - 1) & 1, w_a);
+        tc_fence_after();
+        for (int kc = 0; kc < Cfg::KB; ++kc) {
+          twait(&k_full[ks], kph, w_c);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint8_t* kt = sK + ks * Cfg::K_SLOT;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_bf16_ss(tmem + Cfg::S_COL, sdesc_sw128(sQ + kc * AT_BM * 128 + k * 32), sdesc_sw128(kt + k * 32),
+                          idesc_s, (kc | k) != 0);
+            mma_commit(&k_empty[ks]);
+            if (kc == Cfg::KB - 1) mma_commit(s_full);
+          }
+          __syncwarp();
+          if (++ks == Cfg::NK) { ks = 0; kph ^= 1; }
+        }
+      }
+    } else {
+      int vs = 0;
+      uint32_t vph = 0;
+      for (int j = 0; j < n_kb; ++j) {
+        twait(p_full, j & 1, w_b);
+        tc_fence_after();
+        for (int ka = 0; ka < 2; ++ka) {
+          twait(&v_full[vs], vph, w_c);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint8_t* vt = sV + vs * Cfg::V_SLOT;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+              for (int n = 0; n < Cfg::PV_MMAS; ++n)
+                mma_bf16_ts(tmem + Cfg::O_COL + n * Cfg::PV_N, tmem + Cfg::P_COL + ka * 32 + k * 8,
+                            sdesc_sw128(vt + n * Cfg::PV_N * 128 + k * 32), idesc_o, (j | ka | k) != 0);
+            mma_commit(&v_empty[vs]);
+            if (ka == 1) {
+              mma_commit(p_free);
+              if (j == n_kb - 1) mma_commit(o_full);
+            }
+          }
+          __syncwarp();
+          if (++vs == Cfg::NV) { vs = 0; vph ^= 1; }
+        }
+      }
     }
   } else if (warp >= 4) {
     // ------------------------------------------------ softmax + epilogue
@@ -313,7 +318,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   if (p.dbg && lane == 0) {
     const unsigned long long tot = clock64() - t_start;
     // [0] mma:s_free [1] mma:p_full [2] mma:k/v_full [3] mma total [4] softmax:s_full [5] softmax:p_free [6] sm total
-    if (warp == 1) { atomicAdd(p.dbg + 0, w_a); atomicAdd(p.dbg + 1, w_b); atomicAdd(p.dbg + 2, w_c); atomicAdd(p.dbg + 3, tot); }
+    if (warp == 1) { atomicAdd(p.dbg + 0, w_a); atomicAdd(p.dbg + 2, w_c); atomicAdd(p.dbg + 3, tot); }
+    if (warp == 3) { atomicAdd(p.dbg + 1, w_b); atomicAdd(p.dbg + 2, w_c); }
     if (warp == 4) { atomicAdd(p.dbg + 4, w_a); atomicAdd(p.dbg + 5, w_b); atomicAdd(p.dbg + 6, tot); }
   }
   tc_fence_before();
