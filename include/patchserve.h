@@ -69,6 +69,10 @@ int ps_halo_frames_nchw(void* stream, const void* src, int dtype, const int32_t*
 /* Per-(patch, group) partial moments of an NCHW bf16 array (first half of
  * stitched_group_norm, patched.py:132-137).  partials: fp32 [P, G, 2] (mean, M2). */
 int ps_gn_partials(void* stream, const void* x, int P, int C, int ps, int G, float* partials);
+/* ps_gn_partials over a DEVICE list of n patch indices (the patches a GPU owns
+ * in the split-image path); other rows of `partials` are untouched. */
+int ps_gn_partials_sub(void* stream, const void* x, int P, int C, int ps, int G, const int32_t* patches, int n,
+                       float* partials);
 /* Pool partials per request into mean / rstd (patched.py:135-140, eps).
  * stats: fp32 [R, G, 2] (mean, rstd). */
 int ps_gn_finalize(void* stream, const float* partials, const int32_t* request_offset, int R, int G, int cg_hw,
@@ -83,8 +87,24 @@ int ps_to_cl(void* stream, const void* x, int P, int C, int ps, int Cp, int mode
 int ps_frames_cl(void* stream, const void* x, int P, int C, int ps, int Cp, int mode, const float* stats,
                  const int32_t* request_index, const int32_t* neighbors, int G, const float* gamma,
                  const float* beta, void* out);
+/* ps_frames_cl for a DEVICE list of n patch indices only (split-image path). */
+int ps_frames_cl_sub(void* stream, const void* x, int P, int C, int ps, int Cp, int mode, const float* stats,
+                     const int32_t* request_index, const int32_t* neighbors, int G, const float* gamma,
+                     const float* beta, const int32_t* patches, int n, void* out);
 /* CL tokens -> NCHW bf16, optionally adding an NCHW bf16 residual (patched.py:215-217). */
 int ps_from_cl(void* stream, const void* x_cl, int P, int C, int ps, int Cp, const void* resid, void* out);
+
+/* ------------------------------- split-image exchange movers */
+/* Halo strips of an NCHW bf16 patch array across a shard cut (the cross-GPU part
+ * of exchange_halos, patched.py:57-89): desc DEVICE [n][2] = (patch, code), code
+ * < ps = pixel row, code >= ps = pixel column code-ps; buf [n][C][ps] bf16.
+ * unpack = 0: x -> buf, 1: buf -> x. */
+int ps_halo_strips(void* stream, void* x, int C, int ps, int n, const int32_t* desc, void* buf, int unpack);
+/* n segments of seg_bytes (even): dst + dst_off[i] <- src + src_off[i] (DEVICE
+ * int64 byte offsets).  Packs GroupNorm partials (patched.py:132-140) and
+ * attention K rows / V^T columns (patched.py:164-176) into NCCL buffers and back. */
+int ps_copy_segments(void* stream, const void* src, void* dst, int n, const int64_t* src_off, const int64_t* dst_off,
+                     int64_t seg_bytes);
 
 /* Dense contraction on tcgen05: D[M,N] = A[M,K] B[N,K]^T (+bias), bf16 in, fp32 accumulate.
  * a: CL tokens [M, lda] (a_mode 0), CL frames (a_mode 1: implicit conv3, K = 9*Cp,

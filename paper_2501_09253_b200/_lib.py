@@ -47,9 +47,14 @@ _SIGS = {
     "ps_csp_reassemble": ([p, p, p, p, p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int], C.c_int),
     "ps_halo_frames_nchw": ([p, p, C.c_int, p, C.c_int, C.c_int, C.c_int, p], C.c_int),
     "ps_gn_partials": ([p, p, C.c_int, C.c_int, C.c_int, C.c_int, p], C.c_int),
+    "ps_gn_partials_sub": ([p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, C.c_int, p], C.c_int),
     "ps_gn_finalize": ([p, p, p, C.c_int, C.c_int, C.c_int, f32, p], C.c_int),
     "ps_to_cl": ([p, p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, p, p, C.c_int, p, p, f32, p], C.c_int),
     "ps_frames_cl": ([p, p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, C.c_int, p, p, p], C.c_int),
+    "ps_frames_cl_sub": ([p, p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, C.c_int, p, p, p, C.c_int, p],
+                         C.c_int),
+    "ps_halo_strips": ([p, p, C.c_int, C.c_int, C.c_int, p, p, C.c_int], C.c_int),
+    "ps_copy_segments": ([p, p, p, C.c_int, p, p, i64], C.c_int),
     "ps_from_cl": ([p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, p], C.c_int),
     "ps_gemm": ([p, C.POINTER(GemmArgs)], C.c_int),
     "ps_attention": ([p, p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, C.c_int, p], C.c_int),

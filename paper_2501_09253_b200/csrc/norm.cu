@@ -31,9 +31,10 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // mean and then M2 are reduced from registers (two-pass numerics, one pass of HBM).
 constexpr int GN_REG = 8;
 __global__ void __launch_bounds__(256) gn_partials_kernel(const __nv_bfloat16* __restrict__ x, int C, int hw, int G,
+                                                          const int32_t* __restrict__ plist,
                                                           float* __restrict__ partials) {
   __shared__ float red[32];
-  const int p = blockIdx.x, g = blockIdx.y;
+  const int p = plist ? __ldg(plist + blockIdx.x) : (int)blockIdx.x, g = blockIdx.y;
   const int cg = C / G;
   const int64_t n = (int64_t)cg * hw;
   const __nv_bfloat16* base = x + ((int64_t)p * C + (int64_t)g * cg) * hw;
@@ -184,9 +185,10 @@ __global__ void __launch_bounds__(256) frames_vec_kernel(const __nv_bfloat16* __
                                                          const int32_t* __restrict__ nbr, int G,
                                                          const float* __restrict__ gamma,
                                                          const float* __restrict__ beta, int R,
+                                                         const int32_t* __restrict__ plist,
                                                          __nv_bfloat16* __restrict__ out) {
   extern __shared__ __align__(16) __nv_bfloat16 tile[];
-  const int p = blockIdx.x, c0 = blockIdx.y * 64;
+  const int p = plist ? __ldg(plist + blockIdx.x) : (int)blockIdx.x, c0 = blockIdx.y * 64;
   const int F = FRAMES ? ps + 2 : ps;    // output side
   const int off = FRAMES ? 1 : 0;        // interior offset in the output row
   const int r0 = blockIdx.z * R;
@@ -304,12 +306,12 @@ __global__ void __launch_bounds__(256) frames_vec_kernel(const __nv_bfloat16* __
 template <bool FRAMES>
 static int launch_frames_vec(cudaStream_t st, const void* x, int P, int C, int ps, int Cp, int mode,
                              const float* stats, const int32_t* ri, const int32_t* nbr, int G, const float* gamma,
-                             const float* beta, void* out) {
+                             const float* beta, void* out, const int32_t* plist = nullptr, int n_list = 0) {
   const int F = FRAMES ? ps + 2 : ps;
   int R = 8;
   while (R > 1 && R * F * 64 * 2 > 96 * 1024) R >>= 1;
   const int smem = R * F * 64 * 2;
-  dim3 grid(P, Cp / 64, (F + R - 1) / R);
+  dim3 grid(plist ? n_list : P, Cp / 64, (F + R - 1) / R);
   auto xb = (const __nv_bfloat16*)x;
   auto ob = (__nv_bfloat16*)out;
 #define PS_FRAMES_LAUNCH(V)                                                                                      \
@@ -319,7 +321,7 @@ static int launch_frames_vec(cudaStream_t st, const void* x, int P, int C, int p
       cudaFuncSetAttribute(frames_vec_kernel<FRAMES, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024); \
       attr = true;                                                                                               \
     }                                                                                                            \
-    frames_vec_kernel<FRAMES, V><<<grid, 256, smem, st>>>(xb, C, ps, Cp, mode, stats, ri, nbr, G, gamma, beta, R, ob); \
+    frames_vec_kernel<FRAMES, V><<<grid, 256, smem, st>>>(xb, C, ps, Cp, mode, stats, ri, nbr, G, gamma, beta, R, plist, ob); \
   }
   if (ps % 8 == 0) PS_FRAMES_LAUNCH(8)
   else if (ps % 4 == 0) PS_FRAMES_LAUNCH(4)
@@ -375,9 +377,20 @@ int ps_gn_partials(void* stream, const void* x, int P, int C, int ps_, int G, fl
   if (G < 1 || C % G) return set_error(PS_ERR_INPUT, "groups=%d does not divide channels=%d", G, C);
   if (P == 0) return PS_OK;
   gn_partials_kernel<<<dim3(P, G), 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)x, C, ps_ * ps_, G,
-                                                                   partials);
+                                                                   nullptr, partials);
   count_launch();
   return check_launch("gn_partials");
+}
+
+int ps_gn_partials_sub(void* stream, const void* x, int P, int C, int ps_, int G, const int32_t* patches, int n,
+                       float* partials) {
+  if (G < 1 || C % G) return set_error(PS_ERR_INPUT, "groups=%d does not divide channels=%d", G, C);
+  if (n < 0 || n > P) return set_error(PS_ERR_INPUT, "gn_partials_sub: %d patches listed for P=%d", n, P);
+  if (n == 0) return PS_OK;
+  gn_partials_kernel<<<dim3(n, G), 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)x, C, ps_ * ps_, G,
+                                                                   patches, partials);
+  count_launch();
+  return check_launch("gn_partials_sub");
 }
 
 int ps_gn_finalize(void* stream, const float* partials, const int32_t* request_offset, int R, int G, int cg_hw,
@@ -413,6 +426,17 @@ int ps_frames_cl(void* stream, const void* x, int P, int C, int ps_, int Cp, int
   if (P == 0) return PS_OK;
   return launch_frames_vec<true>((cudaStream_t)stream, x, P, C, ps_, Cp, mode, stats, request_index, neighbors, G,
                                  gamma, beta, out);
+}
+
+int ps_frames_cl_sub(void* stream, const void* x, int P, int C, int ps_, int Cp, int mode, const float* stats,
+                     const int32_t* request_index, const int32_t* neighbors, int G, const float* gamma,
+                     const float* beta, const int32_t* patches, int n, void* out) {
+  if (Cp % 64 || Cp < C) return set_error(PS_ERR_INPUT, "frames_cl: Cp must be >= C and a multiple of 64");
+  if (mode == 1 && (G < 1 || C % G)) return set_error(PS_ERR_INPUT, "groups=%d does not divide channels=%d", G, C);
+  if (n < 0 || n > P) return set_error(PS_ERR_INPUT, "frames_cl_sub: %d patches listed for P=%d", n, P);
+  if (n == 0) return PS_OK;
+  return launch_frames_vec<true>((cudaStream_t)stream, x, P, C, ps_, Cp, mode, stats, request_index, neighbors, G,
+                                 gamma, beta, out, patches, n);
 }
 
 int ps_from_cl(void* stream, const void* x_cl, int P, int C, int ps_, int Cp, const void* resid, void* out) {

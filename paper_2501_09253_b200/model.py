@@ -21,7 +21,7 @@ from ._dev import require_cuda, stream, to_device
 from .csp import CSPBatch
 from .errors import InputError
 from .params import (AttentionParams, ConvParams, FeedForwardParams, GroupNormParams, LayerNormParams)
-from .patched import run_block
+from .patched import run_block, run_block_shard, shard_context
 
 ARCHS = ("unet_like", "dit_like")
 RATE_START = 0.15
@@ -154,4 +154,25 @@ def denoise_batch(cfg: ModelConfig, weights, batch: CSPBatch, prompts: dict, ste
     h = prompt_bias(batch, lat, bias)
     for ops in weights:
         h = run_block(batch, h, ops)
+    return blend_batch(batch, lat, h, rates)
+
+
+def denoise_batch_shard(cfg: ModelConfig, weights, batch: CSPBatch, shard, exch, prompts: dict, step_idx: dict,
+                        total_steps: dict) -> torch.Tensor:
+    """denoise_batch for one rank of the split-image path (patchshard.py).
+
+    `batch` is the rank's local CSP batch (the requests its patch range touches,
+    `shard.requests`); rows of the owned patches (`shard.owned`) of the result
+    equal the single-GPU denoise_batch rows of the same patches; ghost rows are
+    unspecified.
+    """
+    if batch.data.shape[1] != cfg.channels:
+        raise InputError(f"batch has {batch.data.shape[1]} channels, model expects {cfg.channels}")
+    bias, rates = step_inputs(cfg, batch, prompts, step_idx, total_steps)
+    lat = batch.data if batch.data.dtype == torch.float32 else batch.data.float()
+    lat = lat.contiguous()
+    h = prompt_bias(batch, lat, bias)
+    ctx = shard_context(batch, shard, exch)
+    for ops in weights:
+        h = run_block_shard(batch, h, ops, shard, exch, ctx=ctx)
     return blend_batch(batch, lat, h, rates)

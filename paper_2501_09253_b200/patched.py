@@ -104,6 +104,9 @@ class Ctx:
         self.attn_act = None
         self.rows = None        # row set of the stage being run (set by _run_ops)
         self.attn_tiles = None
+        # split-image multi-GPU path (patchshard.py): the owned patches and the exchanger
+        self.owned = None       # device int32 list of owned patches
+        self.exch = None
 
     def empty_cl(self, cp: int) -> torch.Tensor:
         return torch.empty((self.T, cp), dtype=BF16, device=self.device)
@@ -160,7 +163,13 @@ class Ctx:
     def gn_stats(self, x_nchw: torch.Tensor, c: int, dp: dict) -> torch.Tensor:
         g = dp["groups"]
         part = torch.empty((self.P, g, 2), dtype=torch.float32, device=self.device)
-        _lib.call("ps_gn_partials", stream(), x_nchw.data_ptr(), self.P, c, self.ps, g, part.data_ptr())
+        if self.owned is not None:
+            # owned patches here; the split images' other partials arrive from their owners
+            _lib.call("ps_gn_partials_sub", stream(), x_nchw.data_ptr(), self.P, c, self.ps, g,
+                      self.owned[0].data_ptr(), self.owned[1], part.data_ptr())
+            self.exch.gn(part, g)
+        else:
+            _lib.call("ps_gn_partials", stream(), x_nchw.data_ptr(), self.P, c, self.ps, g, part.data_ptr())
         stats = torch.empty((self.b.n_requests, g, 2), dtype=torch.float32, device=self.device)
         _lib.call("ps_gn_finalize", stream(), part.data_ptr(), self.dev["request_offset"].data_ptr(),
                   self.b.n_requests, g, (c // g) * self.hw, C.c_float(dp["eps"]), stats.data_ptr())
@@ -171,24 +180,28 @@ class Ctx:
         x = self.as_nchw(a)
         stats = self.gn_stats(x, a.C, dp)
         if frames:
-            fr = torch.empty((self.P, self.ps + 2, self.ps + 2, a.Cp), dtype=BF16, device=self.device)
-            _lib.call("ps_frames_cl", stream(), x.data_ptr(), self.P, a.C, self.ps, a.Cp, 1, stats.data_ptr(),
-                      self.dev["request_index"].data_ptr(), self.dev["neighbors"].data_ptr(), dp["groups"],
-                      dp["gamma"].data_ptr(), dp["beta"].data_ptr(), fr.data_ptr())
-            return None, fr
+            return None, self._frames(x, a.C, a.Cp, 1, stats, dp["groups"], dp["gamma"], dp["beta"])
         out = self.empty_cl(a.Cp)
         _lib.call("ps_to_cl", stream(), x.data_ptr(), self.P, a.C, self.ps, a.Cp, 1, stats.data_ptr(),
                   self.dev["request_index"].data_ptr(), dp["groups"], dp["gamma"].data_ptr(), dp["beta"].data_ptr(),
                   C.c_float(dp["eps"]), out.data_ptr())
         return Act("cl", out, a.C), None
 
-    def frames_of(self, a: Act) -> torch.Tensor:
-        x = self.as_nchw(a)
-        fr = torch.empty((self.P, self.ps + 2, self.ps + 2, a.Cp), dtype=BF16, device=self.device)
-        _lib.call("ps_frames_cl", stream(), x.data_ptr(), self.P, a.C, self.ps, a.Cp, 0, None,
-                  self.dev["request_index"].data_ptr(), self.dev["neighbors"].data_ptr(), 1, None, None,
-                  fr.data_ptr())
+    def _frames(self, x, c, cp, mode, stats, groups, gamma, beta) -> torch.Tensor:
+        fr = torch.empty((self.P, self.ps + 2, self.ps + 2, cp), dtype=BF16, device=self.device)
+        args = (x.data_ptr(), self.P, c, self.ps, cp, mode, None if stats is None else stats.data_ptr(),
+                self.dev["request_index"].data_ptr(), self.dev["neighbors"].data_ptr(), groups,
+                None if gamma is None else gamma.data_ptr(), None if beta is None else beta.data_ptr())
+        if self.owned is not None:
+            # the stencil rows / columns of neighbours owned by other GPUs land in their ghost slots of x
+            self.exch.halo(x, c)
+            _lib.call("ps_frames_cl_sub", stream(), *args, self.owned[0].data_ptr(), self.owned[1], fr.data_ptr())
+        else:
+            _lib.call("ps_frames_cl", stream(), *args, fr.data_ptr())
         return fr
+
+    def frames_of(self, a: Act) -> torch.Tensor:
+        return self._frames(self.as_nchw(a), a.C, a.Cp, 0, None, 1, None, None)
 
     def conv(self, a: Act, prm, frames, resid):
         dp = device_params(prm, a.C)
@@ -243,6 +256,8 @@ class Ctx:
         vt = torch.empty((dpp, ldv), dtype=BF16, device=self.device)
         self.gemm(x, a.Cp, dp["wqkv"], 3 * dpp, dpp, None, 3, qk, ldo=2 * dpp, out2=vt, ldo2=ldv, n_split=2 * dpp,
                   rows=self.rows_live)
+        if self.owned is not None:
+            self.exch.kv(qk, vt, ldv, dpp)  # K rows / V^T columns of split images from their owners
         o = self.empty_cl(dpp)
         timer = ATTN_TIMER
         if timer is not None:
@@ -373,28 +388,52 @@ def run_block_active(batch: CSPBatch, x, ops, active) -> torch.Tensor:
     act = np.flatnonzero(active)
     live_img = np.unique(batch.request_index[act])
     live = np.flatnonzero(np.isin(batch.request_index, live_img))
+    ctx.rows_live, ctx.rows_act = _row_tiles(ctx, live), _row_tiles(ctx, act)
+    ctx.attn_live, ctx.attn_act = _attn_tiles(ctx, live), _attn_tiles(ctx, act)
+    return _run_ops(ctx, x, ops)
+
+
+def _row_tiles(ctx: "Ctx", pats: np.ndarray):
+    """Device list of the 128-row GEMM tiles of these patches (ps*ps % 128 == 0)."""
     tpp = ctx.hw // 128
+    m = (np.asarray(pats, dtype=np.int64)[:, None] * tpp + np.arange(tpp)[None, :]).ravel().astype(np.int32)
+    return torch.as_tensor(m, device=ctx.device), int(m.size)
 
-    def tiles(pats):
-        m = (pats[:, None] * tpp + np.arange(tpp)[None, :]).ravel().astype(np.int32)
-        return torch.as_tensor(m, device=ctx.device), int(m.size)
 
-    ctx.rows_live, ctx.rows_act = tiles(live), tiles(act)
+def _attn_tiles(ctx: "Ctx", pats: np.ndarray):
+    """Attention query tiles (q0, image, n, pairs) of these patches, longest images first."""
+    batch = ctx.b
     sizes = batch.request_offset[1:] - batch.request_offset[:-1]
-
     pairs = USE_PAIRS and ctx.hw % 256 == 0
     tq = 256 if pairs else 128
+    order = sorted(np.asarray(pats).tolist(), key=lambda p: -int(sizes[batch.request_index[p]]))
+    n = ctx.hw // tq
+    q0 = [p * ctx.hw + tq * j for p in order for j in range(n)]
+    img = [int(batch.request_index[p]) for p in order for _ in range(n)]
+    return (torch.as_tensor(np.asarray(q0, np.int32), device=ctx.device),
+            torch.as_tensor(np.asarray(img, np.int32), device=ctx.device), len(q0), pairs)
 
-    def attn(pats):  # query tiles of these patches, longest images first
-        order = sorted(pats.tolist(), key=lambda p: -int(sizes[batch.request_index[p]]))
-        n = ctx.hw // tq
-        q0 = [p * ctx.hw + tq * j for p in order for j in range(n)]
-        img = [int(batch.request_index[p]) for p in order for _ in range(n)]
-        return (torch.as_tensor(np.asarray(q0, np.int32), device=ctx.device),
-                torch.as_tensor(np.asarray(img, np.int32), device=ctx.device), len(q0), pairs)
 
-    ctx.attn_live, ctx.attn_act = attn(live), attn(act)
-    return _run_ops(ctx, x, ops)
+def shard_context(batch: CSPBatch, shard, exch) -> "Ctx":
+    """Ctx of one rank of the split-image path (patchshard.py): every stage computes the
+    owned patches only; context owned by other ranks arrives through `exch`."""
+    ctx = Ctx(batch)
+    if batch.n_patches != shard.n_patches:
+        raise InputError(f"batch has {batch.n_patches} patches, shard expects {shard.n_patches}")
+    if ctx.hw % 128:
+        raise InputError(f"split-image path needs patch_size^2 % 128 == 0, got patch {ctx.ps}")
+    owned = np.asarray(shard.owned, dtype=np.int64)
+    ctx.owned = (torch.as_tensor(owned.astype(np.int32), device=ctx.device), int(owned.size))
+    ctx.exch = exch
+    ctx.rows_live = ctx.rows_act = _row_tiles(ctx, owned)
+    ctx.attn_live = ctx.attn_act = _attn_tiles(ctx, owned)
+    return ctx
+
+
+def run_block_shard(batch: CSPBatch, x, ops, shard, exch, ctx: "Ctx | None" = None) -> torch.Tensor:
+    """run_block for one rank of the split-image path; rows of ghost patches are unspecified."""
+    x = _check_data(batch, x)
+    return _run_ops(ctx or shard_context(batch, shard, exch), x, ops)
 
 
 def _run_ops(ctx: "Ctx", x: torch.Tensor, ops) -> torch.Tensor:

@@ -1,0 +1,145 @@
+"""Split-image multi-GPU path on the device.
+
+Each rank of a SplitPlan runs denoise_batch_shard on its local CSP batch with
+its ghost context arriving through the three exchanges (GroupNorm partials,
+halo strips, attention K / V^T).  The owned rows must be BIT-IDENTICAL to the
+single-GPU denoise_batch rows of the same patches: the exchanges move exact
+copies and every kernel computes a row from the same inputs in the same order.
+
+One B200 is available per test box, so ranks run (a) as threads over a
+VirtualGroup in one process and (b) as two processes on cuda:0 over gloo
+(DistComm staging through host memory) -- the same pack / unpack kernels and
+exchange tables the NCCL path uses.
+"""
+
+import os
+import socket
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+PS = 16
+REQS = [("big", 64), ("b", 16), ("c", 32), ("d", 16)]
+
+
+def _setup(arch):
+    import paper_2501_09253_b200 as ps
+    cfg = ps.ModelConfig(arch=arch, channels=64, hidden=128, groups=8, n_blocks=2, seed=5)
+    w = ps.init_weights(cfg)
+    rng = np.random.default_rng(11)
+    lats = {rid: torch.tensor(rng.normal(size=(64, d, d)), dtype=torch.float32) for rid, d in REQS}
+    prompts = {rid: ps.make_prompt(cfg, rid) for rid, _ in REQS}
+    return ps, cfg, w, lats, prompts
+
+
+def _full(ps, cfg, w, lats, prompts):
+    b = ps.split([(rid, lats[rid]) for rid, _ in REQS], patch_size=PS)
+    si = {rid: 2 for rid, _ in REQS}
+    ts = {rid: 10 for rid, _ in REQS}
+    return b, ps.denoise_batch(cfg, w, b, prompts, si, ts)
+
+
+def _rank_step(ps, cfg, w, lats, prompts, sh, exch):
+    from paper_2501_09253_b200.model import denoise_batch_shard
+    b = ps.split([(rid, lats[rid]) for rid, _ in sh.requests], patch_size=PS)
+    si = {rid: 2 for rid, _ in sh.requests}
+    ts = {rid: 10 for rid, _ in sh.requests}
+    return b, denoise_batch_shard(cfg, w, b, sh, exch, prompts, si, ts)
+
+
+def _plan(world):
+    from paper_2501_09253_b200.patchshard import SplitPlan, patch_cost
+    return SplitPlan(REQS, PS, world, cost=lambda lat: patch_cost(lat, PS, 64, 128))
+
+
+def _compare(plan, full_b, full_out, rank, b, out):
+    sh = plan.shard(rank)
+    assert [e.request_id for e in full_b.requests] == [r.request_id for r in plan.reqs]
+    for g in range(plan.cuts[rank], plan.cuts[rank + 1]):
+        lp = sh.local(g)
+        assert b.patch_key(lp) == full_b.patch_key(g)
+        if not torch.equal(out[lp], full_out[g]):
+            d = (out[lp] - full_out[g]).abs().max().item()
+            raise AssertionError(f"rank {rank} patch {g}: max |d| {d:.3e} (expected bit-identical)")
+
+
+@pytest.mark.parametrize("arch", ["unet_like", "dit_like"])
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_split_virtual_ranks_bit_identical(arch, world):
+    from paper_2501_09253_b200.patchshard import ShardExchange, VirtualGroup
+    ps, cfg, w, lats, prompts = _setup(arch)
+    full_b, full_out = _full(ps, cfg, w, lats, prompts)
+    plan = _plan(world)
+    assert plan.split_requests(), "the plan must split at least one image"
+    grp = VirtualGroup(world)
+    res, errs = {}, []
+
+    def run(r):
+        try:
+            torch.cuda.set_device(0)
+            sh = plan.shard(r)
+            res[r] = _rank_step(ps, cfg, w, lats, prompts, sh, ShardExchange(sh, grp))
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+            grp._bar.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(300)
+    if errs:
+        raise errs[0]
+    torch.cuda.synchronize()
+    for r in range(world):
+        _compare(plan, full_b, full_out, r, *res[r])
+
+
+def _proc(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2501_09253_b200.patchshard import DistComm, ShardExchange
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ps, cfg, w, lats, prompts = _setup("unet_like")
+        plan = _plan(world)
+        sh = plan.shard(rank)
+        ex = ShardExchange(sh, DistComm())
+        b, out = _rank_step(ps, cfg, w, lats, prompts, sh, ex)
+        q.put((rank, out.cpu(), ex.bytes_moved))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_split_two_processes_gloo():
+    import torch.multiprocessing as mp
+    ps, cfg, w, lats, prompts = _setup("unet_like")
+    full_b, full_out = _full(ps, cfg, w, lats, prompts)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_proc, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in procs:
+        r, out, moved = q.get(timeout=300)
+        got[r] = (out, moved)
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    plan = _plan(2)
+    for r in range(2):
+        sh = plan.shard(r)
+        b = ps.split([(rid, lats[rid]) for rid, _ in sh.requests], patch_size=PS)
+        _compare(plan, full_b, full_out.cpu(), r, b, got[r][0])
+        assert got[r][1] > 0
