@@ -1,0 +1,689 @@
+"""Serving plane around the patch path: cost model, traces, SLO-aware admission
+and the event loop — the caller of the hot path.
+
+The reference (latency.py, workload.py, scheduler.py, engine.py) prices every
+step with an analytic cost model calibrated to nothing in particular, and its
+numeric plane runs the patched model on the CPU while the clock still comes
+from that model.  Here the same policy code drives the B200 path, with three
+clocks:
+
+* ``cost_only`` — analytic step latency, no compute (the reference's
+  cost_only plane; event logs match it exactly, tests/test_serving.py);
+* ``numeric``   — analytic clock, every step computed on the GPU through
+  engine_step.numeric_step with the patch cache in the loop (the reference's
+  numeric plane; same events, latents within the bf16 tolerance);
+* ``wall``      — every step computed on the GPU and the clock advanced by the
+  step's measured device time (CUDA events around the whole step: split,
+  prompt bias, blocks with the cache, blend, reassemble).  SLO attainment in
+  this plane is the B200 number the BASELINE metric asks for.
+
+`fit_cost_model` refits the analytic model's constants to measured B200 step
+times so admission decisions and SLO budgets (workload.py:74, 3x standalone
+latency) are in B200 time.
+"""
+
+from __future__ import annotations
+
+import heapq
+import json
+from dataclasses import dataclass, field, replace
+from typing import Sequence
+
+import numpy as np
+
+from .csp import STANDARD_CLASSES
+from .errors import InputError  # noqa: F401  (re-exported for callers)
+
+CLASS_ORDER = ("low", "med", "high")
+
+# ------------------------------------------------------------ cost model
+
+
+@dataclass(frozen=True)
+class CostModelParams:
+    """latency.py:25-33 (defaults are the reference's)."""
+
+    blocks_per_step: int = 8
+    c_step_fixed: float = 60.0
+    c_res_overhead: float = 2.0
+    c_patch: float = 0.1
+    c_attn_coeff: float = 6e-7
+    attn_exponent: float = 1.5
+    patch_size: int = 32
+
+
+DEFAULT_COST = CostModelParams()
+
+
+def _validated(comp: dict) -> dict:
+    if not comp:
+        raise InputError("empty composition")
+    for k, v in comp.items():
+        if k not in STANDARD_CLASSES:
+            raise InputError(f"unknown resolution class {k!r}")
+        if v < 0:
+            raise InputError(f"negative count for {k!r}")
+    if sum(comp.values()) == 0:
+        raise InputError("composition has no requests")
+    return comp
+
+
+def _terms(comp: dict, p: CostModelParams):
+    """(distinct resolutions, patches, sum of tokens^exponent) of a composition."""
+    n_res, patches, attn = 0, 0, 0.0
+    for cls, n in _validated(comp).items():
+        if n == 0:
+            continue
+        lat = STANDARD_CLASSES[cls].latent
+        if lat % p.patch_size:
+            raise InputError(f"patch size {p.patch_size} does not tile {cls}")
+        n_res += 1
+        patches += n * (lat // p.patch_size) ** 2
+        attn += n * float(lat * lat) ** p.attn_exponent
+    return n_res, patches, attn
+
+
+def step_latency(comp: dict, p: CostModelParams = DEFAULT_COST) -> float:
+    """latency.py:52-77: fixed + per-resolution + blocks x (patch term + attention term), ms."""
+    n_res, patches, attn = _terms(comp, p)
+    return p.c_step_fixed + p.c_res_overhead * n_res + p.blocks_per_step * (p.c_patch * patches
+                                                                            + p.c_attn_coeff * attn)
+
+
+def standalone_latency(cls: str, steps: int, p: CostModelParams = DEFAULT_COST) -> float:
+    """latency.py:80-84."""
+    if steps < 1:
+        raise InputError("steps must be >= 1")
+    return steps * step_latency({cls: 1}, p)
+
+
+class AnalyticPredictor:
+    """latency.py:256-263: the scheduler's default predictor."""
+
+    def __init__(self, p: CostModelParams = DEFAULT_COST):
+        self.cost_params = p
+
+    def predict_step_latency(self, comp: dict) -> float:
+        return step_latency(comp, self.cost_params)
+
+
+def fit_cost_model(samples: Sequence[tuple[dict, float]], base: CostModelParams = DEFAULT_COST) -> CostModelParams:
+    """Least-squares fit of (c_step_fixed, c_res_overhead, c_patch, c_attn_coeff) to
+    measured (composition, step ms) pairs, keeping the exponent and block count.
+    Coefficients are clamped at zero (non-negative least squares by elimination)."""
+    if len(samples) < 4:
+        raise InputError("need at least 4 measured compositions to fit the cost model")
+    rows, y = [], []
+    for comp, ms in samples:
+        n_res, patches, attn = _terms(comp, base)
+        rows.append([1.0, n_res, base.blocks_per_step * patches, base.blocks_per_step * attn])
+        y.append(float(ms))
+    A, y = np.asarray(rows), np.asarray(y)
+    active = list(range(4))
+    while True:
+        coef = np.zeros(4)
+        sol, *_ = np.linalg.lstsq(A[:, active], y, rcond=None)
+        coef[active] = sol
+        neg = [i for i in active if coef[i] < 0]
+        if not neg:
+            break
+        active.remove(min(neg, key=lambda i: coef[i]))
+    return replace(base, c_step_fixed=float(coef[0]), c_res_overhead=float(coef[1]), c_patch=float(coef[2]),
+                   c_attn_coeff=float(coef[3]))
+
+
+# ------------------------------------------------------------- workload
+
+DEFAULT_WEIGHTS = {"low": 0.4, "med": 0.35, "high": 0.25}
+
+
+@dataclass(frozen=True)
+class WorkloadConfig:
+    """workload.py:23-48."""
+
+    seed: int = 0
+    qps: float = 1.0
+    n_requests: int = 100
+    class_weights: dict = field(default_factory=lambda: dict(DEFAULT_WEIGHTS))
+    slo_scale: float = 3.0
+    steps: int = 50
+
+    def __post_init__(self):
+        if self.qps <= 0:
+            raise InputError("qps must be positive")
+        if self.n_requests < 1:
+            raise InputError("n_requests must be >= 1")
+        if self.slo_scale <= 0:
+            raise InputError("slo_scale must be positive")
+        if self.steps < 1:
+            raise InputError("steps must be >= 1")
+        if any(c not in STANDARD_CLASSES for c in self.class_weights):
+            raise InputError(f"unknown resolution class in {sorted(self.class_weights)}")
+        if any(w < 0 for w in self.class_weights.values()):
+            raise InputError("class weights must be nonnegative")
+        if sum(self.class_weights.values()) <= 0:
+            raise InputError("class weights must not all be zero")
+
+
+@dataclass(frozen=True)
+class TraceRow:
+    request_id: str
+    arrival_ms: float
+    resolution_class: str
+    slo_ms: float
+
+
+def generate_trace(cfg: WorkloadConfig, cost: CostModelParams = DEFAULT_COST) -> list[TraceRow]:
+    """workload.py:58-77: exponential gaps then weighted class picks from one seeded stream."""
+    rng = np.random.default_rng(cfg.seed)
+    arrivals = np.cumsum(rng.exponential(scale=1000.0 / cfg.qps, size=cfg.n_requests))
+    names = sorted(cfg.class_weights)
+    w = np.asarray([cfg.class_weights[n] for n in names], dtype=np.float64)
+    picks = rng.choice(len(names), size=cfg.n_requests, p=w / w.sum())
+    budget = {n: cfg.slo_scale * standalone_latency(n, cfg.steps, cost) for n in names}
+    return [TraceRow(f"req-{i:05d}", float(arrivals[i]), names[int(k)], budget[names[int(k)]])
+            for i, k in enumerate(picks)]
+
+
+def write_trace(rows: Sequence[TraceRow], path) -> None:
+    """JSONL, one object per row (workload.py:80-89)."""
+    with open(path, "w") as f:
+        for r in rows:
+            f.write(json.dumps({"request_id": r.request_id, "arrival_ms": r.arrival_ms,
+                                "resolution_class": r.resolution_class, "slo_ms": r.slo_ms}) + "\n")
+
+
+def read_trace(path) -> list[TraceRow]:
+    """workload.py:92-113 (InputError on malformed, empty or unsorted traces)."""
+    rows = []
+    with open(path) as f:
+        for n, line in enumerate(f, 1):
+            if not line.strip():
+                continue
+            try:
+                d = json.loads(line)
+                rows.append(TraceRow(d["request_id"], float(d["arrival_ms"]), d["resolution_class"],
+                                     float(d["slo_ms"])))
+            except (KeyError, ValueError) as exc:
+                raise InputError(f"{path}:{n}: bad trace row: {exc}") from exc
+    if not rows:
+        raise InputError(f"{path}: empty trace")
+    if any(b.arrival_ms < a.arrival_ms for a, b in zip(rows, rows[1:])):
+        raise InputError(f"{path}: arrivals are not sorted")
+    return rows
+
+
+# ------------------------------------------------------------- scheduler
+
+POLICIES = ("slo_aware", "fcfs", "sequential")
+
+
+@dataclass
+class RequestMeta:
+    """scheduler.py:25-50."""
+
+    request_id: str
+    cls: str
+    arrival_ms: float
+    slo_ms: float
+    total_steps: int
+    remaining_steps: int = -1
+
+    def __post_init__(self):
+        if self.cls not in STANDARD_CLASSES:
+            raise InputError(f"unknown resolution class {self.cls!r}")
+        if self.total_steps < 1:
+            raise InputError("total_steps must be >= 1")
+        if self.remaining_steps < 0:
+            self.remaining_steps = self.total_steps
+
+    @property
+    def deadline_ms(self) -> float:
+        return self.arrival_ms + self.slo_ms
+
+    @property
+    def pixels(self) -> int:
+        return STANDARD_CLASSES[self.cls].pixel ** 2
+
+
+@dataclass(frozen=True)
+class SchedulerConfig:
+    """scheduler.py:53-64."""
+
+    policy: str = "slo_aware"
+    max_active: int = 12
+    theta_mode: float = 2.0
+    cost: CostModelParams = field(default_factory=CostModelParams)
+
+    def __post_init__(self):
+        if self.policy not in POLICIES:
+            raise InputError(f"policy must be one of {POLICIES}, got {self.policy!r}")
+        if self.max_active < 1:
+            raise InputError("max_active must be >= 1")
+
+
+@dataclass
+class TickResult:
+    admitted: list
+    discarded: list
+
+
+def composition(requests) -> dict:
+    comp: dict = {}
+    for r in requests:
+        comp[r.cls] = comp.get(r.cls, 0) + 1
+    return comp
+
+
+def slack(req: RequestMeta, now_ms: float, predicted_remaining_ms: float,
+          cost: CostModelParams = DEFAULT_COST) -> float:
+    """scheduler.py:81-90: spare time in units of the request's standalone latency."""
+    return (req.deadline_ms - now_ms - predicted_remaining_ms) / standalone_latency(req.cls, req.total_steps, cost)
+
+
+def time_out(req: RequestMeta, now_ms: float, predicted_remaining_ms: float) -> bool:
+    return now_ms + predicted_remaining_ms > req.deadline_ms
+
+
+class Scheduler:
+    """Admission policy (scheduler.py:98-177); owns no queues."""
+
+    def __init__(self, cfg: SchedulerConfig | None = None, predictor=None):
+        self.cfg = cfg or SchedulerConfig()
+        self.predictor = predictor or AnalyticPredictor(self.cfg.cost)
+
+    def tick(self, now_ms: float, active: list, waiting: list) -> TickResult:
+        if self.cfg.policy == "slo_aware":
+            return self._slo_aware(now_ms, list(active), list(waiting))
+        cap = 1 if self.cfg.policy == "sequential" else self.cfg.max_active
+        queue = sorted(waiting, key=lambda r: (r.arrival_ms, r.request_id))
+        room = max(0, cap - len(active))
+        return TickResult(admitted=queue[:room], discarded=[])
+
+    def _step_ms(self, batch) -> float:
+        return self.predictor.predict_step_latency(composition(batch))
+
+    def _slo_aware(self, now: float, active: list, pool: list) -> TickResult:
+        cost = self.cfg.cost
+        out = TickResult([], [])
+        while pool and len(active) < self.cfg.max_active:
+            # least slack first, each candidate priced at the pace of the batch it would join
+            best = None
+            for w in pool:
+                rem = self._step_ms(active + [w]) * w.remaining_steps
+                key = (slack(w, now, rem, cost), w.arrival_ms, w.request_id)
+                if best is None or key < best[0]:
+                    best = (key, w, rem)
+            (s_min, _, _), cand, rem = best
+            if time_out(cand, now, rem):
+                out.discarded.append(cand)
+                pool.remove(cand)
+                continue
+            if s_min > self.cfg.theta_mode:
+                # nobody urgent: maximise pixel throughput of the grown batch
+                px = sum(r.pixels for r in active)
+                cand = min(pool, key=lambda w: (-(px + w.pixels) / self._step_ms(active + [w]), w.arrival_ms,
+                                                w.request_id))
+            if active:
+                step = self._step_ms(active + [cand])
+                tight = min(active, key=lambda a: (slack(a, now, step * a.remaining_steps, cost), a.arrival_ms,
+                                                   a.request_id))
+                if time_out(tight, now, step * tight.remaining_steps):
+                    break
+            active.append(cand)
+            pool.remove(cand)
+            out.admitted.append(cand)
+        return out
+
+
+# ---------------------------------------------------------------- engine
+
+PLANES = ("cost_only", "numeric", "wall")
+
+
+@dataclass(frozen=True)
+class EngineConfig:
+    """engine.py:34-52, plus the `wall` plane."""
+
+    plane: str = "cost_only"
+    n_workers: int = 1
+    total_steps: int = 50
+    patch_size: int = 32
+    use_cache: bool = True
+    latent_seed: int = 0
+    scheduler: SchedulerConfig = field(default_factory=SchedulerConfig)
+    cost: CostModelParams = field(default_factory=CostModelParams)
+    model: object = None            # model.ModelConfig (None -> the reference default)
+    cache: object = None            # cache.PredictorConfig (None -> defaults)
+
+    def __post_init__(self):
+        if self.plane not in PLANES:
+            raise InputError(f"plane must be one of {PLANES}, got {self.plane!r}")
+        if self.n_workers < 1:
+            raise InputError("n_workers must be >= 1")
+        if self.total_steps < 1:
+            raise InputError("total_steps must be >= 1")
+
+
+@dataclass
+class RunResult:
+    events: list
+    completions: list
+    summary: dict
+    latents: dict = field(default_factory=dict)
+
+
+class _Worker:
+    def __init__(self, wid: int):
+        self.wid = wid
+        self.active: list = []
+        self.waiting: list = []
+        self.busy = False
+        self.steps_run = 0
+        self.latents: dict = {}
+        self.prompts: dict = {}
+        self.cache = None
+        self.step_ms: list = []   # measured device time per step (wall plane)
+
+
+class Engine:
+    """Discrete-event serving loop (engine.py:72-250).
+
+    Events are ordered by (time, insertion sequence); all events sharing a
+    timestamp are applied before any worker ticks, then idle touched workers
+    tick in worker order.  A step's duration is the analytic step latency
+    (cost_only / numeric) or the measured device time of the step (wall).
+    """
+
+    def __init__(self, cfg: EngineConfig | None = None, predictor=None, weights=None):
+        self.cfg = cfg or EngineConfig()
+        self.scheduler = Scheduler(self.cfg.scheduler, predictor)
+        self.model_cfg = self.cfg.model
+        self.weights = weights
+        if self.cfg.plane != "cost_only":
+            from .model import ModelConfig, init_weights
+            if self.model_cfg is None:
+                self.model_cfg = ModelConfig()
+            if self.weights is None:
+                self.weights = init_weights(self.model_cfg)
+
+    # ------------------------------------------------------------ compute
+    def _new_cache(self):
+        from .cache import BlockCache, PredictorConfig
+        return BlockCache(self.model_cfg.n_blocks, self.cfg.cache or PredictorConfig())
+
+    def _admit_latent(self, w: _Worker, meta: RequestMeta, idx: int) -> None:
+        import torch
+
+        from ._dev import require_cuda
+        from .model import make_prompt
+        d = STANDARD_CLASSES[meta.cls].latent
+        lat = np.random.default_rng([self.cfg.latent_seed, idx]).normal(size=(self.model_cfg.channels, d, d))
+        w.latents[meta.request_id] = torch.as_tensor(lat, dtype=torch.float32, device=require_cuda())
+        w.prompts[meta.request_id] = make_prompt(self.model_cfg, meta.request_id)
+
+    def _compute_step(self, w: _Worker) -> float:
+        """One denoising step of w's active batch on the GPU; returns its device time in ms."""
+        import torch
+
+        from ._dev import require_cuda
+        from .csp import reassemble, split
+        from .engine_step import numeric_step
+        from .model import rate_schedule
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        batch = split([(r.request_id, w.latents[r.request_id]) for r in w.active], patch_size=self.cfg.patch_size)
+        order = [self._meta[e.request_id] for e in batch.requests]
+        dev = require_cuda()
+        bias = torch.as_tensor(np.stack([w.prompts[m.request_id] for m in order]), dtype=torch.float32, device=dev)
+        rates = torch.as_tensor([rate_schedule(m.total_steps - m.remaining_steps, m.total_steps) for m in order],
+                                dtype=torch.float32, device=dev)
+        cache = w.cache if self.cfg.use_cache else None
+        new, st = numeric_step(batch, self.weights, cache, bias, rates)
+        for rid, lat in reassemble(batch, new).items():
+            w.latents[rid] = lat
+        t1.record()
+        t1.synchronize()
+        self._skipped += st.skipped
+        self._computed += st.computed
+        return float(t0.elapsed_time(t1))
+
+    # ------------------------------------------------------------ the loop
+    def run(self, trace: Sequence[TraceRow]) -> RunResult:
+        if not trace:
+            raise InputError("empty trace")
+        cfg = self.cfg
+        workers = [_Worker(i) for i in range(cfg.n_workers)]
+        if cfg.plane != "cost_only":
+            for w in workers:
+                w.cache = self._new_cache() if cfg.use_cache else None
+        events, completions, final = [], [], {}
+        self._skipped = self._computed = 0
+        self._meta = {}
+        heap: list = []
+        seq = [0]
+
+        def push(t, kind, payload):
+            heapq.heappush(heap, (t, seq[0], kind, payload))
+            seq[0] += 1
+
+        def log(t, kind, rid, wid):
+            events.append({"t_ms": round(t, 9), "kind": kind, "request_id": rid, "worker": wid})
+
+        index = {}
+        for i, row in enumerate(trace):
+            m = RequestMeta(row.request_id, row.resolution_class, row.arrival_ms, row.slo_ms, cfg.total_steps)
+            self._meta[row.request_id] = m
+            index[row.request_id] = i
+            push(row.arrival_ms, "arrival", row.request_id)
+
+        unit = {c: step_latency({c: 1}, cfg.cost) for c in STANDARD_CLASSES}
+
+        def backlog(w):  # engine.py:120-124
+            return sum(r.remaining_steps * unit[r.cls] for r in w.active + w.waiting)
+
+        def record_done(m, t, wid, discarded):
+            completions.append({
+                "request_id": m.request_id, "resolution_class": m.cls,
+                "arrival_ms": round(m.arrival_ms, 9), "finish_ms": round(t, 9),
+                "latency_ms": round(t - m.arrival_ms, 9), "slo_ms": round(m.slo_ms, 9),
+                "met_slo": bool(not discarded and t <= m.deadline_ms), "discarded": bool(discarded),
+                "worker": wid,
+            })
+
+        def begin(w, now):
+            w.busy = True
+            w.steps_run += 1
+            if cfg.plane == "cost_only":
+                dt = step_latency(composition(w.active), cfg.cost)
+            else:
+                dt_dev = self._compute_step(w)
+                w.step_ms.append(dt_dev)
+                dt = dt_dev if cfg.plane == "wall" else step_latency(composition(w.active), cfg.cost)
+            push(now + dt, "step_end", w.wid)
+
+        def finish(w, now):
+            w.busy = False
+            for r in w.active:
+                r.remaining_steps -= 1
+            done = [r for r in w.active if r.remaining_steps == 0]
+            for r in done:
+                w.active.remove(r)
+                log(now, "complete", r.request_id, w.wid)
+                record_done(r, now, w.wid, False)
+                if cfg.plane != "cost_only":
+                    final[r.request_id] = w.latents.pop(r.request_id)
+                    w.prompts.pop(r.request_id, None)
+            if done and w.cache is not None:
+                live = [(r.request_id, k) for r in w.active
+                        for k in range((STANDARD_CLASSES[r.cls].latent // cfg.patch_size) ** 2)]
+                w.cache.evict_expired(live)
+
+        def tick(w, now):
+            res = self.scheduler.tick(now, w.active, w.waiting)
+            for r in res.discarded:
+                w.waiting.remove(r)
+                log(now, "discard", r.request_id, w.wid)
+                record_done(r, now, w.wid, True)
+            for r in res.admitted:
+                w.waiting.remove(r)
+                w.active.append(r)
+                log(now, "admit", r.request_id, w.wid)
+            if w.active and not w.busy:
+                begin(w, now)
+
+        while heap:
+            now = heap[0][0]
+            touched = []
+            while heap and heap[0][0] == now:
+                _, _, kind, payload = heapq.heappop(heap)
+                if kind == "arrival":
+                    m = self._meta[payload]
+                    w = min(workers, key=lambda k: (backlog(k), k.wid))
+                    w.waiting.append(m)
+                    log(now, "arrival", m.request_id, w.wid)
+                    if cfg.plane != "cost_only":
+                        self._admit_latent(w, m, index[m.request_id])
+                else:
+                    w = workers[payload]
+                    finish(w, now)
+                if w not in touched:
+                    touched.append(w)
+            for w in sorted(touched, key=lambda k: k.wid):
+                if not w.busy:
+                    tick(w, now)
+
+        return RunResult(events, completions, self._summary(trace, completions, workers), final)
+
+    def _summary(self, trace, completions, workers) -> dict:
+        """engine.py:252-280."""
+        met = sum(1 for c in completions if c["met_slo"])
+        fin = sorted(c["latency_ms"] for c in completions if not c["discarded"])
+        horizon = max([c["finish_ms"] for c in completions] + [r.arrival_ms for r in trace])
+        out = {
+            "n_requests": len(trace),
+            "n_completed": len(fin),
+            "n_discarded": len(completions) - len(fin),
+            "n_met_slo": met,
+            "slo_attainment": met / len(trace),
+            "goodput_rps": 1000.0 * met / horizon if horizon > 0 else 0.0,
+            "mean_latency_ms": sum(fin) / len(fin) if fin else 0.0,
+            "p95_latency_ms": fin[int(0.95 * (len(fin) - 1))] if fin else 0.0,
+            "makespan_ms": horizon,
+            "steps_run": sum(w.steps_run for w in workers),
+            "skipped_patches": self._skipped,
+            "computed_patches": self._computed if self.cfg.plane != "cost_only" else 0,
+        }
+        if self.cfg.plane != "cost_only" and self.cfg.use_cache:
+            agg: dict = {}
+            for w in workers:
+                for k, v in w.cache.stats.as_dict().items():
+                    agg[k] = agg.get(k, 0) + v
+            out["cache"] = agg
+        if self.cfg.plane != "cost_only":
+            ms = [x for w in workers for x in w.step_ms]
+            out["device_step_ms_mean"] = float(np.mean(ms)) if ms else 0.0
+        return out
+
+
+# --------------------------------------------------------- calibration
+
+
+def measure_step_ms(model_cfg, weights, comps: Sequence[dict], patch_size: int = 32, reps: int = 3,
+                    use_cache: bool = False, seed: int = 0) -> list[tuple[dict, float]]:
+    """Measured device time (ms, median of `reps` after one warm-up) of one denoising
+    step for each composition, through the same call the wall plane makes."""
+    import torch
+
+    from ._dev import require_cuda
+    from .csp import reassemble, split
+    from .engine_step import numeric_step
+    dev = require_cuda()
+    out = []
+    for comp in comps:
+        reqs = []
+        for cls in CLASS_ORDER:
+            for j in range(comp.get(cls, 0)):
+                d = STANDARD_CLASSES[cls].latent
+                x = np.random.default_rng([seed, len(reqs)]).normal(size=(model_cfg.channels, d, d))
+                reqs.append((f"{cls}{j}", torch.as_tensor(x, dtype=torch.float32, device=dev)))
+        times = []
+        for rep in range(reps + 1):
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0.record()
+            b = split(reqs, patch_size=patch_size)
+            bias = torch.zeros((b.n_requests, model_cfg.channels), dtype=torch.float32, device=dev)
+            rates = torch.full((b.n_requests,), 0.1, dtype=torch.float32, device=dev)
+            new, _ = numeric_step(b, weights, None, bias, rates)
+            reassemble(b, new)
+            t1.record()
+            t1.synchronize()
+            if rep:
+                times.append(t0.elapsed_time(t1))
+        out.append((dict(comp), float(np.median(times))))
+    return out
+
+
+CALIBRATION_COMPS = ({"low": 1}, {"med": 1}, {"high": 1}, {"low": 4, "med": 4, "high": 4},
+                     {"low": 2, "high": 2}, {"med": 3}, {"low": 6}, {"high": 4}, {"low": 1, "med": 1, "high": 1})
+
+
+def slo_run(model_cfg, weights, n_requests: int = 64, load: float = 0.9, steps: int = 50, seed: int = 0,
+            use_cache: bool = True, policy: str = "slo_aware", max_active: int = 12, slo_scale: float = 3.0,
+            calib_reps: int = 3, rank: int = 0, world: int = 1, share=None, gather=None) -> dict:
+    """SLO attainment of the B200 path in the wall plane.
+
+    1. measure one-step device times of CALIBRATION_COMPS and fit the cost model
+       (rank 0's fit is shared with every rank through `share`);
+    2. draw a trace whose SLO budgets are slo_scale x the fitted standalone
+       latency (workload.py:74) at `load` x the fitted capacity of `world` GPUs
+       serving full 12-request mixed batches without the cache;
+    3. dispatch requests to GPUs lowest-outstanding-work first (engine.py:228),
+       decided on the fitted model (a cost_only run with `world` workers, the
+       same on every rank), then each rank serves its requests with the
+       SLO-aware scheduler, every step run and timed on its device; completions
+       are pooled through `gather`.
+    """
+    samples = measure_step_ms(model_cfg, weights, CALIBRATION_COMPS, reps=calib_reps)
+    fit = fit_cost_model(samples)
+    if share is not None:
+        fit = share(fit)
+    full = {"low": 4, "med": 4, "high": 4}
+    capacity_rps = world * 12 * 1000.0 / (steps * step_latency(full, fit))
+    qps = load * capacity_rps
+    wc = WorkloadConfig(seed=seed, qps=qps, n_requests=n_requests, steps=steps, slo_scale=slo_scale)
+    trace = generate_trace(wc, fit)
+    sched = SchedulerConfig(policy=policy, max_active=max_active, cost=fit)
+    mine = trace
+    if world > 1:
+        plan = Engine(EngineConfig(plane="cost_only", n_workers=world, total_steps=steps, cost=fit,
+                                   scheduler=sched)).run(trace)
+        owner = {e["request_id"]: e["worker"] for e in plan.events if e["kind"] == "arrival"}
+        mine = [r for r in trace if owner[r.request_id] == rank]
+    ec = EngineConfig(plane="wall", total_steps=steps, use_cache=use_cache, cost=fit, model=model_cfg,
+                      scheduler=sched)
+    res = Engine(ec, weights=weights).run(mine) if mine else None
+    local = {"completions": res.completions if res else [], "steps_run": res.summary["steps_run"] if res else 0,
+             "skipped": res.summary["skipped_patches"] if res else 0,
+             "computed": res.summary["computed_patches"] if res else 0,
+             "step_ms": res.summary["device_step_ms_mean"] if res else 0.0}
+    parts = gather(local) if gather is not None else [local]
+    comp = [c for p in parts for c in p["completions"]]
+    met = sum(1 for c in comp if c["met_slo"])
+    fin = sorted(c["latency_ms"] for c in comp if not c["discarded"])
+    horizon = max([c["finish_ms"] for c in comp] + [r.arrival_ms for r in trace])
+    rel = [abs(step_latency(c, fit) - ms) / ms for c, ms in samples]
+    return {
+        "slo_attainment": met / len(trace), "goodput_rps": 1000.0 * met / horizon, "qps": qps, "load": load,
+        "n_gpus": world, "n_requests": n_requests, "steps": steps, "policy": policy, "max_active": max_active,
+        "use_cache": use_cache, "slo_scale": slo_scale, "n_met_slo": met,
+        "n_discarded": sum(1 for c in comp if c["discarded"]),
+        "mean_latency_ms": float(np.mean(fin)) if fin else 0.0,
+        "p95_latency_ms": fin[int(0.95 * (len(fin) - 1))] if fin else 0.0, "makespan_ms": horizon,
+        "steps_run": sum(p["steps_run"] for p in parts),
+        "device_step_ms_mean": float(np.mean([p["step_ms"] for p in parts if p["steps_run"]] or [0.0])),
+        "skipped_patches": sum(p["skipped"] for p in parts), "computed_patches": sum(p["computed"] for p in parts),
+        "fitted_cost": {k: getattr(fit, k) for k in ("c_step_fixed", "c_res_overhead", "c_patch", "c_attn_coeff")},
+        "fit_mean_rel_err": float(np.mean(rel)),
+        "calibration": [{"comp": c, "ms": round(ms, 4)} for c, ms in samples],
+    }

@@ -1,0 +1,113 @@
+"""Serving plane (serving.py) against the reference's own outputs.
+
+Golden file: tests/golden/serving.json, written by make_golden_serving.py from
+the real reference (workload.py, latency.py, scheduler.py, engine.py).  The
+cost_only plane must reproduce the reference's traces, event logs,
+completions and summaries EXACTLY; the GPU numeric plane must reproduce the
+event log exactly and the final latents within the north-star tolerance.
+"""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2501_09253_b200 import serving as S
+
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+@pytest.fixture(scope="module")
+def gold():
+    with open(GOLD / "serving.json") as f:
+        return json.load(f)
+
+
+def test_cost_model_kats(gold):
+    for c in gold["comps"]:
+        assert S.step_latency(c["comp"]) == c["step_ms"]
+        for cls, v in c["standalone"].items():
+            assert S.standalone_latency(cls, 50) == v
+
+
+def _run_cost(r):
+    wc = S.WorkloadConfig(steps=r["steps"], **r["workload"])
+    trace = S.generate_trace(wc)
+    ec = S.EngineConfig(plane="cost_only", n_workers=r["workers"], total_steps=r["steps"],
+                        scheduler=S.SchedulerConfig(policy=r["policy"], max_active=r["max_active"]))
+    return trace, S.Engine(ec).run(trace)
+
+
+@pytest.mark.parametrize("i", range(6))
+def test_cost_only_plane_matches_reference(gold, i):
+    r = gold["runs"][i]
+    trace, res = _run_cost(r)
+    assert [vars(t) for t in trace] == r["trace"]
+    assert res.events == r["events"]
+    assert res.completions == r["completions"]
+    assert res.summary == r["summary"]
+
+
+def test_trace_roundtrip(tmp_path):
+    rows = S.generate_trace(S.WorkloadConfig(seed=3, n_requests=10))
+    p = tmp_path / "t.jsonl"
+    S.write_trace(rows, p)
+    assert S.read_trace(p) == rows
+    p.write_text('{"request_id": "a"}\n')
+    with pytest.raises(S.InputError):
+        S.read_trace(p)
+
+
+def test_input_errors():
+    with pytest.raises(S.InputError):
+        S.WorkloadConfig(qps=0)
+    with pytest.raises(S.InputError):
+        S.SchedulerConfig(policy="lifo")
+    with pytest.raises(S.InputError):
+        S.EngineConfig(plane="gpu")
+    with pytest.raises(S.InputError):
+        S.step_latency({})
+    with pytest.raises(S.InputError):
+        S.Engine().run([])
+
+
+def test_fit_cost_model_recovers_constants():
+    true = S.CostModelParams(c_step_fixed=1.5, c_res_overhead=0.2, c_patch=0.004, c_attn_coeff=3e-8)
+    samples = [(c, S.step_latency(c, true)) for c in S.CALIBRATION_COMPS]
+    fit = S.fit_cost_model(samples)
+    for k in ("c_step_fixed", "c_res_overhead", "c_patch", "c_attn_coeff"):
+        assert getattr(fit, k) == pytest.approx(getattr(true, k), rel=1e-6, abs=1e-9)
+
+
+@pytest.mark.gpu
+def test_numeric_plane_matches_reference(gold):
+    from paper_2501_09253_b200.model import ModelConfig
+    g = gold["numeric"]
+    wc = S.WorkloadConfig(**g["config"]["workload"])
+    trace = S.generate_trace(wc)
+    assert [vars(t) for t in trace] == g["trace"]
+    ec = S.EngineConfig(plane="numeric", total_steps=wc.steps, model=ModelConfig(**g["config"]["model"]))
+    res = S.Engine(ec).run(trace)
+    assert res.events == g["events"]
+    want = dict(g["summary"])
+    got = {k: v for k, v in res.summary.items() if k in want}
+    assert got == want  # includes the cache counters: skip masks are bit-exact
+    lat = np.load(GOLD / "serving_numeric.npz")
+    for rid in lat.files:
+        d = np.abs(res.latents[rid].double().cpu().numpy() - lat[rid]).max()
+        assert d <= 1e-2, (rid, d)
+
+
+@pytest.mark.gpu
+def test_wall_plane_runs_on_device():
+    from paper_2501_09253_b200.model import ModelConfig
+    mc = ModelConfig(arch="unet_like", channels=64, hidden=128, n_blocks=2, groups=8)
+    wc = S.WorkloadConfig(seed=1, qps=50.0, n_requests=6, steps=4)
+    ec = S.EngineConfig(plane="wall", total_steps=4, model=mc)
+    res = S.Engine(ec).run(S.generate_trace(wc))
+    s = res.summary
+    assert s["n_completed"] + s["n_discarded"] == 6
+    assert s["device_step_ms_mean"] > 0
+    # the clock advanced by measured device time, not the analytic model (~60 ms a step)
+    assert s["makespan_ms"] < 6 * 4 * 60.0
