@@ -107,6 +107,26 @@ class AnalyticPredictor:
         return step_latency(comp, self.cost_params)
 
 
+class AdaptivePredictor(AnalyticPredictor):
+    """Analytic model x an EWMA of measured / predicted step time (wall plane).
+
+    The analytic model prices a step without the patch cache; once the cache
+    is warm most patch-blocks are skipped and steps run several times faster.
+    The engine reports every measured step (`observe`), so admission and
+    time-out decisions track the pace the GPU actually delivers."""
+
+    def __init__(self, p: CostModelParams = DEFAULT_COST, alpha: float = 0.2):
+        super().__init__(p)
+        self.alpha, self.ratio = alpha, 1.0
+
+    def predict_step_latency(self, comp: dict) -> float:
+        return self.ratio * step_latency(comp, self.cost_params)
+
+    def observe(self, comp: dict, measured_ms: float) -> None:
+        r = measured_ms / step_latency(comp, self.cost_params)
+        self.ratio = (1.0 - self.alpha) * self.ratio + self.alpha * r
+
+
 def fit_cost_model(samples: Sequence[tuple[dict, float]], base: CostModelParams = DEFAULT_COST) -> CostModelParams:
     """Least-squares fit of (c_step_fixed, c_res_overhead, c_patch, c_attn_coeff) to
     measured (composition, step ms) pairs, keeping the exponent and block count.
@@ -499,6 +519,9 @@ class Engine:
             else:
                 dt_dev = self._compute_step(w)
                 w.step_ms.append(dt_dev)
+                observe = getattr(self.scheduler.predictor, "observe", None)
+                if observe is not None and cfg.plane == "wall":
+                    observe(composition(w.active), dt_dev)
                 dt = dt_dev if cfg.plane == "wall" else step_latency(composition(w.active), cfg.cost)
             push(now + dt, "step_end", w.wid)
 
@@ -630,7 +653,8 @@ CALIBRATION_COMPS = ({"low": 1}, {"med": 1}, {"high": 1}, {"low": 4, "med": 4, "
 
 def slo_run(model_cfg, weights, n_requests: int = 64, load: float = 0.9, steps: int = 50, seed: int = 0,
             use_cache: bool = True, policy: str = "slo_aware", max_active: int = 12, slo_scale: float = 3.0,
-            calib_reps: int = 3, rank: int = 0, world: int = 1, share=None, gather=None) -> dict:
+            calib_reps: int = 3, rank: int = 0, world: int = 1, share=None, gather=None,
+            adaptive: bool = True) -> dict:
     """SLO attainment of the B200 path in the wall plane.
 
     1. measure one-step device times of CALIBRATION_COMPS and fit the cost model
@@ -642,7 +666,8 @@ def slo_run(model_cfg, weights, n_requests: int = 64, load: float = 0.9, steps: 
        decided on the fitted model (a cost_only run with `world` workers, the
        same on every rank), then each rank serves its requests with the
        SLO-aware scheduler, every step run and timed on its device; completions
-       are pooled through `gather`.
+       are pooled through `gather`.  With `adaptive` the scheduler's predictor
+       follows the measured pace (AdaptivePredictor); budgets stay on the fit.
     """
     samples = measure_step_ms(model_cfg, weights, CALIBRATION_COMPS, reps=calib_reps)
     fit = fit_cost_model(samples)
@@ -662,7 +687,8 @@ def slo_run(model_cfg, weights, n_requests: int = 64, load: float = 0.9, steps: 
         mine = [r for r in trace if owner[r.request_id] == rank]
     ec = EngineConfig(plane="wall", total_steps=steps, use_cache=use_cache, cost=fit, model=model_cfg,
                       scheduler=sched)
-    res = Engine(ec, weights=weights).run(mine) if mine else None
+    pred = AdaptivePredictor(fit) if adaptive else AnalyticPredictor(fit)
+    res = Engine(ec, predictor=pred, weights=weights).run(mine) if mine else None
     local = {"completions": res.completions if res else [], "steps_run": res.summary["steps_run"] if res else 0,
              "skipped": res.summary["skipped_patches"] if res else 0,
              "computed": res.summary["computed_patches"] if res else 0,
@@ -677,6 +703,7 @@ def slo_run(model_cfg, weights, n_requests: int = 64, load: float = 0.9, steps: 
         "slo_attainment": met / len(trace), "goodput_rps": 1000.0 * met / horizon, "qps": qps, "load": load,
         "n_gpus": world, "n_requests": n_requests, "steps": steps, "policy": policy, "max_active": max_active,
         "use_cache": use_cache, "slo_scale": slo_scale, "n_met_slo": met,
+        "predictor": "fitted analytic x EWMA(measured/predicted)" if adaptive else "fitted analytic",
         "n_discarded": sum(1 for c in comp if c["discarded"]),
         "mean_latency_ms": float(np.mean(fin)) if fin else 0.0,
         "p95_latency_ms": fin[int(0.95 * (len(fin) - 1))] if fin else 0.0, "makespan_ms": horizon,
