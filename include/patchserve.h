@@ -127,6 +127,8 @@ typedef struct ps_gemm_args {
   unsigned long long* dbg;                /* optional device counters [8] of per-role wait cycles, or NULL */
   const int32_t* m_map;                   /* optional DEVICE list of 128-row tiles to compute (compaction) */
   int m_count;                            /* entries in m_map */
+  int cta_pair;                           /* 0 auto, 1 single-CTA 128-row tiles, 2 CTA-pair 256-row tiles
+                                             (tcgen05 cta_group::2) */
 } ps_gemm_args;
 int ps_gemm(void* stream, const ps_gemm_args* args);
 

@@ -33,6 +33,7 @@ class GemmArgs(C.Structure):
         ("epi", C.c_int), ("out", p), ("ldo", C.c_int), ("out2", p), ("ldo2", C.c_int), ("n_split", C.c_int),
         ("resid", p), ("c_real", C.c_int),
         ("bn", C.c_int), ("out_tiled", C.c_int), ("dbg", p), ("m_map", p), ("m_count", C.c_int),
+        ("cta_pair", C.c_int),
     ]
 
 

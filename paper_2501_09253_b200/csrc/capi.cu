@@ -3,6 +3,7 @@
 // attention entry points.
 #include <cudaTypedefs.h>
 #include <stdarg.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -287,6 +288,12 @@ int ps_gemm(void* stream, const ps_gemm_args* a) {
   if (a->N % 16) return set_error(PS_ERR_INPUT, "gemm: N (%d) must be a multiple of 16", a->N);
   const int bn = a->bn ? a->bn : gemm_pick_bn(a->N, a->K);
   const int mma_n = bn <= 256 ? bn : bn / 2;
+  // CTA-pair tiles (cta_group::2) unless asked otherwise or the problem is too small to fill the SMs in pairs
+  const int m_tiles = a->m_map ? a->m_count : (a->M + 127) / 128;
+  // auto = single-CTA tiles: measured faster than pairs on every config-2 GEMM except K = 2880 (+4%)
+  static const int env_pair = getenv("PS_GEMM_PAIR") ? atoi(getenv("PS_GEMM_PAIR")) : 0;
+  const int want = a->cta_pair ? a->cta_pair : env_pair;
+  const int pair = want == 2 && m_tiles >= 2 ? 1 : 0;
   CUtensorMap ta, tb;
   GemmParams p{};
   p.M = a->M;
@@ -322,7 +329,7 @@ int ps_gemm(void* stream, const ps_gemm_args* a) {
     rc = make_tmap_2d(&ta, a->a, a->M, a->K, a->lda, 128);
   }
   if (rc) return rc;
-  rc = make_tmap_2d(&tb, a->b, a->N, a->K, a->K, mma_n);
+  rc = make_tmap_2d(&tb, a->b, a->N, a->K, a->K, pair ? mma_n / 2 : mma_n);
   if (rc) return rc;
   p.epi = a->epi;
   p.bias = a->bias;
@@ -338,11 +345,21 @@ int ps_gemm(void* stream, const ps_gemm_args* a) {
   p.dbg = a->dbg;
   p.m_map = a->m_map;
   p.m_count = a->m_map ? a->m_count : 0;
+  static const int epi_skip = getenv("PS_GEMM_EPI_SKIP") ? atoi(getenv("PS_GEMM_EPI_SKIP")) : 0;
+  p.epi_skip = epi_skip;
+  // defaults from tools/gemm_roles.py on config-2 shapes: splitting every tile's columns over both
+  // epilogue warpgroups drains accumulators sooner (QKV 127 -> 120 us); the L2 prefetch of residual
+  // rows by the TMA producer stalled it (FF2 + residual 223 -> 158 us without it)
+  static const int epi_split = getenv("PS_GEMM_EPI_SPLIT") ? atoi(getenv("PS_GEMM_EPI_SPLIT")) : 1;
+  static const int no_pf = getenv("PS_GEMM_NO_PF") ? atoi(getenv("PS_GEMM_NO_PF")) : 1;
+  p.epi_split = epi_split;
+  p.no_prefetch = no_pf;
   // channels-last outputs leave through TMA stores (32 rows x 16 columns per warp box)
   CUtensorMap tc;
   memset(&tc, 0, sizeof(tc));
   p.store_tma = 0;
-  if ((a->epi == EPI_STORE_CL || a->epi == EPI_GELU_CL || a->epi == EPI_SPLIT_VT) && a->ldo % 8 == 0) {
+  static const int no_tma_store = getenv("PS_GEMM_NO_TMA_STORE") ? atoi(getenv("PS_GEMM_NO_TMA_STORE")) : 0;
+  if (!no_tma_store && (a->epi == EPI_STORE_CL || a->epi == EPI_GELU_CL || a->epi == EPI_SPLIT_VT) && a->ldo % 8 == 0) {
     uint64_t dims[2], strides[1];
     if (a->out_tiled) {
       dims[0] = 64;
@@ -364,7 +381,7 @@ int ps_gemm(void* stream, const ps_gemm_args* a) {
     return set_error(PS_ERR_INPUT, "gemm: NCHW epilogue needs ps and 1 <= c_real <= N");
   if ((a->epi == EPI_STORE_CL || a->epi == EPI_GELU_CL) && (a->ldo < a->N || a->ldo % 8))
     return set_error(PS_ERR_INPUT, "gemm: ldo must be >= N and a multiple of 8");
-  return gemm_launch(ta, tb, tc, p, bn, (cudaStream_t)stream);
+  return gemm_launch(ta, tb, tc, p, bn, pair, (cudaStream_t)stream);
 }
 
 // ----------------------------------------------------------- attention

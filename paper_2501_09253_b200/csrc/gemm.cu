@@ -16,6 +16,13 @@
 // n-fastest order (CTAs running together share A tiles in L2).  The TMEM
 // accumulator is double-buffered (2 x BN columns), so the epilogue of tile i
 // overlaps the MMAs of tile i+1.
+// PAIR = true runs the same tile walk on CTA pairs (cluster of 2 on one TPC,
+// tcgen05 cta_group::2): a pair owns 256 x BN outputs, each CTA loads its own
+// 128 A rows and HALF of the B rows of every MMA, the leader CTA issues M = 256
+// MMAs whose accumulator rows land in each CTA's own TMEM, and MMA completions
+// are multicast to both CTAs.  Per SM this halves the B bytes TMA writes into
+// shared memory and the tensor core reads from it -- the limit of the 1-CTA
+// kernel (shared-memory bandwidth: ~200 B/clk of operand traffic for 128 B/clk).
 // Warp roles (384 threads): w0 TMA producer, w1 MMA issuer (one lane), w2 TMEM
 // allocator, w4..w11 epilogue (warp w reads TMEM lanes 32*(w%4)..+31, and half
 // of the tile's columns).
@@ -35,13 +42,14 @@ constexpr int GEMM_EPI_THREADS = 256;
 // BN <= 256: double-buffered accumulators (2*BN TMEM columns), one MMA per k-step.
 // BN == 320: single accumulator (long-K GEMMs: conv3, FF2), two N=160 MMAs per k-step,
 // so A is read once per 128-token tile.
-template <int BN>
+template <int BN, bool PAIR = false>
 struct GemmCfg {
   static constexpr int NBUF = BN <= 256 ? 2 : 1;
   static constexpr int MMA_N = BN <= 256 ? BN : BN / 2;
   static constexpr int N_MMA = BN / MMA_N;
+  static constexpr int B_ROWS = PAIR ? MMA_N / 2 : MMA_N;  // B rows of one MMA held by this CTA
   static constexpr int A_BYTES = GEMM_BM * 128;
-  static constexpr int B_BYTES = BN * 128;
+  static constexpr int B_BYTES = N_MMA * B_ROWS * 128;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (176 * 1024) / STAGE_BYTES > 8 ? 8 : (176 * 1024) / STAGE_BYTES;
   static constexpr int TMEM_COLS = NBUF * BN <= 128 ? 128 : NBUF * BN <= 256 ? 256 : 512;
@@ -50,6 +58,7 @@ struct GemmCfg {
   static constexpr int STAGE_TMA = 2 * 2 * GEMM_BM * 64;  // per warpgroup: two 128x32 bf16 store boxes
   static constexpr int SMEM = STAGES * STAGE_BYTES + STAGE_EPI + STAGE_TMA + 1024 /*align*/ + 256 /*barriers*/;
   static_assert(MMA_N % 16 == 0 && MMA_N >= 64 && MMA_N <= 256, "invalid UMMA N");
+  static_assert(B_ROWS % 8 == 0, "B half rows must be whole 128B-swizzle atoms");
   static_assert(BN % 32 == 0 && (BN / 2) % 32 == 0 || BN <= 256, "epilogue chunking");
 };
 
@@ -67,11 +76,11 @@ __device__ __forceinline__ void store16_cl(__nv_bfloat16* dst, const float* v) {
   reinterpret_cast<uint4*>(dst)[1] = w1;
 }
 
-template <int BN>
+template <int BN, bool PAIR>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, PAIR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* epi_stage = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
@@ -85,9 +94,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_n = (p.N + BN - 1) / BN;
   const int num_m = p.m_map ? p.m_count : (p.M + GEMM_BM - 1) / GEMM_BM;
-  const int n_tiles = num_m * num_n;
-  // logical -> physical 128-row tile (active-patch compaction)
-  auto phys_m = [&](int lm) { return p.m_map ? __ldg(p.m_map + lm) : lm; };
+  // PAIR: a work item is (pair of m tiles, n tile); CTA `rank` takes m tile 2*mp + rank
+  const uint32_t rank = PAIR ? cluster_rank() : 0;
+  const bool leader = rank == 0;
+  const int unit0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int unit_step = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int num_mu = PAIR ? (num_m + 1) / 2 : num_m;
+  const int n_tiles = num_mu * num_n;
+  const int m_oob = (p.M + GEMM_BM - 1) / GEMM_BM;  // a physical tile past the end: TMA zero-fills it
+  // logical -> physical 128-row tile (active-patch compaction); -1 = no tile (odd pair tail)
+  auto phys_m = [&](int lm) { return lm >= num_m ? -1 : p.m_map ? __ldg(p.m_map + lm) : lm; };
+  auto my_m = [&](int t) { return phys_m(PAIR ? 2 * (t / num_n) + (int)rank : t / num_n); };
   const int num_kb = p.K / GEMM_BK;
 
   if (warp == 0 && lane == 0) {
@@ -100,13 +117,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], Cfg::NBUF == 2 ? GEMM_EPI_THREADS / 2 : GEMM_EPI_THREADS);
+      const bool split = Cfg::NBUF == 1 || (p.epi_split && (BN / 2) % 32 == 0);
+      mbar_init(&acc_empty[b], (PAIR ? 2 : 1) * (split ? GEMM_EPI_THREADS : GEMM_EPI_THREADS / 2));
     }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  if (warp == 2) {
+    if (PAIR) tmem_alloc_2sm(tmem_slot, Cfg::TMEM_COLS);
+    else tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -128,15 +150,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       const int kcb = p.conv_cp / GEMM_BK;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const int m_tile = phys_m(t / num_n), n0 = (t % num_n) * BN;
+      for (int t = unit0; t < n_tiles; t += unit_step) {
+        const int mt = my_m(t);
+        const int m_tile = mt < 0 ? m_oob : mt, n0 = (t % num_n) * BN;
         int p0 = 0, y0 = 0;
         if (p.a_mode == A_CONV3) {
           p0 = (m_tile / p.conv_tpp) * p.conv_np;
           y0 = (m_tile % p.conv_tpp) * p.conv_rows;
         }
         // warm L2 with this tile's residual rows (NCHW, 128 contiguous pixels per channel)
-        const bool pf = p.epi == EPI_RESID_NCHW && p.resid != nullptr && p.hw >= GEMM_BM && n0 < p.c_real;
+        const bool pf = !p.no_prefetch && mt >= 0 && p.epi == EPI_RESID_NCHW && p.resid != nullptr && p.hw >= GEMM_BM && n0 < p.c_real;
         const int tok0 = m_tile * GEMM_BM;
         const int cpk = (p.c_real + num_kb - 1) / num_kb;
         for (int kb = 0; kb < num_kb; ++kb) {
@@ -148,30 +171,48 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           timed_wait(&empty[stage], phase ^ 1, t_wait);
           uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
           uint8_t* sb = sa + Cfg::A_BYTES;
-          mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
-          if (p.a_mode == A_CONV3) {
-            const int tap = kb / kcb, cb = kb % kcb;
-            tma_load_4d(sa, &tmA, &full[stage], cb * GEMM_BK, tap % 3, y0 + tap / 3, p0);
-          } else if (p.a_mode == A_TILED) {
-            // tile-major A: the (m_tile, kb) box is one contiguous 16 KB block
-            tma_load_2d(sa, &tmA, &full[stage], 0, (m_tile * num_kb + kb) * GEMM_BM);
-          } else {
-            tma_load_2d(sa, &tmA, &full[stage], kb * GEMM_BK, m_tile * GEMM_BM);
-          }
+          if (PAIR) {
+            // both CTAs' bytes complete on the leader's barrier
+            const uint32_t fb = mapa_shared(&full[stage], 0);
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+            if (p.a_mode == A_CONV3) {
+              const int tap = kb / kcb, cb = kb % kcb;
+              tma_load_4d_2sm(sa, &tmA, fb, cb * GEMM_BK, tap % 3, y0 + tap / 3, p0);
+            } else if (p.a_mode == A_TILED) {
+              tma_load_2d_2sm(sa, &tmA, fb, 0, (m_tile * num_kb + kb) * GEMM_BM);
+            } else {
+              tma_load_2d_2sm(sa, &tmA, fb, kb * GEMM_BK, m_tile * GEMM_BM);
+            }
 #pragma unroll
-          for (int j = 0; j < Cfg::N_MMA; ++j)
-            tma_load_2d(sb + j * Cfg::MMA_N * 128, &tmB, &full[stage], kb * GEMM_BK, n0 + j * Cfg::MMA_N);
+            for (int j = 0; j < Cfg::N_MMA; ++j)
+              tma_load_2d_2sm(sb + j * Cfg::B_ROWS * 128, &tmB, fb, kb * GEMM_BK,
+                              n0 + j * Cfg::MMA_N + (int)rank * Cfg::B_ROWS);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+            if (p.a_mode == A_CONV3) {
+              const int tap = kb / kcb, cb = kb % kcb;
+              tma_load_4d(sa, &tmA, &full[stage], cb * GEMM_BK, tap % 3, y0 + tap / 3, p0);
+            } else if (p.a_mode == A_TILED) {
+              // tile-major A: the (m_tile, kb) box is one contiguous 16 KB block
+              tma_load_2d(sa, &tmA, &full[stage], 0, (m_tile * num_kb + kb) * GEMM_BM);
+            } else {
+              tma_load_2d(sa, &tmA, &full[stage], kb * GEMM_BK, m_tile * GEMM_BM);
+            }
+#pragma unroll
+            for (int j = 0; j < Cfg::N_MMA; ++j)
+              tma_load_2d(sb + j * Cfg::MMA_N * 128, &tmB, &full[stage], kb * GEMM_BK, n0 + j * Cfg::MMA_N);
+          }
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && leader) {
     // -------------------------------------------------------------- MMA issuer
-    constexpr uint32_t idesc = idesc_bf16_f32(GEMM_BM, Cfg::MMA_N);
+    constexpr uint32_t idesc = idesc_bf16_f32(PAIR ? 2 * GEMM_BM : GEMM_BM, Cfg::MMA_N);
     int stage = 0;
     uint32_t phase = 0;
     int li = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++li) {
+    for (int t = unit0; t < n_tiles; t += unit_step, ++li) {
       const int buf = li % Cfg::NBUF;
       const int use = li / Cfg::NBUF;
       timed_wait(&acc_empty[buf], (use & 1) ^ 1, t_wait2);
@@ -186,11 +227,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < GEMM_BK / 16; ++k)
 #pragma unroll
-            for (int j = 0; j < Cfg::N_MMA; ++j)
-              mma_bf16_ss(d + j * Cfg::MMA_N, sdesc_sw128(sa + k * 32),
-                          sdesc_sw128(sb + j * Cfg::MMA_N * 128 + k * 32), idesc, (kb | k) != 0);
-          mma_commit(&empty[stage]);
-          if (kb == num_kb - 1) mma_commit(&acc_full[buf]);
+            for (int j = 0; j < Cfg::N_MMA; ++j) {
+              if (PAIR)
+                mma_bf16_ss_2sm(d + j * Cfg::MMA_N, sdesc_sw128(sa + k * 32),
+                                sdesc_sw128(sb + j * Cfg::B_ROWS * 128 + k * 32), idesc, (kb | k) != 0);
+              else
+                mma_bf16_ss(d + j * Cfg::MMA_N, sdesc_sw128(sa + k * 32),
+                            sdesc_sw128(sb + j * Cfg::MMA_N * 128 + k * 32), idesc, (kb | k) != 0);
+            }
+          if (PAIR) {
+            mma_commit_2sm(&empty[stage], 0x3);
+            if (kb == num_kb - 1) mma_commit_2sm(&acc_full[buf], 0x3);
+          } else {
+            mma_commit(&empty[stage]);
+            if (kb == num_kb - 1) mma_commit(&acc_full[buf]);
+          }
         }
         __syncwarp();
         if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
@@ -209,20 +260,28 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int wq = warp & 3;         // TMEM lane quadrant
     const int row = wq * 32 + lane;  // tile row = TMEM lane
     const int bar_id = 1 + wg;
-    const bool leader = (warp & 3) == 0 && lane == 0;
+    const bool wg_leader = (warp & 3) == 0 && lane == 0;
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     uint8_t* box_base = tma_stage + wg * 2 * (GEMM_BM * 64);  // two 8 KB boxes per warpgroup
     float* st = epi_stage + wg * 16 * GEMM_BM;                 // [16][128] fp32 transpose tile
     const int ci = row >> 3, seg = row & 7;                    // transposed role
-    const int c_lo = Cfg::NBUF == 1 ? wg * (BN / 2) : 0;
-    const int c_hi = Cfg::NBUF == 1 ? c_lo + BN / 2 : BN;
+    // NBUF == 1 or epi_split: the two warpgroups split every tile's columns (each tile's
+    // accumulator drains in half the time); else warpgroup g takes the tiles of buffer g
+    const bool split = Cfg::NBUF == 1 || (p.epi_split && (BN / 2) % 32 == 0);
+    const int c_lo = split ? wg * (BN / 2) : 0;
+    const int c_hi = split ? c_lo + BN / 2 : BN;
     int n_store = 0;
     int li = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++li) {
+    // the accumulator buffer is released on the leader CTA's barrier (the MMA issuer's)
+    auto release = [&](int b) {
+      if (PAIR) mbar_arrive_cluster(mapa_shared(&acc_empty[b], 0));
+      else mbar_arrive(&acc_empty[b]);
+    };
+    for (int t = unit0; t < n_tiles; t += unit_step, ++li) {
       const int buf = li % Cfg::NBUF;
       const int use = li / Cfg::NBUF;
-      if (Cfg::NBUF == 2 && buf != wg) continue;
-      const int m_tile = phys_m(t / num_n), n_tile = t % num_n;
+      if (!split && buf != wg) continue;
+      const int m_tile = my_m(t), n_tile = t % num_n;
       const int m = m_tile * GEMM_BM + row;
       const bool row_ok = m < p.M;
       const bool tile_full = (m_tile + 1) * GEMM_BM <= p.M;
@@ -235,18 +294,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const bool vec_vt = p.epi == EPI_SPLIT_VT && (p.ldo2 % 8) == 0 && tile_full;
       timed_wait(&acc_full[buf], use & 1, t_wait);
       tc_fence_after();
-      if (n_tile * BN + c_lo >= p.N) {  // no columns of this tile for this warpgroup
+      if (m_tile < 0 || n_tile * BN + c_lo >= p.N) {  // no rows / columns of this tile here
         tc_fence_before();
-        mbar_arrive(&acc_empty[buf]);
+        release(buf);
         continue;
       }
-#pragma unroll 1
-      for (int c = c_lo; c < c_hi; c += 32) {
-        const int nb = n_tile * BN + c;
-        if (nb >= p.N) break;  // uniform across the warpgroup
-        uint32_t r[32];
-        PS_TMEM_LD32(tmem + lane_base + buf * BN + c, r);
-        float bv[32];
+      auto load_bias = [&](float (&bv)[32], int nb) {
         if (p.bias != nullptr) {
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -257,12 +310,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) bv[i] = 0.f;
         }
-        tmem_ld_wait();
-        if (c + 32 >= c_hi || nb + 32 >= p.N) {
-          // last chunk of this tile for this warpgroup: hand the accumulator back early
-          tc_fence_before();
-          mbar_arrive(&acc_empty[buf]);
-        }
+      };
+      // chunk body: bias (+GELU) and store of 32 accumulator columns [c, c + 32) held in r
+      auto body = [&](const uint32_t (&r)[32], const float (&bv)[32], int c) {
+        const int nb = n_tile * BN + c;
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) + bv[i];
@@ -270,7 +321,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                             (p.epi == EPI_STORE_CL || p.epi == EPI_GELU_CL || (p.epi == EPI_SPLIT_VT && nb < p.n_split));
         if (cl_tma) {
           uint8_t* box = box_base + (n_store & 1) * (GEMM_BM * 64);
-          if (leader) bulk_wait_read<1>();  // the TMA store that last used this box has read it
+          if (wg_leader) bulk_wait_read<1>();  // the TMA store that last used this box has read it
           named_bar_sync(bar_id, 128);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -285,7 +336,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
           fence_proxy_async();
           named_bar_sync(bar_id, 128);
-          if (leader) {
+          if (wg_leader) {
             if (p.out_tiled)
               tma_store_2d(&tmC, box, nb & 63, (m_tile * (p.ldo / 64) + nb / 64) * GEMM_BM);
             else
@@ -293,7 +344,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             bulk_commit();
           }
           ++n_store;
-          continue;
+          return;
         }
         if (p.epi == EPI_GELU_CL) {
 #pragma unroll
@@ -342,7 +393,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               store16_cl((tr_vt ? p.out2 : p.out) + off_v, o);
             }
             named_bar_sync(bar_id, 128);
-            continue;
+            continue;  // next 16-column piece
           }
           if (!row_ok) continue;
           if (p.epi == EPI_STORE_CL || p.epi == EPI_GELU_CL || p.epi == EPI_SPLIT_VT) {
@@ -369,6 +420,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
           }
         }
+      };
+      const int c_end = min(c_hi, p.N - n_tile * BN);  // columns of this tile for this warpgroup
+#pragma unroll 1
+      for (int c = c_lo; c < c_end; c += 32) {
+        uint32_t r[32];
+        PS_TMEM_LD32(tmem + lane_base + buf * BN + c, r);
+        float bv[32];
+        load_bias(bv, n_tile * BN + c);
+        tmem_ld_wait();
+        reg_fence32(r);
+        if (c + 32 >= c_end) {
+          // last chunk of this tile for this warpgroup: hand the accumulator back early
+          tc_fence_before();
+          release(buf);
+        }
+        if (!p.epi_skip) body(r, bv, c);
       }
     }
   }
@@ -380,9 +447,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (warp == 4) { atomicAdd(p.dbg + 5, t_wait); atomicAdd(p.dbg + 6, tot); }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem, Cfg::TMEM_COLS);
+  if (warp == 2) {
+    if (PAIR) tmem_dealloc_2sm(tmem, Cfg::TMEM_COLS);
+    else tmem_dealloc(tmem, Cfg::TMEM_COLS);
+  }
 }
 
 static int num_sms() {
@@ -396,34 +467,57 @@ static int num_sms() {
   return n;
 }
 
-template <int BN>
+template <int BN, bool PAIR>
 static int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const GemmParams& p,
                      cudaStream_t st) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, PAIR>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    cudaFuncSetAttribute(gemm_tc_kernel<BN, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr = true;
   }
-  const int tiles = (p.m_map ? p.m_count : (p.M + GEMM_BM - 1) / GEMM_BM) * ((p.N + BN - 1) / BN);
-  if (tiles == 0) return PS_OK;
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  gemm_tc_kernel<BN><<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(a, b, c, p);
+  const int num_m = p.m_map ? p.m_count : (p.M + GEMM_BM - 1) / GEMM_BM;
+  const int units = (PAIR ? (num_m + 1) / 2 : num_m) * ((p.N + BN - 1) / BN);
+  if (units == 0) return PS_OK;
+  const int per_unit = PAIR ? 2 : 1;
+  const int max_units = num_sms() / per_unit;
+  const int grid = (units < max_units ? units : max_units) * per_unit;
+  if (!PAIR) {
+    gemm_tc_kernel<BN, false><<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(a, b, c, p);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(GEMM_THREADS);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, true>, a, b, c, p);
+  }
   count_launch();
-  return check_launch("gemm_tc");
+  return check_launch(PAIR ? "gemm_tc_pair" : "gemm_tc");
 }
 
 int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const GemmParams& p, int bn,
-                cudaStream_t st) {
+                int pair, cudaStream_t st) {
+#define PS_GEMM_CASE(N)                                                           \
+  case N:                                                                         \
+    return pair ? launch_bn<N, true>(a, b, c, p, st) : launch_bn<N, false>(a, b, c, p, st);
   switch (bn) {
-    case 64: return launch_bn<64>(a, b, c, p, st);
-    case 128: return launch_bn<128>(a, b, c, p, st);
-    case 160: return launch_bn<160>(a, b, c, p, st);
-    case 192: return launch_bn<192>(a, b, c, p, st);
-    case 256: return launch_bn<256>(a, b, c, p, st);
-    case 320: return launch_bn<320>(a, b, c, p, st);
+    PS_GEMM_CASE(64)
+    PS_GEMM_CASE(128)
+    PS_GEMM_CASE(160)
+    PS_GEMM_CASE(192)
+    PS_GEMM_CASE(256)
+    PS_GEMM_CASE(320)
     default: return set_error(PS_ERR_INPUT, "unsupported GEMM tile N %d", bn);
   }
+#undef PS_GEMM_CASE
 }
 
 int gemm_pick_bn(int n, int k) {

@@ -30,13 +30,16 @@ struct GemmParams {
   int store_tma;            // channels-last stores through the tmC tensor map
   const int* m_map;         // optional: physical 128-row tile of each logical tile (compaction)
   int m_count;              // number of mapped tiles when m_map != null
+  int epi_skip;             // profiling only (PS_GEMM_EPI_SKIP=1): drain accumulators without storing
+  int epi_split;            // both epilogue warpgroups split each tile's columns (else alternate tiles)
+  int no_prefetch;          // skip the L2 prefetch of residual rows
 };
 
 int set_error(int code, const char* fmt, ...);
 int check_launch(const char* what);
 void count_launch();
 int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const GemmParams& p, int bn,
-                cudaStream_t st);
+                int pair, cudaStream_t st);
 int gemm_pick_bn(int n, int k);
 // widest element span of `group` consecutive leaves of numpy's pairwise tree over n elements
 int64_t pairwise_max_span(int64_t n, int group);
