@@ -8,10 +8,17 @@
 // layer_norm (kernels.py:209-227) normalises every position over channels.
 // Here: per-(patch, group) (mean, M2) in fp32 from a CTA-local two-pass, pooled
 // per request with Chan's formula in fp64; halos are zero outside the image.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "ps_internal.h"
 
 namespace ps {
+
+static bool getenv_flag(const char* name) {
+  const char* v = getenv(name);
+  return v && atoi(v) != 0;
+}
 
 __device__ __forceinline__ float block_sum(float v, float* red) {
 #pragma unroll
@@ -29,8 +36,8 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // grid (P, G): partial mean / M2 over cg*hw contiguous elements.  The CTA's
 // slice is read once into registers (up to GN_REG 16-byte vectors per thread);
 // mean and then M2 are reduced from registers (two-pass numerics, one pass of HBM).
-constexpr int GN_REG = 8;
-__global__ void __launch_bounds__(256) gn_partials_kernel(const __nv_bfloat16* __restrict__ x, int C, int hw, int G,
+constexpr int GN_REG = 5;
+__global__ void __launch_bounds__(256, 4) gn_partials_kernel(const __nv_bfloat16* __restrict__ x, int C, int hw, int G,
                                                           const int32_t* __restrict__ plist,
                                                           float* __restrict__ partials) {
   __shared__ float red[32];
@@ -67,6 +74,27 @@ __global__ void __launch_bounds__(256) gn_partials_kernel(const __nv_bfloat16* _
         }
       }
     }
+  } else if ((n % 8 == 0) && (((uintptr_t)base & 15) == 0)) {
+    // slice larger than the register budget: two vectorised passes (the second hits L2)
+    const uint4* b4 = reinterpret_cast<const uint4*>(base);
+    const int64_t nv = n / 8;
+    float s = 0.f;
+    for (int64_t k = threadIdx.x; k < nv; k += blockDim.x) {
+      const uint4 r = __ldg(b4 + k);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) s += __low2float(h[e]) + __high2float(h[e]);
+    }
+    mean = block_sum(s, red) / (float)n;
+    for (int64_t k = threadIdx.x; k < nv; k += blockDim.x) {
+      const uint4 r = __ldg(b4 + k);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float a = __low2float(h[e]) - mean, b = __high2float(h[e]) - mean;
+        m2 += a * a + b * b;
+      }
+    }
   } else {
     float s = 0.f;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += bf(base[i]);
@@ -81,6 +109,91 @@ __global__ void __launch_bounds__(256) gn_partials_kernel(const __nv_bfloat16* _
     partials[((int64_t)p * G + g) * 2] = mean;
     partials[((int64_t)p * G + g) * 2 + 1] = m2;
   }
+}
+
+// Persistent, software-pipelined partials: CTA b walks slices s = b, b + grid, ... (slice =
+// one (patch, group) run of cg*hw contiguous bf16, <= 256*V vectors); the next slice's
+// 16-byte loads are in flight while the current one is reduced (two-pass from registers).
+template <int V>
+__device__ __forceinline__ void gn_load(const __nv_bfloat16* base, int nv, uint4 (&r)[V]) {
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int k = threadIdx.x + i * 256;
+    r[i] = k < nv ? __ldg(reinterpret_cast<const uint4*>(base) + k) : make_uint4(0, 0, 0, 0);
+  }
+}
+template <int V>
+__device__ __forceinline__ void gn_reduce(const uint4 (&r)[V], int nv, int64_t n, float* red, float* out) {
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r[i]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s += __low2float(h[k]) + __high2float(h[k]);
+  }
+  const float mean = block_sum(s, red) / (float)n;
+  float m2 = 0.f;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    if (threadIdx.x + i * 256 < nv) {
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r[i]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float a = __low2float(h[k]) - mean, b = __high2float(h[k]) - mean;
+        m2 += a * a + b * b;
+      }
+    }
+  }
+  m2 = block_sum(m2, red + 32);
+  if (threadIdx.x == 0) {
+    out[0] = mean;
+    out[1] = m2;
+  }
+}
+template <int V>
+__global__ void __launch_bounds__(256, 2) gn_partials_pipe_kernel(const __nv_bfloat16* __restrict__ x, int C, int hw,
+                                                                  int G, const int32_t* __restrict__ plist,
+                                                                  int n_slices, float* __restrict__ partials) {
+  __shared__ float red[64];
+  const int cg = C / G;
+  const int64_t n = (int64_t)cg * hw;
+  const int nv = (int)(n / 8);
+  auto slice_base = [&](int sl, int& p, int& g) {
+    p = plist ? __ldg(plist + sl / G) : sl / G;
+    g = sl % G;
+    return x + ((int64_t)p * C + (int64_t)g * cg) * hw;
+  };
+  uint4 ra[V], rb[V];
+  int s = blockIdx.x;
+  int pa, ga, pb, gb;
+  if (s < n_slices) gn_load<V>(slice_base(s, pa, ga), nv, ra);
+  for (; s < n_slices; s += 2 * gridDim.x) {
+    const int s2 = s + gridDim.x;
+    if (s2 < n_slices) gn_load<V>(slice_base(s2, pb, gb), nv, rb);
+    gn_reduce<V>(ra, nv, n, red, partials + ((int64_t)pa * G + ga) * 2);
+    if (s2 >= n_slices) break;
+    const int s3 = s2 + gridDim.x;
+    if (s3 < n_slices) gn_load<V>(slice_base(s3, pa, ga), nv, ra);
+    gn_reduce<V>(rb, nv, n, red, partials + ((int64_t)pb * G + gb) * 2);
+  }
+}
+
+// host: pipelined kernel when a slice fits 256*8 vectors and is 16-byte aligned, else the simple one
+static void launch_gn_partials(cudaStream_t st, const void* x, int P, int C, int hw, int G, const int32_t* plist,
+                               int n, float* partials) {
+  const int64_t elems = (int64_t)(C / G) * hw;
+  const int64_t nv = elems / 8;
+  const int n_slices = n * G;
+  int grid = 148 * 2;
+  if (grid > n_slices) grid = n_slices;
+  const auto xb = (const __nv_bfloat16*)x;
+  if (elems % 8 == 0 && nv <= 256 * 6 && getenv_flag("PS_GN_PIPE")) {
+    if (nv <= 256 * 2) gn_partials_pipe_kernel<2><<<grid, 256, 0, st>>>(xb, C, hw, G, plist, n_slices, partials);
+    else if (nv <= 256 * 4) gn_partials_pipe_kernel<4><<<grid, 256, 0, st>>>(xb, C, hw, G, plist, n_slices, partials);
+    else gn_partials_pipe_kernel<6><<<grid, 256, 0, st>>>(xb, C, hw, G, plist, n_slices, partials);
+    return;
+  }
+  gn_partials_kernel<<<dim3(n, G), 256, 0, st>>>(xb, C, hw, G, plist, partials);
 }
 
 // grid R, block G (<=1024): Chan-combine the equal-size partials of each request.
@@ -303,11 +416,128 @@ __global__ void __launch_bounds__(256) frames_vec_kernel(const __nv_bfloat16* __
   }
 }
 
+// Register-transposing NCHW -> CL copy with optional GroupNorm (C % 8 == 0, ps % 8 == 0).
+// One thread = 8 channels x 8 consecutive pixels of one output row: eight 16-byte loads
+// (one per channel row; 4-8 consecutive threads cover a 64-128 B channel row segment),
+// an 8x8 bf16 transpose in registers with the per-channel affine applied in fp32, and
+// eight 16-byte stores (one per pixel; 8 consecutive channel groups = 128 B of a pixel).
+// No shared memory and no per-element index math: the kernel is a streaming copy.
+// FRAMES adds the 1-pixel neighbour ring of patched.py:64-88 (zero outside the image):
+// rows 0 / F-1 read the N / S neighbour's edge row through the same vector path, and
+// the border columns are gathered per pixel (8 channels per thread).
+template <bool FRAMES>
+__global__ void __launch_bounds__(256, 4) frames_t8_kernel(const __nv_bfloat16* __restrict__ x, int C, int ps, int Cp,
+                                                        int mode, const float* __restrict__ stats,
+                                                        const int32_t* __restrict__ ri,
+                                                        const int32_t* __restrict__ nbr, int G,
+                                                        const float* __restrict__ gamma,
+                                                        const float* __restrict__ beta,
+                                                        const int32_t* __restrict__ plist,
+                                                        __nv_bfloat16* __restrict__ out) {
+  const int p = plist ? __ldg(plist + blockIdx.y) : (int)blockIdx.y;
+  const int F = FRAMES ? ps + 2 : ps, off = FRAMES ? 1 : 0;
+  const int nPB = ps >> 3, nCG = Cp >> 3;
+  const int hw = ps * ps;
+  const int n_int = F * nPB * nCG;
+  const int n_brd = FRAMES ? F * 2 * nCG : 0;
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n_int + n_brd) return;
+  int cg, fy, q, sy, pb = 0, side = 0, sx = 0;
+  if (u < n_int) {
+    // 4-8 consecutive lanes: the pixel blocks of one row (a 64-128 B run of each channel
+    // plane); 8 consecutive channel groups: one 128 B run of each output pixel
+    pb = u % nPB;
+    cg = (u / nPB) % nCG;
+    fy = u / (nPB * nCG);
+    q = p;
+    sy = fy - off;
+    if (FRAMES) {
+      if (fy == 0) { q = __ldg(nbr + (int64_t)p * 8 + 0); sy = ps - 1; }
+      else if (fy == F - 1) { q = __ldg(nbr + (int64_t)p * 8 + 4); sy = 0; }
+    }
+  } else {
+    const int v = u - n_int;
+    side = v & 1;
+    cg = (v >> 1) % nCG;
+    fy = (v >> 1) / nCG;
+    const int ry = fy == 0 ? -1 : (fy == F - 1 ? 1 : 0);
+    const int d = side == 0 ? (ry < 0 ? 7 : (ry > 0 ? 5 : 6)) : (ry < 0 ? 1 : (ry > 0 ? 3 : 2));
+    q = __ldg(nbr + (int64_t)p * 8 + d);
+    sy = ry < 0 ? ps - 1 : (ry > 0 ? 0 : fy - 1);
+    sx = side == 0 ? ps - 1 : 0;
+  }
+  const int c0 = cg * 8;
+  const int64_t obase = ((int64_t)p * F + fy) * F;
+  if (q < 0 || c0 >= C) {  // outside the image (zero halo) or padding channels
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    if (u < n_int) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) *reinterpret_cast<uint4*>(out + (obase + off + pb * 8 + i) * Cp + c0) = z;
+    } else {
+      *reinterpret_cast<uint4*>(out + (obase + (side ? F - 1 : 0)) * Cp + c0) = z;
+    }
+    return;
+  }
+  float a[8], b[8];
+  const int req = mode == 1 ? __ldg(ri + p) : 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    a[j] = 1.f;
+    b[j] = 0.f;
+    if (mode == 1) {
+      const int c = c0 + j;
+      const int g = c / (C / G);
+      const float mu = __ldg(stats + ((int64_t)req * G + g) * 2), rs = __ldg(stats + ((int64_t)req * G + g) * 2 + 1);
+      a[j] = rs * __ldg(gamma + c);
+      b[j] = __ldg(beta + c) - mu * a[j];
+    }
+  }
+  const __nv_bfloat16* src = x + ((int64_t)q * C + c0) * hw + sy * ps;
+  if (u < n_int) {
+    uint4 raw[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) raw[j] = __ldg(reinterpret_cast<const uint4*>(src + (int64_t)j * hw + pb * 8));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uint32_t w[4];
+#pragma unroll
+      for (int j2 = 0; j2 < 4; ++j2) {
+        float v2[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int j = 2 * j2 + h;
+          const uint32_t word = (&raw[j].x)[i >> 1];
+          const float f = __uint_as_float((i & 1) ? (word & 0xFFFF0000u) : (word << 16));
+          v2[h] = fmaf(f, a[j], b[j]);
+        }
+        w[j2] = pack_bf16(v2[0], v2[1]);
+      }
+      *reinterpret_cast<uint4*>(out + (obase + off + pb * 8 + i) * Cp + c0) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  } else {
+    uint32_t w[4];
+#pragma unroll
+    for (int j2 = 0; j2 < 4; ++j2) {
+      const float f0 = bf(src[(int64_t)(2 * j2) * hw + sx]), f1 = bf(src[(int64_t)(2 * j2 + 1) * hw + sx]);
+      w[j2] = pack_bf16(fmaf(f0, a[2 * j2], b[2 * j2]), fmaf(f1, a[2 * j2 + 1], b[2 * j2 + 1]));
+    }
+    *reinterpret_cast<uint4*>(out + (obase + (side ? F - 1 : 0)) * Cp + c0) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
 template <bool FRAMES>
 static int launch_frames_vec(cudaStream_t st, const void* x, int P, int C, int ps, int Cp, int mode,
                              const float* stats, const int32_t* ri, const int32_t* nbr, int G, const float* gamma,
                              const float* beta, void* out, const int32_t* plist = nullptr, int n_list = 0) {
   const int F = FRAMES ? ps + 2 : ps;
+  if (ps % 8 == 0 && C % 8 == 0 && !getenv_flag("PS_FRAMES_SMEM")) {
+    const int units = F * (ps / 8) * (Cp / 8) + (FRAMES ? F * 2 * (Cp / 8) : 0);
+    dim3 g2((units + 255) / 256, plist ? n_list : P);
+    frames_t8_kernel<FRAMES><<<g2, 256, 0, st>>>((const __nv_bfloat16*)x, C, ps, Cp, mode, stats, ri, nbr, G, gamma,
+                                                beta, plist, (__nv_bfloat16*)out);
+    count_launch();
+    return check_launch(FRAMES ? "frames_cl" : "to_cl");
+  }
   int R = 8;
   while (R > 1 && R * F * 64 * 2 > 96 * 1024) R >>= 1;
   const int smem = R * F * 64 * 2;
@@ -376,8 +606,7 @@ extern "C" {
 int ps_gn_partials(void* stream, const void* x, int P, int C, int ps_, int G, float* partials) {
   if (G < 1 || C % G) return set_error(PS_ERR_INPUT, "groups=%d does not divide channels=%d", G, C);
   if (P == 0) return PS_OK;
-  gn_partials_kernel<<<dim3(P, G), 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)x, C, ps_ * ps_, G,
-                                                                   nullptr, partials);
+  launch_gn_partials((cudaStream_t)stream, x, P, C, ps_ * ps_, G, nullptr, P, partials);
   count_launch();
   return check_launch("gn_partials");
 }
@@ -387,8 +616,7 @@ int ps_gn_partials_sub(void* stream, const void* x, int P, int C, int ps_, int G
   if (G < 1 || C % G) return set_error(PS_ERR_INPUT, "groups=%d does not divide channels=%d", G, C);
   if (n < 0 || n > P) return set_error(PS_ERR_INPUT, "gn_partials_sub: %d patches listed for P=%d", n, P);
   if (n == 0) return PS_OK;
-  gn_partials_kernel<<<dim3(n, G), 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)x, C, ps_ * ps_, G,
-                                                                   patches, partials);
+  launch_gn_partials((cudaStream_t)stream, x, P, C, ps_ * ps_, G, patches, n, partials);
   count_launch();
   return check_launch("gn_partials_sub");
 }

@@ -141,3 +141,53 @@ def test_feed_forward_residual_sdxl_vs_torch():
     h = 0.5 * h * (1 + torch.tanh(0.7978845608028654 * (h + 0.044715 * h ** 3)))
     want = (h @ w2.cuda().T + b2.cuda()).T.reshape(lat.shape) + lat
     _rel_close(got["r0"].float(), want, 5e-2, 2e-2)
+
+
+@pytest.mark.parametrize("C,ps,mode", [(64, 16, 1), (320, 32, 1), (320, 32, 0), (24, 8, 1), (64, 64, 1)])
+def test_frames_cl_register_transpose_matches_smem_kernel(C, ps, mode, monkeypatch):
+    """ps_frames_cl / ps_to_cl: the register-transposing streaming kernel (C % 8 == 0,
+    ps % 8 == 0) against the shared-memory transposer, bit for bit (same fp32 affine)."""
+    import ctypes as Cc
+    import paper_2501_09253_b200 as ps_
+    from paper_2501_09253_b200 import _lib
+    from paper_2501_09253_b200._dev import stream
+    torch.manual_seed(0)
+    dims = [2 * ps, 3 * ps, ps]
+    b = ps_.split([(f"r{i}", torch.randn(C, d, d)) for i, d in enumerate(dims)], patch_size=ps)
+    P = b.n_patches
+    Cp = (C + 63) // 64 * 64
+    x = torch.randn(P, C, ps, ps, device="cuda").to(torch.bfloat16)
+    G = 8 if C % 8 == 0 else 4
+    stats = torch.rand(b.n_requests, G, 2, device="cuda") + 0.5
+    gamma = torch.randn(C, device="cuda")
+    beta = torch.randn(C, device="cuda")
+    dev = b.device()
+    owned = torch.tensor([0, P - 1], dtype=torch.int32, device="cuda")
+
+    def run(smem):
+        if smem:
+            monkeypatch.setenv("PS_FRAMES_SMEM", "1")
+        else:
+            monkeypatch.delenv("PS_FRAMES_SMEM", raising=False)
+        fr = torch.full((P, ps + 2, ps + 2, Cp), 7.0, device="cuda").to(torch.bfloat16)
+        _lib.call("ps_frames_cl", stream(), x.data_ptr(), P, C, ps, Cp, mode, stats.data_ptr(),
+                  dev["request_index"].data_ptr(), dev["neighbors"].data_ptr(), G, gamma.data_ptr(),
+                  beta.data_ptr(), fr.data_ptr())
+        cl = torch.full((P * ps * ps, Cp), 7.0, device="cuda").to(torch.bfloat16)
+        _lib.call("ps_to_cl", stream(), x.data_ptr(), P, C, ps, Cp, mode, stats.data_ptr(),
+                  dev["request_index"].data_ptr(), G, gamma.data_ptr(), beta.data_ptr(), Cc.c_float(1e-5),
+                  cl.data_ptr())
+        sub = torch.full((P, ps + 2, ps + 2, Cp), 7.0, device="cuda").to(torch.bfloat16)
+        _lib.call("ps_frames_cl_sub", stream(), x.data_ptr(), P, C, ps, Cp, mode, stats.data_ptr(),
+                  dev["request_index"].data_ptr(), dev["neighbors"].data_ptr(), G, gamma.data_ptr(),
+                  beta.data_ptr(), owned.data_ptr(), 2, sub.data_ptr())
+        torch.cuda.synchronize()
+        return fr, cl, sub
+
+    a, b2 = run(False), run(True)
+    for u, v in zip(a, b2):
+        assert torch.equal(u, v)
+    # the interior of each frame is the patch itself (mode 0) / its affine image (mode 1)
+    if mode == 0:
+        inner = a[0][:, 1:-1, 1:-1, :C].permute(0, 3, 1, 2)
+        assert torch.equal(inner, x)
