@@ -144,6 +144,20 @@ int ps_attention(void* stream, const void* qk, const void* vt, int ldv, int T, i
 int ps_attention_pairs(void* stream, const void* qk, const void* vt, int ldv, int T, int Dp, int D,
                        const int32_t* img_tok0, const int32_t* pair_q0, const int32_t* pair_img, int n_pairs,
                        void* out);
+/* Split-KV attention for few query tiles (a large image split across GPUs leaves a
+ * GPU ~64 query tiles for 148 SMs): tile t (DEVICE arrays) covers key blocks
+ * [tile_kb0[t], +tile_nkb[t]) of 128 keys of its image; tile_slot[t] >= 0 writes the
+ * unnormalised fp32 O [slot][128][Dp] and (m, l) [slot][128][2] instead of `out`.
+ * ps_attention_combine merges n query tiles: slots [slot0[i], +nsplit[i]) -> out rows
+ * q0s[i] .. +128 (clipped to the image end via img_of / img_tok0).  Same math as
+ * patched.py:154-176 (online softmax partials merged in log2 space). */
+int ps_attention_splitkv(void* stream, const void* qk, const void* vt, int ldv, int T, int Dp, int D,
+                         const int32_t* img_tok0, const int32_t* tile_q0, const int32_t* tile_img,
+                         const int32_t* tile_kb0, const int32_t* tile_nkb, const int32_t* tile_slot, int n_tiles,
+                         float* part_o, float* part_ml, void* out);
+int ps_attention_combine(void* stream, const float* part_o, const float* part_ml, const int32_t* q0s,
+                         const int32_t* slot0, const int32_t* nsplit, const int32_t* img_of,
+                         const int32_t* img_tok0, int n, int Dp, void* out);
 /* Profiling: device counters [8] of per-role barrier-wait cycles for later ps_attention launches (NULL = off). */
 int ps_attention_debug(unsigned long long* counters);
 

@@ -144,6 +144,8 @@ class CSPBatch:
                 sides=i32([e.side for e in self.requests], dev),
                 img_tok0=i32(tok0, dev),
                 tile_q0=i32(q0s, dev),
+                tile_q0_host=np.asarray(q0s, dtype=np.int64),
+                tile_img_host=np.asarray(imgs, dtype=np.int64),
                 tile_img=i32(imgs, dev),
                 n_tiles=len(q0s),
                 pair_q0=i32(pq0, dev),

@@ -88,8 +88,12 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   const int tile = blockIdx.x;
   const int q0 = p.tile_q0[tile];
   const int img = p.tile_img[tile];
-  const int k_begin = p.img_tok0[img], k_end = p.img_tok0[img + 1];
-  const int n_kb = (k_end - k_begin + AT_BN - 1) / AT_BN;
+  const int k_img = p.img_tok0[img], k_end = p.img_tok0[img + 1];
+  // split-KV: this tile's key blocks start at tile_kb0 (k_begin is its first key)
+  const int kb0 = p.tile_kb0 ? p.tile_kb0[tile] : 0;
+  const int k_begin = k_img + kb0 * AT_BN;
+  const int n_kb = p.tile_nkb ? p.tile_nkb[tile] : (k_end - k_img + AT_BN - 1) / AT_BN;
+  const int slot = p.tile_slot ? p.tile_slot[tile] : -1;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmQ);
@@ -289,11 +293,29 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       tc_fence_before();
       mbar_arrive(p_full);
     }
-    // epilogue: O / l -> bf16 channels-last
+    // epilogue: O / l -> bf16 channels-last (or the unnormalised split-KV partial)
     mbar_wait(o_full, 0);
     tc_fence_after();
     const int q = q0 + row;
     const bool ok = q < k_end;
+    if (slot >= 0) {
+      float* po = p.part_o + ((size_t)slot * AT_BM + row) * DP;
+      if (row < AT_BM) {
+        p.part_ml[((size_t)slot * AT_BM + row) * 2] = m_run;
+        p.part_ml[((size_t)slot * AT_BM + row) * 2 + 1] = l_run;
+      }
+#pragma unroll 1
+      for (int c = 0; c < DP; c += 32) {
+        uint32_t o[32];
+        PS_TMEM_LD32(tmem + lane_base + Cfg::O_COL + c, o);
+        tmem_ld_wait();
+        float4* d4 = reinterpret_cast<float4*>(po + c);
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          d4[v] = make_float4(__uint_as_float(o[4 * v]), __uint_as_float(o[4 * v + 1]), __uint_as_float(o[4 * v + 2]),
+                              __uint_as_float(o[4 * v + 3]));
+      }
+    } else {
     const float inv = 1.f / l_run;
     __nv_bfloat16* dst = p.out + (size_t)q * p.Dp;
 #pragma unroll 1
@@ -313,6 +335,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           d4[v] = w;
         }
       }
+    }
     }
   }
   if (p.dbg && lane == 0) {
@@ -340,6 +363,55 @@ static int launch_dp(const CUtensorMap& q, const CUtensorMap& k, const CUtensorM
   attn_kernel<DP><<<p.n_tiles, AT_THREADS, Cfg::SMEM, st>>>(q, k, v, p);
   count_launch();
   return check_launch("attention");
+}
+
+// Split-KV combine: query tile i has partials in slots [slot0[i], slot0[i] + nsplit[i]);
+// O = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s, M = max_s m_s (m in log2 units).
+// grid = tiles, 256 threads; thread = (row, 8 columns).
+__global__ void __launch_bounds__(256) attn_combine_kernel(const float* __restrict__ part_o,
+                                                           const float* __restrict__ part_ml,
+                                                           const int* __restrict__ q0s, const int* __restrict__ slot0,
+                                                           const int* __restrict__ nsplit,
+                                                           const int* __restrict__ img_of, const int* __restrict__ img_tok0,
+                                                           int Dp, __nv_bfloat16* __restrict__ out) {
+  const int i = blockIdx.x;
+  const int q0 = __ldg(q0s + i), s0 = __ldg(slot0 + i), ns = __ldg(nsplit + i);
+  const int k_end = __ldg(img_tok0 + __ldg(img_of + i) + 1);
+  const int groups = Dp / 8;
+  for (int w = threadIdx.x; w < AT_BM * groups; w += blockDim.x) {
+    const int row = w / groups, c = (w - row * groups) * 8;
+    if (q0 + row >= k_end) continue;
+    float M = -INFINITY;
+    for (int s = 0; s < ns; ++s) M = fmaxf(M, __ldg(part_ml + ((size_t)(s0 + s) * AT_BM + row) * 2));
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float L = 0.f;
+    for (int s = 0; s < ns; ++s) {
+      const size_t r = (size_t)(s0 + s) * AT_BM + row;
+      const float m = __ldg(part_ml + r * 2), l = __ldg(part_ml + r * 2 + 1);
+      const float wgt = m == -INFINITY ? 0.f : exp2f(m - M);
+      L += wgt * l;
+      const float4* src = reinterpret_cast<const float4*>(part_o + r * Dp + c);
+      const float4 a = __ldg(src), b = __ldg(src + 1);
+      acc[0] += wgt * a.x; acc[1] += wgt * a.y; acc[2] += wgt * a.z; acc[3] += wgt * a.w;
+      acc[4] += wgt * b.x; acc[5] += wgt * b.y; acc[6] += wgt * b.z; acc[7] += wgt * b.w;
+    }
+    const float inv = 1.f / L;
+    uint4 o;
+    o.x = pack_bf16(acc[0] * inv, acc[1] * inv);
+    o.y = pack_bf16(acc[2] * inv, acc[3] * inv);
+    o.z = pack_bf16(acc[4] * inv, acc[5] * inv);
+    o.w = pack_bf16(acc[6] * inv, acc[7] * inv);
+    *reinterpret_cast<uint4*>(out + (size_t)(q0 + row) * Dp + c) = o;
+  }
+}
+
+int attention_combine_launch(const float* part_o, const float* part_ml, const int* q0s, const int* slot0,
+                             const int* nsplit, const int* img_of, const int* img_tok0, int n, int Dp,
+                             __nv_bfloat16* out, cudaStream_t st) {
+  if (n == 0) return PS_OK;
+  attn_combine_kernel<<<n, 256, 0, st>>>(part_o, part_ml, q0s, slot0, nsplit, img_of, img_tok0, Dp, out);
+  count_launch();
+  return check_launch("attention_combine");
 }
 
 int attention_launch(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& vt, const AttnParams& p, int dp,

@@ -409,3 +409,46 @@ int ps_attention(void* stream, const void* qk, const void* vt, int ldv, int T, i
 }
 
 }  // extern "C"
+
+extern "C" {
+// Split-KV attention (few query tiles per GPU, e.g. one large image split across GPUs):
+// tile t = (q0, img, first key block kb0, key blocks nkb, partial slot or -1).
+int ps_attention_splitkv(void* stream, const void* qk, const void* vt, int ldv, int T, int Dp, int D,
+                         const int32_t* img_tok0, const int32_t* tile_q0, const int32_t* tile_img,
+                         const int32_t* tile_kb0, const int32_t* tile_nkb, const int32_t* tile_slot, int n_tiles,
+                         float* part_o, float* part_ml, void* out) {
+  if (Dp % 64 || Dp < 64 || Dp > 320) return set_error(PS_ERR_INPUT, "attention: Dp %d unsupported", Dp);
+  if (D < 1 || D > Dp) return set_error(PS_ERR_INPUT, "attention: bad D");
+  if (!tile_kb0 || !tile_nkb || !tile_slot) return set_error(PS_ERR_INPUT, "attention_splitkv: null tile arrays");
+  if (n_tiles < 1) return PS_OK;
+  CUtensorMap tq, tk, tv;
+  int rc = make_tmap_2d(&tq, qk, T, Dp, 2 * (uint64_t)Dp, 128);
+  if (!rc) rc = make_tmap_2d(&tk, (const __nv_bfloat16*)qk + Dp, T, Dp, 2 * (uint64_t)Dp, 128);
+  if (!rc) rc = make_tmap_2d(&tv, vt, Dp, T, ldv, 64);
+  if (rc) return rc;
+  AttnParams p{};
+  p.T_total = T;
+  p.Dp = Dp;
+  p.n_tiles = n_tiles;
+  p.tile_q0 = tile_q0;
+  p.tile_img = tile_img;
+  p.img_tok0 = img_tok0;
+  p.scale_log2 = 1.4426950408889634f / sqrtf((float)D);
+  p.out = (__nv_bfloat16*)out;
+  p.dbg = g_attn_dbg;
+  p.tile_kb0 = tile_kb0;
+  p.tile_nkb = tile_nkb;
+  p.tile_slot = tile_slot;
+  p.part_o = part_o;
+  p.part_ml = part_ml;
+  return attention_launch(tq, tk, tv, p, Dp, (cudaStream_t)stream);
+}
+
+int ps_attention_combine(void* stream, const float* part_o, const float* part_ml, const int32_t* q0s,
+                         const int32_t* slot0, const int32_t* nsplit, const int32_t* img_of,
+                         const int32_t* img_tok0, int n, int Dp, void* out) {
+  if (Dp % 8) return set_error(PS_ERR_INPUT, "attention_combine: Dp %% 8 != 0");
+  return attention_combine_launch(part_o, part_ml, q0s, slot0, nsplit, img_of, img_tok0, n, Dp,
+                                  (__nv_bfloat16*)out, (cudaStream_t)stream);
+}
+}  // extern "C"

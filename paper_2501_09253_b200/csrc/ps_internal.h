@@ -54,9 +54,19 @@ struct AttnParams {
   float scale_log2;      // log2(e) / sqrt(D_real)
   __nv_bfloat16* out;    // [T_total, Dp] channels-last
   unsigned long long* dbg;  // optional per-role wait counters (profiling)
+  // split-KV (optional): tile t covers key blocks [tile_kb0[t], +tile_nkb[t]) of its image and,
+  // when tile_slot[t] >= 0, writes unnormalised fp32 O [slot][128][Dp] and (m, l) [slot][128]
+  const int* tile_kb0;
+  const int* tile_nkb;
+  const int* tile_slot;
+  float* part_o;
+  float* part_ml;
 };
 int attention_launch(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& vt, const AttnParams& p,
                      int dp, cudaStream_t st);
+int attention_combine_launch(const float* part_o, const float* part_ml, const int* q0s, const int* slot0,
+                             const int* nsplit, const int* img_of, const int* img_tok0, int n, int Dp,
+                             __nv_bfloat16* out, cudaStream_t st);
 int attention2_launch(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& vt, const AttnParams& p,
                       int dp, cudaStream_t st);
 int attention2_v_rows(int dp);

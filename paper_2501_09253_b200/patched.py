@@ -108,6 +108,17 @@ class Ctx:
         self.owned = None       # device int32 list of owned patches
         self.exch = None
 
+    def _splitkv(self, q0_host, img_host):
+        """Split-KV plan when the query tiles cannot fill the SMs (cached per tile list)."""
+        tok0 = self.b.request_offset * self.hw
+        key = (np.asarray(q0_host).tobytes(), np.asarray(img_host).tobytes(), np.asarray(tok0).tobytes(),
+               sm_count(), SPLITKV_MIN_BLOCKS, str(self.device))
+        if key not in _SKV_CACHE:
+            if len(_SKV_CACHE) > 64:
+                _SKV_CACHE.clear()
+            _SKV_CACHE[key] = splitkv_plan(q0_host, img_host, tok0, sm_count(), self.device)
+        return _SKV_CACHE[key]
+
     def empty_cl(self, cp: int) -> torch.Tensor:
         return torch.empty((self.T, cp), dtype=BF16, device=self.device)
 
@@ -264,14 +275,35 @@ class Ctx:
             ext = torch.cuda.is_current_stream_capturing()  # event nodes inside a captured graph
             ev = (torch.cuda.Event(enable_timing=True, external=ext), torch.cuda.Event(enable_timing=True, external=ext))
             ev[0].record()
+        host = None
         if self.attn_tiles is not None:
-            tq0, timg, nt, pairs = self.attn_tiles
+            tq0, timg, nt, pairs = self.attn_tiles[:4]
+            host = self.attn_tiles[4:]
         elif USE_PAIRS:
             tq0, timg, nt, pairs = self.dev["pair_q0"], self.dev["pair_img"], self.dev["n_pairs"], True
         else:
             tq0, timg, nt, pairs = self.dev["tile_q0"], self.dev["tile_img"], self.dev["n_tiles"], False
-        _lib.call("ps_attention_pairs" if pairs else "ps_attention", stream(), qk.data_ptr(), vt.data_ptr(), ldv,
-                  self.T, dpp, d, self.dev["img_tok0"].data_ptr(), tq0.data_ptr(), timg.data_ptr(), nt, o.data_ptr())
+            host = (self.dev["tile_q0_host"], self.dev["tile_img_host"])
+        # split-KV on the split-image path (few long query tiles per GPU); single-GPU batches keep
+        # the one-pass kernel so compacted and full runs stay bit-identical
+        use_skv = SPLITKV and (self.owned is not None or SPLITKV_ALL)
+        skv = None if pairs or host is None or not use_skv else self._splitkv(*host)
+        if skv is not None:
+            # few query tiles for the SMs: keys split over several CTAs per tile, partials merged
+            kb0, nkb, slot, n_split_tiles, cq0, cslot0, cns, cimg, n_q = skv[:9]
+            part_o = torch.empty((n_split_tiles, 128, dpp), dtype=torch.float32, device=self.device)
+            part_ml = torch.empty((n_split_tiles, 128, 2), dtype=torch.float32, device=self.device)
+            _lib.call("ps_attention_splitkv", stream(), qk.data_ptr(), vt.data_ptr(), ldv, self.T, dpp, d,
+                      self.dev["img_tok0"].data_ptr(), skv_q0(skv).data_ptr(), skv_img(skv).data_ptr(),
+                      kb0.data_ptr(), nkb.data_ptr(), slot.data_ptr(), n_split_tiles, part_o.data_ptr(),
+                      part_ml.data_ptr(), o.data_ptr())
+            _lib.call("ps_attention_combine", stream(), part_o.data_ptr(), part_ml.data_ptr(), cq0.data_ptr(),
+                      cslot0.data_ptr(), cns.data_ptr(), cimg.data_ptr(), self.dev["img_tok0"].data_ptr(), n_q, dpp,
+                      o.data_ptr())
+        else:
+            _lib.call("ps_attention_pairs" if pairs else "ps_attention", stream(), qk.data_ptr(), vt.data_ptr(),
+                      ldv, self.T, dpp, d, self.dev["img_tok0"].data_ptr(), tq0.data_ptr(), timg.data_ptr(), nt,
+                      o.data_ptr())
         if timer is not None:
             ev[1].record()
             timer.append(ev)
@@ -400,8 +432,96 @@ def _row_tiles(ctx: "Ctx", pats: np.ndarray):
     return torch.as_tensor(m, device=ctx.device), int(m.size)
 
 
+_SMS = None
+
+
+def sm_count() -> int:
+    global _SMS
+    if _SMS is None:
+        _SMS = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    return _SMS
+
+
+# split-KV planning (splitkv_plan); PS_SPLITKV=0 disables it
+SPLITKV = os.environ.get("PS_SPLITKV", "1") != "0"
+SPLITKV_ALL = os.environ.get("PS_SPLITKV_ALL", "0") == "1"  # also outside the split-image path
+_SKV_CACHE: dict = {}
+SPLITKV_MIN_BLOCKS = 8  # key blocks (of 128) per split
+
+
+def _lpt_makespan(pieces, sms: int) -> int:
+    """Greedy longest-first makespan of `pieces` (key blocks) on `sms` SMs (one CTA per SM)."""
+    import heapq
+    loads = [0] * min(sms, max(1, len(pieces)))
+    heapq.heapify(loads)
+    for w in sorted(pieces, reverse=True):
+        heapq.heappush(loads, heapq.heappop(loads) + w)
+    return max(loads)
+
+
+def splitkv_plan(q0_host, img_host, img_tok0_host, sms: int, device):
+    """Split long query tiles' keys over several CTAs when that shortens the kernel.
+
+    The attention kernel is one CTA per (query tile, key range); a tile costs its
+    number of 128-key blocks.  When few long tiles (a large image split across GPUs)
+    cannot keep `sms` SMs busy, every tile longer than a target is cut into equal key
+    ranges; the target is chosen to minimise the simulated longest-first makespan plus
+    a small charge per partial (fp32 O write + combine read).  Returns None when no
+    split helps; else device arrays for ps_attention_splitkv (kb0, nkb, slot per split
+    tile, longest first) and ps_attention_combine (q0, first slot, splits, image per
+    query tile), plus counts and the split tiles' (q0, image)."""
+    n = len(q0_host)
+    if n == 0:
+        return None
+    nkb_img = [(int(img_tok0_host[i + 1] - img_tok0_host[i]) + 127) // 128 for i in range(len(img_tok0_host) - 1)]
+    units = [nkb_img[int(i)] for i in img_host]
+    base = _lpt_makespan(units, sms)
+    best, best_cost = None, base
+    for k in range(2, 17):
+        target = max(SPLITKV_MIN_BLOCKS, -(-max(units) // k))
+        pieces, n_part = [], 0
+        for nb in units:
+            ns = -(-nb // target) if nb > target else 1
+            q, r = divmod(nb, ns)
+            pieces.extend([q + 1] * r + [q] * (ns - r))
+            n_part += ns if ns > 1 else 0
+        # a partial costs its fp32 O write + combine read (~320 KB/128 rows at Dp=320) ~ 4 key blocks of SM time
+        cost = _lpt_makespan(pieces, sms) + 4.0 * n_part / max(1, sms)
+        if cost < 0.97 * best_cost:
+            best, best_cost = target, cost
+    if best is None:
+        return None
+    rows = []  # (q0, img, kb0, nkb, slot)
+    cq0, cs0, cns, cimg = [], [], [], []
+    slot = 0
+    for q0, img, nb in zip(q0_host, img_host, units):
+        ns = -(-nb // best) if nb > best else 1
+        q, r = divmod(nb, ns)
+        cq0.append(int(q0)); cs0.append(slot); cns.append(ns); cimg.append(int(img))
+        k = 0
+        for s_ in range(ns):
+            m = q + (1 if s_ < r else 0)
+            rows.append((int(q0), int(img), k, m, slot))
+            k += m
+            slot += 1
+    rows.sort(key=lambda r_: -r_[3])  # longest ranges first
+    t = lambda v: torch.as_tensor(np.asarray(v, dtype=np.int32), device=device)
+    cols = list(zip(*rows))
+    return (t(cols[2]), t(cols[3]), t(cols[4]), len(rows), t(cq0), t(cs0), t(cns), t(cimg), len(cq0),
+            t(cols[0]), t(cols[1]))
+
+
+def skv_q0(plan):
+    return plan[9]
+
+
+def skv_img(plan):
+    return plan[10]
+
+
 def _attn_tiles(ctx: "Ctx", pats: np.ndarray):
-    """Attention query tiles (q0, image, n, pairs) of these patches, longest images first."""
+    """Attention query tiles (q0, image, n, pairs, q0 host, image host) of these patches,
+    longest images first."""
     batch = ctx.b
     sizes = batch.request_offset[1:] - batch.request_offset[:-1]
     pairs = USE_PAIRS and ctx.hw % 256 == 0
@@ -410,8 +530,9 @@ def _attn_tiles(ctx: "Ctx", pats: np.ndarray):
     n = ctx.hw // tq
     q0 = [p * ctx.hw + tq * j for p in order for j in range(n)]
     img = [int(batch.request_index[p]) for p in order for _ in range(n)]
-    return (torch.as_tensor(np.asarray(q0, np.int32), device=ctx.device),
-            torch.as_tensor(np.asarray(img, np.int32), device=ctx.device), len(q0), pairs)
+    q0h, imgh = np.asarray(q0, np.int64), np.asarray(img, np.int64)
+    return (torch.as_tensor(q0h.astype(np.int32), device=ctx.device),
+            torch.as_tensor(imgh.astype(np.int32), device=ctx.device), len(q0), pairs, q0h, imgh)
 
 
 def shard_context(batch: CSPBatch, shard, exch) -> "Ctx":

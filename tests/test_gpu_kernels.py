@@ -191,3 +191,39 @@ def test_frames_cl_register_transpose_matches_smem_kernel(C, ps, mode, monkeypat
     if mode == 0:
         inner = a[0][:, 1:-1, 1:-1, :C].permute(0, 3, 1, 2)
         assert torch.equal(inner, x)
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_splitkv_attention_matches_single_pass(world, monkeypatch):
+    """Split-KV attention (few query tiles: a rank of a split 2048 px image) against the
+    one-pass kernel on the same QKV: the merged partials agree to bf16 rounding."""
+    import paper_2501_09253_b200 as ps_
+    from paper_2501_09253_b200 import patched
+    from paper_2501_09253_b200.patchshard import SplitPlan
+    torch.manual_seed(0)
+    reqs = [("big", 128), ("s0", 32), ("s1", 64)]
+    plan = SplitPlan(reqs, 32, world)
+    sh = plan.shard(world - 1)
+    b = ps_.split([(rid, torch.randn(64, d, d)) for rid, d in sh.requests], patch_size=32)
+    cfg = ps_.ModelConfig(arch="dit_like", channels=64, hidden=128, n_blocks=1, groups=8, seed=2)
+    at = ps_.init_weights(cfg)[0][1][1]
+    x = torch.randn(b.n_patches, 64, 32, 32, device="cuda").to(torch.bfloat16)
+    ctx = patched.Ctx(b)
+    owned = np.asarray(sh.owned)
+    ctx.attn_tiles = patched._attn_tiles(ctx, owned)
+    monkeypatch.setattr(patched, "SPLITKV", False)   # never split
+    ref = ctx.as_nchw(ctx.attention(patched.Act("nchw", x, 64), at, None)).float()
+    monkeypatch.setattr(patched, "SPLITKV", True)
+    monkeypatch.setattr(patched, "SPLITKV_ALL", True)
+    patched._SKV_CACHE.clear()
+    monkeypatch.setattr(patched, "SPLITKV_MIN_BLOCKS", 1)
+    monkeypatch.setattr(patched, "sm_count", lambda: 1000)   # more SMs than tiles: forces splits
+    b._dev.clear()
+    ctx2 = patched.Ctx(b)
+    ctx2.attn_tiles = patched._attn_tiles(ctx2, owned)
+    plan = ctx2._splitkv(*ctx2.attn_tiles[4:])
+    assert plan is not None and plan[3] > plan[8], "expected split tiles"
+    got = ctx2.as_nchw(ctx2.attention(patched.Act("nchw", x, 64), at, None)).float()
+    torch.cuda.synchronize()
+    d = (got[owned] - ref[owned]).abs().max().item()
+    assert d <= 2e-2 + 2e-2 * ref[owned].abs().max().item(), d

@@ -2,9 +2,12 @@
 
 Each rank of a SplitPlan runs denoise_batch_shard on its local CSP batch with
 its ghost context arriving through the three exchanges (GroupNorm partials,
-halo strips, attention K / V^T).  The owned rows must be BIT-IDENTICAL to the
-single-GPU denoise_batch rows of the same patches: the exchanges move exact
-copies and every kernel computes a row from the same inputs in the same order.
+halo strips, attention K / V^T).  With the one-pass attention kernel the owned
+rows must be BIT-IDENTICAL to the single-GPU denoise_batch rows of the same
+patches: the exchanges move exact copies and every kernel computes a row from
+the same inputs in the same order.  With split-KV attention (the default on
+this path when a rank's few long query tiles cannot fill the SMs) the rows
+agree to the partial merge's rounding (<= 1e-2).
 
 One B200 is available per test box, so ranks run (a) as threads over a
 VirtualGroup in one process and (b) as two processes on cuda:0 over gloo
@@ -56,21 +59,34 @@ def _plan(world):
     return SplitPlan(REQS, PS, world, cost=lambda lat: patch_cost(lat, PS, 64, 128))
 
 
-def _compare(plan, full_b, full_out, rank, b, out):
+def _compare(plan, full_b, full_out, rank, b, out, tol=0.0):
     sh = plan.shard(rank)
     assert [e.request_id for e in full_b.requests] == [r.request_id for r in plan.reqs]
     for g in range(plan.cuts[rank], plan.cuts[rank + 1]):
         lp = sh.local(g)
         assert b.patch_key(lp) == full_b.patch_key(g)
-        if not torch.equal(out[lp], full_out[g]):
+        if tol == 0.0:
+            if not torch.equal(out[lp], full_out[g]):
+                d = (out[lp] - full_out[g]).abs().max().item()
+                raise AssertionError(f"rank {rank} patch {g}: max |d| {d:.3e} (expected bit-identical)")
+        else:
             d = (out[lp] - full_out[g]).abs().max().item()
-            raise AssertionError(f"rank {rank} patch {g}: max |d| {d:.3e} (expected bit-identical)")
+            assert d <= tol, f"rank {rank} patch {g}: max |d| {d:.3e} > {tol}"
 
 
+@pytest.mark.parametrize("splitkv", [False, True])
 @pytest.mark.parametrize("arch", ["unet_like", "dit_like"])
 @pytest.mark.parametrize("world", [2, 3, 5])
-def test_split_virtual_ranks_bit_identical(arch, world):
+def test_split_virtual_ranks_bit_identical(arch, world, splitkv, monkeypatch):
+    """Without split-KV the owned rows are bit-identical; with it (the default when a rank's
+    few long query tiles cannot fill the SMs) they agree to the merge's fp32 rounding."""
+    from paper_2501_09253_b200 import patched
     from paper_2501_09253_b200.patchshard import ShardExchange, VirtualGroup
+    monkeypatch.setattr(patched, "SPLITKV", splitkv)
+    if splitkv:  # tiny test images: pretend many SMs so the planner splits
+        monkeypatch.setattr(patched, "sm_count", lambda: 1000)
+        monkeypatch.setattr(patched, "SPLITKV_MIN_BLOCKS", 1)
+        patched._SKV_CACHE.clear()
     ps, cfg, w, lats, prompts = _setup(arch)
     full_b, full_out = _full(ps, cfg, w, lats, prompts)
     plan = _plan(world)
@@ -96,13 +112,15 @@ def test_split_virtual_ranks_bit_identical(arch, world):
         raise errs[0]
     torch.cuda.synchronize()
     for r in range(world):
-        _compare(plan, full_b, full_out, r, *res[r])
+        _compare(plan, full_b, full_out, r, *res[r], tol=1e-2 if splitkv else 0.0)
 
 
 def _proc(rank, world, port, q):
     import torch.distributed as dist
 
+    from paper_2501_09253_b200 import patched
     from paper_2501_09253_b200.patchshard import DistComm, ShardExchange
+    patched.SPLITKV = False  # bit-identity check
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
