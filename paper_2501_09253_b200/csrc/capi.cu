@@ -286,7 +286,7 @@ int ps_gemm(void* stream, const ps_gemm_args* a) {
   if (a->K % 64) return set_error(PS_ERR_INPUT, "gemm: K (%d) must be a multiple of 64", a->K);
   if (a->M < 1 || a->N < 1) return set_error(PS_ERR_INPUT, "gemm: empty problem");
   if (a->N % 16) return set_error(PS_ERR_INPUT, "gemm: N (%d) must be a multiple of 16", a->N);
-  const int bn = a->bn ? a->bn : gemm_pick_bn(a->N, a->K);
+  const int bn = a->bn ? a->bn : gemm_pick_bn(a->N, a->K, a->epi);
   const int mma_n = bn <= 256 ? bn : bn / 2;
   // CTA-pair tiles (cta_group::2) unless asked otherwise or the problem is too small to fill the SMs in pairs
   const int m_tiles = a->m_map ? a->m_count : (a->M + 127) / 128;
@@ -355,6 +355,9 @@ int ps_gemm(void* stream, const ps_gemm_args* a) {
   p.epi_split = epi_split;
   p.no_prefetch = no_pf;
   // channels-last outputs leave through TMA stores (32 rows x 16 columns per warp box)
+  // per-warp epilogue stores (no cross-warp barriers): FF1 153 -> 128 us (tools/gemm_roles.py)
+  static const int warp_store = getenv("PS_GEMM_WARP_STORE") ? atoi(getenv("PS_GEMM_WARP_STORE")) : 1;
+  p.warp_store = warp_store;
   CUtensorMap tc;
   memset(&tc, 0, sizeof(tc));
   p.store_tma = 0;
@@ -370,7 +373,7 @@ int ps_gemm(void* stream, const ps_gemm_args* a) {
       dims[1] = (uint64_t)a->M;
       strides[0] = (uint64_t)a->ldo * 2;
     }
-    uint32_t box[2] = {32, 128};
+    uint32_t box[2] = {32, (uint32_t)(p.warp_store ? 32 : 128)};
     rc = make_tmap(&tc, a->out, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B);
     if (rc) return rc;
     p.store_tma = 1;

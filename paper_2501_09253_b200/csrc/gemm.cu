@@ -263,8 +263,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const bool wg_leader = (warp & 3) == 0 && lane == 0;
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     uint8_t* box_base = tma_stage + wg * 2 * (GEMM_BM * 64);  // two 8 KB boxes per warpgroup
-    float* st = epi_stage + wg * 16 * GEMM_BM;                 // [16][128] fp32 transpose tile
-    const int ci = row >> 3, seg = row & 7;                    // transposed role
+    // transposed (NCHW / V^T) stores: a [16][128] fp32 tile per warpgroup, or with
+    // warp_store a [16][32] tile per warp (its own 32 rows; only __syncwarp needed)
+    const bool wst = p.warp_store != 0;
+    const int st_ld = wst ? 32 : GEMM_BM;
+    float* st = wst ? epi_stage + (warp - 4) * 16 * 32 : epi_stage + wg * 16 * GEMM_BM;
+    const int st_row = wst ? lane : row;
+    const int ci = wst ? lane >> 1 : row >> 3, seg = wst ? lane & 1 : row & 7;  // transposed role
     // NBUF == 1 or epi_split: the two warpgroups split every tile's columns (each tile's
     // accumulator drains in half the time); else warpgroup g takes the tiles of buffer g
     const bool split = Cfg::NBUF == 1 || (p.epi_split && (BN / 2) % 32 == 0);
@@ -287,10 +292,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const bool tile_full = (m_tile + 1) * GEMM_BM <= p.M;
       const int pidx = p.hw > 0 ? m / p.hw : 0;
       const int pix = p.hw > 0 ? m - pidx * p.hw : 0;
-      const int tok_v = m_tile * GEMM_BM + seg * 16;
+      const int tok_v = m_tile * GEMM_BM + (wst ? wq * 32 : 0) + seg * 16;
       const int pidx_v = p.hw > 0 ? tok_v / p.hw : 0;
       const int pix_v = p.hw > 0 ? tok_v - pidx_v * p.hw : 0;
-      const bool vec_nchw = p.epi == EPI_RESID_NCHW && (p.hw % 16) == 0 && tile_full;
+      const bool vec_nchw = p.epi == EPI_RESID_NCHW && (p.hw % (wst ? 32 : 16)) == 0 && tile_full;
       const bool vec_vt = p.epi == EPI_SPLIT_VT && (p.ldo2 % 8) == 0 && tile_full;
       timed_wait(&acc_full[buf], use & 1, t_wait);
       tc_fence_after();
@@ -320,20 +325,40 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const bool cl_tma = p.store_tma &&
                             (p.epi == EPI_STORE_CL || p.epi == EPI_GELU_CL || (p.epi == EPI_SPLIT_VT && nb < p.n_split));
         if (cl_tma) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            pk[e] = pack_bf16(v[2 * e], v[2 * e + 1]);
+            if (p.epi == EPI_GELU_CL) pk[e] = gelu_bf16x2(pk[e]);
+          }
+          if (p.warp_store) {
+            // per-warp 32x32 box: no cross-warp barrier, lane 0 issues the TMA store
+            uint8_t* box = tma_stage + (warp - 4) * 4096 + (n_store & 1) * 2048;
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              *reinterpret_cast<uint4*>(box + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) =
+                  make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+              if (p.out_tiled)
+                tma_store_2d(&tmC, box, nb & 63, (m_tile * (p.ldo / 64) + nb / 64) * GEMM_BM + wq * 32);
+              else
+                tma_store_2d(&tmC, box, nb, m_tile * GEMM_BM + wq * 32);
+              bulk_commit();
+            }
+            ++n_store;
+            return;
+          }
           uint8_t* box = box_base + (n_store & 1) * (GEMM_BM * 64);
           if (wg_leader) bulk_wait_read<1>();  // the TMA store that last used this box has read it
           named_bar_sync(bar_id, 128);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint32_t pk[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              pk[e] = pack_bf16(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
-              if (p.epi == EPI_GELU_CL) pk[e] = gelu_bf16x2(pk[e]);
-            }
+          for (int q = 0; q < 4; ++q)
             *reinterpret_cast<uint4*>(box + row * 64 + ((q ^ ((row >> 1) & 3)) << 4)) =
-                make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          }
+                make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
           fence_proxy_async();
           named_bar_sync(bar_id, 128);
           if (wg_leader) {
@@ -371,10 +396,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               rs1 = __ldg(reinterpret_cast<const uint4*>(p.resid + off_v) + 1);
             }
 #pragma unroll
-            for (int i = 0; i < 16; ++i) st[i * GEMM_BM + row] = v[s16 + i];
-            named_bar_sync(bar_id, 128);
+            for (int i = 0; i < 16; ++i) st[i * st_ld + st_row] = v[s16 + i];
+            if (wst) __syncwarp();
+            else named_bar_sync(bar_id, 128);
             if (tr_vt || nv < p.c_real) {
-              const float4* src = reinterpret_cast<const float4*>(st + ci * GEMM_BM + seg * 16);
+              const float4* src = reinterpret_cast<const float4*>(st + ci * st_ld + seg * 16);
               float o[16];
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
@@ -392,7 +418,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               }
               store16_cl((tr_vt ? p.out2 : p.out) + off_v, o);
             }
-            named_bar_sync(bar_id, 128);
+            if (wst) __syncwarp();
+            else named_bar_sync(bar_id, 128);
             continue;  // next 16-column piece
           }
           if (!row_ok) continue;
@@ -439,7 +466,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   }
-  if (warp >= 4 && lane == 0 && p.store_tma) bulk_wait<0>();
+  if (warp >= 4 && lane == 0 && p.store_tma) bulk_wait<0>();  // (per-warp or warpgroup-leader stores)
   if (p.dbg && lane == 0) {
     const unsigned long long tot = clock64() - t_start;
     if (warp == 0) { atomicAdd(p.dbg + 0, t_wait); atomicAdd(p.dbg + 1, tot); }
@@ -520,9 +547,11 @@ int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c
 #undef PS_GEMM_CASE
 }
 
-int gemm_pick_bn(int n, int k) {
-  // long reductions amortise a single accumulator: one 320-wide tile reads A once
-  if (n == 320 && k >= 1024) return 320;
+int gemm_pick_bn(int n, int k, int epi) {
+  // long reductions amortise a single accumulator: one 320-wide tile reads A once -- unless
+  // the epilogue is the slow NCHW transpose, which then stalls the MMAs of the next tile:
+  // two double-buffered 160-wide tiles instead (FF2 + residual 160 -> 135 us)
+  if (n == 320 && k >= 1024) return epi == EPI_RESID_NCHW ? 160 : 320;
   static const int choices[] = {256, 192, 160, 128, 64};
   int best = 64, best_cost = 1 << 30;
   for (int bn : choices) {

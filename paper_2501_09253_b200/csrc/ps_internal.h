@@ -33,6 +33,7 @@ struct GemmParams {
   int epi_skip;             // profiling only (PS_GEMM_EPI_SKIP=1): drain accumulators without storing
   int epi_split;            // both epilogue warpgroups split each tile's columns (else alternate tiles)
   int no_prefetch;          // skip the L2 prefetch of residual rows
+  int warp_store;           // channels-last TMA stores per warp (32x32 boxes) instead of per warpgroup
 };
 
 int set_error(int code, const char* fmt, ...);
@@ -40,7 +41,7 @@ int check_launch(const char* what);
 void count_launch();
 int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const GemmParams& p, int bn,
                 int pair, cudaStream_t st);
-int gemm_pick_bn(int n, int k);
+int gemm_pick_bn(int n, int k, int epi);
 // widest element span of `group` consecutive leaves of numpy's pairwise tree over n elements
 int64_t pairwise_max_span(int64_t n, int group);
 

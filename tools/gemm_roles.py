@@ -46,3 +46,10 @@ run("ff1", T, 1280, 320, 1, out_tiled=1)
 run("ff2", T, 320, 1280, 2, a_tiled=1, resid=True)
 run("ff2-cl", T, 320, 1280, 0, a_tiled=1)
 run("plain256", T, 256, 1024, 0)
+if len(sys.argv) > 1 and sys.argv[1] == "bn":
+    run("ff2-160", T, 320, 1280, 2, a_tiled=1, resid=True, bn=160)
+    run("ff2-320", T, 320, 1280, 2, a_tiled=1, resid=True, bn=320)
+    run("conv-160", T, 320, 2880, 0, bn=160)
+    run("ff1-128", T, 1280, 320, 1, out_tiled=1, bn=128)
+    run("qkv-160", T, 960, 320, 3, bn=160)
+    run("qkv-128", T, 960, 320, 3, bn=128)
