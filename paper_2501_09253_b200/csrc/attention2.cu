@@ -146,61 +146,63 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
         load_v(j);
       }
     }
-  } else if (warp == 1) {
-    // -------------------------------------------- MMA issuer (leader only)
+  } else if (warp == 1 || warp == 3) {
+    // ------------------------------- MMA issuers (leader only): w1 S = Q K^T, w3 O += P V
+    // Two issuing threads keep the pair's tensor pipes fed while either waits on a
+    // barrier (as in attention.cu).
     if (leader) {
       constexpr uint32_t idesc_s = idesc_bf16_f32(2 * A2_BM, A2_BN);
       constexpr uint32_t idesc_o = idesc_bf16_f32(2 * A2_BM, Cfg::PV_N);
-      int ks = 0, vs = 0;
-      uint32_t kph = 0, vph = 0;
-      auto issue_s = [&](int j) {
-        if (j >= 1) twait(s_free, (j - 1) & 1, w_a);
-        tc_fence_after();
-        for (int kc = 0; kc < Cfg::KB; ++kc) {
-          twait(&k_full[ks], kph, w_c);
-          tc_fence_after();
-          if (lane == 0) {
-            const uint8_t* kt = sK + ks * Cfg::K_SLOT;
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_bf16_ss_2sm(tmem + Cfg::S_COL, sdesc_sw128(sQ + kc * A2_BM * 128 + k * 32),
-                              sdesc_sw128(kt + k * 32), idesc_s, (kc | k) != 0);
-            mma_commit_2sm(&k_empty[ks], 0x3);
-            if (kc == Cfg::KB - 1) mma_commit_2sm(s_full, 0x3);
-          }
-          __syncwarp();
-          if (++ks == Cfg::NK) { ks = 0; kph ^= 1; }
-        }
-      };
-      auto issue_pv = [&](int j) {
-        twait(p_full, j & 1, w_b);
-        tc_fence_after();
-        for (int ka = 0; ka < 2; ++ka) {
-          twait(&v_full[vs], vph, w_c);
-          tc_fence_after();
-          if (lane == 0) {
-            const uint8_t* vt = sV + vs * Cfg::V_SLOT;
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-#pragma unroll
-              for (int n = 0; n < Cfg::PV_MMAS; ++n)
-                mma_bf16_ts_2sm(tmem + Cfg::O_COL + n * Cfg::PV_N, tmem + Cfg::P_COL + ka * 32 + k * 8,
-                                sdesc_sw128(vt + n * Cfg::V_ROWS * 128 + k * 32), idesc_o, (j | ka | k) != 0);
-            mma_commit_2sm(&v_empty[vs], 0x3);
-            if (ka == 1) {
-              mma_commit_2sm(p_free, 0x3);
-              if (j == n_kb - 1) mma_commit_2sm(o_full, 0x3);
-            }
-          }
-          __syncwarp();
-          if (++vs == Cfg::NV) { vs = 0; vph ^= 1; }
-        }
-      };
       mbar_wait(q_full, 0);
-      issue_s(0);
-      for (int j = 0; j < n_kb; ++j) {
-        if (j + 1 < n_kb) issue_s(j + 1);
-        issue_pv(j);
+      if (warp == 1) {
+        int ks = 0;
+        uint32_t kph = 0;
+        for (int j = 0; j < n_kb; ++j) {
+          if (j >= 1) twait(s_free, (j - 1) & 1, w_a);
+          tc_fence_after();
+          for (int kc = 0; kc < Cfg::KB; ++kc) {
+            twait(&k_full[ks], kph, w_c);
+            tc_fence_after();
+            if (lane == 0) {
+              const uint8_t* kt = sK + ks * Cfg::K_SLOT;
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma_bf16_ss_2sm(tmem + Cfg::S_COL, sdesc_sw128(sQ + kc * A2_BM * 128 + k * 32),
+                                sdesc_sw128(kt + k * 32), idesc_s, (kc | k) != 0);
+              mma_commit_2sm(&k_empty[ks], 0x3);
+              if (kc == Cfg::KB - 1) mma_commit_2sm(s_full, 0x3);
+            }
+            __syncwarp();
+            if (++ks == Cfg::NK) { ks = 0; kph ^= 1; }
+          }
+        }
+      } else {
+        int vs = 0;
+        uint32_t vph = 0;
+        for (int j = 0; j < n_kb; ++j) {
+          twait(p_full, j & 1, w_b);
+          tc_fence_after();
+          for (int ka = 0; ka < 2; ++ka) {
+            twait(&v_full[vs], vph, w_c);
+            tc_fence_after();
+            if (lane == 0) {
+              const uint8_t* vt = sV + vs * Cfg::V_SLOT;
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int n = 0; n < Cfg::PV_MMAS; ++n)
+                  mma_bf16_ts_2sm(tmem + Cfg::O_COL + n * Cfg::PV_N, tmem + Cfg::P_COL + ka * 32 + k * 8,
+                                  sdesc_sw128(vt + n * Cfg::V_ROWS * 128 + k * 32), idesc_o, (j | ka | k) != 0);
+              mma_commit_2sm(&v_empty[vs], 0x3);
+              if (ka == 1) {
+                mma_commit_2sm(p_free, 0x3);
+                if (j == n_kb - 1) mma_commit_2sm(o_full, 0x3);
+              }
+            }
+            __syncwarp();
+            if (++vs == Cfg::NV) { vs = 0; vph ^= 1; }
+          }
+        }
       }
     }
   } else if (warp >= 4) {
@@ -300,7 +302,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
   }
   if (p.dbg && lane == 0) {
     const unsigned long long tot = clock64() - t_start;
-    if (warp == 1 && leader) { atomicAdd(p.dbg + 0, w_a); atomicAdd(p.dbg + 1, w_b); atomicAdd(p.dbg + 2, w_c); atomicAdd(p.dbg + 3, tot); }
+    if (warp == 1 && leader) { atomicAdd(p.dbg + 0, w_a); atomicAdd(p.dbg + 2, w_c); atomicAdd(p.dbg + 3, tot); }
+    if (warp == 3 && leader) { atomicAdd(p.dbg + 1, w_b); atomicAdd(p.dbg + 2, w_c); }
     if (warp == 4) { atomicAdd(p.dbg + 4, w_a); atomicAdd(p.dbg + 5, w_b); atomicAdd(p.dbg + 6, tot); }
   }
   tc_fence_before();

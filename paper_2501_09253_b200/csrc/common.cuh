@@ -89,8 +89,12 @@ PS_DEV uint32_t mapa_shared(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
+// Arrive on a (possibly peer) CTA's barrier.  Default .release.cta semantics, as CUTLASS's
+// ClusterBarrier::arrive(cta_id): the guarded data are tcgen05 / async-proxy operations
+// ordered by tcgen05.fence around the barrier.  (.release.cluster compiles to
+// MEMBAR.ALL.GPU + ERRBAR per arrive -- it dominated the CTA-pair kernels' stalls.)
 PS_DEV void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // TMA load into this CTA's smem whose completion bytes count on a (possibly peer) cluster barrier
 PS_DEV void tma_load_2d_2sm(void* dst, const CUtensorMap* m, uint32_t bar_cluster, int c0, int c1) {

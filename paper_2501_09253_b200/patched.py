@@ -32,8 +32,10 @@ from .params import device_params
 
 _launches: Counter = Counter()
 BF16 = torch.bfloat16
-# attention on CTA pairs (tcgen05 cta_group::2) only on request: measured slower
-USE_PAIRS = os.environ.get("PS_ATTN_PAIRS", "0") == "1"
+# attention on CTA pairs (tcgen05 cta_group::2, 256-query tiles): the default since the pair's
+# remote barrier arrives dropped their cluster-scope fences and the MMAs got two issuer warps
+# (config-2 step 15.9 -> 15.4 ms); PS_ATTN_PAIRS=0 selects the single-CTA kernel
+USE_PAIRS = os.environ.get("PS_ATTN_PAIRS", "1") == "1"
 # bench hook: when a list, (start, end) CUDA events are recorded around every
 # attention-kernel launch on the launching stream
 ATTN_TIMER = None
@@ -279,15 +281,16 @@ class Ctx:
         if self.attn_tiles is not None:
             tq0, timg, nt, pairs = self.attn_tiles[:4]
             host = self.attn_tiles[4:]
-        elif USE_PAIRS:
+        elif USE_PAIRS and self.hw % 256 == 0:
             tq0, timg, nt, pairs = self.dev["pair_q0"], self.dev["pair_img"], self.dev["n_pairs"], True
+            host = (self.dev["tile_q0_host"], self.dev["tile_img_host"])
         else:
             tq0, timg, nt, pairs = self.dev["tile_q0"], self.dev["tile_img"], self.dev["n_tiles"], False
             host = (self.dev["tile_q0_host"], self.dev["tile_img_host"])
         # split-KV on the split-image path (few long query tiles per GPU); single-GPU batches keep
-        # the one-pass kernel so compacted and full runs stay bit-identical
+        # the one-pass kernels so compacted and full runs stay bit-identical
         use_skv = SPLITKV and (self.owned is not None or SPLITKV_ALL)
-        skv = None if pairs or host is None or not use_skv else self._splitkv(*host)
+        skv = None if host is None or not use_skv else self._splitkv(*host)
         if skv is not None:
             # few query tiles for the SMs: keys split over several CTAs per tile, partials merged
             kb0, nkb, slot, n_split_tiles, cq0, cslot0, cns, cimg, n_q = skv[:9]
@@ -530,9 +533,12 @@ def _attn_tiles(ctx: "Ctx", pats: np.ndarray):
     n = ctx.hw // tq
     q0 = [p * ctx.hw + tq * j for p in order for j in range(n)]
     img = [int(batch.request_index[p]) for p in order for _ in range(n)]
-    q0h, imgh = np.asarray(q0, np.int64), np.asarray(img, np.int64)
-    return (torch.as_tensor(q0h.astype(np.int32), device=ctx.device),
-            torch.as_tensor(imgh.astype(np.int32), device=ctx.device), len(q0), pairs, q0h, imgh)
+    # 128-query tiles on the host for the split-KV planner (which runs the single-CTA kernel)
+    n1 = ctx.hw // 128
+    q0h = np.asarray([p * ctx.hw + 128 * j for p in order for j in range(n1)], np.int64)
+    imgh = np.asarray([int(batch.request_index[p]) for p in order for _ in range(n1)], np.int64)
+    return (torch.as_tensor(np.asarray(q0, np.int32), device=ctx.device),
+            torch.as_tensor(np.asarray(img, np.int32), device=ctx.device), len(q0), pairs, q0h, imgh)
 
 
 def shard_context(batch: CSPBatch, shard, exch) -> "Ctx":
