@@ -158,6 +158,18 @@ int ps_attention_splitkv(void* stream, const void* qk, const void* vt, int ldv, 
 int ps_attention_combine(void* stream, const float* part_o, const float* part_ml, const int32_t* q0s,
                          const int32_t* slot0, const int32_t* nsplit, const int32_t* img_of,
                          const int32_t* img_tok0, int n, int Dp, void* out);
+/* Split images across GPUs without a K/V gather: ps_kv_peer_maps writes [2n] tensor maps
+ * (K, V^T of each rank's persistent buffers, as this GPU addresses them over NVLink) into
+ * device memory once; ps_attention_peer then TMA-loads every key block whose kb_src (per
+ * local 128-token block, -1 = local) names a peer from that peer's buffers at token row
+ * kb_row.  tile_kb0/tile_nkb/tile_slot/part_* are the optional split-KV arrays. */
+int ps_kv_peer_maps(void* dst_device, int n, const uint64_t* qk_ptrs, const int32_t* T, const uint64_t* vt_ptrs,
+                    const int32_t* ldv, int Dp);
+int ps_attention_peer(void* stream, const void* qk, const void* vt, int ldv, int T, int Dp, int D,
+                      const int32_t* img_tok0, const int32_t* tile_q0, const int32_t* tile_img,
+                      const int32_t* tile_kb0, const int32_t* tile_nkb, const int32_t* tile_slot, int n_tiles,
+                      float* part_o, float* part_ml, const int32_t* kb_src, const int32_t* kb_row,
+                      const void* peer_maps, void* out);
 /* Profiling: device counters [8] of per-role barrier-wait cycles for later ps_attention launches (NULL = off). */
 int ps_attention_debug(unsigned long long* counters);
 

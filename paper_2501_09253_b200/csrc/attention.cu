@@ -140,21 +140,43 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       for (int kc = 0; kc < Cfg::KB; ++kc) tma_load_2d(sQ + kc * AT_BM * 128, &tmQ, q_full, kc * 64, q0);
       int ks = 0, vs = 0;
       uint32_t kph = 0, vph = 0;
+      // key block j lives here or, for a split image, possibly in a peer GPU's buffers
+      // (read over NVLink by TMA through that peer's tensor maps -- no gather copy)
+      auto src_of = [&](int j, const CUtensorMap*& mk, const CUtensorMap*& mv, int& row) {
+        const int tok = k_begin + j * AT_BN;
+        mk = &tmK;
+        mv = &tmV;
+        row = tok;
+        if (p.kb_src != nullptr) {
+          const int s = __ldg(p.kb_src + tok / AT_BN);
+          if (s >= 0) {
+            mk = p.peer_maps + 2 * s;
+            mv = p.peer_maps + 2 * s + 1;
+            row = __ldg(p.kb_row + tok / AT_BN);
+          }
+        }
+      };
       auto load_k = [&](int j) {
+        const CUtensorMap *mk, *mv;
+        int row;
+        src_of(j, mk, mv, row);
         for (int kc = 0; kc < Cfg::KB; ++kc) {
           mbar_wait(&k_empty[ks], kph ^ 1);
           mbar_arrive_expect_tx(&k_full[ks], Cfg::K_SLOT);
-          tma_load_2d(sK + ks * Cfg::K_SLOT, &tmK, &k_full[ks], kc * 64, k_begin + j * AT_BN);
+          tma_load_2d(sK + ks * Cfg::K_SLOT, mk, &k_full[ks], kc * 64, row);
           if (++ks == Cfg::NK) { ks = 0; kph ^= 1; }
         }
       };
       auto load_v = [&](int j) {
+        const CUtensorMap *mk, *mv;
+        int row;
+        src_of(j, mk, mv, row);
         for (int ka = 0; ka < 2; ++ka) {
           mbar_wait(&v_empty[vs], vph ^ 1);
           mbar_arrive_expect_tx(&v_full[vs], Cfg::V_SLOT);
           uint8_t* dst = sV + vs * Cfg::V_SLOT;
           for (int dc = 0; dc < Cfg::KB; ++dc)
-            tma_load_2d(dst + dc * 64 * 128, &tmV, &v_full[vs], k_begin + j * AT_BN + ka * 64, dc * 64);
+            tma_load_2d(dst + dc * 64 * 128, mv, &v_full[vs], row + ka * 64, dc * 64);
           if (++vs == Cfg::NV) { vs = 0; vph ^= 1; }
         }
       };

@@ -455,3 +455,62 @@ int ps_attention_combine(void* stream, const float* part_o, const float* part_ml
                                   (__nv_bfloat16*)out, (cudaStream_t)stream);
 }
 }  // extern "C"
+
+extern "C" {
+// Tensor maps of n ranks' attention operand buffers (K = columns [Dp, 2 Dp) of qk [T, 2 Dp],
+// V^T [Dp, ldv]) written to dst_device as [2 n] CUtensorMap (K, V^T per rank).  Setup-time
+// (synchronous copy); the pointers are the ranks' persistent buffers as this GPU addresses
+// them (peer-mapped symmetric memory, or local buffers of virtual ranks).
+int ps_kv_peer_maps(void* dst_device, int n, const uint64_t* qk_ptrs, const int32_t* T, const uint64_t* vt_ptrs,
+                    const int32_t* ldv, int Dp) {
+  if (n < 1 || n > 64) return set_error(PS_ERR_INPUT, "kv_peer_maps: n=%d", n);
+  if (Dp % 64 || Dp < 64 || Dp > 320) return set_error(PS_ERR_INPUT, "kv_peer_maps: Dp %d unsupported", Dp);
+  std::vector<CUtensorMap> maps(2 * (size_t)n);
+  for (int i = 0; i < n; ++i) {
+    int rc = make_tmap_2d(&maps[2 * i], (const __nv_bfloat16*)qk_ptrs[i] + Dp, T[i], Dp, 2 * (uint64_t)Dp, 128);
+    if (!rc) rc = make_tmap_2d(&maps[2 * i + 1], (const void*)vt_ptrs[i], Dp, T[i], ldv[i], 64);
+    if (rc) return rc;
+  }
+  if (cudaMemcpy(dst_device, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice) != cudaSuccess)
+    return set_error(PS_ERR_CUDA, "kv_peer_maps: copy failed");
+  return PS_OK;
+}
+
+// Attention whose keys of split images are read from peer GPUs' K / V^T buffers
+// (kb_src / kb_row per local 128-token key block, maps from ps_kv_peer_maps); split-KV
+// arrays may be NULL (whole key range per tile, direct output).
+int ps_attention_peer(void* stream, const void* qk, const void* vt, int ldv, int T, int Dp, int D,
+                      const int32_t* img_tok0, const int32_t* tile_q0, const int32_t* tile_img,
+                      const int32_t* tile_kb0, const int32_t* tile_nkb, const int32_t* tile_slot, int n_tiles,
+                      float* part_o, float* part_ml, const int32_t* kb_src, const int32_t* kb_row,
+                      const void* peer_maps, void* out) {
+  if (Dp % 64 || Dp < 64 || Dp > 320) return set_error(PS_ERR_INPUT, "attention: Dp %d unsupported", Dp);
+  if (D < 1 || D > Dp) return set_error(PS_ERR_INPUT, "attention: bad D");
+  if (!kb_src || !kb_row || !peer_maps) return set_error(PS_ERR_INPUT, "attention_peer: null peer tables");
+  if (n_tiles < 1) return PS_OK;
+  CUtensorMap tq, tk, tv;
+  int rc = make_tmap_2d(&tq, qk, T, Dp, 2 * (uint64_t)Dp, 128);
+  if (!rc) rc = make_tmap_2d(&tk, (const __nv_bfloat16*)qk + Dp, T, Dp, 2 * (uint64_t)Dp, 128);
+  if (!rc) rc = make_tmap_2d(&tv, vt, Dp, T, ldv, 64);
+  if (rc) return rc;
+  AttnParams p{};
+  p.T_total = T;
+  p.Dp = Dp;
+  p.n_tiles = n_tiles;
+  p.tile_q0 = tile_q0;
+  p.tile_img = tile_img;
+  p.img_tok0 = img_tok0;
+  p.scale_log2 = 1.4426950408889634f / sqrtf((float)D);
+  p.out = (__nv_bfloat16*)out;
+  p.dbg = g_attn_dbg;
+  p.tile_kb0 = tile_kb0;
+  p.tile_nkb = tile_nkb;
+  p.tile_slot = tile_slot;
+  p.part_o = part_o;
+  p.part_ml = part_ml;
+  p.kb_src = kb_src;
+  p.kb_row = kb_row;
+  p.peer_maps = (const CUtensorMap*)peer_maps;
+  return attention_launch(tq, tk, tv, p, Dp, (cudaStream_t)stream);
+}
+}  // extern "C"

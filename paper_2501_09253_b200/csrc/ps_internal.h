@@ -62,6 +62,12 @@ struct AttnParams {
   const int* tile_slot;
   float* part_o;
   float* part_ml;
+  // peer K / V (optional, split images across GPUs): key block b (128 local tokens) with
+  // kb_src[b] >= 0 is read by TMA from peer kb_src[b]'s buffers, token row kb_row[b],
+  // through the tensor maps peer_maps[2 s] (K) and peer_maps[2 s + 1] (V^T) in global memory
+  const int* kb_src;
+  const int* kb_row;
+  const CUtensorMap* peer_maps;
 };
 int attention_launch(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& vt, const AttnParams& p,
                      int dp, cudaStream_t st);

@@ -110,6 +110,14 @@ class Ctx:
         self.owned = None       # device int32 list of owned patches
         self.exch = None
 
+    def _tiles128(self, host):
+        """Device copies of 128-query tile lists (cached by content)."""
+        key = ("t128", np.asarray(host[0]).tobytes(), np.asarray(host[1]).tobytes(), str(self.device))
+        if key not in _SKV_CACHE:
+            _SKV_CACHE[key] = (torch.as_tensor(np.asarray(host[0], np.int32), device=self.device),
+                               torch.as_tensor(np.asarray(host[1], np.int32), device=self.device))
+        return _SKV_CACHE[key]
+
     def _splitkv(self, q0_host, img_host):
         """Split-KV plan when the query tiles cannot fill the SMs (cached per tile list)."""
         tok0 = self.b.request_offset * self.hw
@@ -264,12 +272,20 @@ class Ctx:
         dp = device_params(prm, a.C)
         x = self.as_cl(a)
         d, dpp = dp["d"], dp["dp"]
-        qk = torch.empty((self.T, 2 * dpp), dtype=BF16, device=self.device)
-        ldv = round_up(self.T, 64)
-        vt = torch.empty((dpp, ldv), dtype=BF16, device=self.device)
+        peer = self.owned is not None and getattr(self.exch, "peer_kv", False)
+        if peer:
+            # persistent peer-visible operand buffers: peers read our K / V^T in place
+            par, (qk, vt, ldv, _, _, _) = self.exch.kv_buffers(dpp, self.T, self.device)
+        else:
+            qk = torch.empty((self.T, 2 * dpp), dtype=BF16, device=self.device)
+            ldv = round_up(self.T, 64)
+            vt = torch.empty((dpp, ldv), dtype=BF16, device=self.device)
         self.gemm(x, a.Cp, dp["wqkv"], 3 * dpp, dpp, None, 3, qk, ldo=2 * dpp, out2=vt, ldo2=ldv, n_split=2 * dpp,
                   rows=self.rows_live)
-        if self.owned is not None:
+        if peer:
+            self.exch.kv_sync()
+            kb_src, kb_row, maps = self.exch.kv_tables(dpp, par)
+        elif self.owned is not None:
             self.exch.kv(qk, vt, ldv, dpp)  # K rows / V^T columns of split images from their owners
         o = self.empty_cl(dpp)
         timer = ATTN_TIMER
@@ -291,15 +307,27 @@ class Ctx:
         # the one-pass kernels so compacted and full runs stay bit-identical
         use_skv = SPLITKV and (self.owned is not None or SPLITKV_ALL)
         skv = None if host is None or not use_skv else self._splitkv(*host)
-        if skv is not None:
+        if peer and skv is None:
+            # one-pass kernel over 128-query tiles, remote key blocks read from their owners
+            q0d, imgd = self._tiles128(host)
+            _lib.call("ps_attention_peer", stream(), qk.data_ptr(), vt.data_ptr(), ldv, self.T, dpp, d,
+                      self.dev["img_tok0"].data_ptr(), q0d.data_ptr(), imgd.data_ptr(), None, None, None,
+                      len(host[0]), None, None, kb_src.data_ptr(), kb_row.data_ptr(), maps.data_ptr(), o.data_ptr())
+        elif skv is not None:
             # few query tiles for the SMs: keys split over several CTAs per tile, partials merged
             kb0, nkb, slot, n_split_tiles, cq0, cslot0, cns, cimg, n_q = skv[:9]
             part_o = torch.empty((n_split_tiles, 128, dpp), dtype=torch.float32, device=self.device)
             part_ml = torch.empty((n_split_tiles, 128, 2), dtype=torch.float32, device=self.device)
-            _lib.call("ps_attention_splitkv", stream(), qk.data_ptr(), vt.data_ptr(), ldv, self.T, dpp, d,
-                      self.dev["img_tok0"].data_ptr(), skv_q0(skv).data_ptr(), skv_img(skv).data_ptr(),
-                      kb0.data_ptr(), nkb.data_ptr(), slot.data_ptr(), n_split_tiles, part_o.data_ptr(),
-                      part_ml.data_ptr(), o.data_ptr())
+            if peer:
+                _lib.call("ps_attention_peer", stream(), qk.data_ptr(), vt.data_ptr(), ldv, self.T, dpp, d,
+                          self.dev["img_tok0"].data_ptr(), skv_q0(skv).data_ptr(), skv_img(skv).data_ptr(),
+                          kb0.data_ptr(), nkb.data_ptr(), slot.data_ptr(), n_split_tiles, part_o.data_ptr(),
+                          part_ml.data_ptr(), kb_src.data_ptr(), kb_row.data_ptr(), maps.data_ptr(), o.data_ptr())
+            else:
+                _lib.call("ps_attention_splitkv", stream(), qk.data_ptr(), vt.data_ptr(), ldv, self.T, dpp, d,
+                          self.dev["img_tok0"].data_ptr(), skv_q0(skv).data_ptr(), skv_img(skv).data_ptr(),
+                          kb0.data_ptr(), nkb.data_ptr(), slot.data_ptr(), n_split_tiles, part_o.data_ptr(),
+                          part_ml.data_ptr(), o.data_ptr())
             _lib.call("ps_attention_combine", stream(), part_o.data_ptr(), part_ml.data_ptr(), cq0.data_ptr(),
                       cslot0.data_ptr(), cns.data_ptr(), cimg.data_ptr(), self.dev["img_tok0"].data_ptr(), n_q, dpp,
                       o.data_ptr())

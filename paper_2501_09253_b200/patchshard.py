@@ -348,6 +348,18 @@ class VirtualGroup:
             return [g] * self.world
         return self._meet(rank, t, comb)
 
+    def peer_buffers(self, rank: int, shape, dtype, device):
+        """Each virtual rank's buffer of `shape` and every rank's device pointer (one GPU:
+        plain allocations, addressed directly)."""
+        import torch
+        t = torch.empty(shape, dtype=dtype, device=device)
+        ptrs = self._meet(rank, t.data_ptr(), lambda xs: [list(xs)] * self.world)
+        return t, ptrs
+
+    def device_barrier(self, rank: int) -> None:
+        """All ranks' preceding work is enqueued (shared stream on one GPU: also ordered)."""
+        self._meet(rank, None, lambda xs: [None] * self.world)
+
     def exchange(self, rank: int, sends: dict, recv_like: dict | None = None):
         """sends: {dst: tensor}; returns {src: tensor} addressed to `rank`."""
         def comb(xs):
@@ -383,6 +395,27 @@ class DistComm:
         self.dist.all_gather_into_tensor(out, src, group=self.group)
         return out
 
+    def peer_buffers(self, rank: int, shape, dtype, device):
+        """Symmetric-memory buffer mapped into every rank's address space over NVLink
+        (torch.distributed._symmetric_memory); returns (local tensor, peer pointers)."""
+        import torch.distributed._symmetric_memory as symm_mem
+        t = symm_mem.empty(shape, dtype=dtype, device=device)
+        name = self.group.group_name if self.group is not None else self.dist.group.WORLD.group_name
+        hdl = symm_mem.rendezvous(t, name)
+        self._handles = getattr(self, "_handles", []) + [hdl]
+        return t, list(hdl.buffer_ptrs)
+
+    def device_barrier(self, rank: int) -> None:
+        """Stream-ordered cross-GPU barrier: a 1-element all-reduce after this rank's
+        producer kernels; later kernels see every rank's writes."""
+        import torch
+        if not hasattr(self, "_bar"):
+            self._bar = torch.zeros(1, dtype=torch.int32, device="cuda")
+        if self.stage:
+            self.dist.barrier(group=self.group)
+        else:
+            self.dist.all_reduce(self._bar, group=self.group)
+
     def exchange(self, rank: int, sends: dict, recv_like: dict) -> dict:
         """Point-to-point: sends {dst: tensor}, recv_like {src: (shape, dtype, device)}."""
         import torch
@@ -406,11 +439,15 @@ class ShardExchange:
     """The three per-block exchanges of one rank (module docstring), as library
     pack / unpack kernels around `comm` collectives."""
 
-    def __init__(self, shard: LocalShard, comm):
+    def __init__(self, shard: LocalShard, comm, peer_kv: bool = False):
+        """peer_kv: attention reads the split images' remote K / V directly from the owners'
+        buffers over NVLink (ps_attention_peer) instead of all-gathering them."""
         self.sh, self.comm = shard, comm
         self.rank = shard.rank
+        self.peer_kv = peer_kv and bool(shard.plan.split_requests())
         self.bytes_moved = 0  # payload bytes this rank sent (telemetry)
         self._cache: dict = {}
+        self._parity = 0
 
     def _dev_i64(self, key, values):
         import torch
@@ -495,3 +532,68 @@ class ShardExchange:
         for i, (vs, vd, nb) in enumerate(pl["v_unpack"]):
             self._copy(got, vt, key + ("vu", i), vs, vd, nb)
         self.bytes_moved += send.numel()
+
+    # 3'. attention K / V read in place from the owners (peer_kv) ----------
+    def kv_buffers(self, dpp: int, T: int, device):
+        """Persistent, peer-visible qk [T, 2 Dp] and V^T [Dp, ldv] of this call's parity
+        (double-buffered: a peer may still read block j's buffers while block j+1 writes)."""
+        from ._dev import round_up
+        import torch
+        par = self._parity
+        self._parity ^= 1
+        key = ("pkv", dpp, par)
+        if key not in self._cache:
+            ldv = round_up(T, 64)
+            qk, qk_ptrs = self.comm.peer_buffers(self.rank, (T, 2 * dpp), torch.bfloat16, device)
+            vt, vt_ptrs = self.comm.peer_buffers(self.rank, (dpp, ldv), torch.bfloat16, device)
+            self._cache[key] = (qk, vt, ldv, qk_ptrs, vt_ptrs, None)
+        return par, self._cache[key]
+
+    def kv_tables(self, dpp: int, par: int):
+        """(kb_src, kb_row, device tensor maps) for ps_attention_peer, built once per parity."""
+        import ctypes as C
+        import torch
+
+        from . import _lib
+        from ._dev import require_cuda, round_up
+        key = ("pkv", dpp, par)
+        qk, vt, ldv, qk_ptrs, vt_ptrs, tabs = self._cache[key]
+        if tabs is None:
+            sh, pl = self.sh, self.sh.plan
+            hw = pl.ps * pl.ps
+            world = pl.world
+            shards = [pl.shard(r) for r in range(world)]
+            T = [int(x.n_patches) * hw for x in shards]
+            ldvs = [round_up(t, 64) for t in T]
+            split = set(pl.split_requests())
+            nblk = (sh.n_patches * hw + 127) // 128
+            src = np.full(nblk, -1, dtype=np.int32)
+            row = np.zeros(nblk, dtype=np.int32)
+            owned = set(int(x) for x in sh.owned)
+            for k in sh.slots:
+                if k not in split:
+                    continue
+                rq = pl.reqs[k]
+                for g in range(rq.g0, rq.g0 + rq.count):
+                    lp = sh.local(g)
+                    if lp in owned:
+                        continue
+                    s_ = pl.owner(g)
+                    rp = shards[s_].local(g)
+                    for t in range(0, hw, 128):
+                        src[(lp * hw + t) // 128] = s_
+                        row[(lp * hw + t) // 128] = rp * hw + t
+            dev = require_cuda()
+            maps = torch.empty(2 * world * 128, dtype=torch.uint8, device=dev)  # 2 x 128-B CUtensorMap per rank
+            arr64 = lambda v: (C.c_uint64 * world)(*[int(x) for x in v])
+            arr32 = lambda v: (C.c_int32 * world)(*[int(x) for x in v])
+            _lib.call("ps_kv_peer_maps", maps.data_ptr(), world, arr64(qk_ptrs), arr32(T), arr64(vt_ptrs),
+                      arr32(ldvs), dpp)
+            tabs = (torch.as_tensor(src, device=dev), torch.as_tensor(row, device=dev), maps)
+            self._cache[key] = (qk, vt, ldv, qk_ptrs, vt_ptrs, tabs)
+        return tabs
+
+    def kv_sync(self) -> None:
+        """Every rank's QKV projection of this block is done (and visible) before any
+        rank's attention reads it."""
+        self.comm.device_barrier(self.rank)

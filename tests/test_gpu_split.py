@@ -74,12 +74,15 @@ def _compare(plan, full_b, full_out, rank, b, out, tol=0.0):
             assert d <= tol, f"rank {rank} patch {g}: max |d| {d:.3e} > {tol}"
 
 
+@pytest.mark.parametrize("peer_kv", [False, True])
 @pytest.mark.parametrize("splitkv", [False, True])
 @pytest.mark.parametrize("arch", ["unet_like", "dit_like"])
 @pytest.mark.parametrize("world", [2, 3, 5])
-def test_split_virtual_ranks_bit_identical(arch, world, splitkv, monkeypatch):
+def test_split_virtual_ranks_bit_identical(arch, world, splitkv, peer_kv, monkeypatch):
     """Without split-KV the owned rows are bit-identical; with it (the default when a rank's
-    few long query tiles cannot fill the SMs) they agree to the merge's fp32 rounding."""
+    few long query tiles cannot fill the SMs) they agree to the merge's fp32 rounding.
+    peer_kv: attention TMA-loads remote key blocks from the owner ranks' buffers (virtual
+    ranks on one GPU address each other's buffers directly) instead of all-gathering K/V."""
     from paper_2501_09253_b200 import patched
     from paper_2501_09253_b200.patchshard import ShardExchange, VirtualGroup
     monkeypatch.setattr(patched, "SPLITKV", splitkv)
@@ -92,13 +95,14 @@ def test_split_virtual_ranks_bit_identical(arch, world, splitkv, monkeypatch):
     plan = _plan(world)
     assert plan.split_requests(), "the plan must split at least one image"
     grp = VirtualGroup(world)
-    res, errs = {}, []
+    res, errs, exs = {}, [], {}
 
     def run(r):
         try:
             torch.cuda.set_device(0)
             sh = plan.shard(r)
-            res[r] = _rank_step(ps, cfg, w, lats, prompts, sh, ShardExchange(sh, grp))
+            exs[r] = ShardExchange(sh, grp, peer_kv=peer_kv)
+            res[r] = _rank_step(ps, cfg, w, lats, prompts, sh, exs[r])
         except BaseException as e:  # noqa: BLE001
             errs.append(e)
             grp._bar.abort()
@@ -113,6 +117,8 @@ def test_split_virtual_ranks_bit_identical(arch, world, splitkv, monkeypatch):
     torch.cuda.synchronize()
     for r in range(world):
         _compare(plan, full_b, full_out, r, *res[r], tol=1e-2 if splitkv else 0.0)
+        used_peer = any(k[0] == "pkv" for k in exs[r]._cache)
+        assert used_peer == peer_kv  # the remote-K/V path ran (and only when asked)
 
 
 def _proc(rank, world, port, q):
