@@ -14,7 +14,7 @@ from paper_2501_09253_b200 import _lib  # noqa: E402
 from paper_2501_09253_b200._dev import stream  # noqa: E402
 
 
-def _gemm(a, b, bias=None, epi=0, bn=0, out=None, ldo=None):
+def _gemm(a, b, bias=None, epi=0, bn=0, out=None, ldo=None, pair=0):
     M, K = a.shape
     N = b.shape[0]
     if out is None:
@@ -26,6 +26,7 @@ def _gemm(a, b, bias=None, epi=0, bn=0, out=None, ldo=None):
     g.bias = None if bias is None else bias.data_ptr()
     g.epi, g.out, g.ldo = epi, out.data_ptr(), ldo or N
     g.bn = bn
+    g.cta_pair = pair
     _lib.check(_lib.load().ps_gemm(stream(), C.byref(g)))
     return out
 
@@ -227,3 +228,39 @@ def test_splitkv_attention_matches_single_pass(world, monkeypatch):
     torch.cuda.synchronize()
     d = (got[owned] - ref[owned]).abs().max().item()
     assert d <= 2e-2 + 2e-2 * ref[owned].abs().max().item(), d
+
+
+@pytest.mark.parametrize("M,N,K,bn", [(1000, 320, 320, 160), (512, 256, 640, 256), (640, 320, 1280, 320),
+                                      (384, 192, 64, 192), (200, 1280, 320, 256)])
+def test_gemm_cta_pair_tiles_bit_identical(M, N, K, bn):
+    """tcgen05 cta_group::2 tiles (M = 256 per CTA pair, B halves per CTA, odd tile counts
+    leave the pair's second CTA a zero-filled tile) equal the single-CTA tiles bit for bit."""
+    torch.manual_seed(M + N)
+    a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    b = (torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
+    bias = torch.randn(N, device="cuda")
+    one = _gemm(a, b, bias, bn=bn, pair=1).clone()
+    two = _gemm(a, b, bias, bn=bn, pair=2)
+    torch.cuda.synchronize()
+    assert torch.equal(one, two)
+
+
+def test_attention_pair_kernel_bit_identical_to_single():
+    """The default CTA-pair attention (attention2.cu) and the single-CTA kernel agree bit for
+    bit on a mixed batch (same MMA accumulation order and softmax arithmetic)."""
+    import paper_2501_09253_b200 as ps
+    from paper_2501_09253_b200 import patched
+    torch.manual_seed(3)
+    cfg = ps.ModelConfig(arch="dit_like", channels=128, hidden=256, n_blocks=1, groups=8, seed=4)
+    at = ps.init_weights(cfg)[0][1][1]
+    b = ps.split([(f"r{i}", torch.randn(128, d, d)) for i, d in enumerate((32, 64, 48, 32))], patch_size=16)
+    x = torch.randn(b.n_patches, 128, 16, 16, device="cuda").to(torch.bfloat16)
+    outs = []
+    for pairs in (False, True):
+        patched.USE_PAIRS = pairs
+        try:
+            outs.append(ps.patched_self_attention(b, x, at).clone())
+        finally:
+            patched.USE_PAIRS = True
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
