@@ -238,6 +238,8 @@ def run_ours(args):
     if rank == 0:
         if args.slo:
             line["slo"] = slo
+        if args.cache_run:
+            line["config3_cache"] = measure_cache(cfg, weights, reqs)
         if args.cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline_sample(repeats=1)
         print(json.dumps(line), flush=True)
@@ -270,6 +272,41 @@ def measure_slo(cfg, weights, rank, world, barrier):
                   "cache, blend, reassemble); SLO budgets and admission on the cost model fitted to measured "
                   "B200 step times")
     return r
+
+
+def measure_cache(cfg, weights, reqs, steps=12, sigma=0.1, max_streak=3):
+    """BASELINE config 3: the config-2 batch with the patch cache in the loop at the reference's
+    default predictor (sigma 0.1, streak cap 3, cache.py:25-26) -- engine_step.numeric_step with the
+    bit-exact reuse test, compaction of the recomputed patches and one mask read-back per block
+    (engine.py:143-144).  Steps 3.. are timed with CUDA events (the cache warms up in steps 0-2)."""
+    import torch
+
+    import paper_2501_09253_b200 as ps
+    from paper_2501_09253_b200.engine_step import numeric_step
+    from paper_2501_09253_b200.model import step_inputs
+    b = ps.split([(r, torch.tensor(x, dtype=torch.float32)) for r, x in reqs], patch_size=PATCH)
+    prompts = {rid: ps.make_prompt(cfg, rid) for rid, _ in reqs}
+    cache = ps.BlockCache(cfg.n_blocks, ps.PredictorConfig(sigma, max_streak))
+    keys = b.patch_keys()
+    data = b.data.clone()
+    times, skipped, total = [], 0, 0
+    for s_ in range(steps):
+        bias, rates = step_inputs(cfg, b, prompts, dict.fromkeys(prompts, s_), dict.fromkeys(prompts, 50))
+        b.data = data
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        data, st = numeric_step(b, weights, cache, bias, rates, keys=keys)
+        e1.record()
+        torch.cuda.synchronize()
+        if s_ >= 3:
+            times.append(e0.elapsed_time(e1))
+            skipped += st.skipped
+            total += st.skipped + st.computed
+    ms = float(np.mean(times))
+    return {"value": b.n_patches / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "steps_timed": len(times),
+            "reuse_rate": skipped / max(1, total), "sigma": sigma, "max_streak": max_streak,
+            "path": "numeric_step: bit-exact fp64 reuse test -> compacted block on recomputed patches -> fused "
+                    "splice/streak/snapshot; one mask read-back per block (eager, not graph-captured)"}
 
 
 def _peaks():
@@ -344,6 +381,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-slo", dest="slo", action="store_false", help="skip the SLO-attainment serving run")
+    ap.add_argument("--no-cache-run", dest="cache_run", action="store_false",
+                    help="skip the config-3 (patch cache in the loop) measurement")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
