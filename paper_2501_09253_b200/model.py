@@ -158,21 +158,23 @@ def denoise_batch(cfg: ModelConfig, weights, batch: CSPBatch, prompts: dict, ste
 
 
 def denoise_batch_shard(cfg: ModelConfig, weights, batch: CSPBatch, shard, exch, prompts: dict, step_idx: dict,
-                        total_steps: dict) -> torch.Tensor:
+                        total_steps: dict, inputs=None, ctx=None) -> torch.Tensor:
     """denoise_batch for one rank of the split-image path (patchshard.py).
 
     `batch` is the rank's local CSP batch (the requests its patch range touches,
     `shard.requests`); rows of the owned patches (`shard.owned`) of the result
     equal the single-GPU denoise_batch rows of the same patches; ghost rows are
-    unspecified.
+    unspecified.  `inputs` = precomputed (bias, rates) device tensors and `ctx` = a
+    shard_context reused across steps make the call free of host->device copies, so a
+    fixed-composition step can be captured in a CUDA graph.
     """
     if batch.data.shape[1] != cfg.channels:
         raise InputError(f"batch has {batch.data.shape[1]} channels, model expects {cfg.channels}")
-    bias, rates = step_inputs(cfg, batch, prompts, step_idx, total_steps)
+    bias, rates = inputs if inputs is not None else step_inputs(cfg, batch, prompts, step_idx, total_steps)
     lat = batch.data if batch.data.dtype == torch.float32 else batch.data.float()
     lat = lat.contiguous()
     h = prompt_bias(batch, lat, bias)
-    ctx = shard_context(batch, shard, exch)
+    ctx = ctx or shard_context(batch, shard, exch)
     for ops in weights:
         h = run_block_shard(batch, h, ops, shard, exch, ctx=ctx)
     return blend_batch(batch, lat, h, rates)

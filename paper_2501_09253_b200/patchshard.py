@@ -31,7 +31,7 @@ The plan is pure host arithmetic, identical on every rank (no negotiation).
 
 from __future__ import annotations
 
-import bisect
+import bisect  # noqa: F401
 import threading
 from dataclasses import dataclass, field
 from typing import Callable, Sequence
@@ -121,8 +121,18 @@ class SplitPlan:
     """Global CSP order, per-rank patch ranges and the exchange tables."""
 
     def __init__(self, requests: Sequence[tuple], patch_size: int, world: int,
-                 cost: Callable[[int], float] | None = None):
-        """`requests`: (request_id, latent_dim) in arrival order."""
+                 cost: Callable[[int], float] | None = None, mode: str = "balanced"):
+        """`requests`: (request_id, latent_dim) in arrival order.
+
+        mode "contiguous": the CSP patch list is cut into `world` contiguous ranges (optimal
+        linear partition of per-patch cost).  mode "balanced" (default): only requests that
+        cost more than a GPU's share are split -- their patches, in CSP order, are cut into
+        contiguous ranges over all ranks by the same linear partition -- and every other
+        request stays whole, placed longest-first on the least loaded rank (the
+        reference's lowest-load dispatch, engine.py:228).  Config 5 then gives every GPU
+        two patches of the 2048 px image and one 512 px image."""
+        if mode not in ("balanced", "contiguous"):
+            raise InputError(f"unknown split mode {mode!r}")
         if world < 1:
             raise InputError("world must be >= 1")
         ps = int(patch_size)
@@ -140,14 +150,44 @@ class SplitPlan:
         self.n_patches = g
         cost = cost or (lambda lat: patch_cost(lat, ps))
         w = [cost(r.latent) for r in self.reqs for _ in range(r.count)]
-        self.cuts = linear_partition(w, world)
-        self.load = [float(sum(w[self.cuts[k]:self.cuts[k + 1]])) for k in range(world)]
+        self.mode = mode
         self._g0 = [r.g0 for r in self.reqs]
         self._shards: dict = {}
+        owner = np.zeros(g, dtype=np.int32)
+        if mode == "contiguous" or world == 1:
+            self.cuts = linear_partition(w, world)
+            for k in range(world):
+                owner[self.cuts[k]:self.cuts[k + 1]] = k
+        else:
+            self.cuts = None
+            share = sum(w) / world
+            req_cost = [sum(w[r.g0:r.g0 + r.count]) for r in self.reqs]
+            big = [k for k, c in enumerate(req_cost) if c > share * (1 + 1e-9) and self.reqs[k].count > 1]
+            loads = np.zeros(world)
+            if big:
+                pats = [gg for k in big for gg in range(self.reqs[k].g0, self.reqs[k].g0 + self.reqs[k].count)]
+                cuts = linear_partition([w[gg] for gg in pats], world)
+                for r_ in range(world):
+                    for i in range(cuts[r_], cuts[r_ + 1]):
+                        owner[pats[i]] = r_
+                        loads[r_] += w[pats[i]]
+            bigset = set(big)
+            for k in sorted((k for k in range(len(self.reqs)) if k not in bigset), key=lambda k: -req_cost[k]):
+                r_ = int(np.argmin(loads))
+                rq = self.reqs[k]
+                owner[rq.g0:rq.g0 + rq.count] = r_
+                loads[r_] += req_cost[k]
+        self.owner_tab = owner
+        self._owned = [np.flatnonzero(owner == r_).tolist() for r_ in range(world)]
+        self.load = [float(sum(w[gg] for gg in self._owned[r_])) for r_ in range(world)]
 
     # ---------------------------------------------------------- geometry
     def owner(self, g: int) -> int:
-        return bisect.bisect_right(self.cuts, g) - 1 if g < self.n_patches else self.world - 1
+        return int(self.owner_tab[g])
+
+    def owned_by(self, r: int) -> list:
+        """Global patches owned by rank r, ascending."""
+        return self._owned[r]
 
     def req_of(self, g: int) -> int:
         return bisect.bisect_right(self._g0, g) - 1
@@ -175,7 +215,7 @@ class SplitPlan:
         if src == dst:
             return []
         need = set()
-        for g in range(self.cuts[dst], self.cuts[dst + 1]):
+        for g in self.owned_by(dst):
             for d in range(8):
                 q = self.neighbour(g, d)
                 if q >= 0 and self.owner(q) == src:
@@ -200,8 +240,8 @@ class LocalShard:
 
     def __post_init__(self):
         pl, r = self.plan, self.rank
-        lo, hi = pl.cuts[r], pl.cuts[r + 1]
-        ks = sorted({pl.req_of(g) for g in range(lo, hi)})
+        mine = pl.owned_by(r)
+        ks = sorted({pl.req_of(g) for g in mine})
         self.slots = ks                                   # global CSP slots held, in CSP order
         self.local_slot = {k: i for i, k in enumerate(ks)}
         off = [0]
@@ -210,14 +250,14 @@ class LocalShard:
         self.request_offset = np.asarray(off, dtype=np.int64)
         self.n_patches = off[-1]
         self.requests = [(pl.reqs[k].request_id, pl.reqs[k].latent) for k in ks]
-        self.owned = np.asarray([self.local(g) for g in range(lo, hi)], dtype=np.int64)
+        self.owned = np.asarray([self.local(g) for g in mine], dtype=np.int64)
         split = set(pl.split_requests())
         self.split_slots = [k for k in ks if k in split]
 
         # GroupNorm partials: every rank's owned patches of split images, global order
         self.gn_lists = []
         for s in range(pl.world):
-            self.gn_lists.append([g for g in range(pl.cuts[s], pl.cuts[s + 1]) if pl.req_of(g) in split])
+            self.gn_lists.append([g for g in pl.owned_by(s) if pl.req_of(g) in split])
         self.gn_max = max((len(x) for x in self.gn_lists), default=0)
         self.gn_send = [self.local(g) for g in self.gn_lists[r]]
         self.gn_recv = []  # (src rank, slot in src's list, local patch)
@@ -240,8 +280,11 @@ class LocalShard:
             segs = []
             for k in sorted(split):
                 rq = pl.reqs[k]
-                a, b = max(rq.g0, pl.cuts[s]), min(rq.g0 + rq.count, pl.cuts[s + 1])
-                if a < b:
+                mine_k = [g for g in pl.owned_by(s) if rq.g0 <= g < rq.g0 + rq.count]
+                if mine_k:
+                    a, b = mine_k[0], mine_k[-1] + 1
+                    if b - a != len(mine_k):
+                        raise InputError("split image ranges must be contiguous per rank")
                     segs.append((k, a - rq.g0, b - a))
             self.kv_segs.append(segs)
         hw = pl.ps * pl.ps

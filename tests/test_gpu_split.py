@@ -54,15 +54,15 @@ def _rank_step(ps, cfg, w, lats, prompts, sh, exch):
     return b, denoise_batch_shard(cfg, w, b, sh, exch, prompts, si, ts)
 
 
-def _plan(world):
+def _plan(world, mode="balanced"):
     from paper_2501_09253_b200.patchshard import SplitPlan, patch_cost
-    return SplitPlan(REQS, PS, world, cost=lambda lat: patch_cost(lat, PS, 64, 128))
+    return SplitPlan(REQS, PS, world, cost=lambda lat: patch_cost(lat, PS, 64, 128), mode=mode)
 
 
 def _compare(plan, full_b, full_out, rank, b, out, tol=0.0):
     sh = plan.shard(rank)
     assert [e.request_id for e in full_b.requests] == [r.request_id for r in plan.reqs]
-    for g in range(plan.cuts[rank], plan.cuts[rank + 1]):
+    for g in plan.owned_by(rank):
         lp = sh.local(g)
         assert b.patch_key(lp) == full_b.patch_key(g)
         if tol == 0.0:
@@ -74,11 +74,12 @@ def _compare(plan, full_b, full_out, rank, b, out, tol=0.0):
             assert d <= tol, f"rank {rank} patch {g}: max |d| {d:.3e} > {tol}"
 
 
+@pytest.mark.parametrize("mode", ["balanced", "contiguous"])
 @pytest.mark.parametrize("peer_kv", [False, True])
 @pytest.mark.parametrize("splitkv", [False, True])
 @pytest.mark.parametrize("arch", ["unet_like", "dit_like"])
 @pytest.mark.parametrize("world", [2, 3, 5])
-def test_split_virtual_ranks_bit_identical(arch, world, splitkv, peer_kv, monkeypatch):
+def test_split_virtual_ranks_bit_identical(arch, world, splitkv, peer_kv, mode, monkeypatch):
     """Without split-KV the owned rows are bit-identical; with it (the default when a rank's
     few long query tiles cannot fill the SMs) they agree to the merge's fp32 rounding.
     peer_kv: attention TMA-loads remote key blocks from the owner ranks' buffers (virtual
@@ -92,7 +93,7 @@ def test_split_virtual_ranks_bit_identical(arch, world, splitkv, peer_kv, monkey
         patched._SKV_CACHE.clear()
     ps, cfg, w, lats, prompts = _setup(arch)
     full_b, full_out = _full(ps, cfg, w, lats, prompts)
-    plan = _plan(world)
+    plan = _plan(world, mode)
     assert plan.split_requests(), "the plan must split at least one image"
     grp = VirtualGroup(world)
     res, errs, exs = {}, [], {}

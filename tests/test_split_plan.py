@@ -44,7 +44,7 @@ def test_linear_partition_optimal(seed):
 def test_config5_plan():
     """Config 5: 1x2048 px + 8x512 px, patch 64, 8 GPUs."""
     reqs = [("big", 256)] + [(f"s{i}", 64) for i in range(8)]
-    plan = SplitPlan(reqs, 64, 8)
+    plan = SplitPlan(reqs, 64, 8, mode="contiguous")
     assert plan.n_patches == 24
     assert plan.split_requests() == [8]  # the 2048 px image, last in CSP order
     per_patch = patch_cost(256, 64)
@@ -53,14 +53,34 @@ def test_config5_plan():
     for r in range(8):
         sh = plan.shard(r)
         assert len(sh.owned) == plan.cuts[r + 1] - plan.cuts[r]
+    # balanced: every GPU gets 2 patches of the 2048 px image and one whole 512 px image
+    bal = SplitPlan(reqs, 64, 8)
+    assert bal.split_requests() == [8]
+    for r in range(8):
+        own = bal.owned_by(r)
+        assert len(own) == 3
+        assert sum(1 for g in own if bal.req_of(g) == 8) == 2
+    assert max(bal.load) / min(bal.load) < 1.01
+
+
+def test_balanced_keeps_small_requests_whole():
+    reqs = [(f"r{i}", d) for i, d in enumerate([64, 96, 128] * 4)]
+    plan = SplitPlan(reqs, 32, 8)
+    split = set(plan.split_requests())
+    for k, rq in enumerate(plan.reqs):
+        owners = {plan.owner(g) for g in range(rq.g0, rq.g0 + rq.count)}
+        assert (len(owners) > 1) == (k in split)
+    assert SplitPlan(reqs, 32, 1).split_requests() == []
 
 
 def _cases():
-    yield [("a", 64), ("b", 16), ("c", 32), ("d", 16)], 16, 2
-    yield [("a", 64), ("b", 16), ("c", 32), ("d", 16)], 16, 3
-    yield [("big", 128), ("x", 32), ("y", 64)], 32, 4
-    yield [("big", 96), ("x", 48), ("y", 48)], 16, 5
-    yield [("only", 64)], 16, 4
+    for mode in ("balanced", "contiguous"):
+        yield [("a", 64), ("b", 16), ("c", 32), ("d", 16)], 16, 2, mode
+        yield [("a", 64), ("b", 16), ("c", 32), ("d", 16)], 16, 3, mode
+        yield [("big", 128), ("x", 32), ("y", 64)], 32, 4, mode
+        yield [("big", 96), ("x", 48), ("y", 48)], 16, 5, mode
+        yield [("only", 64)], 16, 4, mode
+        yield [("big", 256)] + [(f"s{i}", 64) for i in range(8)], 64, 8, mode
 
 
 def _neighbour_frames(arr, plan, sh, g):
@@ -97,8 +117,8 @@ def _strip_io(arr, q, code, ps, buf=None):
 
 @pytest.mark.parametrize("case", list(_cases()))
 def test_halo_exchange_simulated(case):
-    reqs, ps, world = case
-    plan = SplitPlan(reqs, ps, world)
+    reqs, ps, world, mode = case
+    plan = SplitPlan(reqs, ps, world, mode=mode)
     C = 3
     rng = np.random.default_rng(1)
     full = rng.normal(size=(plan.n_patches, C, ps, ps))
@@ -106,7 +126,7 @@ def test_halo_exchange_simulated(case):
     local = []
     for sh in shards:
         a = np.full((sh.n_patches, C, ps, ps), np.nan)
-        for g in range(plan.cuts[sh.rank], plan.cuts[sh.rank + 1]):
+        for g in plan.owned_by(sh.rank):
             a[sh.local(g)] = full[g]
         local.append(a)
     # pack on every sender, then unpack on every receiver
@@ -123,7 +143,7 @@ def test_halo_exchange_simulated(case):
     assert not msgs
     # every owned patch's frame equals the single-GPU frame (no NaN ghost read)
     for sh in shards:
-        for g in range(plan.cuts[sh.rank], plan.cuts[sh.rank + 1]):
+        for g in plan.owned_by(sh.rank):
             got = _neighbour_frames(local[sh.rank], plan, sh, g)
             ref = _frames_full(full, plan, g)
             assert not np.isnan(got).any()
@@ -145,8 +165,8 @@ def _copy_segments(src: np.ndarray, dst: np.ndarray, so, do, nbytes):
 
 @pytest.mark.parametrize("case", list(_cases()))
 def test_gn_partials_exchange_simulated(case):
-    reqs, ps, world = case
-    plan = SplitPlan(reqs, ps, world)
+    reqs, ps, world, mode = case
+    plan = SplitPlan(reqs, ps, world, mode=mode)
     G = 4
     rng = np.random.default_rng(2)
     full = rng.normal(size=(plan.n_patches, G, 2)).astype(np.float32)
@@ -154,7 +174,7 @@ def test_gn_partials_exchange_simulated(case):
     loc = []
     for sh in shards:
         a = np.full((sh.n_patches, G, 2), np.nan, np.float32)
-        for g in range(plan.cuts[sh.rank], plan.cuts[sh.rank + 1]):
+        for g in plan.owned_by(sh.rank):
             a[sh.local(g)] = full[g]
         loc.append(a)
     if shards[0].gn_max == 0:
@@ -179,8 +199,8 @@ def test_gn_partials_exchange_simulated(case):
 
 @pytest.mark.parametrize("case", list(_cases()))
 def test_kv_exchange_simulated(case):
-    reqs, ps, world = case
-    plan = SplitPlan(reqs, ps, world)
+    reqs, ps, world, mode = case
+    plan = SplitPlan(reqs, ps, world, mode=mode)
     hw = ps * ps
     dpp = 64
     rng = np.random.default_rng(3)
@@ -196,7 +216,7 @@ def test_kv_exchange_simulated(case):
         ldv = (T + 63) // 64 * 64
         qk = np.zeros((T, 2 * dpp), np.uint16)
         vt = np.zeros((dpp, ldv), np.uint16)
-        for g in range(plan.cuts[sh.rank], plan.cuts[sh.rank + 1]):
+        for g in plan.owned_by(sh.rank):
             t = sh.local(g) * hw
             qk[t:t + hw, dpp:] = Kf[g * hw:(g + 1) * hw]
             vt[:, t:t + hw] = Vf[g * hw:(g + 1) * hw].T

@@ -16,10 +16,13 @@ import numpy as np
 import torch
 
 import paper_2501_09253_b200 as ps
-from paper_2501_09253_b200.model import denoise_batch_shard
+from paper_2501_09253_b200.model import denoise_batch_shard, step_inputs
+from paper_2501_09253_b200.patched import shard_context
 from paper_2501_09253_b200.patchshard import ShardExchange, SplitPlan
 
 NVLINK_GBS = 770.0
+GRAPH = os.environ.get("SPLIT_GRAPH", "1") == "1"
+MODE = os.environ.get("SPLIT_MODE", "balanced")
 C, H, G, NB, PS = 320, 1280, 32, 7, 64
 REQS = [("big", 256)] + [(f"s{i}", 64) for i in range(8)]
 
@@ -43,18 +46,36 @@ def time_rank(cfg, w, plan, r, reps=3):
     si = {rid: 3 for rid, _ in sh.requests}
     ts = {rid: 50 for rid, _ in sh.requests}
     ex = ShardExchange(sh, NullComm(plan.world))
-    denoise_batch_shard(cfg, w, b, sh, ex, prompts, si, ts)  # warm-up
+    denoise_batch_shard(cfg, w, b, sh, ex, prompts, si, ts)  # warm-up (plans, tables, allocations)
     torch.cuda.synchronize()
     ex.bytes_moved = 0
+    denoise_batch_shard(cfg, w, b, sh, ex, prompts, si, ts)
+    sent = ex.bytes_moved
+    torch.cuda.synchronize()
+    inputs = step_inputs(cfg, b, prompts, si, ts)
+    ctx = shard_context(b, sh, ex)
+    step = lambda: denoise_batch_shard(cfg, w, b, sh, ex, prompts, si, ts, inputs=inputs, ctx=ctx)
+    if GRAPH:
+        # the whole rank step as one CUDA graph: device time without host launch gaps
+        # (with NCCL the collectives are captured too)
+        g = torch.cuda.CUDAGraph()
+        s_ = torch.cuda.Stream()
+        s_.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s_):
+            step()
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=s_):
+                step()
+        torch.cuda.current_stream().wait_stream(s_)
+        step = g.replay
     ts_ms = []
     for _ in range(reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        denoise_batch_shard(cfg, w, b, sh, ex, prompts, si, ts)
+        step()
         e1.record()
         torch.cuda.synchronize()
         ts_ms.append(e0.elapsed_time(e1))
-    sent = ex.bytes_moved / reps
     # received: every all-gather delivers (world-1) peer buffers of the same size; halos ~ sent
     return float(np.median(ts_ms)), sent, len(sh.owned)
 
@@ -64,7 +85,7 @@ def main():
     w = ps.init_weights(cfg)
     out = []
     for world in (1, 2, 4, 8):
-        plan = SplitPlan(REQS, PS, world)
+        plan = SplitPlan(REQS, PS, world, mode=MODE)
         ranks = []
         for r in range(world):
             ms, sent, owned = time_rank(cfg, w, plan, r)
@@ -72,7 +93,8 @@ def main():
             ranks.append({"rank": r, "owned_patches": owned, "device_ms": ms, "sent_MB": sent / 1e6,
                           "comm_ms_est": comm_ms, "total_ms": ms + comm_ms})
         step = max(x["total_ms"] for x in ranks)
-        line = {"world": world, "cuts": plan.cuts, "split_images": len(plan.split_requests()),
+        line = {"world": world, "graph": GRAPH, "mode": plan.mode,
+                "owned": [len(plan.owned_by(r)) for r in range(world)], "split_images": len(plan.split_requests()),
                 "step_ms_projected": step, "patches_per_s": 24 / (step * 1e-3), "ranks": ranks}
         out.append(line)
         print(json.dumps(line), flush=True)
