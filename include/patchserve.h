@@ -172,6 +172,11 @@ int ps_attention_peer(void* stream, const void* qk, const void* vt, int ldv, int
                       const void* peer_maps, void* out);
 /* Profiling: device counters [8] of per-role barrier-wait cycles for later ps_attention launches (NULL = off). */
 int ps_attention_debug(unsigned long long* counters);
+/* Profiling: device buffer [11][64] of clock64 stamps (per event, first 64 key blocks) of the
+ * first CTA of later ps_attention_pairs launches: S issue start/end, PV issue start/end,
+ * softmax S-ready / S-loaded / exp-done / P-free / P-stored, then the S / PV issuers' K / V wait
+ * cycles per block (NULL = off). */
+int ps_attention_trace(long long* stamps);
 
 /* ------------------------------------------------------ patch cache (cache.py) */
 /* Pairwise-summation plan of numpy's add-reduce for n elements (cache.py:54-55

@@ -67,6 +67,7 @@ _SIGS = {
     "ps_attention_peer": ([p, p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, p, p, p, C.c_int, p, p, p, p, p, p],
                           C.c_int),
     "ps_attention_debug": ([p], C.c_int),
+    "ps_attention_trace": ([p], C.c_int),
     "ps_pairwise_plan": ([i64, p, p, p, p, p, p], C.c_int),
     "ps_cache_predict": ([p, p, C.c_int, i64, p, p, p, p, f64, C.c_int, p, C.c_int, p, C.c_int, p, C.c_int, p, p, p],
                          C.c_int),

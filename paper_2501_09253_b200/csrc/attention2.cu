@@ -12,6 +12,8 @@
 //     leader's barriers; MMA completions are multicast to both CTAs.
 // Per SM this halves the K/V bytes loaded and read by the tensor core, which is
 // what limited the single-CTA kernel (shared-memory bandwidth).
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "ps_internal.h"
 
@@ -21,7 +23,7 @@ constexpr int A2_BM = 128;  // query rows per CTA (256 per pair)
 constexpr int A2_BN = 128;  // keys per block (64 per CTA)
 constexpr int A2_THREADS = 256;
 
-template <int DP>
+template <int DP, int NV_ = 4>
 struct Attn2Cfg {
   static constexpr int KB = DP / 64;
   static constexpr int Q_BYTES = KB * A2_BM * 128;
@@ -30,7 +32,7 @@ struct Attn2Cfg {
   static constexpr int PV_MMAS = DP / PV_N;
   static constexpr int V_ROWS = PV_N / 2;                   // V^T rows per CTA per PV MMA
   static constexpr int V_SLOT = PV_MMAS * V_ROWS * 128;     // one 64-key atom, this CTA's rows
-  static constexpr int NV = 4;
+  static constexpr int NV = NV_;  // V ring (64-key slots); 3 leaves room for 10 K slots (2 key blocks)
   static constexpr int BUDGET = 227 * 1024 - Q_BYTES - NV * V_SLOT - 1024 - 512 - 2048;
   static constexpr int NK = BUDGET / K_SLOT > 10 ? 10 : BUDGET / K_SLOT;
   static constexpr int O_COL = 0;
@@ -42,11 +44,15 @@ struct Attn2Cfg {
   static_assert(V_ROWS % 8 == 0, "V^T half rows must be whole swizzle atoms");
 };
 
-template <int DP>
+// trace events (profiling): [ev * 64 + block], block < 64, first pair's leader CTA only
+#define A2_TRACE(ev, j)                                                                  \
+  if (p.trace != nullptr && blockIdx.x == 0 && (j) < 64) p.trace[(ev) * 64 + (j)] = clock64();
+
+template <int DP, int NV_>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
     attn2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                  const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
-  using Cfg = Attn2Cfg<DP>;
+  using Cfg = Attn2Cfg<DP, NV_>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
@@ -160,8 +166,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
         for (int j = 0; j < n_kb; ++j) {
           if (j >= 1) twait(s_free, (j - 1) & 1, w_a);
           tc_fence_after();
+          if (lane == 0) { A2_TRACE(0, j) }
+          long long kw = 0;
           for (int kc = 0; kc < Cfg::KB; ++kc) {
+            const long long tk0 = p.trace ? clock64() : 0;
             twait(&k_full[ks], kph, w_c);
+            if (p.trace) kw += clock64() - tk0;
             tc_fence_after();
             if (lane == 0) {
               const uint8_t* kt = sK + ks * Cfg::K_SLOT;
@@ -175,6 +185,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
             __syncwarp();
             if (++ks == Cfg::NK) { ks = 0; kph ^= 1; }
           }
+          if (lane == 0) { A2_TRACE(1, j) }
+          if (lane == 0 && p.trace != nullptr && blockIdx.x == 0 && j < 64) p.trace[9 * 64 + j] = kw;
         }
       } else {
         int vs = 0;
@@ -182,8 +194,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
         for (int j = 0; j < n_kb; ++j) {
           twait(p_full, j & 1, w_b);
           tc_fence_after();
+          if (lane == 0) { A2_TRACE(2, j) }
+          long long vw = 0;
           for (int ka = 0; ka < 2; ++ka) {
+            const long long tv0 = p.trace ? clock64() : 0;
             twait(&v_full[vs], vph, w_c);
+            if (p.trace) vw += clock64() - tv0;
             tc_fence_after();
             if (lane == 0) {
               const uint8_t* vt = sV + vs * Cfg::V_SLOT;
@@ -202,6 +218,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
             __syncwarp();
             if (++vs == Cfg::NV) { vs = 0; vph ^= 1; }
           }
+          if (lane == 0) { A2_TRACE(3, j) }
+          if (lane == 0 && p.trace != nullptr && blockIdx.x == 0 && j < 64) p.trace[10 * 64 + j] = vw;
         }
       }
     }
@@ -216,12 +234,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
     for (int j = 0; j < n_kb; ++j) {
       twait(s_full, j & 1, w_a);
       tc_fence_after();
+      if (threadIdx.x == 128) { A2_TRACE(4, j) }
       uint32_t sr[128];
 #pragma unroll
       for (int c = 0; c < 4; ++c) PS_TMEM_LD32(tmem + lane_base + Cfg::S_COL + 32 * c, (sr + 32 * c));
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive_cluster(s_free_l);
+      if (threadIdx.x == 128) { A2_TRACE(5, j) }
       const int kvalid = k_end - (k_begin + j * A2_BN);  // keys valid in this block
       if (kvalid < A2_BN) {  // only the last block of an image can be ragged
 #pragma unroll
@@ -251,9 +271,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
         sr[i] = pack_bf16(a, b);  // packed P overwrites the consumed half of sr
       }
       l_run = l_run * alpha + (sum0 + sum1);
+      if (threadIdx.x == 128) { A2_TRACE(6, j) }
       // P columns and O are owned by the MMAs of block j-1 until they complete
       if (j >= 1) twait(p_free, (j - 1) & 1, w_b);
       tc_fence_after();
+      if (threadIdx.x == 128) { A2_TRACE(7, j) }
       const bool warp_rescale = __any_sync(0xffffffffu, need && j >= 1 && alpha != 1.f);
       if (warp_rescale) {
         const float sc = (need && j >= 1) ? alpha : 1.f;
@@ -273,6 +295,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive_cluster(p_full_l);
+      if (threadIdx.x == 128) { A2_TRACE(8, j) }
     }
     // epilogue: O / l -> bf16 channels-last
     mbar_wait(o_full, 0);
@@ -312,18 +335,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
   if (warp == 2) tmem_dealloc_2sm(tmem, Cfg::TMEM_COLS);
 }
 
+template <int DP, int NV_>
+static int launch2_nv(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const AttnParams& p,
+                      cudaStream_t st) {
+  using Cfg = Attn2Cfg<DP, NV_>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn2_kernel<DP, NV_>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    attr = true;
+  }
+  attn2_kernel<DP, NV_><<<2 * p.n_tiles, A2_THREADS, Cfg::SMEM, st>>>(q, k, v, p);
+  count_launch();
+  return check_launch("attention_2cta");
+}
+
 template <int DP>
 static int launch2_dp(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const AttnParams& p,
                       cudaStream_t st) {
-  using Cfg = Attn2Cfg<DP>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attn2_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-    attr = true;
-  }
-  attn2_kernel<DP><<<2 * p.n_tiles, A2_THREADS, Cfg::SMEM, st>>>(q, k, v, p);
-  count_launch();
-  return check_launch("attention_2cta");
+  // V ring depth (PS_ATTN2_NV=3|4): A/B switch for tools/attn_pair_check.py
+  static const int nv = getenv("PS_ATTN2_NV") ? atoi(getenv("PS_ATTN2_NV")) : 4;
+  return nv == 3 ? launch2_nv<DP, 3>(q, k, v, p, st) : launch2_nv<DP, 4>(q, k, v, p, st);
 }
 
 int attention2_launch(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& vt, const AttnParams& p, int dp,

@@ -107,6 +107,7 @@ int64_t pairwise_max_span(int64_t n, int group) {
 using namespace ps;
 
 static unsigned long long* g_attn_dbg = nullptr;  // profiling hook (ps_attention_debug)
+static long long* g_attn_trace = nullptr;           // profiling hook (ps_attention_trace)
 
 extern "C" {
 
@@ -217,11 +218,17 @@ int ps_attention_pairs(void* stream, const void* qk, const void* vt, int ldv, in
   p.scale_log2 = 1.4426950408889634f / sqrtf((float)D);
   p.out = (__nv_bfloat16*)out;
   p.dbg = g_attn_dbg;
+  p.trace = g_attn_trace;
   return attention2_launch(tq, tk, tv, p, Dp, (cudaStream_t)stream);
 }
 
 // Profiling only: device counters [8] that later attention launches accumulate
 // per-role barrier-wait cycles into (NULL disables).
+int ps_attention_trace(long long* stamps) {
+  g_attn_trace = stamps;
+  return PS_OK;
+}
+
 int ps_attention_debug(unsigned long long* counters) {
   g_attn_dbg = counters;
   return PS_OK;

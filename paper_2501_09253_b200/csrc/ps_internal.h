@@ -68,6 +68,8 @@ struct AttnParams {
   const int* kb_src;
   const int* kb_row;
   const CUtensorMap* peer_maps;
+  // profiling (ps_attention_trace): clock64 stamps of the first CTA (pair leader), [event][block]
+  long long* trace;
 };
 int attention_launch(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& vt, const AttnParams& p,
                      int dp, cudaStream_t st);
