@@ -108,7 +108,40 @@ class Ctx:
         self.attn_tiles = None
         # split-image multi-GPU path (patchshard.py): the owned patches and the exchanger
         self.owned = None       # device int32 list of owned patches
+        self.owned_host = None
         self.exch = None
+
+    def _attention_overlapped(self, qk, vt, ldv, dpp, d, host, finish, o):
+        """Two-phase attention on the split-image path: phase A (owned keys of split images,
+        all keys of whole images) runs while the K / V^T all-gather is in flight; phase B
+        (remote keys) after finish(); partials merged by the combine kernel."""
+        plan = self._overlap_plan(host)
+        a_tiles, b_tiles, n_slots, comb = plan
+        part_o = torch.empty((max(1, n_slots), 128, dpp), dtype=torch.float32, device=self.device)
+        part_ml = torch.empty((max(1, n_slots), 128, 2), dtype=torch.float32, device=self.device)
+
+        def launch(t):
+            q0, img, kb0, nkb, slot, n = t
+            if n:
+                _lib.call("ps_attention_splitkv", stream(), qk.data_ptr(), vt.data_ptr(), ldv, self.T, dpp, d,
+                          self.dev["img_tok0"].data_ptr(), q0.data_ptr(), img.data_ptr(), kb0.data_ptr(),
+                          nkb.data_ptr(), slot.data_ptr(), n, part_o.data_ptr(), part_ml.data_ptr(), o.data_ptr())
+        launch(a_tiles)
+        finish()
+        launch(b_tiles)
+        cq0, cs0, cns, cimg, n_q = comb
+        if n_q:
+            _lib.call("ps_attention_combine", stream(), part_o.data_ptr(), part_ml.data_ptr(), cq0.data_ptr(),
+                      cs0.data_ptr(), cns.data_ptr(), cimg.data_ptr(), self.dev["img_tok0"].data_ptr(), n_q, dpp,
+                      o.data_ptr())
+
+    def _overlap_plan(self, host):
+        key = ("ovl", np.asarray(host[0]).tobytes(), np.asarray(host[1]).tobytes(),
+               np.asarray(self.owned_host).tobytes(), sm_count(), str(self.device))
+        if key not in _SKV_CACHE:
+            _SKV_CACHE[key] = overlap_plan(host[0], host[1], self.b.request_offset, self.hw,
+                                           np.asarray(self.owned_host), sm_count(), self.device)
+        return _SKV_CACHE[key]
 
     def _tiles128(self, host):
         """Device copies of 128-query tile lists (cached by content)."""
@@ -282,9 +315,13 @@ class Ctx:
             vt = torch.empty((dpp, ldv), dtype=BF16, device=self.device)
         self.gemm(x, a.Cp, dp["wqkv"], 3 * dpp, dpp, None, 3, qk, ldo=2 * dpp, out2=vt, ldo2=ldv, n_split=2 * dpp,
                   rows=self.rows_live)
+        finish = None
         if peer:
             self.exch.kv_sync()
             kb_src, kb_row, maps = self.exch.kv_tables(dpp, par)
+        elif self.owned is not None and OVERLAP_KV and self.attn_tiles is not None:
+            # start the K / V^T all-gather; attention over keys already here runs meanwhile
+            finish = self.exch.kv_start(qk, vt, ldv, dpp)
         elif self.owned is not None:
             self.exch.kv(qk, vt, ldv, dpp)  # K rows / V^T columns of split images from their owners
         o = self.empty_cl(dpp)
@@ -307,7 +344,9 @@ class Ctx:
         # the one-pass kernels so compacted and full runs stay bit-identical
         use_skv = SPLITKV and (self.owned is not None or SPLITKV_ALL)
         skv = None if host is None or not use_skv else self._splitkv(*host)
-        if peer and skv is None:
+        if finish is not None:
+            self._attention_overlapped(qk, vt, ldv, dpp, d, host, finish, o)
+        elif peer and skv is None:
             # one-pass kernel over 128-query tiles, remote key blocks read from their owners
             q0d, imgd = self._tiles128(host)
             _lib.call("ps_attention_peer", stream(), qk.data_ptr(), vt.data_ptr(), ldv, self.T, dpp, d,
@@ -476,6 +515,9 @@ def sm_count() -> int:
 # split-KV planning (splitkv_plan); PS_SPLITKV=0 disables it
 SPLITKV = os.environ.get("PS_SPLITKV", "1") != "0"
 SPLITKV_ALL = os.environ.get("PS_SPLITKV_ALL", "0") == "1"  # also outside the split-image path
+# split-image path: overlap the K / V^T all-gather with attention over the keys already local
+# (opt-in: at config 5 the second phase costs more than the ~0.1 ms/block gather it hides)
+OVERLAP_KV = os.environ.get("PS_OVERLAP_KV", "0") == "1"
 _SKV_CACHE: dict = {}
 SPLITKV_MIN_BLOCKS = 8  # key blocks (of 128) per split
 
@@ -542,6 +584,67 @@ def splitkv_plan(q0_host, img_host, img_tok0_host, sms: int, device):
             t(cols[0]), t(cols[1]))
 
 
+def overlap_plan(q0_host, img_host, req_off, hw: int, owned, sms: int, device):
+    """Pieces of the two attention phases of a split-image rank.
+
+    Per 128-query tile: an image held whole -> one piece over all its keys (phase A); an
+    image split across GPUs -> the key blocks of this rank's patches (phase A, contiguous)
+    and the remote ranges before / after them (phase B).  Pieces longer than the SM-balance
+    target are cut further.  A tile with a single piece writes its output directly; the
+    others write partials merged by ps_attention_combine."""
+    owned = set(int(x) for x in owned)
+    tpb = max(1, hw // 128)  # key blocks per patch
+    segs = []  # per tile: list of (kb0, nkb, phase)
+    for q0, img in zip(q0_host, img_host):
+        img = int(img)
+        p0, p1 = int(req_off[img]), int(req_off[img + 1])
+        nkb = (p1 - p0) * hw // 128
+        mine = [p for p in range(p0, p1) if p in owned]
+        if len(mine) == p1 - p0:
+            segs.append([(0, nkb, 0)])
+            continue
+        a, b = (mine[0] - p0) * tpb, (mine[-1] + 1 - p0) * tpb
+        tile = [(a, b - a, 0)]
+        if a > 0:
+            tile.append((0, a, 1))
+        if b < nkb:
+            tile.append((b, nkb - b, 1))
+        segs.append(tile)
+    total = sum(n for t in segs for _, n, _ in t)
+    target = max(SPLITKV_MIN_BLOCKS, -(-total // max(1, 2 * sms)))
+    rows = {0: [], 1: []}
+    cq0, cs0, cns, cimg = [], [], [], []
+    slot = 0
+    for (q0, img), tile in zip(zip(q0_host, img_host), segs):
+        pieces = []
+        for k0, n, ph in tile:
+            ns = -(-n // target) if n > target else 1
+            q, r = divmod(n, ns)
+            k = k0
+            for i in range(ns):
+                m = q + (1 if i < r else 0)
+                pieces.append((k, m, ph))
+                k += m
+        if len(pieces) == 1:
+            k, m, ph = pieces[0]
+            rows[ph].append((int(q0), int(img), k, m, -1))
+            continue
+        cq0.append(int(q0)); cs0.append(slot); cns.append(len(pieces)); cimg.append(int(img))
+        for k, m, ph in pieces:
+            rows[ph].append((int(q0), int(img), k, m, slot))
+            slot += 1
+    t = lambda v: torch.as_tensor(np.asarray(v, dtype=np.int32), device=device)
+
+    def launch_list(rs):
+        rs = sorted(rs, key=lambda r_: -r_[3])
+        if not rs:
+            return (None, None, None, None, None, 0)
+        c = list(zip(*rs))
+        return (t(c[0]), t(c[1]), t(c[2]), t(c[3]), t(c[4]), len(rs))
+    comb = (t(cq0), t(cs0), t(cns), t(cimg), len(cq0)) if cq0 else (None, None, None, None, 0)
+    return launch_list(rows[0]), launch_list(rows[1]), slot, comb
+
+
 def skv_q0(plan):
     return plan[9]
 
@@ -579,6 +682,7 @@ def shard_context(batch: CSPBatch, shard, exch) -> "Ctx":
         raise InputError(f"split-image path needs patch_size^2 % 128 == 0, got patch {ctx.ps}")
     owned = np.asarray(shard.owned, dtype=np.int64)
     ctx.owned = (torch.as_tensor(owned.astype(np.int32), device=ctx.device), int(owned.size))
+    ctx.owned_host = owned
     ctx.exch = exch
     ctx.rows_live = ctx.rows_act = _row_tiles(ctx, owned)
     ctx.attn_live = ctx.attn_act = _attn_tiles(ctx, owned)

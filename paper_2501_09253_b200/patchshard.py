@@ -438,6 +438,16 @@ class DistComm:
         self.dist.all_gather_into_tensor(out, src, group=self.group)
         return out
 
+    def all_gather_async(self, rank: int, t):
+        """(gathered, wait): NCCL runs the gather on its own stream, so kernels enqueued
+        before wait() overlap it; wait() makes the current stream wait for it."""
+        if self.stage:
+            return self.all_gather(rank, t), (lambda: None)
+        import torch
+        out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        work = self.dist.all_gather_into_tensor(out, t, group=self.group, async_op=True)
+        return out, work.wait
+
     def peer_buffers(self, rank: int, shape, dtype, device):
         """Symmetric-memory buffer mapped into every rank's address space over NVLink
         (torch.distributed._symmetric_memory); returns (local tensor, peer pointers)."""
@@ -555,6 +565,38 @@ class ShardExchange:
                       self._desc(("hr", s), strips).data_ptr(), got[s].contiguous().data_ptr(), 1)
 
     # 3. attention K / V^T -------------------------------------------------
+    def kv_start(self, qk, vt, ldv: int, dpp: int):
+        """Pack this rank's K / V^T of split images and start their all-gather; returns the
+        finish() that waits for it and unpacks the peers' segments into the ghost rows.
+        Kernels enqueued between the two (attention over the owned keys) overlap the gather
+        when the backend runs it asynchronously (NCCL)."""
+        import torch
+        sh = self.sh
+        if sh.kv_max_tokens == 0:
+            return lambda: None
+        key = ("kv", dpp, ldv)
+        if key not in self._cache:
+            self._cache[key] = kv_plan(sh, dpp, ldv)
+        pl = self._cache[key]
+        send = torch.empty(pl["buf_bytes"], dtype=torch.uint8, device=qk.device)
+        ks, kd, kb = pl["k_pack"]
+        self._copy(qk, send, key + ("kp",), ks, kd, kb)
+        for i, (vs, vd, nb) in enumerate(pl["v_pack"]):
+            self._copy(vt, send, key + ("vp", i), vs, vd, nb)
+        self.bytes_moved += send.numel()
+        if hasattr(self.comm, "all_gather_async"):
+            got, wait = self.comm.all_gather_async(self.rank, send)
+        else:
+            got, wait = self.comm.all_gather(self.rank, send), (lambda: None)
+
+        def finish():
+            wait()
+            ks_, kd_, kb_ = pl["k_unpack"]
+            self._copy(got, qk, key + ("ku",), ks_, kd_, kb_)
+            for i, (vs_, vd_, nb_) in enumerate(pl["v_unpack"]):
+                self._copy(got, vt, key + ("vu", i), vs_, vd_, nb_)
+        return finish
+
     def kv(self, qk, vt, ldv: int, dpp: int) -> None:
         import torch
         sh = self.sh

@@ -122,6 +122,41 @@ def test_split_virtual_ranks_bit_identical(arch, world, splitkv, peer_kv, mode, 
         assert used_peer == peer_kv  # the remote-K/V path ran (and only when asked)
 
 
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_split_overlapped_kv_gather(world, monkeypatch):
+    """Two-phase attention (owned keys while the K/V all-gather runs, then remote keys,
+    partials merged): owned rows agree with the single-GPU run to the merge rounding."""
+    from paper_2501_09253_b200 import patched
+    from paper_2501_09253_b200.patchshard import ShardExchange, VirtualGroup
+    monkeypatch.setattr(patched, "OVERLAP_KV", True)
+    patched._SKV_CACHE.clear()
+    ps, cfg, w, lats, prompts = _setup("unet_like")
+    full_b, full_out = _full(ps, cfg, w, lats, prompts)
+    plan = _plan(world)
+    grp = VirtualGroup(world)
+    res, errs = {}, []
+
+    def run(r):
+        try:
+            torch.cuda.set_device(0)
+            sh = plan.shard(r)
+            res[r] = _rank_step(ps, cfg, w, lats, prompts, sh, ShardExchange(sh, grp))
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+            grp._bar.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(300)
+    if errs:
+        raise errs[0]
+    torch.cuda.synchronize()
+    for r in range(world):
+        _compare(plan, full_b, full_out, r, *res[r], tol=1e-2)
+
+
 def _proc(rank, world, port, q):
     import torch.distributed as dist
 
