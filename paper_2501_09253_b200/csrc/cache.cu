@@ -13,6 +13,8 @@
 // ordinal; exists/streak are per-slot arrays.  The engine's per-block sequence
 // (engine.py:137-142) is fused into substitute (before the block) and finish
 // (after it).
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "ps_internal.h"
 
@@ -86,13 +88,19 @@ __global__ void __launch_bounds__(LEAVES_PER_CTA) mse_leaf_kernel(
   __nv_bfloat16* sa = stage;
   __nv_bfloat16* sb = stage + (v1 - v0);
   const bool vec = (n % 8 == 0) && v1 <= n;
+  __shared__ __align__(8) uint64_t bar;
   if (vec) {
-    const int nv = (int)((v1 - v0) / 8);
-#pragma unroll 4
-    for (int i = threadIdx.x; i < nv; i += blockDim.x) {
-      reinterpret_cast<uint4*>(sa)[i] = __ldg(reinterpret_cast<const uint4*>(xa + v0) + i);
-      reinterpret_cast<uint4*>(sb)[i] = __ldg(reinterpret_cast<const uint4*>(xb + v0) + i);
+    // two bulk copies (TMA engine, no register staging): the whole span is in flight at once
+    const uint32_t bytes = (uint32_t)((v1 - v0) * 2);
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      fence_mbar_init();
+      mbar_arrive_expect_tx(&bar, 2 * bytes);
+      bulk_load(sa, xa + v0, bytes, &bar);
+      bulk_load(sb, xb + v0, bytes, &bar);
     }
+    __syncthreads();
+    mbar_wait(&bar, 0);
   } else {
     for (int64_t i = e0 + threadIdx.x; i < e1; i += blockDim.x) {
       sa[i - v0] = xa[i];
@@ -113,22 +121,32 @@ __global__ void __launch_bounds__(256) mse_combine_kernel(
     int64_t n, const int32_t* __restrict__ slots, const uint8_t* __restrict__ exists,
     const int32_t* __restrict__ streak, int max_streak, double sigma, int L, const int32_t* __restrict__ nodes,
     int I, const int32_t* __restrict__ level_off, int H, int stride_nodes, double* __restrict__ scratch,
-    uint8_t* __restrict__ mask, int64_t* __restrict__ counters) {
+    uint8_t* __restrict__ mask, int64_t* __restrict__ counters, int smem_nodes) {
   const int p = blockIdx.x;
   const int slot = slots[p];
   const bool live = entry_live(slot, exists, streak, max_streak);
   double* v = scratch + (int64_t)p * stride_nodes;
+  extern __shared__ double sv[];  // leaf sums + internal nodes when they fit (else in place in scratch)
+  __shared__ double root_s;
+  const bool in_smem = smem_nodes >= L + I;
   if (live) {
+    double* w = v;
+    if (in_smem) {
+      for (int i = threadIdx.x; i < L; i += blockDim.x) sv[i] = v[i];
+      __syncthreads();
+      w = sv;
+    }
     for (int h = 0; h < H; ++h) {
       for (int i = level_off[h] + threadIdx.x; i < level_off[h + 1]; i += blockDim.x)
-        v[L + i] = __dadd_rn(v[nodes[2 * i]], v[nodes[2 * i + 1]]);
+        w[L + i] = __dadd_rn(w[nodes[2 * i]], w[nodes[2 * i + 1]]);
       __syncthreads();
     }
+    if (threadIdx.x == 0) root_s = I > 0 ? w[L + I - 1] : w[0];
   }
   if (threadIdx.x == 0) {
     bool m = false;
     if (live) {
-      const double root = I > 0 ? v[L + I - 1] : v[0];
+      const double root = root_s;
       const double mse = __ddiv_rn(__dadd_rn(0.0, root), (double)n);
       m = mse < sigma;
     }
@@ -331,8 +349,17 @@ int ps_cache_predict(void* stream, const void* x, int P, int64_t n, const int32_
   count_launch();
   int rc = check_launch("mse_leaf");
   if (rc) return rc;
-  mse_combine_kernel<<<P, 256, 0, st>>>(n, slots, exists, streak, max_streak, sigma, n_leaves, nodes, n_internal,
-                                        level_off, n_levels, stride, scratch, mask, counters);
+  // the tree in shared memory when it fits (levels then cost smem latency, not L2 round trips)
+  const int nodes_all = n_leaves + n_internal;
+  // (measured: the shared-memory variant is slower at config 2 -- 23 vs 18 us -- so it is off)
+  const int smem_c = (getenv("PS_MSE_SMEM_COMBINE") && nodes_all * 8 <= 200 * 1024) ? nodes_all * 8 : 0;
+  static bool attr_c = false;
+  if (!attr_c) {
+    cudaFuncSetAttribute(mse_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_c = true;
+  }
+  mse_combine_kernel<<<P, 256, smem_c, st>>>(n, slots, exists, streak, max_streak, sigma, n_leaves, nodes, n_internal,
+                                        level_off, n_levels, stride, scratch, mask, counters, smem_c / 8);
   count_launch();
   return check_launch("mse_combine");
 }

@@ -58,13 +58,201 @@ __global__ void csp_copy_kernel(const uint64_t* __restrict__ img_ptrs, const int
   }
 }
 
+// Patch-major variants (config-2 sizes): one CTA per (patch, CPB channels); the owning
+// request is resolved once per CTA, and every thread keeps 8 independent 16-byte loads in
+// flight before storing (the grid-stride versions above are latency-bound: index math and
+// a dependent request lookup per 16 bytes).
+constexpr int PM_UNR = 8;
+
+__device__ __forceinline__ void pm_locate(int p, const int32_t* req_off, const int32_t* sides, int n_req,
+                                          int& req, int& side, int& k) {
+  int lo = 0, hi = n_req - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(req_off + mid) <= p) lo = mid; else hi = mid - 1;
+  }
+  req = lo;
+  side = __ldg(sides + lo);
+  k = p - __ldg(req_off + lo);
+}
+
+template <typename T, bool TO_PATCHES>
+__global__ void __launch_bounds__(256) csp_copy_pm_kernel(const uint64_t* __restrict__ img_ptrs,
+                                                          const int32_t* __restrict__ req_off,
+                                                          const int32_t* __restrict__ sides, int n_req, int C,
+                                                          int ps, int cpb, T* __restrict__ patches) {
+  constexpr int VEC = 16 / sizeof(T);
+  const int p = blockIdx.x, c0 = blockIdx.y * cpb;
+  int req, side, k;
+  pm_locate(p, req_off, sides, n_req, req, side, k);
+  const int r = k / side, cc = k - r * side, L = side * ps;
+  T* img = reinterpret_cast<T*>(img_ptrs[req]);
+  const int vps = ps / VEC;
+  const int nc = min(cpb, C - c0);
+  const int n = nc * ps * vps;
+  for (int base = threadIdx.x; base < n; base += 256 * PM_UNR) {
+    uint4 v[PM_UNR];
+    int64_t dst[PM_UNR];
+#pragma unroll
+    for (int u = 0; u < PM_UNR; ++u) {
+      const int i = base + u * 256;
+      dst[u] = -1;
+      if (i < n) {
+        const int xv = i % vps, y = (i / vps) % ps, c = c0 + i / (vps * ps);
+        const int64_t io = ((int64_t)c * L + (int64_t)r * ps + y) * L + (int64_t)cc * ps + xv * VEC;
+        const int64_t po = (((int64_t)p * C + c) * ps + y) * ps + xv * VEC;
+        v[u] = __ldg(reinterpret_cast<const uint4*>(TO_PATCHES ? img + io : patches + po));
+        dst[u] = TO_PATCHES ? po : io;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PM_UNR; ++u)
+      if (dst[u] >= 0) *reinterpret_cast<uint4*>((TO_PATCHES ? patches : img) + dst[u]) = v[u];
+  }
+}
+
+// h = bf16(latent + prompt[request]) over (patch, CPB channels) CTAs, 8 float4 in flight
+__global__ void __launch_bounds__(256) prompt_bias_pm_kernel(const float* __restrict__ lat,
+                                                             const float* __restrict__ prompts,
+                                                             const int32_t* __restrict__ ri, int C, int hw, int cpb,
+                                                             __nv_bfloat16* __restrict__ h) {
+  const int p = blockIdx.x, c0 = blockIdx.y * cpb;
+  const int nc = min(cpb, C - c0);
+  const int n = nc * hw / 4;
+  const float* pr = prompts + (int64_t)__ldg(ri + p) * C;
+  const int64_t off4 = (((int64_t)p * C + c0) * hw) / 4;
+  for (int base = threadIdx.x; base < n; base += 256 * PM_UNR) {
+    float4 x[PM_UNR];
+#pragma unroll
+    for (int u = 0; u < PM_UNR; ++u) {
+      const int i = base + u * 256;
+      if (i < n) x[u] = __ldg(reinterpret_cast<const float4*>(lat) + off4 + i);
+    }
+#pragma unroll
+    for (int u = 0; u < PM_UNR; ++u) {
+      const int i = base + u * 256;
+      if (i < n) {
+        const float b = __ldg(pr + c0 + (i * 4) / hw);
+        uint2 o;
+        o.x = pack_bf16(x[u].x + b, x[u].y + b);
+        o.y = pack_bf16(x[u].z + b, x[u].w + b);
+        reinterpret_cast<uint2*>(h)[off4 + i] = o;
+      }
+    }
+  }
+}
+
+// (1 - r) x + r tanh(h) per request rate, over (patch, CPB channels) CTAs
+__global__ void __launch_bounds__(256) blend_pm_kernel(const float* __restrict__ lat,
+                                                       const __nv_bfloat16* __restrict__ hh,
+                                                       const float* __restrict__ rates,
+                                                       const int32_t* __restrict__ ri, int C, int hw, int cpb,
+                                                       float* __restrict__ out) {
+  const int p = blockIdx.x, c0 = blockIdx.y * cpb;
+  const int nc = min(cpb, C - c0);
+  const int n = nc * hw / 4;
+  const float r = __ldg(rates + __ldg(ri + p));
+  const int64_t off4 = (((int64_t)p * C + c0) * hw) / 4;
+  for (int base = threadIdx.x; base < n; base += 256 * PM_UNR) {
+    float4 x[PM_UNR];
+    uint2 hv[PM_UNR];
+#pragma unroll
+    for (int u = 0; u < PM_UNR; ++u) {
+      const int i = base + u * 256;
+      if (i < n) {
+        x[u] = __ldg(reinterpret_cast<const float4*>(lat) + off4 + i);
+        hv[u] = __ldg(reinterpret_cast<const uint2*>(hh) + off4 + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PM_UNR; ++u) {
+      const int i = base + u * 256;
+      if (i < n) {
+        const __nv_bfloat162 h01 = *reinterpret_cast<const __nv_bfloat162*>(&hv[u].x);
+        const __nv_bfloat162 h23 = *reinterpret_cast<const __nv_bfloat162*>(&hv[u].y);
+        float4 o;
+        o.x = (1.f - r) * x[u].x + r * tanhf(__low2float(h01));
+        o.y = (1.f - r) * x[u].y + r * tanhf(__high2float(h01));
+        o.z = (1.f - r) * x[u].z + r * tanhf(__low2float(h23));
+        o.w = (1.f - r) * x[u].w + r * tanhf(__high2float(h23));
+        reinterpret_cast<float4*>(out)[off4 + i] = o;
+      }
+    }
+  }
+}
+
+// channels per CTA so one CTA moves ~32 KB of the patch array
+static inline int pm_cpb(int C, int ps, int elem_bytes) {
+  int cpb = (32 * 1024) / (ps * ps * elem_bytes);
+  if (cpb < 1) cpb = 1;
+  if (cpb > C) cpb = C;
+  return cpb;
+}
+
+// Split along image rows: one CTA per (request, patch row, CPB channels) reads whole image
+// rows (side * ps contiguous pixels per channel row) and scatters them to that patch row's
+// patches -- long contiguous DRAM reads; the writes land as full 16-byte patch-row pieces.
+template <typename T>
+__global__ void __launch_bounds__(256) csp_split_rows_kernel(const uint64_t* __restrict__ img_ptrs,
+                                                             const int32_t* __restrict__ req_off,
+                                                             const int32_t* __restrict__ sides, int n_req, int C,
+                                                             int ps, int cpb, T* __restrict__ patches) {
+  constexpr int VEC = 16 / sizeof(T);
+  // blockIdx.x -> (request, patch row): walk the requests' row counts
+  int pr = blockIdx.x, req = 0;
+  for (; req < n_req; ++req) {
+    const int sd = __ldg(sides + req);
+    if (pr < sd) break;
+    pr -= sd;
+  }
+  if (req >= n_req) return;  // the grid is sized by P >= the number of patch rows
+  const int side = __ldg(sides + req), L = side * ps, p0 = __ldg(req_off + req) + pr * side;
+  const T* img = reinterpret_cast<const T*>(img_ptrs[req]);
+  const int c0 = blockIdx.y * cpb, nc = min(cpb, C - c0);
+  const int vrow = L / VEC;                      // 16-byte vectors per image row
+  const int n = nc * ps * vrow;
+  for (int base = threadIdx.x; base < n; base += 256 * PM_UNR) {
+    uint4 v[PM_UNR];
+    int64_t dst[PM_UNR];
+#pragma unroll
+    for (int u = 0; u < PM_UNR; ++u) {
+      const int i = base + u * 256;
+      dst[u] = -1;
+      if (i < n) {
+        const int xv = i % vrow, y = (i / vrow) % ps, c = c0 + i / (vrow * ps);
+        const int x = xv * VEC, pc = x / ps, xp = x - pc * ps;
+        v[u] = __ldg(reinterpret_cast<const uint4*>(img + ((int64_t)c * L + (int64_t)pr * ps + y) * L + x));
+        dst[u] = (((int64_t)(p0 + pc) * C + c) * ps + y) * ps + xp;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PM_UNR; ++u)
+      if (dst[u] >= 0) *reinterpret_cast<uint4*>(patches + dst[u]) = v[u];
+  }
+}
+
 template <bool TO_PATCHES>
 static int csp_copy(cudaStream_t st, const uint64_t* ptrs, const int32_t* off, const int32_t* sides, int n_req,
                     int C, int ps, int dtype, void* patches, int P) {
   const int64_t elems = (int64_t)P * C * ps * ps;
   if (elems == 0) return PS_OK;
   const int th = 256;
-  if (dtype == PS_DTYPE_F32) {
+  if (TO_PATCHES && dtype == PS_DTYPE_F32 && ps % 4 == 0 && P <= 65535) {
+    // one CTA per patch row; the row count (sum of the sides, <= P) is on the device, so the
+    // grid is sized by P and surplus CTAs return at once
+    const int rows = P;
+    const int cpb = pm_cpb(C, ps, 4);
+    csp_split_rows_kernel<float><<<dim3(rows, (C + cpb - 1) / cpb), th, 0, st>>>(ptrs, off, sides, n_req, C, ps,
+                                                                               cpb, (float*)patches);
+  } else if (dtype == PS_DTYPE_F32 && ps % 4 == 0 && P <= 65535) {
+    const int cpb = pm_cpb(C, ps, 4);
+    csp_copy_pm_kernel<float, TO_PATCHES><<<dim3(P, (C + cpb - 1) / cpb), th, 0, st>>>(ptrs, off, sides, n_req, C,
+                                                                                    ps, cpb, (float*)patches);
+  } else if (dtype == PS_DTYPE_BF16 && ps % 8 == 0 && P <= 65535) {
+    const int cpb = pm_cpb(C, ps, 2);
+    csp_copy_pm_kernel<__nv_bfloat16, TO_PATCHES><<<dim3(P, (C + cpb - 1) / cpb), th, 0, st>>>(
+        ptrs, off, sides, n_req, C, ps, cpb, (__nv_bfloat16*)patches);
+  } else if (dtype == PS_DTYPE_F32) {
     if (ps % 4 == 0)
       csp_copy_kernel<float, 4, TO_PATCHES><<<grid_for(elems / 4, th), th, 0, st>>>(ptrs, off, sides, n_req, C, ps,
                                                                                  (float*)patches, elems / 4);
@@ -202,6 +390,13 @@ int ps_prompt_bias(void* stream, const float* latent, const float* prompts, cons
   if (hw % 4) return set_error(PS_ERR_INPUT, "prompt_bias: ps*ps must be a multiple of 4");
   const int64_t n4 = (int64_t)P * C * hw / 4;
   if (n4 == 0) return PS_OK;
+  if (hw >= 64 && P <= 65535) {
+    const int cpb = pm_cpb(C, ps_, 4);
+    prompt_bias_pm_kernel<<<dim3(P, (C + cpb - 1) / cpb), 256, 0, (cudaStream_t)stream>>>(
+        latent, prompts, request_index, C, hw, cpb, (__nv_bfloat16*)h);
+    count_launch();
+    return check_launch("prompt_bias");
+  }
   prompt_bias_kernel<<<grid_for(n4, 256), 256, 0, (cudaStream_t)stream>>>(latent, prompts, request_index, P, C, hw,
                                                                           (__nv_bfloat16*)h);
   count_launch();
@@ -214,6 +409,13 @@ int ps_blend(void* stream, const float* latent, const void* h, const float* rate
   if (hw % 4) return set_error(PS_ERR_INPUT, "blend: ps*ps must be a multiple of 4");
   const int64_t n4 = (int64_t)P * C * hw / 4;
   if (n4 == 0) return PS_OK;
+  if (hw >= 64 && P <= 65535) {
+    const int cpb = pm_cpb(C, ps_, 4);
+    blend_pm_kernel<<<dim3(P, (C + cpb - 1) / cpb), 256, 0, (cudaStream_t)stream>>>(
+        latent, (const __nv_bfloat16*)h, rates, request_index, C, hw, cpb, out);
+    count_launch();
+    return check_launch("blend");
+  }
   blend_kernel<<<grid_for(n4, 256), 256, 0, (cudaStream_t)stream>>>(latent, (const __nv_bfloat16*)h, rates,
                                                                     request_index, P, C, hw, out);
   count_launch();
