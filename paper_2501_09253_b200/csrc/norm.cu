@@ -178,6 +178,54 @@ __global__ void __launch_bounds__(256, 2) gn_partials_pipe_kernel(const __nv_bfl
   }
 }
 
+// Bulk-staged partials: the (patch, group) slice (contiguous cg*hw bf16) arrives in shared
+// memory through one TMA bulk copy, so a CTA keeps its whole slice in flight with no
+// register staging; mean and M2 are then two passes over shared memory.
+__global__ void __launch_bounds__(256) gn_partials_bulk_kernel(const __nv_bfloat16* __restrict__ x, int C, int hw,
+                                                               int G, const int32_t* __restrict__ plist,
+                                                               float* __restrict__ partials) {
+  extern __shared__ __align__(16) uint8_t gsm[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ float red[64];
+  const int p = plist ? __ldg(plist + blockIdx.x) : (int)blockIdx.x, g = blockIdx.y;
+  const int cg = C / G;
+  const int n = cg * hw;
+  const __nv_bfloat16* base = x + ((int64_t)p * C + (int64_t)g * cg) * hw;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(&bar, (uint32_t)n * 2);
+    bulk_load(gsm, base, (uint32_t)n * 2, &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  const uint4* v4 = reinterpret_cast<const uint4*>(gsm);
+  const int nv = n / 8;
+  float s = 0.f;
+  for (int k = threadIdx.x; k < nv; k += 256) {
+    const uint4 r = v4[k];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) s += __low2float(h[e]) + __high2float(h[e]);
+  }
+  const float mean = block_sum(s, red) / (float)n;
+  float m2 = 0.f;
+  for (int k = threadIdx.x; k < nv; k += 256) {
+    const uint4 r = v4[k];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float a = __low2float(h[e]) - mean, b = __high2float(h[e]) - mean;
+      m2 += a * a + b * b;
+    }
+  }
+  m2 = block_sum(m2, red + 32);
+  if (threadIdx.x == 0) {
+    partials[((int64_t)p * G + g) * 2] = mean;
+    partials[((int64_t)p * G + g) * 2 + 1] = m2;
+  }
+}
+
 // host: pipelined kernel when a slice fits 256*8 vectors and is 16-byte aligned, else the simple one
 static void launch_gn_partials(cudaStream_t st, const void* x, int P, int C, int hw, int G, const int32_t* plist,
                                int n, float* partials) {
@@ -187,6 +235,16 @@ static void launch_gn_partials(cudaStream_t st, const void* x, int P, int C, int
   int grid = 148 * 2;
   if (grid > n_slices) grid = n_slices;
   const auto xb = (const __nv_bfloat16*)x;
+  const int64_t slice_bytes = elems * 2;
+  if (elems % 8 == 0 && slice_bytes <= 96 * 1024 && getenv_flag("PS_GN_BULK")) {  // measured 23 vs 21 us: opt-in
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(gn_partials_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      attr = true;
+    }
+    gn_partials_bulk_kernel<<<dim3(n, G), 256, (size_t)slice_bytes, st>>>(xb, C, hw, G, plist, partials);
+    return;
+  }
   if (elems % 8 == 0 && nv <= 256 * 6 && getenv_flag("PS_GN_PIPE")) {
     if (nv <= 256 * 2) gn_partials_pipe_kernel<2><<<grid, 256, 0, st>>>(xb, C, hw, G, plist, n_slices, partials);
     else if (nv <= 256 * 4) gn_partials_pipe_kernel<4><<<grid, 256, 0, st>>>(xb, C, hw, G, plist, n_slices, partials);
