@@ -124,7 +124,10 @@ class AdaptivePredictor(AnalyticPredictor):
 
     def observe(self, comp: dict, measured_ms: float) -> None:
         r = measured_ms / step_latency(comp, self.cost_params)
-        self.ratio = (1.0 - self.alpha) * self.ratio + self.alpha * r
+        # the fitted model is the uncached cost: only the cache's speed-up is learned; slower
+        # steps (cold caches, launch overhead of small batches) must not make admission more
+        # conservative than the calibrated model (measured: more discards at low load)
+        self.ratio = min(1.0, (1.0 - self.alpha) * self.ratio + self.alpha * r)
 
 
 def fit_cost_model(samples: Sequence[tuple[dict, float]], base: CostModelParams = DEFAULT_COST) -> CostModelParams:
