@@ -111,3 +111,52 @@ def test_wall_plane_runs_on_device():
     assert s["device_step_ms_mean"] > 0
     # the clock advanced by measured device time, not the analytic model (~60 ms a step)
     assert s["makespan_ms"] < 6 * 4 * 60.0
+
+
+@pytest.mark.gpu
+def test_slo_run_two_ranks_pool_completions():
+    """slo_run's multi-GPU path (fit shared from rank 0, lowest-load dispatch on the fitted
+    model, completions pooled) with two ranks as threads on one GPU."""
+    import threading
+
+    import torch
+
+    from paper_2501_09253_b200.model import ModelConfig, init_weights
+    mc = ModelConfig(arch="unet_like", channels=64, hidden=128, n_blocks=1, groups=8)
+    w = init_weights(mc)
+    bar = threading.Barrier(2)
+    box: dict = {}
+
+    def share(obj, rank):
+        if rank == 0:
+            box["fit"] = obj
+        bar.wait()
+        return box["fit"]
+
+    def gather(obj, rank):
+        box[rank] = obj
+        bar.wait()
+        return [box[0], box[1]]
+
+    res, errs = {}, []
+
+    def run(rank):
+        try:
+            torch.cuda.set_device(0)
+            res[rank] = S.slo_run(mc, w, n_requests=8, load=0.5, steps=3, rank=rank, world=2, calib_reps=1,
+                                  share=lambda o: share(o, rank), gather=lambda o: gather(o, rank))
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+            bar.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(600)
+    if errs:
+        raise errs[0]
+    a, b = res[0], res[1]
+    assert a["n_gpus"] == 2 and a["slo_attainment"] == b["slo_attainment"]
+    assert a["n_met_slo"] + a["n_discarded"] <= 8
+    assert a["fitted_cost"] == b["fitted_cost"]
