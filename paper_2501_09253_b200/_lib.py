@@ -12,7 +12,8 @@ import os
 
 from .errors import InputError, IntegrityError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpatchserve.so")
+LIB_PATH = os.environ.get("PS_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                         "libpatchserve.so")  # override: experiments only
 
 PS_OK, PS_ERR_INPUT, PS_ERR_INTEGRITY, PS_ERR_CUDA = 0, 1, 2, 3
 DTYPE_F32, DTYPE_BF16 = 0, 1

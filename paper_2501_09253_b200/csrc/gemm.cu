@@ -36,8 +36,15 @@ namespace ps {
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
-constexpr int GEMM_THREADS = 384;
-constexpr int GEMM_EPI_THREADS = 256;
+#ifndef PS_GEMM_LAZY_BIAS
+#define PS_GEMM_LAZY_BIAS (PS_GEMM_NWG > 2)
+#endif
+#ifndef PS_GEMM_NWG
+#define PS_GEMM_NWG 3
+#endif
+constexpr int GEMM_NWG = PS_GEMM_NWG;  // epilogue warpgroups
+constexpr int GEMM_THREADS = 128 + 128 * GEMM_NWG;
+constexpr int GEMM_EPI_THREADS = 128 * GEMM_NWG;
 
 // BN <= 256: double-buffered accumulators (2*BN TMEM columns), one MMA per k-step.
 // BN == 320: single accumulator (long-K GEMMs: conv3, FF2), two N=160 MMAs per k-step,
@@ -51,11 +58,12 @@ struct GemmCfg {
   static constexpr int A_BYTES = GEMM_BM * 128;
   static constexpr int B_BYTES = N_MMA * B_ROWS * 128;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (176 * 1024) / STAGE_BYTES > 8 ? 8 : (176 * 1024) / STAGE_BYTES;
+  static constexpr int STAGE_BUDGET = 176 * 1024;
+  static constexpr int STAGES = STAGE_BUDGET / STAGE_BYTES > 8 ? 8 : STAGE_BUDGET / STAGE_BYTES;
   static constexpr int TMEM_COLS = NBUF * BN <= 128 ? 128 : NBUF * BN <= 256 ? 256 : 512;
   static constexpr int HALF = BN / 2;  // columns per epilogue warp
-  static constexpr int STAGE_EPI = 2 * 16 * GEMM_BM * 4;  // transposed-store staging, per epilogue warpgroup
-  static constexpr int STAGE_TMA = 2 * 2 * GEMM_BM * 64;  // per warpgroup: two 128x32 bf16 store boxes
+  static constexpr int STAGE_EPI = GEMM_NWG > 2 ? 0 : GEMM_NWG * 16 * GEMM_BM * 4;  // transposed-store staging
+  static constexpr int STAGE_TMA = GEMM_NWG * 2 * GEMM_BM * 64;  // per warpgroup: two 128x32 bf16 store boxes
   static constexpr int SMEM = STAGES * STAGE_BYTES + STAGE_EPI + STAGE_TMA + 1024 /*align*/ + 256 /*barriers*/;
   static_assert(MMA_N % 16 == 0 && MMA_N >= 64 && MMA_N <= 256, "invalid UMMA N");
   static_assert(B_ROWS % 8 == 0, "B half rows must be whole 128B-swizzle atoms");
@@ -117,7 +125,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      const bool split = Cfg::NBUF == 1 || (p.epi_split && (BN / 2) % 32 == 0);
+      const bool split = GEMM_NWG > 2 || Cfg::NBUF == 1 || (p.epi_split && (BN / 2) % 32 == 0);
       mbar_init(&acc_empty[b], (PAIR ? 2 : 1) * (split ? GEMM_EPI_THREADS : GEMM_EPI_THREADS / 2));
     }
     fence_mbar_init();
@@ -265,16 +273,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint8_t* box_base = tma_stage + wg * 2 * (GEMM_BM * 64);  // two 8 KB boxes per warpgroup
     // transposed (NCHW / V^T) stores: a [16][128] fp32 tile per warpgroup, or with
     // warp_store a [16][32] tile per warp (its own 32 rows; only __syncwarp needed)
-    const bool wst = p.warp_store != 0;
+    const bool wst = GEMM_NWG > 2 || p.warp_store != 0;
     const int st_ld = wst ? 32 : GEMM_BM;
-    float* st = wst ? epi_stage + (warp - 4) * 16 * 32 : epi_stage + wg * 16 * GEMM_BM;
+    // GEMM_NWG > 2: the per-warp transpose tile aliases the warp's idle TMA-store box
+    // (2 KB; the box two stores back has been read once bulk_wait_read<1> returns)
+    float* st = GEMM_NWG > 2 ? nullptr : wst ? epi_stage + (warp - 4) * 16 * 32 : epi_stage + wg * 16 * GEMM_BM;
     const int st_row = wst ? lane : row;
     const int ci = wst ? lane >> 1 : row >> 3, seg = wst ? lane & 1 : row & 7;  // transposed role
     // NBUF == 1 or epi_split: the two warpgroups split every tile's columns (each tile's
     // accumulator drains in half the time); else warpgroup g takes the tiles of buffer g
-    const bool split = Cfg::NBUF == 1 || (p.epi_split && (BN / 2) % 32 == 0);
-    const int c_lo = split ? wg * (BN / 2) : 0;
-    const int c_hi = split ? c_lo + BN / 2 : BN;
+    const bool split = GEMM_NWG > 2 || Cfg::NBUF == 1 || (p.epi_split && (BN / 2) % 32 == 0);
+    // GEMM_NWG > 2: 32-column chunks dealt round-robin to the warpgroups
+    const int c_step = GEMM_NWG > 2 ? 32 * GEMM_NWG : 32;
+    const int c_lo = GEMM_NWG > 2 ? wg * 32 : split ? wg * (BN / 2) : 0;
+    const int c_hi = GEMM_NWG > 2 ? BN : split ? c_lo + BN / 2 : BN;
     int n_store = 0;
     int li = 0;
     // the accumulator buffer is released on the leader CTA's barrier (the MMA issuer's)
@@ -321,7 +333,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int nb = n_tile * BN + c;
         float v[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) + bv[i];
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) + (PS_GEMM_LAZY_BIAS ? 0.f : bv[i]);
+        if (PS_GEMM_LAZY_BIAS && p.bias != nullptr) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + nb) + q);
+            v[4 * q] += b4.x; v[4 * q + 1] += b4.y; v[4 * q + 2] += b4.z; v[4 * q + 3] += b4.w;
+          }
+        }
         const bool cl_tma = p.store_tma &&
                             (p.epi == EPI_STORE_CL || p.epi == EPI_GELU_CL || (p.epi == EPI_SPLIT_VT && nb < p.n_split));
         if (cl_tma) {
@@ -395,6 +414,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               rs0 = __ldg(reinterpret_cast<const uint4*>(p.resid + off_v));
               rs1 = __ldg(reinterpret_cast<const uint4*>(p.resid + off_v) + 1);
             }
+            if constexpr (GEMM_NWG > 2) {
+              if (lane == 0 && p.store_tma) bulk_wait_read<1>();
+              __syncwarp();
+              st = reinterpret_cast<float*>(tma_stage + (warp - 4) * 4096 + (n_store & 1) * 2048);
+            }
 #pragma unroll
             for (int i = 0; i < 16; ++i) st[i * st_ld + st_row] = v[s16 + i];
             if (wst) __syncwarp();
@@ -450,14 +474,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       };
       const int c_end = min(c_hi, p.N - n_tile * BN);  // columns of this tile for this warpgroup
 #pragma unroll 1
-      for (int c = c_lo; c < c_end; c += 32) {
+      for (int c = c_lo; c < c_end; c += c_step) {
         uint32_t r[32];
         PS_TMEM_LD32(tmem + lane_base + buf * BN + c, r);
         float bv[32];
-        load_bias(bv, n_tile * BN + c);
+        if (!PS_GEMM_LAZY_BIAS) load_bias(bv, n_tile * BN + c);
         tmem_ld_wait();
         reg_fence32(r);
-        if (c + 32 >= c_end) {
+        if (c + c_step >= c_end) {
           // last chunk of this tile for this warpgroup: hand the accumulator back early
           tc_fence_before();
           release(buf);
