@@ -231,6 +231,106 @@ __global__ void __launch_bounds__(256) csp_split_rows_kernel(const uint64_t* __r
   }
 }
 
+// Fused step ends for the fixed-composition pipeline (pipeline.py):
+//  * split + prompt bias: the image rows land in the CSP fp32 latents AND as the first block
+//    input h = bf16(latent + prompt[request]) (model.py:163) -- one read of the latents;
+//  * blend + reassemble: (1 - r) x + r tanh(h) (model.py:129-131) written straight into the
+//    per-request output images -- no CSP intermediate.
+__global__ void __launch_bounds__(256) csp_split_bias_rows_kernel(const uint64_t* __restrict__ img_ptrs,
+                                                                  const int32_t* __restrict__ req_off,
+                                                                  const int32_t* __restrict__ sides, int n_req,
+                                                                  int C, int ps, int cpb,
+                                                                  const float* __restrict__ prompts,
+                                                                  float* __restrict__ patches,
+                                                                  __nv_bfloat16* __restrict__ h) {
+  int pr = blockIdx.x, req = 0;
+  for (; req < n_req; ++req) {
+    const int sd = __ldg(sides + req);
+    if (pr < sd) break;
+    pr -= sd;
+  }
+  if (req >= n_req) return;
+  const int side = __ldg(sides + req), L = side * ps, p0 = __ldg(req_off + req) + pr * side;
+  const float* img = reinterpret_cast<const float*>(img_ptrs[req]);
+  const float* pr_bias = prompts + (int64_t)req * C;
+  const int c0 = blockIdx.y * cpb, nc = min(cpb, C - c0);
+  const int vrow = L / 4;
+  const int n = nc * ps * vrow;
+  for (int base = threadIdx.x; base < n; base += 256 * PM_UNR) {
+    float4 v[PM_UNR];
+    int64_t dst[PM_UNR];
+    float bb[PM_UNR];
+#pragma unroll
+    for (int u = 0; u < PM_UNR; ++u) {
+      const int i = base + u * 256;
+      dst[u] = -1;
+      if (i < n) {
+        const int xv = i % vrow, y = (i / vrow) % ps, c = c0 + i / (vrow * ps);
+        const int x = xv * 4, pc = x / ps, xp = x - pc * ps;
+        v[u] = __ldg(reinterpret_cast<const float4*>(img + ((int64_t)c * L + (int64_t)pr * ps + y) * L + x));
+        dst[u] = (((int64_t)(p0 + pc) * C + c) * ps + y) * ps + xp;
+        bb[u] = __ldg(pr_bias + c);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PM_UNR; ++u)
+      if (dst[u] >= 0) {
+        *reinterpret_cast<float4*>(patches + dst[u]) = v[u];
+        uint2 o;
+        o.x = pack_bf16(v[u].x + bb[u], v[u].y + bb[u]);
+        o.y = pack_bf16(v[u].z + bb[u], v[u].w + bb[u]);
+        *reinterpret_cast<uint2*>(h + dst[u]) = o;
+      }
+  }
+}
+
+__global__ void __launch_bounds__(256) blend_reassemble_kernel(const float* __restrict__ lat,
+                                                               const __nv_bfloat16* __restrict__ hh,
+                                                               const float* __restrict__ rates,
+                                                               const uint64_t* __restrict__ img_ptrs,
+                                                               const int32_t* __restrict__ req_off,
+                                                               const int32_t* __restrict__ sides, int n_req, int C,
+                                                               int ps, int cpb) {
+  const int p = blockIdx.x, c0 = blockIdx.y * cpb;
+  int req, side, k;
+  pm_locate(p, req_off, sides, n_req, req, side, k);
+  const int r = k / side, cc = k - r * side, L = side * ps;
+  float* img = reinterpret_cast<float*>(img_ptrs[req]);
+  const float rate = __ldg(rates + req);
+  const int vps = ps / 4;
+  const int nc = min(cpb, C - c0);
+  const int n = nc * ps * vps;
+  for (int base = threadIdx.x; base < n; base += 256 * PM_UNR) {
+    float4 x[PM_UNR];
+    uint2 hv[PM_UNR];
+    int64_t io[PM_UNR];
+#pragma unroll
+    for (int u = 0; u < PM_UNR; ++u) {
+      const int i = base + u * 256;
+      io[u] = -1;
+      if (i < n) {
+        const int xv = i % vps, y = (i / vps) % ps, c = c0 + i / (vps * ps);
+        const int64_t po = (((int64_t)p * C + c) * ps + y) * ps + xv * 4;
+        x[u] = __ldg(reinterpret_cast<const float4*>(lat + po));
+        hv[u] = __ldg(reinterpret_cast<const uint2*>(hh + po));
+        io[u] = ((int64_t)c * L + (int64_t)r * ps + y) * L + (int64_t)cc * ps + xv * 4;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PM_UNR; ++u)
+      if (io[u] >= 0) {
+        const __nv_bfloat162 h01 = *reinterpret_cast<const __nv_bfloat162*>(&hv[u].x);
+        const __nv_bfloat162 h23 = *reinterpret_cast<const __nv_bfloat162*>(&hv[u].y);
+        float4 o;
+        o.x = (1.f - rate) * x[u].x + rate * tanhf(__low2float(h01));
+        o.y = (1.f - rate) * x[u].y + rate * tanhf(__high2float(h01));
+        o.z = (1.f - rate) * x[u].z + rate * tanhf(__low2float(h23));
+        o.w = (1.f - rate) * x[u].w + rate * tanhf(__high2float(h23));
+        *reinterpret_cast<float4*>(img + io[u]) = o;
+      }
+  }
+}
+
 template <bool TO_PATCHES>
 static int csp_copy(cudaStream_t st, const uint64_t* ptrs, const int32_t* off, const int32_t* sides, int n_req,
                     int C, int ps, int dtype, void* patches, int P) {
@@ -353,6 +453,31 @@ __global__ void convert_kernel(const S* __restrict__ src, D* __restrict__ dst, i
 using namespace ps;
 
 extern "C" {
+
+int ps_csp_split_bias(void* stream, const uint64_t* src_ptrs, const int32_t* request_offset, const int32_t* sides,
+                      int n_req, int C, int ps_, float* dst, int n_patches, const float* prompts, void* h) {
+  if (n_req < 1 || C < 1 || ps_ < 1 || ps_ % 4) return set_error(PS_ERR_INPUT, "csp_split_bias: bad sizes");
+  if (n_patches == 0) return PS_OK;
+  if (n_patches > 65535) return set_error(PS_ERR_INPUT, "csp_split_bias: too many patches");
+  const int cpb = pm_cpb(C, ps_, 4);
+  csp_split_bias_rows_kernel<<<dim3(n_patches, (C + cpb - 1) / cpb), 256, 0, (cudaStream_t)stream>>>(
+      src_ptrs, request_offset, sides, n_req, C, ps_, cpb, prompts, dst, (__nv_bfloat16*)h);
+  count_launch();
+  return check_launch("csp_split_bias");
+}
+
+int ps_blend_reassemble(void* stream, const float* latent, const void* h, const float* rates,
+                        const int32_t* request_offset, const int32_t* sides, int n_req, int C, int ps_,
+                        const uint64_t* dst_ptrs, int n_patches) {
+  if (n_req < 1 || C < 1 || ps_ < 1 || ps_ % 4) return set_error(PS_ERR_INPUT, "blend_reassemble: bad sizes");
+  if (n_patches == 0) return PS_OK;
+  if (n_patches > 65535) return set_error(PS_ERR_INPUT, "blend_reassemble: too many patches");
+  const int cpb = pm_cpb(C, ps_, 4);
+  blend_reassemble_kernel<<<dim3(n_patches, (C + cpb - 1) / cpb), 256, 0, (cudaStream_t)stream>>>(
+      latent, (const __nv_bfloat16*)h, rates, dst_ptrs, request_offset, sides, n_req, C, ps_, cpb);
+  count_launch();
+  return check_launch("blend_reassemble");
+}
 
 int ps_csp_split(void* stream, const uint64_t* src_ptrs, const int32_t* request_offset, const int32_t* sides,
                  int n_req, int C, int ps_, int dtype, void* dst, int n_patches) {

@@ -28,7 +28,7 @@ import torch
 from . import _lib
 from ._dev import require_cuda
 from .csp import split
-from .model import ModelConfig, blend_batch, prompt_bias, rate_schedule
+from .model import ModelConfig, rate_schedule
 from .patched import run_block
 
 
@@ -67,16 +67,18 @@ class DenoisePipeline:
     def _step(self, k: int) -> None:
         b = self.batches[k]
         src_ptrs = b.device()
-        _lib.call("ps_csp_split", torch.cuda.current_stream().cuda_stream, self._in_ptrs[k].data_ptr(),
-                  src_ptrs["request_offset"].data_ptr(), src_ptrs["sides"].data_ptr(), b.n_requests, self.C,
-                  self.ps, _lib.DTYPE_F32, b.data.data_ptr(), b.n_patches)
-        h = prompt_bias(b, b.data, self.bias[k])
+        st = torch.cuda.current_stream().cuda_stream
+        # split + prompt bias in one pass over the input latents (csp.py:161-167, model.py:163)
+        h = torch.empty(b.data.shape, dtype=torch.bfloat16, device=self.dev)
+        _lib.call("ps_csp_split_bias", st, self._in_ptrs[k].data_ptr(), src_ptrs["request_offset"].data_ptr(),
+                  src_ptrs["sides"].data_ptr(), b.n_requests, self.C, self.ps, b.data.data_ptr(), b.n_patches,
+                  self.bias[k].data_ptr(), h.data_ptr())
         for ops in self.weights:
             h = run_block(b, h, ops)
-        new = blend_batch(b, b.data, h, self.rates[k])
-        _lib.call("ps_csp_reassemble", torch.cuda.current_stream().cuda_stream, new.data_ptr(),
-                  self._out_ptrs[k].data_ptr(), src_ptrs["request_offset"].data_ptr(), src_ptrs["sides"].data_ptr(),
-                  b.n_requests, self.C, self.ps, _lib.DTYPE_F32, b.n_patches)
+        # blend straight into the per-request outputs (model.py:129-131, csp.py:196-214)
+        _lib.call("ps_blend_reassemble", st, b.data.data_ptr(), h.data_ptr(), self.rates[k].data_ptr(),
+                  src_ptrs["request_offset"].data_ptr(), src_ptrs["sides"].data_ptr(), b.n_requests, self.C,
+                  self.ps, self._out_ptrs[k].data_ptr(), b.n_patches)
 
     def prepare(self) -> None:
         """Upload weights (eager warm-up) and capture one graph per buffer set."""
