@@ -248,7 +248,7 @@ def run_ours(args):
 
 
 def measure_slo(cfg, weights, rank, world, barrier):
-    """SLO-satisfaction % of the metric: a 64-request mixed trace (0.4/0.35/0.25 low/med/high,
+    """SLO-satisfaction % of the metric: a 128-request mixed trace (0.4/0.35/0.25 low/med/high,
     50 steps, SLO = 3x standalone latency) served in the wall plane (serving.slo_run): every
     denoising step runs on the GPU with the patch cache in the loop and the clock is its
     measured device time; offered load = 0.9 x the fitted capacity of `world` GPUs."""
@@ -267,7 +267,7 @@ def measure_slo(cfg, weights, rank, world, barrier):
             dist.all_gather_object(out, obj)
             return out
     barrier()
-    r = slo_run(cfg, weights, n_requests=64, load=0.9, rank=rank, world=world, share=share, gather=gather)
+    r = slo_run(cfg, weights, n_requests=128, load=0.9, rank=rank, world=world, share=share, gather=gather)
     r["plane"] = ("wall: step time = measured device time of each eager step (split, bias, 7 blocks with the "
                   "cache, blend, reassemble); SLO budgets and admission on the cost model fitted to measured "
                   "B200 step times")
