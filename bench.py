@@ -10,7 +10,7 @@ seconds).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 The SLO-satisfaction half of the metric ("slo" in the JSON line) serves a
-64-request mixed trace in the wall-clock serving plane (serving.slo_run):
+128-request mixed trace in the wall-clock serving plane (serving.slo_run):
 every denoising step runs on the GPU(s) and advances the clock by its measured
 device time; SLO budgets are 3x the standalone latency of the cost model fitted
 to measured B200 step times.  --no-slo skips it.
