@@ -142,6 +142,17 @@ typedef struct ps_gemm_args {
 } ps_gemm_args;
 int ps_gemm(void* stream, const ps_gemm_args* args);
 
+/* Fused feed-forward + residual on CTA pairs (kernels.py:124-127 + patched.py:215-217):
+ * out NCHW (P, c_real, ps, ps) = W2 gelu_tanh(W1 x + b1) + b2 (+ resid NCHW), x CL [M, Cp],
+ * W1 [Hp, Cp], W2 [Cp, Hp] bf16, biases fp32; the hidden activations never leave the SM.
+ * Cp in {128, 192, 256, 320}, Hp % 128 == 0, ps*ps and M multiples of 128; m_map optional
+ * (DEVICE list of 128-row tiles).  Bit-identical to the FF1 / FF2 ps_gemm pair. */
+/* Profiling: device counters [14] of per-role barrier-wait cycles of later ps_feed_forward launches. */
+int ps_feed_forward_debug(unsigned long long* counters);
+int ps_feed_forward(void* stream, const void* x, int M, int Cp, const void* w1, const float* b1, const void* w2,
+                    const float* b2, int Hp, int c_real, int ps, const void* resid, void* out, const int32_t* m_map,
+                    int m_count);
+
 /* Per-image attention over the CSP token order (patched_self_attention,
  * patched.py:154-176 -> attend_tokens/_attend_single, kernels.py:230-267).
  * qk: [T, 2*Dp] bf16 (Q then K per token), vt: [Dp, ldv] bf16 (V transposed, ldv % 8 == 0),

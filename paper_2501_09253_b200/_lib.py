@@ -61,6 +61,7 @@ _SIGS = {
     "ps_copy_segments": ([p, p, p, C.c_int, p, p, i64], C.c_int),
     "ps_from_cl": ([p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, p], C.c_int),
     "ps_gemm": ([p, C.POINTER(GemmArgs)], C.c_int),
+    "ps_feed_forward": ([p, p, C.c_int, C.c_int, p, p, p, p, C.c_int, C.c_int, C.c_int, p, p, p, C.c_int], C.c_int),
     "ps_attention": ([p, p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, C.c_int, p], C.c_int),
     "ps_attention_pairs": ([p, p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, C.c_int, p], C.c_int),
     "ps_attention_splitkv": ([p, p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, p, p, p, C.c_int, p, p, p],
@@ -71,6 +72,7 @@ _SIGS = {
                           C.c_int),
     "ps_attention_debug": ([p], C.c_int),
     "ps_attention_trace": ([p], C.c_int),
+    "ps_feed_forward_debug": ([p], C.c_int),
     "ps_pairwise_plan": ([i64, p, p, p, p, p, p], C.c_int),
     "ps_cache_predict": ([p, p, C.c_int, i64, p, p, p, p, f64, C.c_int, p, C.c_int, p, C.c_int, p, C.c_int, p, p, p],
                          C.c_int),

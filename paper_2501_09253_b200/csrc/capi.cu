@@ -108,6 +108,7 @@ using namespace ps;
 
 static unsigned long long* g_attn_dbg = nullptr;  // profiling hook (ps_attention_debug)
 static long long* g_attn_trace = nullptr;           // profiling hook (ps_attention_trace)
+static unsigned long long* g_ff_dbg = nullptr;      // profiling hook (ps_feed_forward_debug)
 
 extern "C" {
 
@@ -224,6 +225,11 @@ int ps_attention_pairs(void* stream, const void* qk, const void* vt, int ldv, in
 
 // Profiling only: device counters [8] that later attention launches accumulate
 // per-role barrier-wait cycles into (NULL disables).
+int ps_feed_forward_debug(unsigned long long* counters) {
+  g_ff_dbg = counters;
+  return PS_OK;
+}
+
 int ps_attention_trace(long long* stamps) {
   g_attn_trace = stamps;
   return PS_OK;
@@ -520,5 +526,40 @@ int ps_attention_peer(void* stream, const void* qk, const void* vt, int ldv, int
   p.kb_row = kb_row;
   p.peer_maps = (const CUtensorMap*)peer_maps;
   return attention_launch(tq, tk, tv, p, Dp, (cudaStream_t)stream);
+}
+}  // extern "C"
+
+extern "C" {
+// Fused feed-forward + residual (ffused.cu): out NCHW = W2 gelu(W1 x + b1) + b2 + resid.
+int ps_feed_forward(void* stream, const void* x, int M, int Cp, const void* w1, const float* b1, const void* w2,
+                    const float* b2, int Hp, int c_real, int ps, const void* resid, void* out, const int32_t* m_map,
+                    int m_count) {
+  if (!x || !w1 || !w2 || !b1 || !b2 || !out) return set_error(PS_ERR_INPUT, "feed_forward: null pointer");
+  if (Cp % 64 || Cp < 128 || Cp > 320) return set_error(PS_ERR_INPUT, "feed_forward: Cp %d unsupported", Cp);
+  if (Hp % 128 || Hp < 128) return set_error(PS_ERR_INPUT, "feed_forward: hidden %d must be a multiple of 128", Hp);
+  const int hw = ps * ps;
+  if (hw % 128 || M % 128) return set_error(PS_ERR_INPUT, "feed_forward: ps*ps and M must be multiples of 128");
+  if (c_real < 1 || c_real > Cp) return set_error(PS_ERR_INPUT, "feed_forward: bad c_real");
+  CUtensorMap tx, t1, t2;
+  int rc = make_tmap_2d(&tx, x, M, Cp, Cp, 128);
+  if (!rc) rc = make_tmap_2d(&t1, w1, Hp, Cp, Cp, 64);
+  if (!rc) rc = make_tmap_2d(&t2, w2, Cp, Hp, Hp, Cp / 4);
+  if (rc) return rc;
+  FfParams p{};
+  p.M = M;
+  p.m_map = m_map;
+  p.m_count = m_map ? m_count : 0;
+  p.hp = Hp;
+  p.b1 = b1;
+  p.b2 = b2;
+  p.c_real = c_real;
+  p.hw = hw;
+  p.resid = (const __nv_bfloat16*)resid;
+  p.out = (__nv_bfloat16*)out;
+  p.dbg = g_ff_dbg;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return ff_launch(tx, t1, t2, p, Cp, sms, (cudaStream_t)stream);
 }
 }  // extern "C"

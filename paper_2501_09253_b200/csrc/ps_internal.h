@@ -36,6 +36,21 @@ struct GemmParams {
   int warp_store;           // channels-last TMA stores per warp (32x32 boxes) instead of per warpgroup
 };
 
+struct FfParams {
+  int M;                       // tokens (rows of x)
+  const int* m_map;            // optional device list of 128-row tiles (compaction)
+  int m_count;
+  int hp;                      // hidden units (multiple of 128)
+  const float* b1;             // [hp]
+  const float* b2;             // [Cp]
+  int c_real, hw;              // output channels, pixels per patch (NCHW output)
+  const __nv_bfloat16* resid;  // NCHW residual or null
+  __nv_bfloat16* out;          // NCHW (P, c_real, ps, ps)
+  unsigned long long* dbg;     // optional role wait counters [12] (profiling)
+};
+int ff_launch(const CUtensorMap& x, const CUtensorMap& w1, const CUtensorMap& w2, const FfParams& p, int cp,
+              int sms, cudaStream_t st);
+
 int set_error(int code, const char* fmt, ...);
 int check_launch(const char* what);
 void count_launch();

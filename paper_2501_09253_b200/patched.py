@@ -285,6 +285,16 @@ class Ctx:
     def feed_forward(self, a: Act, prm, resid):
         dp = device_params(prm, a.C)
         x = self.as_cl(a)
+        if (resid is not None and FF_FUSED and dp["cp"] in (128, 192, 256, 320) and dp["hp"] % 128 == 0
+                and self.hw % 128 == 0 and self.T % 128 == 0):
+            # one fused kernel: the hidden activations stay on chip (ffused.cu)
+            out = self.empty_nchw(dp["c_out"])
+            rows = self.rows
+            _lib.call("ps_feed_forward", stream(), x.data_ptr(), self.T, dp["cp"], dp["w1"].data_ptr(),
+                      dp["b1"].data_ptr(), dp["w2"].data_ptr(), dp["b2"].data_ptr(), dp["hp"], dp["c_out"], self.ps,
+                      resid.data_ptr(), out.data_ptr(), None if rows is None else rows[0].data_ptr(),
+                      0 if rows is None else rows[1])
+            return Act("nchw", out, dp["c_out"])
         # hidden activations in 128x64 tile-major order: the second GEMM streams
         # each of its A boxes as one contiguous 16 KB block from HBM
         h = torch.empty((round_up(self.T, 128), dp["hp"]), dtype=BF16, device=self.device)
@@ -512,6 +522,8 @@ def sm_count() -> int:
     return _SMS
 
 
+# fused FF1 + GELU + FF2 + residual on CTA pairs (ffused.cu); PS_FF_FUSED=0 -> two GEMMs
+FF_FUSED = os.environ.get("PS_FF_FUSED", "1") == "1"
 # split-KV planning (splitkv_plan); PS_SPLITKV=0 disables it
 SPLITKV = os.environ.get("PS_SPLITKV", "1") != "0"
 SPLITKV_ALL = os.environ.get("PS_SPLITKV_ALL", "0") == "1"  # also outside the split-image path

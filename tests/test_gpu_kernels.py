@@ -264,3 +264,33 @@ def test_attention_pair_kernel_bit_identical_to_single():
             patched.USE_PAIRS = True
     torch.cuda.synchronize()
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("C,H,lat,compact", [(320, 1280, (64, 32, 96), False), (320, 1280, (64, 96), True),
+                                             (128, 256, (32, 64), False), (192, 384, (64,), False)])
+def test_fused_feed_forward_bit_identical_to_two_gemms(C, H, lat, compact, monkeypatch):
+    """ps_feed_forward (FF1 + GELU + FF2 + residual with the hidden kept on chip, CTA pairs)
+    equals the two-GEMM path bit for bit, with and without a compaction tile map."""
+    import paper_2501_09253_b200 as ps
+    from paper_2501_09253_b200 import patched
+    torch.manual_seed(1)
+    cfg = ps.ModelConfig(arch="dit_like", channels=C, hidden=H, n_blocks=1, groups=8, seed=3)
+    ff = ps.init_weights(cfg)[0][2][1]
+    b = ps.split([(f"r{i}", torch.randn(C, d, d)) for i, d in enumerate(lat)], patch_size=32)
+    x = torch.randn(b.n_patches, C, 32, 32, device="cuda").to(torch.bfloat16)
+    res = torch.randn(b.n_patches, C, 32, 32, device="cuda").to(torch.bfloat16)
+    outs = []
+    for fused in (False, True):
+        monkeypatch.setattr(patched, "FF_FUSED", fused)
+        ctx = patched.Ctx(b)
+        if compact:
+            act = np.arange(0, b.n_patches, 2)
+            ctx.rows = patched._row_tiles(ctx, act)
+        y = ctx.feed_forward(patched.Act("nchw", x, C), ff, res)
+        outs.append(y.t.clone())
+    torch.cuda.synchronize()
+    if compact:
+        act = np.arange(0, b.n_patches, 2)
+        assert torch.equal(outs[0][act], outs[1][act])
+    else:
+        assert torch.equal(outs[0], outs[1])
