@@ -557,6 +557,8 @@ int ps_feed_forward(void* stream, const void* x, int M, int Cp, const void* w1, 
   p.resid = (const __nv_bfloat16*)resid;
   p.out = (__nv_bfloat16*)out;
   p.dbg = g_ff_dbg;
+  static const int ff_ts = getenv("PS_FF_TS") ? atoi(getenv("PS_FF_TS")) : 1;  // GELU(H) through TMEM (TS MMA) vs shared memory
+  p.ts = ff_ts;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

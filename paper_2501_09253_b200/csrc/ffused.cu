@@ -6,9 +6,9 @@
 // to HBM and reads them back.  Here a CTA pair owns 256 tokens and walks the hidden
 // dimension in chunks of 128:
 //   MMA1(c): H = X W1[c]^T           (M = 256, N = 128, K = Cp; A = X resident in smem)
-//   epilogue: H -> +b1 -> bf16 -> GELU -> shared memory (the A operand of MMA2)
+//   epilogue: H -> +b1 -> bf16 -> GELU -> TMEM (the A operand of MMA2; shared memory with p.ts = 0)
 //   MMA2(c): O += H W2[:, c]^T       (M = 256, N = Cp as two MMAs, K = 128)
-// O (Cp fp32 columns) and the H chunk (128 columns) live in TMEM (<= 448 of 512);
+// O (Cp fp32 columns), the H chunk (128) and its bf16 GELU (64) live in TMEM (<= 512);
 // weights stream through one ring of 10 KB slots, each CTA loading its half of every
 // MMA's B operand.  MMA1(c + 1) runs while the epilogue turns H(c) into MMA2's operand.
 // Arithmetic is the 2-GEMM path's exactly (same MMA accumulation order, same bf16 GELU,
@@ -37,9 +37,10 @@ struct FfCfg {
   static constexpr int W1_ROWS = FF_HC / 2;   // this CTA's B rows of one MMA1 (64)
   static constexpr int STG = 12 * 2048;       // per-warp transpose tiles of the output epilogue
   static constexpr int SMEM = X_BYTES + H_BYTES + FF_NS * FF_SLOT + STG + 1024 + 512;
-  static constexpr int O_COL = 0, H_COL = CP;
+  // TMEM: O (Cp fp32) | H chunk (128 fp32) | GELU(H) chunk as bf16 pairs (64), MMA2's A (p.ts)
+  static constexpr int O_COL = 0, H_COL = CP, HB_COL = CP + FF_HC;
   static_assert(CP % 64 == 0 && NHALF % 16 == 0 && W2_ROWS % 8 == 0 && W2_ROWS * 128 <= FF_SLOT, "Cp");
-  static_assert(CP + FF_HC <= 512, "TMEM");
+  static_assert(CP + FF_HC + FF_HC / 2 <= 512, "TMEM");
 };
 
 template <int CP>
@@ -215,10 +216,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
                 if (lane == 0) {
                   const uint8_t* wt = sW + s * FF_SLOT;
 #pragma unroll
-                  for (int k = 0; k < 4; ++k)
-                    mma_bf16_ss_2sm(tmem + Cfg::O_COL + nn * Cfg::NHALF,
-                                    sdesc_sw128(sH + kk * FF_BM * 128 + k * 32), sdesc_sw128(wt + k * 32), idesc2,
-                                    (c | kk | k) != 0);
+                  for (int k = 0; k < 4; ++k) {
+                    if (p.ts)
+                      mma_bf16_ts_2sm(tmem + Cfg::O_COL + nn * Cfg::NHALF, tmem + Cfg::HB_COL + kk * 32 + k * 8,
+                                      sdesc_sw128(wt + k * 32), idesc2, (c | kk | k) != 0);
+                    else
+                      mma_bf16_ss_2sm(tmem + Cfg::O_COL + nn * Cfg::NHALF,
+                                      sdesc_sw128(sH + kk * FF_BM * 128 + k * 32), sdesc_sw128(wt + k * 32), idesc2,
+                                      (c | kk | k) != 0);
+                  }
                   mma_commit_2sm(&w_empty[s], 0x3);
                   if (kk == 1 && nn == 1) {
                     mma_commit_2sm(hs_empty, 0x3);
@@ -276,6 +282,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
                                                      __uint_as_float(r1[4 * i + 3]) + bq[8 + i].w));
         }
         tw(hs_empty, (g & 1) ^ 1, 1);  // MMA2 of the previous chunk has read the buffer
+        if (p.ts) {  // A operand in TMEM: 32 columns of bf16 pairs per warpgroup, no smem traffic
+          PS_TMEM_ST16(tmem + lane_base + Cfg::HB_COL + wg * 32, pk);
+          PS_TMEM_ST16(tmem + lane_base + Cfg::HB_COL + wg * 32 + 16, (pk + 16));
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive_cluster(hs_full_l);
+          continue;
+        }
         uint8_t* hrow = sH + wg * FF_BM * 128 + row * 128;
 #pragma unroll
         for (int j = 0; j < 8; ++j)

@@ -41,6 +41,7 @@ struct FfParams {
   const int* m_map;            // optional device list of 128-row tiles (compaction)
   int m_count;
   int hp;                      // hidden units (multiple of 128)
+  int ts;                      // MMA2 reads GELU(H) from TMEM (else from shared memory)
   const float* b1;             // [hp]
   const float* b2;             // [Cp]
   int c_real, hw;              // output channels, pixels per patch (NCHW output)

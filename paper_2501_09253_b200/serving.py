@@ -692,6 +692,14 @@ def slo_run(model_cfg, weights, n_requests: int = 64, load: float = 0.9, steps: 
     # -- makes budgets ~3x tighter than the mixed, churning batches can meet: FCFS 0.05 at 0.9)
     samples = measure_step_ms(model_cfg, weights, CALIBRATION_COMPS, reps=calib_reps)
     fit = fit_cost_model(samples)
+    # a transient on the box (seen once: one composition measured 6x its steady time) skews the
+    # whole fit; re-measure compositions the fit misses by > 50% once and refit
+    bad = [i for i, (c, ms) in enumerate(samples) if abs(step_latency(c, fit) - ms) > 0.5 * ms]
+    if bad:
+        again = measure_step_ms(model_cfg, weights, [samples[i][0] for i in bad], reps=calib_reps)
+        for i, (c, ms) in zip(bad, again):
+            samples[i] = (c, min(ms, samples[i][1]))
+        fit = fit_cost_model(samples)
     if share is not None:
         fit = share(fit)
     full = {"low": 4, "med": 4, "high": 4}
