@@ -37,6 +37,39 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // slice is read once into registers (up to GN_REG 16-byte vectors per thread);
 // mean and then M2 are reduced from registers (two-pass numerics, one pass of HBM).
 constexpr int GN_REG = 5;
+// (mean, M2) of one slice of nv 16-byte vectors held in registers (nv <= GN_REG * 256);
+// shared by gn_partials_kernel and the fused gn_frames_kernel (identical arithmetic)
+__device__ __forceinline__ void gn_slice_regs(const __nv_bfloat16* __restrict__ base, int nv, float n, float* red,
+                                              float& mean, float& m2) {
+  uint4 reg[GN_REG];
+#pragma unroll
+  for (int i = 0; i < GN_REG; ++i) {
+    const int k = threadIdx.x + i * blockDim.x;
+    reg[i] = k < nv ? __ldg(reinterpret_cast<const uint4*>(base) + k) : make_uint4(0, 0, 0, 0);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < GN_REG; ++i) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&reg[i]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s += __low2float(h[k]) + __high2float(h[k]);
+  }
+  mean = block_sum(s, red) / n;
+  m2 = 0.f;
+#pragma unroll
+  for (int i = 0; i < GN_REG; ++i) {
+    if (threadIdx.x + i * blockDim.x < nv) {
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&reg[i]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float a = __low2float(h[k]) - mean, b = __high2float(h[k]) - mean;
+        m2 += a * a + b * b;
+      }
+    }
+  }
+  m2 = block_sum(m2, red);
+}
+
 __global__ void __launch_bounds__(256, 4) gn_partials_kernel(const __nv_bfloat16* __restrict__ x, int C, int hw, int G,
                                                           const int32_t* __restrict__ plist,
                                                           float* __restrict__ partials) {
@@ -48,32 +81,12 @@ __global__ void __launch_bounds__(256, 4) gn_partials_kernel(const __nv_bfloat16
   const bool vec = (n % 8 == 0) && (((uintptr_t)base & 15) == 0) && (n / 8 <= (int64_t)GN_REG * blockDim.x);
   float mean, m2 = 0.f;
   if (vec) {
-    uint4 reg[GN_REG];
-    const int nv = (int)(n / 8);
-#pragma unroll
-    for (int i = 0; i < GN_REG; ++i) {
-      const int k = threadIdx.x + i * blockDim.x;
-      reg[i] = k < nv ? __ldg(reinterpret_cast<const uint4*>(base) + k) : make_uint4(0, 0, 0, 0);
+    gn_slice_regs(base, (int)(n / 8), (float)n, red, mean, m2);
+    if (threadIdx.x == 0) {
+      partials[((int64_t)p * G + g) * 2] = mean;
+      partials[((int64_t)p * G + g) * 2 + 1] = m2;
     }
-    float s = 0.f;
-#pragma unroll
-    for (int i = 0; i < GN_REG; ++i) {
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&reg[i]);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) s += __low2float(h[k]) + __high2float(h[k]);
-    }
-    mean = block_sum(s, red) / (float)n;
-#pragma unroll
-    for (int i = 0; i < GN_REG; ++i) {
-      if (threadIdx.x + i * blockDim.x < nv) {
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&reg[i]);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float a = __low2float(h[k]) - mean, b = __high2float(h[k]) - mean;
-          m2 += a * a + b * b;
-        }
-      }
-    }
+    return;
   } else if ((n % 8 == 0) && (((uintptr_t)base & 15) == 0)) {
     // slice larger than the register budget: two vectorised passes (the second hits L2)
     const uint4* b4 = reinterpret_cast<const uint4*>(base);
@@ -254,25 +267,32 @@ static void launch_gn_partials(cudaStream_t st, const void* x, int P, int C, int
   gn_partials_kernel<<<dim3(n, G), 256, 0, st>>>(xb, C, hw, G, plist, partials);
 }
 
+// Chan-combine the equal-size partials of patches [p0, p1) for group g -> (mean, rstd).
+// COHERENT: the partials were written by other CTAs of the same launch (L2 loads).
+template <bool COHERENT>
+__device__ __forceinline__ void gn_finalize_group(const float* partials, int p0, int p1, int G, int g, int64_t n_each,
+                                                  float eps, float* out) {
+  auto ld = [&](int64_t i) { return COHERENT ? __ldcg(partials + i) : partials[i]; };
+  const int K = p1 - p0;
+  double msum = 0.0;
+  for (int p = p0; p < p1; ++p) msum += ld(((int64_t)p * G + g) * 2);
+  const double mean = msum / K;
+  double m2 = 0.0;
+  for (int p = p0; p < p1; ++p) {
+    const double d = ld(((int64_t)p * G + g) * 2) - mean;
+    m2 += ld(((int64_t)p * G + g) * 2 + 1) + (double)n_each * d * d;
+  }
+  const double var = m2 / ((double)K * n_each);
+  out[0] = (float)mean;
+  out[1] = (float)(1.0 / sqrt(var + (double)eps));
+}
+
 // grid R, block G (<=1024): Chan-combine the equal-size partials of each request.
 __global__ void gn_finalize_kernel(const float* __restrict__ partials, const int32_t* __restrict__ req_off, int G,
                                    int64_t n_each, float eps, float* __restrict__ stats) {
   const int r = blockIdx.x;
-  for (int g = threadIdx.x; g < G; g += blockDim.x) {
-    const int p0 = req_off[r], p1 = req_off[r + 1];
-    const int K = p1 - p0;
-    double msum = 0.0;
-    for (int p = p0; p < p1; ++p) msum += partials[((int64_t)p * G + g) * 2];
-    const double mean = msum / K;
-    double m2 = 0.0;
-    for (int p = p0; p < p1; ++p) {
-      const double d = partials[((int64_t)p * G + g) * 2] - mean;
-      m2 += partials[((int64_t)p * G + g) * 2 + 1] + (double)n_each * d * d;
-    }
-    const double var = m2 / ((double)K * n_each);
-    stats[((int64_t)r * G + g) * 2] = (float)mean;
-    stats[((int64_t)r * G + g) * 2 + 1] = (float)(1.0 / sqrt(var + (double)eps));
-  }
+  for (int g = threadIdx.x; g < G; g += blockDim.x)
+    gn_finalize_group<false>(partials, req_off[r], req_off[r + 1], G, g, n_each, eps, stats + ((int64_t)r * G + g) * 2);
 }
 
 // NCHW -> CL over a 64-token x 64-channel tile per loop step.
@@ -483,22 +503,25 @@ __global__ void __launch_bounds__(256) frames_vec_kernel(const __nv_bfloat16* __
 // FRAMES adds the 1-pixel neighbour ring of patched.py:64-88 (zero outside the image):
 // rows 0 / F-1 read the N / S neighbour's edge row through the same vector path, and
 // the border columns are gathered per pixel (8 channels per thread).
-template <bool FRAMES>
-__global__ void __launch_bounds__(256, 4) frames_t8_kernel(const __nv_bfloat16* __restrict__ x, int C, int ps, int Cp,
-                                                        int mode, const float* __restrict__ stats,
-                                                        const int32_t* __restrict__ ri,
-                                                        const int32_t* __restrict__ nbr, int G,
-                                                        const float* __restrict__ gamma,
-                                                        const float* __restrict__ beta,
-                                                        const int32_t* __restrict__ plist,
-                                                        __nv_bfloat16* __restrict__ out) {
-  const int p = plist ? __ldg(plist + blockIdx.y) : (int)blockIdx.y;
+// One 8-pixel x 8-channel unit u of patch p of the (framed) channels-last output; the
+// units of a patch are [0, n_int) interior rows and [n_int, n_int + n_brd) frame columns.
+// PUSH (every patch's frame is written in the same launch): no frame-column units -- the
+// units holding column 0 / ps-1 of a row also store that pixel into the west / east
+// neighbour's frame (the same value the neighbour's pull unit would compute: same image,
+// same statistics), or zero their own frame column when that neighbour does not exist.
+// The pull units gathered one pixel of 8 channel planes per thread (2 useful bytes per
+// 32-byte sector, a third of the units).
+template <bool FRAMES, bool PUSH>
+__device__ __forceinline__ void frames_t8_unit(const __nv_bfloat16* __restrict__ x, int C, int ps, int Cp, int mode,
+                                               const float* stats, const int32_t* __restrict__ ri,
+                                               const int32_t* __restrict__ nbr, int G,
+                                               const float* __restrict__ gamma, const float* __restrict__ beta,
+                                               int p, int u, __nv_bfloat16* __restrict__ out) {
   const int F = FRAMES ? ps + 2 : ps, off = FRAMES ? 1 : 0;
   const int nPB = ps >> 3, nCG = Cp >> 3;
   const int hw = ps * ps;
   const int n_int = F * nPB * nCG;
-  const int n_brd = FRAMES ? F * 2 * nCG : 0;
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n_brd = FRAMES && !PUSH ? F * 2 * nCG : 0;
   if (u >= n_int + n_brd) return;
   int cg, fy, q, sy, pb = 0, side = 0, sx = 0;
   if (u < n_int) {
@@ -526,11 +549,30 @@ __global__ void __launch_bounds__(256, 4) frames_t8_kernel(const __nv_bfloat16* 
   }
   const int c0 = cg * 8;
   const int64_t obase = ((int64_t)p * F + fy) * F;
+  // PUSH: the row's column 0 / ps-1 pixel goes to the west / east neighbour's frame
+  auto push_w = [&](uint4 v) {
+    if (pb == 0) {
+      const int wq = __ldg(nbr + (int64_t)p * 8 + 6);
+      if (wq >= 0) *reinterpret_cast<uint4*>(out + (((int64_t)wq * F + fy) * F + F - 1) * Cp + c0) = v;
+      else *reinterpret_cast<uint4*>(out + obase * Cp + c0) = make_uint4(0, 0, 0, 0);
+    }
+  };
+  auto push_e = [&](uint4 v) {
+    if (pb == nPB - 1) {
+      const int eq = __ldg(nbr + (int64_t)p * 8 + 2);
+      if (eq >= 0) *reinterpret_cast<uint4*>(out + ((int64_t)eq * F + fy) * F * Cp + c0) = v;
+      else *reinterpret_cast<uint4*>(out + (obase + F - 1) * Cp + c0) = make_uint4(0, 0, 0, 0);
+    }
+  };
   if (q < 0 || c0 >= C) {  // outside the image (zero halo) or padding channels
     const uint4 z = make_uint4(0, 0, 0, 0);
     if (u < n_int) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) *reinterpret_cast<uint4*>(out + (obase + off + pb * 8 + i) * Cp + c0) = z;
+      if (PUSH) {
+        push_w(z);
+        push_e(z);
+      }
     } else {
       *reinterpret_cast<uint4*>(out + (obase + (side ? F - 1 : 0)) * Cp + c0) = z;
     }
@@ -545,7 +587,8 @@ __global__ void __launch_bounds__(256, 4) frames_t8_kernel(const __nv_bfloat16* 
     if (mode == 1) {
       const int c = c0 + j;
       const int g = c / (C / G);
-      const float mu = __ldg(stats + ((int64_t)req * G + g) * 2), rs = __ldg(stats + ((int64_t)req * G + g) * 2 + 1);
+      const float* sp = stats + ((int64_t)req * G + g) * 2;
+      const float mu = __ldg(sp), rs = __ldg(sp + 1);
       a[j] = rs * __ldg(gamma + c);
       b[j] = __ldg(beta + c) - mu * a[j];
     }
@@ -570,7 +613,10 @@ __global__ void __launch_bounds__(256, 4) frames_t8_kernel(const __nv_bfloat16* 
         }
         w[j2] = pack_bf16(v2[0], v2[1]);
       }
-      *reinterpret_cast<uint4*>(out + (obase + off + pb * 8 + i) * Cp + c0) = make_uint4(w[0], w[1], w[2], w[3]);
+      const uint4 wv = make_uint4(w[0], w[1], w[2], w[3]);
+      *reinterpret_cast<uint4*>(out + (obase + off + pb * 8 + i) * Cp + c0) = wv;
+      if (PUSH && i == 0) push_w(wv);
+      if (PUSH && i == 7) push_e(wv);
     }
   } else {
     uint32_t w[4];
@@ -583,16 +629,42 @@ __global__ void __launch_bounds__(256, 4) frames_t8_kernel(const __nv_bfloat16* 
   }
 }
 
+template <bool FRAMES, bool PUSH>
+__global__ void __launch_bounds__(256, PUSH ? 3 : 4) frames_t8_kernel(const __nv_bfloat16* __restrict__ x, int C, int ps, int Cp,
+                                                        int mode, const float* __restrict__ stats,
+                                                        const int32_t* __restrict__ ri,
+                                                        const int32_t* __restrict__ nbr, int G,
+                                                        const float* __restrict__ gamma,
+                                                        const float* __restrict__ beta,
+                                                        const int32_t* __restrict__ plist,
+                                                        __nv_bfloat16* __restrict__ out) {
+  const int p = plist ? __ldg(plist + blockIdx.y) : (int)blockIdx.y;
+  frames_t8_unit<FRAMES, PUSH>(x, C, ps, Cp, mode, stats, ri, nbr, G, gamma, beta, p,
+                                blockIdx.x * blockDim.x + threadIdx.x, out);
+}
+
 template <bool FRAMES>
 static int launch_frames_vec(cudaStream_t st, const void* x, int P, int C, int ps, int Cp, int mode,
                              const float* stats, const int32_t* ri, const int32_t* nbr, int G, const float* gamma,
                              const float* beta, void* out, const int32_t* plist = nullptr, int n_list = 0) {
   const int F = FRAMES ? ps + 2 : ps;
   if (ps % 8 == 0 && C % 8 == 0 && !getenv_flag("PS_FRAMES_SMEM")) {
-    const int units = F * (ps / 8) * (Cp / 8) + (FRAMES ? F * 2 * (Cp / 8) : 0);
+    // full launches push the frame columns; patch lists (split path: neighbours may be
+    // ghosts nobody frames here) pull them
+    static const bool pull = getenv_flag("PS_FRAMES_PULL");
+    const bool push = FRAMES && plist == nullptr && !pull;
+    const int units = F * (ps / 8) * (Cp / 8) + (FRAMES && !push ? F * 2 * (Cp / 8) : 0);
     dim3 g2((units + 255) / 256, plist ? n_list : P);
-    frames_t8_kernel<FRAMES><<<g2, 256, 0, st>>>((const __nv_bfloat16*)x, C, ps, Cp, mode, stats, ri, nbr, G, gamma,
-                                                beta, plist, (__nv_bfloat16*)out);
+    if constexpr (FRAMES) {
+      if (push) {
+        frames_t8_kernel<true, true><<<g2, 256, 0, st>>>((const __nv_bfloat16*)x, C, ps, Cp, mode, stats, ri, nbr, G,
+                                                         gamma, beta, plist, (__nv_bfloat16*)out);
+        count_launch();
+        return check_launch("frames_cl");
+      }
+    }
+      frames_t8_kernel<FRAMES, false><<<g2, 256, 0, st>>>((const __nv_bfloat16*)x, C, ps, Cp, mode, stats, ri, nbr, G,
+                                                          gamma, beta, plist, (__nv_bfloat16*)out);
     count_launch();
     return check_launch(FRAMES ? "frames_cl" : "to_cl");
   }

@@ -188,6 +188,15 @@ def test_frames_cl_register_transpose_matches_smem_kernel(C, ps, mode, monkeypat
     a, b2 = run(False), run(True)
     for u, v in zip(a, b2):
         assert torch.equal(u, v)
+    # full launches push the frame columns from the neighbours' units, patch lists pull them:
+    # every patch listed -> the same frames
+    allp = torch.arange(P, dtype=torch.int32, device="cuda")
+    pull = torch.full((P, ps + 2, ps + 2, Cp), 7.0, device="cuda").to(torch.bfloat16)
+    _lib.call("ps_frames_cl_sub", stream(), x.data_ptr(), P, C, ps, Cp, mode, stats.data_ptr(),
+              dev["request_index"].data_ptr(), dev["neighbors"].data_ptr(), G, gamma.data_ptr(),
+              beta.data_ptr(), allp.data_ptr(), P, pull.data_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(pull, a[0])
     # the interior of each frame is the patch itself (mode 0) / its affine image (mode 1)
     if mode == 0:
         inner = a[0][:, 1:-1, 1:-1, :C].permute(0, 3, 1, 2)
