@@ -511,12 +511,26 @@ __global__ void __launch_bounds__(256) frames_vec_kernel(const __nv_bfloat16* __
 // same statistics), or zero their own frame column when that neighbour does not exist.
 // The pull units gathered one pixel of 8 channel planes per thread (2 useful bytes per
 // 32-byte sector, a third of the units).
+// GroupNorm affine of request ri[p] for every channel: sab[c] = rstd * gamma[c],
+// sab[Cp + c] = beta[c] - mean * sab[c] (the expressions of the other stitcher kernels).
+__device__ __forceinline__ void frames_affine(const float* __restrict__ stats, const int32_t* __restrict__ ri,
+                                              const float* __restrict__ gamma, const float* __restrict__ beta,
+                                              int C, int Cp, int G, int p, float* sab) {
+  const int req = __ldg(ri + p), cg = C / G;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const float* sp = stats + ((int64_t)req * G + c / cg) * 2;
+    const float mu = __ldg(sp), rs = __ldg(sp + 1);
+    const float a = rs * __ldg(gamma + c);
+    sab[c] = a;
+    sab[Cp + c] = __ldg(beta + c) - mu * a;
+  }
+  __syncthreads();
+}
+
 template <bool FRAMES, bool PUSH>
 __device__ __forceinline__ void frames_t8_unit(const __nv_bfloat16* __restrict__ x, int C, int ps, int Cp, int mode,
-                                               const float* stats, const int32_t* __restrict__ ri,
-                                               const int32_t* __restrict__ nbr, int G,
-                                               const float* __restrict__ gamma, const float* __restrict__ beta,
-                                               int p, int u, __nv_bfloat16* __restrict__ out) {
+                                               const float* sab, const int32_t* __restrict__ nbr, int p, int u,
+                                               __nv_bfloat16* __restrict__ out) {
   const int F = FRAMES ? ps + 2 : ps, off = FRAMES ? 1 : 0;
   const int nPB = ps >> 3, nCG = Cp >> 3;
   const int hw = ps * ps;
@@ -579,18 +593,17 @@ __device__ __forceinline__ void frames_t8_unit(const __nv_bfloat16* __restrict__
     return;
   }
   float a[8], b[8];
-  const int req = mode == 1 ? __ldg(ri + p) : 0;
+  if (mode == 1) {  // the patch's per-channel affine, staged once per CTA (frames_affine)
+    const float4* a4 = reinterpret_cast<const float4*>(sab + c0);
+    const float4* b4 = reinterpret_cast<const float4*>(sab + Cp + c0);
+    const float4 a0 = a4[0], a1 = a4[1], b0 = b4[0], b1 = b4[1];
+    a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w; a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
+    b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w; b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+  } else {
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    a[j] = 1.f;
-    b[j] = 0.f;
-    if (mode == 1) {
-      const int c = c0 + j;
-      const int g = c / (C / G);
-      const float* sp = stats + ((int64_t)req * G + g) * 2;
-      const float mu = __ldg(sp), rs = __ldg(sp + 1);
-      a[j] = rs * __ldg(gamma + c);
-      b[j] = __ldg(beta + c) - mu * a[j];
+    for (int j = 0; j < 8; ++j) {
+      a[j] = 1.f;
+      b[j] = 0.f;
     }
   }
   const __nv_bfloat16* src = x + ((int64_t)q * C + c0) * hw + sy * ps;
@@ -638,9 +651,10 @@ __global__ void __launch_bounds__(256, PUSH ? 3 : 4) frames_t8_kernel(const __nv
                                                         const float* __restrict__ beta,
                                                         const int32_t* __restrict__ plist,
                                                         __nv_bfloat16* __restrict__ out) {
+  extern __shared__ __align__(16) float sab[];  // [2][Cp] (mode 1)
   const int p = plist ? __ldg(plist + blockIdx.y) : (int)blockIdx.y;
-  frames_t8_unit<FRAMES, PUSH>(x, C, ps, Cp, mode, stats, ri, nbr, G, gamma, beta, p,
-                                blockIdx.x * blockDim.x + threadIdx.x, out);
+  if (mode == 1) frames_affine(stats, ri, gamma, beta, C, Cp, G, p, sab);
+  frames_t8_unit<FRAMES, PUSH>(x, C, ps, Cp, mode, sab, nbr, p, blockIdx.x * blockDim.x + threadIdx.x, out);
 }
 
 template <bool FRAMES>
@@ -655,15 +669,16 @@ static int launch_frames_vec(cudaStream_t st, const void* x, int P, int C, int p
     const bool push = FRAMES && plist == nullptr && !pull;
     const int units = F * (ps / 8) * (Cp / 8) + (FRAMES && !push ? F * 2 * (Cp / 8) : 0);
     dim3 g2((units + 255) / 256, plist ? n_list : P);
+    const size_t sab_bytes = mode == 1 ? 2 * Cp * sizeof(float) : 0;  // <= 48 KB for Cp <= 6144
     if constexpr (FRAMES) {
       if (push) {
-        frames_t8_kernel<true, true><<<g2, 256, 0, st>>>((const __nv_bfloat16*)x, C, ps, Cp, mode, stats, ri, nbr, G,
+        frames_t8_kernel<true, true><<<g2, 256, sab_bytes, st>>>((const __nv_bfloat16*)x, C, ps, Cp, mode, stats, ri, nbr, G,
                                                          gamma, beta, plist, (__nv_bfloat16*)out);
         count_launch();
         return check_launch("frames_cl");
       }
     }
-      frames_t8_kernel<FRAMES, false><<<g2, 256, 0, st>>>((const __nv_bfloat16*)x, C, ps, Cp, mode, stats, ri, nbr, G,
+    frames_t8_kernel<FRAMES, false><<<g2, 256, sab_bytes, st>>>((const __nv_bfloat16*)x, C, ps, Cp, mode, stats, ri, nbr, G,
                                                           gamma, beta, plist, (__nv_bfloat16*)out);
     count_launch();
     return check_launch(FRAMES ? "frames_cl" : "to_cl");

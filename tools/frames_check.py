@@ -19,15 +19,20 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 stats = ctx.gn_stats(x, 320, patched.device_params(prm, 320))
 dp = patched.device_params(prm, 320)
 nbytes = x.numel() * 2 + b.n_patches * 34 * 34 * 320 * 2
-ts = []
-for it in range(23):
-    flush.zero_()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    ctx._frames(x, 320, 320, 1, stats, 32, dp["gamma"], dp["beta"])
-    e1.record()
-    torch.cuda.synchronize()
-    if it >= 3:
-        ts.append(e0.elapsed_time(e1) * 1e3)
-us = float(np.median(ts))
-print(f"frames pull={os.environ.get('PS_FRAMES_PULL', '0')}: {us:.1f} us, {nbytes / us / 1e3:.0f} GB/s algorithmic")
+for mode in (1, 0):
+    ts = []
+    for it in range(23):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        if mode == 1:
+            ctx._frames(x, 320, 320, 1, stats, 32, dp["gamma"], dp["beta"])
+        else:
+            ctx._frames(x, 320, 320, 0, None, 1, None, None)
+        e1.record()
+        torch.cuda.synchronize()
+        if it >= 3:
+            ts.append(e0.elapsed_time(e1) * 1e3)
+    us = float(np.median(ts))
+    print(f"frames mode={mode} pull={os.environ.get('PS_FRAMES_PULL', '0')}: {us:.1f} us, "
+          f"{nbytes / us / 1e3:.0f} GB/s algorithmic")
