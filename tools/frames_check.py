@@ -19,6 +19,18 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 stats = ctx.gn_stats(x, 320, patched.device_params(prm, 320))
 dp = patched.device_params(prm, 320)
 nbytes = x.numel() * 2 + b.n_patches * 34 * 34 * 320 * 2
+ts = []
+for it in range(23):
+    flush.zero_()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    ctx.gn_stats(x, 320, dp)
+    e1.record()
+    torch.cuda.synchronize()
+    if it >= 3:
+        ts.append(e0.elapsed_time(e1) * 1e3)
+us = float(np.median(ts))
+print(f"gn partials + finalize: {us:.1f} us, {x.numel() * 2 / us / 1e3:.0f} GB/s of x")
 for mode in (1, 0):
     ts = []
     for it in range(23):
