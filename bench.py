@@ -277,25 +277,27 @@ def measure_slo(cfg, weights, rank, world, barrier):
 def measure_cache(cfg, weights, reqs, steps=12, sigma=0.1, max_streak=3):
     """BASELINE config 3: the config-2 batch with the patch cache in the loop at the reference's
     default predictor (sigma 0.1, streak cap 3, cache.py:25-26) -- engine_step.numeric_step with the
-    bit-exact reuse test, compaction of the recomputed patches and one mask read-back per block
-    (engine.py:143-144).  Steps 3.. are timed with CUDA events (the cache warms up in steps 0-2)."""
+    bit-exact reuse test and compaction of the recomputed patches, the whole step replayed as one CUDA
+    graph with every reuse decision on the device (engine_step.CachedStepGraph; the reference reads
+    the mask on the host, engine.py:143-144).  Steps 3.. are timed with CUDA events (the cache warms
+    up in steps 0-2; step 0 is eager, step 1 captures)."""
     import torch
 
     import paper_2501_09253_b200 as ps
-    from paper_2501_09253_b200.engine_step import numeric_step
+    from paper_2501_09253_b200.engine_step import CachedStepGraph
     from paper_2501_09253_b200.model import step_inputs
     b = ps.split([(r, torch.tensor(x, dtype=torch.float32)) for r, x in reqs], patch_size=PATCH)
     prompts = {rid: ps.make_prompt(cfg, rid) for rid, _ in reqs}
     cache = ps.BlockCache(cfg.n_blocks, ps.PredictorConfig(sigma, max_streak))
     keys = b.patch_keys()
     data = b.data.clone()
+    step = CachedStepGraph(b, weights, cache, keys)
     times, skipped, total = [], 0, 0
     for s_ in range(steps):
         bias, rates = step_inputs(cfg, b, prompts, dict.fromkeys(prompts, s_), dict.fromkeys(prompts, 50))
-        b.data = data
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        data, st = numeric_step(b, weights, cache, bias, rates, keys=keys)
+        data, st = step.run(data, bias, rates)
         e1.record()
         torch.cuda.synchronize()
         if s_ >= 3:
@@ -305,8 +307,10 @@ def measure_cache(cfg, weights, reqs, steps=12, sigma=0.1, max_streak=3):
     ms = float(np.mean(times))
     return {"value": b.n_patches / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "steps_timed": len(times),
             "reuse_rate": skipped / max(1, total), "sigma": sigma, "max_streak": max_streak,
-            "path": "numeric_step: bit-exact fp64 reuse test -> compacted block on recomputed patches -> fused "
-                    "splice/streak/snapshot; one mask read-back per block (eager, not graph-captured)"}
+            "path": "CachedStepGraph (one CUDA graph per step): bit-exact fp64 reuse test -> device-built "
+                    "compaction lists -> compacted block on recomputed patches (kernels read their work counts "
+                    "from device memory) -> fused splice/streak/snapshot; no host round trip inside the step, "
+                    "one counter read-back after it"}
 
 
 def _peaks():

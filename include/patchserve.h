@@ -82,7 +82,7 @@ int ps_gn_partials(void* stream, const void* x, int P, int C, int ps, int G, flo
 /* ps_gn_partials over a DEVICE list of n patch indices (the patches a GPU owns
  * in the split-image path); other rows of `partials` are untouched. */
 int ps_gn_partials_sub(void* stream, const void* x, int P, int C, int ps, int G, const int32_t* patches, int n,
-                       float* partials);
+                       float* partials, const int32_t* n_dev);
 /* Pool partials per request into mean / rstd (patched.py:135-140, eps).
  * stats: fp32 [R, G, 2] (mean, rstd). */
 int ps_gn_finalize(void* stream, const float* partials, const int32_t* request_offset, int R, int G, int cg_hw,
@@ -100,7 +100,7 @@ int ps_frames_cl(void* stream, const void* x, int P, int C, int ps, int Cp, int 
 /* ps_frames_cl for a DEVICE list of n patch indices only (split-image path). */
 int ps_frames_cl_sub(void* stream, const void* x, int P, int C, int ps, int Cp, int mode, const float* stats,
                      const int32_t* request_index, const int32_t* neighbors, int G, const float* gamma,
-                     const float* beta, const int32_t* patches, int n, void* out);
+                     const float* beta, const int32_t* patches, int n, void* out, const int32_t* n_dev);
 /* CL tokens -> NCHW bf16, optionally adding an NCHW bf16 residual (patched.py:215-217). */
 int ps_from_cl(void* stream, const void* x_cl, int P, int C, int ps, int Cp, const void* resid, void* out);
 
@@ -139,6 +139,8 @@ typedef struct ps_gemm_args {
   int m_count;                            /* entries in m_map */
   int cta_pair;                           /* 0 auto, 1 single-CTA 128-row tiles, 2 CTA-pair 256-row tiles
                                              (tcgen05 cta_group::2) */
+  const int32_t* m_count_dev;             /* optional DEVICE count of m_map entries (m_count is then an upper
+                                             bound): compaction decided on the device, no host round trip */
 } ps_gemm_args;
 int ps_gemm(void* stream, const ps_gemm_args* args);
 
@@ -151,7 +153,7 @@ int ps_gemm(void* stream, const ps_gemm_args* args);
 int ps_feed_forward_debug(unsigned long long* counters);
 int ps_feed_forward(void* stream, const void* x, int M, int Cp, const void* w1, const float* b1, const void* w2,
                     const float* b2, int Hp, int c_real, int ps, const void* resid, void* out, const int32_t* m_map,
-                    int m_count);
+                    int m_count, const int32_t* m_count_dev);
 
 /* Per-image attention over the CSP token order (patched_self_attention,
  * patched.py:154-176 -> attend_tokens/_attend_single, kernels.py:230-267).
@@ -161,10 +163,11 @@ int ps_feed_forward(void* stream, const void* x, int M, int Cp, const void* w1, 
 int ps_attention(void* stream, const void* qk, const void* vt, int ldv, int T, int Dp, int D, const int32_t* img_tok0,
                  const int32_t* tile_q0, const int32_t* tile_img, int n_tiles, void* out);
 /* Same as ps_attention on CTA pairs (cta_group::2, M = 256): each tile is 256
- * queries of one image (pair_q0 steps by 256); default path on B200. */
+ * queries of one image (pair_q0 steps by 256); default path on B200.  n_dev: optional
+ * DEVICE tile count (n_pairs is then an upper bound). */
 int ps_attention_pairs(void* stream, const void* qk, const void* vt, int ldv, int T, int Dp, int D,
                        const int32_t* img_tok0, const int32_t* pair_q0, const int32_t* pair_img, int n_pairs,
-                       void* out);
+                       void* out, const int32_t* n_dev);
 /* Split-KV attention for few query tiles (a large image split across GPUs leaves a
  * GPU ~64 query tiles for 148 SMs): tile t (DEVICE arrays) covers key blocks
  * [tile_kb0[t], +tile_nkb[t]) of 128 keys of its image; tile_slot[t] >= 0 writes the
@@ -216,6 +219,16 @@ int ps_cache_predict(void* stream, const void* x, int P, int64_t n, const int32_
                      const int32_t* leaves, int n_leaves, const int32_t* nodes, int n_internal,
                      const int32_t* level_off, int n_levels, double* scratch, uint8_t* mask, int64_t* counters);
 /* Active-patch compaction (np.flatnonzero(~mask), ascending) + count. */
+/* All lists of a compacted block on the device (run_block_active without a host round trip):
+ * mask [P] (1 = reused); rows_act / rows_live: 128-row GEMM tiles (tpp per patch) of the
+ * active patches / of every patch of an image with an active patch, ascending; attention
+ * query tiles (qpp of tq queries per patch: q0 = p*hw + tq*j, image) of the same sets in
+ * `order` (the attention patch order), and the live patches ascending.  counts [6]: rows_act,
+ * rows_live, attn_act, attn_live, active patches, live patches.  live_scratch: int32 [R]. */
+int ps_compact_lists(void* stream, const uint8_t* mask, int P, const int32_t* request_index, int R,
+                     const int32_t* order, int tpp, int qpp, int tq, int hw, int32_t* live_scratch, int32_t* rows_act,
+                     int32_t* rows_live, int32_t* live_patches, int32_t* attn_q0_act, int32_t* attn_img_act,
+                     int32_t* attn_q0_live, int32_t* attn_img_live, int32_t* counts);
 int ps_compact(void* stream, const uint8_t* mask, int P, int32_t* active, int32_t* n_active, int32_t* reused,
                int32_t* n_reused);
 /* gather(): cache.py:124-137 — cached (inputs, outputs) at masked rows, zeros elsewhere.

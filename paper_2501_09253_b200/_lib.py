@@ -34,7 +34,7 @@ class GemmArgs(C.Structure):
         ("epi", C.c_int), ("out", p), ("ldo", C.c_int), ("out2", p), ("ldo2", C.c_int), ("n_split", C.c_int),
         ("resid", p), ("c_real", C.c_int),
         ("bn", C.c_int), ("out_tiled", C.c_int), ("dbg", p), ("m_map", p), ("m_count", C.c_int),
-        ("cta_pair", C.c_int),
+        ("cta_pair", C.c_int), ("m_count_dev", p),
     ]
 
 
@@ -51,19 +51,20 @@ _SIGS = {
     "ps_csp_reassemble": ([p, p, p, p, p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int], C.c_int),
     "ps_halo_frames_nchw": ([p, p, C.c_int, p, C.c_int, C.c_int, C.c_int, p], C.c_int),
     "ps_gn_partials": ([p, p, C.c_int, C.c_int, C.c_int, C.c_int, p], C.c_int),
-    "ps_gn_partials_sub": ([p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, C.c_int, p], C.c_int),
+    "ps_gn_partials_sub": ([p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, C.c_int, p, p], C.c_int),
     "ps_gn_finalize": ([p, p, p, C.c_int, C.c_int, C.c_int, f32, p], C.c_int),
     "ps_to_cl": ([p, p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, p, p, C.c_int, p, p, f32, p], C.c_int),
     "ps_frames_cl": ([p, p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, C.c_int, p, p, p], C.c_int),
-    "ps_frames_cl_sub": ([p, p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, C.c_int, p, p, p, C.c_int, p],
-                         C.c_int),
+    "ps_frames_cl_sub": ([p, p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, C.c_int, p, p, p, C.c_int, p,
+                          p], C.c_int),
     "ps_halo_strips": ([p, p, C.c_int, C.c_int, C.c_int, p, p, C.c_int], C.c_int),
     "ps_copy_segments": ([p, p, p, C.c_int, p, p, i64], C.c_int),
     "ps_from_cl": ([p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, p], C.c_int),
     "ps_gemm": ([p, C.POINTER(GemmArgs)], C.c_int),
-    "ps_feed_forward": ([p, p, C.c_int, C.c_int, p, p, p, p, C.c_int, C.c_int, C.c_int, p, p, p, C.c_int], C.c_int),
+    "ps_feed_forward": ([p, p, C.c_int, C.c_int, p, p, p, p, C.c_int, C.c_int, C.c_int, p, p, p, C.c_int, p],
+                        C.c_int),
     "ps_attention": ([p, p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, C.c_int, p], C.c_int),
-    "ps_attention_pairs": ([p, p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, C.c_int, p], C.c_int),
+    "ps_attention_pairs": ([p, p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, C.c_int, p, p], C.c_int),
     "ps_attention_splitkv": ([p, p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, p, p, p, C.c_int, p, p, p],
                              C.c_int),
     "ps_attention_combine": ([p, p, p, p, p, p, p, p, C.c_int, C.c_int, p], C.c_int),
@@ -77,6 +78,7 @@ _SIGS = {
     "ps_cache_predict": ([p, p, C.c_int, i64, p, p, p, p, f64, C.c_int, p, C.c_int, p, C.c_int, p, C.c_int, p, p, p],
                          C.c_int),
     "ps_compact": ([p, p, C.c_int, p, p, p, p], C.c_int),
+    "ps_compact_lists": ([p, p, C.c_int, p, C.c_int, p, C.c_int, C.c_int, C.c_int, C.c_int] + [p] * 9, C.c_int),
     "ps_cache_gather": ([p, p, p, p, C.c_int, i64, p, p, p, p, p], C.c_int),
     "ps_cache_fill": ([p, p, p, p, p, C.c_int, i64, p, p, p], C.c_int),
     "ps_cache_update": ([p, p, p, p, p, C.c_int, i64, p, p, p, p, p], C.c_int),

@@ -75,6 +75,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1;
+  if (p.n_dev != nullptr && pair >= *p.n_dev) return;  // past the device tile count (both CTAs)
   const int q0 = p.tile_q0[pair] + (int)rank * A2_BM;
   const int img = p.tile_img[pair];
   const int k_begin = p.img_tok0[img], k_end = p.img_tok0[img + 1];

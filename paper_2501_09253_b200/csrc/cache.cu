@@ -324,6 +324,93 @@ static int launch_op(cudaStream_t st, int P, int64_t n, const PatchOpArgs& a, co
 
 using namespace ps;
 
+namespace ps {
+// Block-wide exclusive scan of one 0/1 flag per thread (1024 threads); returns the
+// thread's position, *total gets the chunk's count.
+__device__ __forceinline__ int block_excl_scan(int a, int* warp_tot, int* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int incl = a;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  __syncthreads();
+  if (lane == 31) warp_tot[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    const int t = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0;
+    int s2 = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, s2, o);
+      if (lane >= o) s2 += u;
+    }
+    warp_tot[lane] = s2 - t;
+    if (lane == 31) *total = s2;
+  }
+  __syncthreads();
+  return warp_tot[w] + incl - a;
+}
+
+// Device-side lists of a compacted block (run_block_active without a host round trip):
+// GEMM row tiles of the active patches (mask == 0) and of every patch of an image with an
+// active patch ("live"), attention query tiles of the same two sets over the attention patch
+// order `order` (longest images first), and the live patches.  counts: [rows_act, rows_live,
+// attn_act, attn_live, active patches, live patches].  Single CTA of 1024 threads; live: int scratch [R].
+__global__ void __launch_bounds__(1024) compact_lists_kernel(
+    const uint8_t* __restrict__ mask, int P, const int32_t* __restrict__ ri, int R, const int32_t* __restrict__ order,
+    int tpp, int qpp, int tq, int hw, int32_t* live, int32_t* __restrict__ rows_act, int32_t* __restrict__ rows_live,
+    int32_t* __restrict__ live_patches,
+    int32_t* __restrict__ aq_act, int32_t* __restrict__ ai_act, int32_t* __restrict__ aq_live,
+    int32_t* __restrict__ ai_live, int32_t* __restrict__ counts) {
+  __shared__ int warp_tot[32];
+  __shared__ int total;
+  for (int r = threadIdx.x; r < R; r += blockDim.x) live[r] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < P; i += blockDim.x)
+    if (mask[i] == 0) live[ri[i]] = 1;
+  __threadfence_block();
+  __syncthreads();
+  int c[4] = {0, 0, 0, 0};
+  for (int base = 0; base < P; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const bool in = i < P;
+    const int po = in ? order[i] : 0;
+    const int f[4] = {in && mask[i] == 0, in && live[ri[i]] != 0, in && mask[po] == 0, in && live[ri[po]] != 0};
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const int pos = c[l] + block_excl_scan(f[l], warp_tot, &total);
+      if (f[l]) {
+        if (l < 2) {
+          int32_t* dst = l == 0 ? rows_act : rows_live;
+          for (int j = 0; j < tpp; ++j) dst[pos * tpp + j] = i * tpp + j;
+          if (l == 1) live_patches[pos] = i;
+        } else {
+          int32_t* dq = l == 2 ? aq_act : aq_live;
+          int32_t* di = l == 2 ? ai_act : ai_live;
+          for (int j = 0; j < qpp; ++j) {
+            dq[pos * qpp + j] = po * hw + tq * j;
+            di[pos * qpp + j] = ri[po];
+          }
+        }
+      }
+      c[l] += total;
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) {
+    counts[0] = c[0] * tpp;
+    counts[1] = c[1] * tpp;
+    counts[2] = c[2] * qpp;
+    counts[3] = c[3] * qpp;
+    counts[4] = c[0];
+    counts[5] = c[1];
+  }
+}
+
+}  // namespace ps
+
 extern "C" {
 
 int ps_cache_predict(void* stream, const void* x, int P, int64_t n, const int32_t* slots, const void* snap_in,
@@ -362,6 +449,19 @@ int ps_cache_predict(void* stream, const void* x, int P, int64_t n, const int32_
                                         level_off, n_levels, stride, scratch, mask, counters, smem_c / 8);
   count_launch();
   return check_launch("mse_combine");
+}
+
+int ps_compact_lists(void* stream, const uint8_t* mask, int P, const int32_t* request_index, int R,
+                     const int32_t* order, int tpp, int qpp, int tq, int hw, int32_t* live_scratch, int32_t* rows_act,
+                     int32_t* rows_live, int32_t* live_patches, int32_t* attn_q0_act, int32_t* attn_img_act,
+                     int32_t* attn_q0_live, int32_t* attn_img_live, int32_t* counts) {
+  if (P < 0 || R < 1 || tpp < 1 || qpp < 1) return set_error(PS_ERR_INPUT, "compact_lists: bad geometry");
+  ps::compact_lists_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(mask, P, request_index, R, order, tpp, qpp, tq, hw,
+                                                                live_scratch, rows_act, rows_live, live_patches,
+                                                                attn_q0_act,
+                                                                attn_img_act, attn_q0_live, attn_img_live, counts);
+  count_launch();
+  return check_launch("compact_lists");
 }
 
 int ps_compact(void* stream, const uint8_t* mask, int P, int32_t* active, int32_t* n_active, int32_t* reused,

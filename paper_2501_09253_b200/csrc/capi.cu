@@ -200,7 +200,7 @@ int ps_csp_build(int n_req, const int32_t* dims, int32_t ps, int32_t* order, int
 // internal nodes grouped by height so a level can be evaluated in parallel.
 int ps_attention_pairs(void* stream, const void* qk, const void* vt, int ldv, int T, int Dp, int D,
                        const int32_t* img_tok0, const int32_t* pair_q0, const int32_t* pair_img, int n_pairs,
-                       void* out) {
+                       void* out, const int32_t* n_dev) {
   if (Dp % 64 || Dp < 64 || Dp > 320) return set_error(PS_ERR_INPUT, "attention: Dp %d unsupported", Dp);
   if (D < 1 || D > Dp) return set_error(PS_ERR_INPUT, "attention: bad D");
   if (n_pairs < 1) return PS_OK;
@@ -215,6 +215,7 @@ int ps_attention_pairs(void* stream, const void* qk, const void* vt, int ldv, in
   p.n_tiles = n_pairs;
   p.tile_q0 = pair_q0;
   p.tile_img = pair_img;
+  p.n_dev = n_dev;
   p.img_tok0 = img_tok0;
   p.scale_log2 = 1.4426950408889634f / sqrtf((float)D);
   p.out = (__nv_bfloat16*)out;
@@ -359,6 +360,7 @@ int ps_gemm(void* stream, const ps_gemm_args* a) {
   p.dbg = a->dbg;
   p.m_map = a->m_map;
   p.m_count = a->m_map ? a->m_count : 0;
+  p.m_count_dev = a->m_map ? a->m_count_dev : nullptr;
   static const int epi_skip = getenv("PS_GEMM_EPI_SKIP") ? atoi(getenv("PS_GEMM_EPI_SKIP")) : 0;
   p.epi_skip = epi_skip;
   // defaults from tools/gemm_roles.py on config-2 shapes: splitting every tile's columns over both
@@ -533,7 +535,7 @@ extern "C" {
 // Fused feed-forward + residual (ffused.cu): out NCHW = W2 gelu(W1 x + b1) + b2 + resid.
 int ps_feed_forward(void* stream, const void* x, int M, int Cp, const void* w1, const float* b1, const void* w2,
                     const float* b2, int Hp, int c_real, int ps, const void* resid, void* out, const int32_t* m_map,
-                    int m_count) {
+                    int m_count, const int32_t* m_count_dev) {
   if (!x || !w1 || !w2 || !b1 || !b2 || !out) return set_error(PS_ERR_INPUT, "feed_forward: null pointer");
   if (Cp % 64 || Cp < 128 || Cp > 320) return set_error(PS_ERR_INPUT, "feed_forward: Cp %d unsupported", Cp);
   if (Hp % 128 || Hp < 128) return set_error(PS_ERR_INPUT, "feed_forward: hidden %d must be a multiple of 128", Hp);
@@ -549,6 +551,7 @@ int ps_feed_forward(void* stream, const void* x, int M, int Cp, const void* w1, 
   p.M = M;
   p.m_map = m_map;
   p.m_count = m_map ? m_count : 0;
+  p.m_count_dev = m_map ? m_count_dev : nullptr;
   p.hp = Hp;
   p.b1 = b1;
   p.b2 = b2;

@@ -70,7 +70,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
-  const int num_m = p.m_map ? p.m_count : (p.M + FF_BM - 1) / FF_BM;
+  const int num_m = p.m_map ? (p.m_count_dev ? *p.m_count_dev : p.m_count) : (p.M + FF_BM - 1) / FF_BM;
   const int n_units = (num_m + 1) / 2;
   const int unit0 = blockIdx.x >> 1, unit_step = gridDim.x >> 1;
   const int m_oob = (p.M + FF_BM - 1) / FF_BM;

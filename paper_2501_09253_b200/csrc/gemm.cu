@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_n = (p.N + BN - 1) / BN;
-  const int num_m = p.m_map ? p.m_count : (p.M + GEMM_BM - 1) / GEMM_BM;
+  const int num_m = p.m_map ? (p.m_count_dev ? *p.m_count_dev : p.m_count) : (p.M + GEMM_BM - 1) / GEMM_BM;
   // PAIR: a work item is (pair of m tiles, n tile); CTA `rank` takes m tile 2*mp + rank
   const uint32_t rank = PAIR ? cluster_rank() : 0;
   const bool leader = rank == 0;

@@ -72,8 +72,10 @@ __device__ __forceinline__ void gn_slice_regs(const __nv_bfloat16* __restrict__ 
 
 __global__ void __launch_bounds__(256, 4) gn_partials_kernel(const __nv_bfloat16* __restrict__ x, int C, int hw, int G,
                                                           const int32_t* __restrict__ plist,
+                                                          const int32_t* __restrict__ n_dev,
                                                           float* __restrict__ partials) {
   __shared__ float red[32];
+  if (n_dev != nullptr && (int)blockIdx.x >= *n_dev) return;  // past the device list length
   const int p = plist ? __ldg(plist + blockIdx.x) : (int)blockIdx.x, g = blockIdx.y;
   const int cg = C / G;
   const int64_t n = (int64_t)cg * hw;
@@ -241,7 +243,7 @@ __global__ void __launch_bounds__(256) gn_partials_bulk_kernel(const __nv_bfloat
 
 // host: pipelined kernel when a slice fits 256*8 vectors and is 16-byte aligned, else the simple one
 static void launch_gn_partials(cudaStream_t st, const void* x, int P, int C, int hw, int G, const int32_t* plist,
-                               int n, float* partials) {
+                               int n, float* partials, const int32_t* n_dev = nullptr) {
   const int64_t elems = (int64_t)(C / G) * hw;
   const int64_t nv = elems / 8;
   const int n_slices = n * G;
@@ -249,7 +251,7 @@ static void launch_gn_partials(cudaStream_t st, const void* x, int P, int C, int
   if (grid > n_slices) grid = n_slices;
   const auto xb = (const __nv_bfloat16*)x;
   const int64_t slice_bytes = elems * 2;
-  if (elems % 8 == 0 && slice_bytes <= 96 * 1024 && getenv_flag("PS_GN_BULK")) {  // measured 23 vs 21 us: opt-in
+  if (elems % 8 == 0 && slice_bytes <= 96 * 1024 && getenv_flag("PS_GN_BULK") && !n_dev) {  // measured 23 vs 21 us: opt-in
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(gn_partials_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
@@ -258,13 +260,13 @@ static void launch_gn_partials(cudaStream_t st, const void* x, int P, int C, int
     gn_partials_bulk_kernel<<<dim3(n, G), 256, (size_t)slice_bytes, st>>>(xb, C, hw, G, plist, partials);
     return;
   }
-  if (elems % 8 == 0 && nv <= 256 * 6 && getenv_flag("PS_GN_PIPE")) {
+  if (elems % 8 == 0 && nv <= 256 * 6 && getenv_flag("PS_GN_PIPE") && !n_dev) {
     if (nv <= 256 * 2) gn_partials_pipe_kernel<2><<<grid, 256, 0, st>>>(xb, C, hw, G, plist, n_slices, partials);
     else if (nv <= 256 * 4) gn_partials_pipe_kernel<4><<<grid, 256, 0, st>>>(xb, C, hw, G, plist, n_slices, partials);
     else gn_partials_pipe_kernel<6><<<grid, 256, 0, st>>>(xb, C, hw, G, plist, n_slices, partials);
     return;
   }
-  gn_partials_kernel<<<dim3(n, G), 256, 0, st>>>(xb, C, hw, G, plist, partials);
+  gn_partials_kernel<<<dim3(n, G), 256, 0, st>>>(xb, C, hw, G, plist, n_dev, partials);
 }
 
 // Chan-combine the equal-size partials of patches [p0, p1) for group g -> (mean, rstd).
@@ -650,8 +652,10 @@ __global__ void __launch_bounds__(256, PUSH ? 3 : 4) frames_t8_kernel(const __nv
                                                         const float* __restrict__ gamma,
                                                         const float* __restrict__ beta,
                                                         const int32_t* __restrict__ plist,
+                                                        const int32_t* __restrict__ n_dev,
                                                         __nv_bfloat16* __restrict__ out) {
   extern __shared__ __align__(16) float sab[];  // [2][Cp] (mode 1)
+  if (n_dev != nullptr && (int)blockIdx.y >= *n_dev) return;  // past the device list length
   const int p = plist ? __ldg(plist + blockIdx.y) : (int)blockIdx.y;
   if (mode == 1) frames_affine(stats, ri, gamma, beta, C, Cp, G, p, sab);
   frames_t8_unit<FRAMES, PUSH>(x, C, ps, Cp, mode, sab, nbr, p, blockIdx.x * blockDim.x + threadIdx.x, out);
@@ -660,9 +664,12 @@ __global__ void __launch_bounds__(256, PUSH ? 3 : 4) frames_t8_kernel(const __nv
 template <bool FRAMES>
 static int launch_frames_vec(cudaStream_t st, const void* x, int P, int C, int ps, int Cp, int mode,
                              const float* stats, const int32_t* ri, const int32_t* nbr, int G, const float* gamma,
-                             const float* beta, void* out, const int32_t* plist = nullptr, int n_list = 0) {
+                             const float* beta, void* out, const int32_t* plist = nullptr, int n_list = 0,
+                             const int32_t* n_dev = nullptr) {
   const int F = FRAMES ? ps + 2 : ps;
-  if (ps % 8 == 0 && C % 8 == 0 && !getenv_flag("PS_FRAMES_SMEM")) {
+  if (n_dev && (ps % 8 || C % 8))
+    return set_error(PS_ERR_INPUT, "frames: a device patch count needs ps %% 8 == 0 and C %% 8 == 0");
+  if (ps % 8 == 0 && C % 8 == 0 && (!getenv_flag("PS_FRAMES_SMEM") || n_dev)) {
     // full launches push the frame columns; patch lists (split path: neighbours may be
     // ghosts nobody frames here) pull them
     static const bool pull = getenv_flag("PS_FRAMES_PULL");
@@ -673,13 +680,13 @@ static int launch_frames_vec(cudaStream_t st, const void* x, int P, int C, int p
     if constexpr (FRAMES) {
       if (push) {
         frames_t8_kernel<true, true><<<g2, 256, sab_bytes, st>>>((const __nv_bfloat16*)x, C, ps, Cp, mode, stats, ri, nbr, G,
-                                                         gamma, beta, plist, (__nv_bfloat16*)out);
+                                                         gamma, beta, plist, n_dev, (__nv_bfloat16*)out);
         count_launch();
         return check_launch("frames_cl");
       }
     }
     frames_t8_kernel<FRAMES, false><<<g2, 256, sab_bytes, st>>>((const __nv_bfloat16*)x, C, ps, Cp, mode, stats, ri, nbr, G,
-                                                          gamma, beta, plist, (__nv_bfloat16*)out);
+                                                          gamma, beta, plist, n_dev, (__nv_bfloat16*)out);
     count_launch();
     return check_launch(FRAMES ? "frames_cl" : "to_cl");
   }
@@ -757,11 +764,11 @@ int ps_gn_partials(void* stream, const void* x, int P, int C, int ps_, int G, fl
 }
 
 int ps_gn_partials_sub(void* stream, const void* x, int P, int C, int ps_, int G, const int32_t* patches, int n,
-                       float* partials) {
+                       float* partials, const int32_t* n_dev) {
   if (G < 1 || C % G) return set_error(PS_ERR_INPUT, "groups=%d does not divide channels=%d", G, C);
   if (n < 0 || n > P) return set_error(PS_ERR_INPUT, "gn_partials_sub: %d patches listed for P=%d", n, P);
   if (n == 0) return PS_OK;
-  launch_gn_partials((cudaStream_t)stream, x, P, C, ps_ * ps_, G, patches, n, partials);
+  launch_gn_partials((cudaStream_t)stream, x, P, C, ps_ * ps_, G, patches, n, partials, n_dev);
   count_launch();
   return check_launch("gn_partials_sub");
 }
@@ -803,13 +810,13 @@ int ps_frames_cl(void* stream, const void* x, int P, int C, int ps_, int Cp, int
 
 int ps_frames_cl_sub(void* stream, const void* x, int P, int C, int ps_, int Cp, int mode, const float* stats,
                      const int32_t* request_index, const int32_t* neighbors, int G, const float* gamma,
-                     const float* beta, const int32_t* patches, int n, void* out) {
+                     const float* beta, const int32_t* patches, int n, void* out, const int32_t* n_dev) {
   if (Cp % 64 || Cp < C) return set_error(PS_ERR_INPUT, "frames_cl: Cp must be >= C and a multiple of 64");
   if (mode == 1 && (G < 1 || C % G)) return set_error(PS_ERR_INPUT, "groups=%d does not divide channels=%d", G, C);
   if (n < 0 || n > P) return set_error(PS_ERR_INPUT, "frames_cl_sub: %d patches listed for P=%d", n, P);
   if (n == 0) return PS_OK;
   return launch_frames_vec<true>((cudaStream_t)stream, x, P, C, ps_, Cp, mode, stats, request_index, neighbors, G,
-                                 gamma, beta, out, patches, n);
+                                 gamma, beta, out, patches, n, n_dev);
 }
 
 int ps_from_cl(void* stream, const void* x_cl, int P, int C, int ps_, int Cp, const void* resid, void* out) {

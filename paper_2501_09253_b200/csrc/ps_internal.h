@@ -29,7 +29,8 @@ struct GemmParams {
   unsigned long long* dbg;  // optional per-role wait-cycle counters (profiling)
   int store_tma;            // channels-last stores through the tmC tensor map
   const int* m_map;         // optional: physical 128-row tile of each logical tile (compaction)
-  int m_count;              // number of mapped tiles when m_map != null
+  int m_count;              // number of mapped tiles when m_map != null (upper bound with m_count_dev)
+  const int* m_count_dev;   // optional DEVICE count of mapped tiles (compaction without a host round trip)
   int epi_skip;             // profiling only (PS_GEMM_EPI_SKIP=1): drain accumulators without storing
   int epi_split;            // both epilogue warpgroups split each tile's columns (else alternate tiles)
   int no_prefetch;          // skip the L2 prefetch of residual rows
@@ -40,6 +41,7 @@ struct FfParams {
   int M;                       // tokens (rows of x)
   const int* m_map;            // optional device list of 128-row tiles (compaction)
   int m_count;
+  const int* m_count_dev;      // optional DEVICE count (m_count is then an upper bound)
   int hp;                      // hidden units (multiple of 128)
   int ts;                      // MMA2 reads GELU(H) from TMEM (else from shared memory)
   const float* b1;             // [hp]
@@ -86,6 +88,7 @@ struct AttnParams {
   const CUtensorMap* peer_maps;
   // profiling (ps_attention_trace): clock64 stamps of the first CTA (pair leader), [event][block]
   long long* trace;
+  const int* n_dev;      // optional DEVICE tile count (n_tiles is then an upper bound)
 };
 int attention_launch(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& vt, const AttnParams& p,
                      int dp, cudaStream_t st);

@@ -17,10 +17,18 @@ also reads `mask.sum()` on the host, engine.py:143-144); then
 and one fused kernel that splices cached outputs, bumps streaks and stores
 fresh snapshots (K9).  The results equal the reference sequence's: the
 compacted rows are bit-identical to an uncompacted run.
+
+Where the kernels cover the geometry (patched.device_compaction_ok) the read-back is
+gone: the mask stays on the device, ps_compact_lists builds the compaction lists there
+and every kernel of the block reads its work count from device memory
+(patched.run_block_masked), so the host never waits inside a step; the per-block counts
+are read once at the end of the step for StepStats.  PS_DEVICE_COMPACTION=0 restores the
+per-block read-back.
 """
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -29,7 +37,82 @@ import torch
 from .cache import BlockCache
 from .csp import CSPBatch
 from .model import blend_batch, prompt_bias
-from .patched import _bf16_nchw, run_block, run_block_active
+from .patched import _bf16_nchw, device_compaction_ok, run_block, run_block_active, run_block_masked
+
+# eager steps: per-block mask read-back (default) or device-built compaction lists; the
+# device form pays off inside a CUDA graph (CachedStepGraph), where no host work is left --
+# eagerly its ~15 launches per block cost more host time than the read-back's bubble when
+# whole blocks are reused
+DEVICE_COMPACTION = os.environ.get("PS_DEVICE_COMPACTION", "0") == "1"
+
+
+def _device_blocks(batch, weights, cache, keys, slots, lat, h, rates):
+    """The blocks of a cached step with every decision on the device (no host round trip):
+    returns (new latents, device int32 [n_blocks] of recomputed patches per block)."""
+    counts = []
+    for b, ops in enumerate(weights):
+        mask = cache.predict_reuse(b, keys, h, slots=slots)
+        x_sub = cache.block_substitute(b, slots, mask, h)
+        y, cnt = run_block_masked(batch, x_sub, ops, mask)
+        y = _bf16_nchw(y)
+        cache.block_finish(b, slots, mask, h, y)
+        counts.append(cnt[4:5])
+        h = y
+    return blend_batch(batch, lat, h, rates), torch.cat(counts)
+
+
+class CachedStepGraph:
+    """numeric_step with the patch cache in the loop for a FIXED batch composition, captured
+    as one CUDA graph: reuse test, compaction lists, compacted blocks, cache splice / streak
+    / snapshot and blend all replay without the host (engine.py:126-160 on the device).
+
+    The first run() is an eager step (it also allocates the cache storage and warms every
+    plan); the graph is captured on the second call and replayed from then on.  Inputs are
+    copied into static buffers; the returned latents are a static buffer overwritten by the
+    next run().  Results equal numeric_step's bit for bit.  Needs the default predictor and
+    patched.device_compaction_ok(batch)."""
+
+    def __init__(self, batch: CSPBatch, weights, cache: BlockCache, keys=None):
+        if not device_compaction_ok(batch) or batch.n_patches == 0:
+            raise ValueError("CachedStepGraph: batch geometry not covered by the device compaction path")
+        if cache._predictor is not None:
+            raise ValueError("CachedStepGraph: a custom predictor runs on the host")
+        self.batch, self.weights, self.cache = batch, weights, cache
+        self.keys = batch.patch_keys() if keys is None else keys
+        self.lat = batch.data.float().clone()
+        self.bias = None
+        self.rates = None
+        self.slots = None
+        self.graph = None
+        self._out = self._counts = None
+
+    def _body(self):
+        self.batch.data = self.lat
+        h = prompt_bias(self.batch, self.lat, self.bias)
+        return _device_blocks(self.batch, self.weights, self.cache, self.keys, self.slots, self.lat, h, self.rates)
+
+    def run(self, lat: torch.Tensor, bias: torch.Tensor, rates: torch.Tensor):
+        """One step; returns (new latents [static buffer], StepStats)."""
+        self.lat.copy_(lat)
+        if self.bias is None:
+            self.bias, self.rates = bias.clone(), rates.clone()
+            self.cache._ensure_shape(self.lat.shape[1:])
+            self.slots = self.cache.slots_for(self.keys, allocate=True)
+            out, counts = self._body()           # eager first step
+        else:
+            self.bias.copy_(bias)
+            self.rates.copy_(rates)
+            if self.graph is None:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._out, self._counts = self._body()
+                self.graph = g
+            self.graph.replay()
+            out, counts = self._out, self._counts
+        st = StepStats()
+        st.computed = st.rows_run = int(counts.sum().item())
+        st.skipped = self.batch.n_patches * len(self.weights) - st.computed
+        return out, st
 
 
 @dataclass
@@ -51,6 +134,12 @@ def numeric_step(batch: CSPBatch, weights, cache: BlockCache | None, bias: torch
     if cache is not None and slots is None:
         cache._ensure_shape(h.shape[1:])
         slots = cache.slots_for(keys, allocate=True)
+    if cache is not None and compact and DEVICE_COMPACTION and P and device_compaction_ok(batch):
+        out, counts = _device_blocks(batch, weights, cache, keys, slots, lat, h, rates)
+        computed = int(counts.sum().item())  # the step's only read-back
+        st.computed = st.rows_run = computed
+        st.skipped = P * len(weights) - computed
+        return out, st
     for b, ops in enumerate(weights):
         if cache is None:
             h = run_block(batch, h, ops)

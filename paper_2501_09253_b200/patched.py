@@ -110,6 +110,8 @@ class Ctx:
         self.owned = None       # device int32 list of owned patches
         self.owned_host = None
         self.exch = None
+        # device-decided compaction (run_block_masked): live patch list, upper bound, device count
+        self.gn_live = None
 
     def _attention_overlapped(self, qk, vt, ldv, dpp, d, host, finish, o):
         """Two-phase attention on the split-image path: phase A (owned keys of split images,
@@ -192,6 +194,8 @@ class Ctx:
         g = _lib.GemmArgs()
         if rows is not None:
             g.m_map, g.m_count = rows[0].data_ptr(), rows[1]
+            if len(rows) > 2:  # device-decided count (rows[1] is then an upper bound)
+                g.m_count_dev = rows[2].data_ptr()
         g.a, g.lda, g.M = a.data_ptr(), lda, self.T
         g.a_mode, g.P, g.ps, g.Cp = (1 if conv else 2 if a_tiled else 0), self.P, self.ps, cp_in
         g.out_tiled = 1 if out_tiled else 0
@@ -220,8 +224,13 @@ class Ctx:
         if self.owned is not None:
             # owned patches here; the split images' other partials arrive from their owners
             _lib.call("ps_gn_partials_sub", stream(), x_nchw.data_ptr(), self.P, c, self.ps, g,
-                      self.owned[0].data_ptr(), self.owned[1], part.data_ptr())
+                      self.owned[0].data_ptr(), self.owned[1], part.data_ptr(), None)
             self.exch.gn(part, g)
+        elif self.gn_live is not None:
+            # device-decided compaction: the patches of images with a patch to recompute
+            lp, n_ub, n_dev = self.gn_live
+            _lib.call("ps_gn_partials_sub", stream(), x_nchw.data_ptr(), self.P, c, self.ps, g, lp.data_ptr(), n_ub,
+                      part.data_ptr(), n_dev.data_ptr())
         else:
             _lib.call("ps_gn_partials", stream(), x_nchw.data_ptr(), self.P, c, self.ps, g, part.data_ptr())
         stats = torch.empty((self.b.n_requests, g, 2), dtype=torch.float32, device=self.device)
@@ -249,7 +258,11 @@ class Ctx:
         if self.owned is not None:
             # the stencil rows / columns of neighbours owned by other GPUs land in their ghost slots of x
             self.exch.halo(x, c)
-            _lib.call("ps_frames_cl_sub", stream(), *args, self.owned[0].data_ptr(), self.owned[1], fr.data_ptr())
+            _lib.call("ps_frames_cl_sub", stream(), *args, self.owned[0].data_ptr(), self.owned[1], fr.data_ptr(),
+                      None)
+        elif self.gn_live is not None:
+            lp, n_ub, n_dev = self.gn_live
+            _lib.call("ps_frames_cl_sub", stream(), *args, lp.data_ptr(), n_ub, fr.data_ptr(), n_dev.data_ptr())
         else:
             _lib.call("ps_frames_cl", stream(), *args, fr.data_ptr())
         return fr
@@ -293,7 +306,7 @@ class Ctx:
             _lib.call("ps_feed_forward", stream(), x.data_ptr(), self.T, dp["cp"], dp["w1"].data_ptr(),
                       dp["b1"].data_ptr(), dp["w2"].data_ptr(), dp["b2"].data_ptr(), dp["hp"], dp["c_out"], self.ps,
                       resid.data_ptr(), out.data_ptr(), None if rows is None else rows[0].data_ptr(),
-                      0 if rows is None else rows[1])
+                      0 if rows is None else rows[1], None if rows is None or len(rows) < 3 else rows[2].data_ptr())
             return Act("nchw", out, dp["c_out"])
         # hidden activations in 128x64 tile-major order: the second GEMM streams
         # each of its A boxes as one contiguous 16 KB block from HBM
@@ -380,10 +393,14 @@ class Ctx:
             _lib.call("ps_attention_combine", stream(), part_o.data_ptr(), part_ml.data_ptr(), cq0.data_ptr(),
                       cslot0.data_ptr(), cns.data_ptr(), cimg.data_ptr(), self.dev["img_tok0"].data_ptr(), n_q, dpp,
                       o.data_ptr())
+        elif pairs:
+            n_dev = self.attn_tiles[6] if self.attn_tiles is not None and len(self.attn_tiles) > 6 else None
+            _lib.call("ps_attention_pairs", stream(), qk.data_ptr(), vt.data_ptr(), ldv, self.T, dpp, d,
+                      self.dev["img_tok0"].data_ptr(), tq0.data_ptr(), timg.data_ptr(), nt, o.data_ptr(),
+                      None if n_dev is None else n_dev.data_ptr())
         else:
-            _lib.call("ps_attention_pairs" if pairs else "ps_attention", stream(), qk.data_ptr(), vt.data_ptr(),
-                      ldv, self.T, dpp, d, self.dev["img_tok0"].data_ptr(), tq0.data_ptr(), timg.data_ptr(), nt,
-                      o.data_ptr())
+            _lib.call("ps_attention", stream(), qk.data_ptr(), vt.data_ptr(), ldv, self.T, dpp, d,
+                      self.dev["img_tok0"].data_ptr(), tq0.data_ptr(), timg.data_ptr(), nt, o.data_ptr())
         if timer is not None:
             ev[1].record()
             timer.append(ev)
@@ -503,6 +520,62 @@ def run_block_active(batch: CSPBatch, x, ops, active) -> torch.Tensor:
     ctx.rows_live, ctx.rows_act = _row_tiles(ctx, live), _row_tiles(ctx, act)
     ctx.attn_live, ctx.attn_act = _attn_tiles(ctx, live), _attn_tiles(ctx, act)
     return _run_ops(ctx, x, ops)
+
+
+def device_compaction_ok(batch: CSPBatch) -> bool:
+    """run_block_masked's kernels cover this geometry: 256-query attention pairs per patch,
+    8-pixel stitcher units, 8-channel groups."""
+    ps_ = batch.patch_size
+    return USE_PAIRS and (ps_ * ps_) % 256 == 0 and ps_ % 8 == 0 and batch.data.shape[1] % 8 == 0
+
+
+def run_block_masked(batch: CSPBatch, x, ops, mask: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """run_block_active with the reuse decision left on the device: `mask` is the cache's
+    DEVICE bool mask (True = reused).  ps_compact_lists turns it into the GEMM row tiles,
+    attention query tiles and GroupNorm / stitcher patch lists of the active and live sets,
+    and every kernel reads its own work count from device memory -- no host round trip, so
+    the host enqueues the next block while this one runs.  The active rows are bit-identical
+    to run_block_active's (same kernels and tile contents; only the tile counts move).
+    Returns (output, counts) with counts the device int32 [6] of ps_compact_lists."""
+    x = _check_data(batch, x)
+    if not device_compaction_ok(batch):
+        raise InputError("run_block_masked: geometry not covered (see device_compaction_ok)")
+    m = mask.to(device=require_cuda(), dtype=torch.bool).contiguous()
+    if tuple(m.shape) != (batch.n_patches,):
+        raise InputError(f"mask must be ({batch.n_patches},) bool")
+    ctx = Ctx(batch)
+    counts = _device_lists(ctx, m)
+    return _run_ops(ctx, x, ops), counts
+
+
+def _attn_order(ctx: "Ctx") -> torch.Tensor:
+    """Device copy of the attention patch order of _attn_tiles (longest images first, stable)."""
+    b = ctx.b
+    sizes = b.request_offset[1:] - b.request_offset[:-1]
+    key = ("order", np.asarray(b.request_index).tobytes(), np.asarray(sizes).tobytes(), str(ctx.device))
+    if key not in _SKV_CACHE:
+        order = sorted(range(ctx.P), key=lambda p: -int(sizes[b.request_index[p]]))
+        _SKV_CACHE[key] = torch.as_tensor(np.asarray(order, np.int32), device=ctx.device)
+    return _SKV_CACHE[key]
+
+
+def _device_lists(ctx: "Ctx", mask: torch.Tensor) -> torch.Tensor:
+    P, R, hw = ctx.P, ctx.b.n_requests, ctx.hw
+    tpp, tq = hw // 128, 256
+    qpp = hw // tq
+    sizes = [R, P * tpp, P * tpp, P, P * qpp, P * qpp, P * qpp, P * qpp, 6]
+    buf = torch.empty(sum(sizes), dtype=torch.int32, device=ctx.device)
+    live, rows_act, rows_live, live_p, aq_a, ai_a, aq_l, ai_l, counts = torch.split(buf, sizes)
+    _lib.call("ps_compact_lists", stream(), mask.view(torch.uint8).data_ptr(), P, ctx.dev["request_index"].data_ptr(),
+              R, _attn_order(ctx).data_ptr(), tpp, qpp, tq, hw, live.data_ptr(), rows_act.data_ptr(),
+              rows_live.data_ptr(), live_p.data_ptr(), aq_a.data_ptr(), ai_a.data_ptr(), aq_l.data_ptr(),
+              ai_l.data_ptr(), counts.data_ptr())
+    ctx.rows_act = (rows_act, P * tpp, counts[0:1])
+    ctx.rows_live = (rows_live, P * tpp, counts[1:2])
+    ctx.attn_act = (aq_a, ai_a, P * qpp, True, None, None, counts[2:3])
+    ctx.attn_live = (aq_l, ai_l, P * qpp, True, None, None, counts[3:4])
+    ctx.gn_live = (live_p, P, counts[5:6])
+    return counts
 
 
 def _row_tiles(ctx: "Ctx", pats: np.ndarray):

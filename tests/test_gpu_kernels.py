@@ -181,7 +181,7 @@ def test_frames_cl_register_transpose_matches_smem_kernel(C, ps, mode, monkeypat
         sub = torch.full((P, ps + 2, ps + 2, Cp), 7.0, device="cuda").to(torch.bfloat16)
         _lib.call("ps_frames_cl_sub", stream(), x.data_ptr(), P, C, ps, Cp, mode, stats.data_ptr(),
                   dev["request_index"].data_ptr(), dev["neighbors"].data_ptr(), G, gamma.data_ptr(),
-                  beta.data_ptr(), owned.data_ptr(), 2, sub.data_ptr())
+                  beta.data_ptr(), owned.data_ptr(), 2, sub.data_ptr(), None)
         torch.cuda.synchronize()
         return fr, cl, sub
 
@@ -194,7 +194,7 @@ def test_frames_cl_register_transpose_matches_smem_kernel(C, ps, mode, monkeypat
     pull = torch.full((P, ps + 2, ps + 2, Cp), 7.0, device="cuda").to(torch.bfloat16)
     _lib.call("ps_frames_cl_sub", stream(), x.data_ptr(), P, C, ps, Cp, mode, stats.data_ptr(),
               dev["request_index"].data_ptr(), dev["neighbors"].data_ptr(), G, gamma.data_ptr(),
-              beta.data_ptr(), allp.data_ptr(), P, pull.data_ptr())
+              beta.data_ptr(), allp.data_ptr(), P, pull.data_ptr(), None)
     torch.cuda.synchronize()
     assert torch.equal(pull, a[0])
     # the interior of each frame is the patch itself (mode 0) / its affine image (mode 1)
