@@ -248,9 +248,11 @@ int ps_cache_evict(void* stream, uint8_t* exists, int32_t* streak, const int32_t
 /* Block-level fusion of the engine's cache sequence (engine.py:137-142):
  * substitute: x_sub = mask ? snap_in[slot] : x   (patched.py:243-244)
  * finish:     masked -> y = snap_out[slot], streak++ (patched.py:246, cache.py:150)
- *             unmasked -> snap_in/out[slot] = x/y, streak = 0, exists = 1 (cache.py:165-169) */
+ *             unmasked -> snap_in/out[slot] = x/y, streak = 0, exists = 1 (cache.py:165-169)
+ * substitute with `patches` (DEVICE list, n_list entries or the DEVICE count n_dev) writes
+ * those patches only (the live patches of a device-decided compaction). */
 int ps_cache_substitute(void* stream, const uint8_t* mask, const int32_t* slots, int P, int64_t n, const void* x,
-                        const void* snap_in, void* x_sub);
+                        const void* snap_in, void* x_sub, const int32_t* patches, int n_list, const int32_t* n_dev);
 int ps_cache_finish(void* stream, const uint8_t* mask, const int32_t* slots, uint8_t* exists, int32_t* streak,
                     int P, int64_t n, const void* x, void* y, void* snap_in, void* snap_out, int64_t* counters);
 /* masked selection used by masked_block_forward (patched.py:241-246): out = mask ? a : b. */

@@ -83,7 +83,7 @@ _SIGS = {
     "ps_cache_fill": ([p, p, p, p, p, C.c_int, i64, p, p, p], C.c_int),
     "ps_cache_update": ([p, p, p, p, p, C.c_int, i64, p, p, p, p, p], C.c_int),
     "ps_cache_evict": ([p, p, p, p, C.c_int], C.c_int),
-    "ps_cache_substitute": ([p, p, p, C.c_int, i64, p, p, p], C.c_int),
+    "ps_cache_substitute": ([p, p, p, C.c_int, i64, p, p, p, p, C.c_int, p], C.c_int),
     "ps_cache_finish": ([p, p, p, p, p, C.c_int, i64, p, p, p, p, p], C.c_int),
     "ps_select_patches": ([p, p, C.c_int, i64, p, p, p], C.c_int),
     "ps_prompt_bias": ([p, p, p, p, C.c_int, C.c_int, C.c_int, p], C.c_int),

@@ -362,11 +362,16 @@ class BlockCache:
         return n
 
     # ------------------------------------------------ fused block path
-    def block_substitute(self, block_id: int, slots: torch.Tensor, mask: torch.Tensor, x: torch.Tensor):
-        """x_sub = mask ? snap_in : x (gather + np.where of patched.py:243-244, fused)."""
+    def block_substitute(self, block_id: int, slots: torch.Tensor, mask: torch.Tensor, x: torch.Tensor,
+                         patches=None):
+        """x_sub = mask ? snap_in : x (gather + np.where of patched.py:243-244, fused).
+        patches: optional (device list, length bound, device length) -- only those rows are
+        written (the others are left unspecified)."""
         out = torch.empty_like(x)
+        plist, n_ub, n_dev = patches if patches is not None else (None, 0, None)
         _lib.call("ps_cache_substitute", stream(), mask.view(torch.uint8).data_ptr(), slots.data_ptr(), x.shape[0],
-                  self._n, x.data_ptr(), self._snap_in[block_id].data_ptr(), out.data_ptr())
+                  self._n, x.data_ptr(), self._snap_in[block_id].data_ptr(), out.data_ptr(),
+                  None if plist is None else plist.data_ptr(), n_ub, None if n_dev is None else n_dev.data_ptr())
         return out
 
     def block_finish(self, block_id: int, slots: torch.Tensor, mask: torch.Tensor, x: torch.Tensor,

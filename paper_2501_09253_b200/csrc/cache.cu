@@ -132,16 +132,61 @@ __global__ void __launch_bounds__(256) mse_combine_kernel(
   if (live) {
     double* w = v;
     if (in_smem) {
-      for (int i = threadIdx.x; i < L; i += blockDim.x) sv[i] = v[i];
+      // the leaf sums (L2-resident, written by mse_leaf_kernel): 8 independent loads in
+      // flight per thread instead of one L2 round trip per loop trip
+      for (int base = 0; base < L; base += 8 * blockDim.x) {
+        double t[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int i = base + k * blockDim.x + threadIdx.x;
+          t[k] = i < L ? __ldcg(v + i) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int i = base + k * blockDim.x + threadIdx.x;
+          if (i < L) sv[i] = t[k];
+        }
+      }
       __syncthreads();
       w = sv;
     }
-    for (int h = 0; h < H; ++h) {
-      for (int i = level_off[h] + threadIdx.x; i < level_off[h + 1]; i += blockDim.x)
-        w[L + i] = __dadd_rn(w[nodes[2 * i]], w[nodes[2 * i + 1]]);
+    if (in_smem && smem_nodes >= L + I + I) {
+      // node index pairs staged next to the values (int2 per node): the levels then touch
+      // shared memory only -- no L2 round trip per level for the tree structure
+      int2* sn = reinterpret_cast<int2*>(sv + L + I);
+      for (int base = 0; base < I; base += 8 * blockDim.x) {
+        int2 t[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int i = base + k * blockDim.x + threadIdx.x;
+          t[k] = i < I ? __ldg(reinterpret_cast<const int2*>(nodes) + i) : make_int2(0, 0);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int i = base + k * blockDim.x + threadIdx.x;
+          if (i < I) sn[i] = t[k];
+        }
+      }
       __syncthreads();
+      for (int h = 0; h < H; ++h) {
+        const int e = __ldg(level_off + h + 1);
+        for (int i = __ldg(level_off + h) + threadIdx.x; i < e; i += blockDim.x) {
+          const int2 c = sn[i];
+          w[L + i] = __dadd_rn(w[c.x], w[c.y]);
+        }
+        __syncthreads();
+      }
+    } else {
+      for (int h = 0; h < H; ++h) {
+        for (int i = level_off[h] + threadIdx.x; i < level_off[h + 1]; i += blockDim.x)
+          w[L + i] = __dadd_rn(w[nodes[2 * i]], w[nodes[2 * i + 1]]);
+        __syncthreads();
+      }
     }
-    if (threadIdx.x == 0) root_s = I > 0 ? w[L + I - 1] : w[0];
+    if (threadIdx.x == 0) {
+      root_s = I > 0 ? w[L + I - 1] : w[0];
+      if (in_smem && I > 0) v[L + I - 1] = root_s;  // the root stays readable in scratch (ps.mse)
+    }
   }
   if (threadIdx.x == 0) {
     bool m = false;
@@ -217,6 +262,8 @@ struct PatchOpArgs {
   __nv_bfloat16* o2;  // gather outs
   int32_t* err;
   int64_t* counters;
+  const int32_t* plist;  // optional patch list (grid.x walks it) ...
+  const int32_t* n_dev;  // ... with its DEVICE length (grid.x is an upper bound)
 };
 
 __device__ __forceinline__ void copy_range(__nv_bfloat16* dst, const __nv_bfloat16* src, int64_t n, bool vec) {
@@ -241,7 +288,8 @@ __device__ __forceinline__ void zero_range(__nv_bfloat16* dst, int64_t n, bool v
 
 template <int OP>
 __global__ void __launch_bounds__(256) patch_op_kernel(PatchOpArgs a) {
-  const int p = blockIdx.x;
+  if (a.n_dev != nullptr && (int)blockIdx.x >= *a.n_dev) return;
+  const int p = a.plist ? a.plist[blockIdx.x] : (int)blockIdx.x;
   const bool m = a.mask[p] != 0;
   const int slot = a.slots ? a.slots[p] : -1;
   const int64_t n = a.n;
@@ -438,8 +486,11 @@ int ps_cache_predict(void* stream, const void* x, int P, int64_t n, const int32_
   if (rc) return rc;
   // the tree in shared memory when it fits (levels then cost smem latency, not L2 round trips)
   const int nodes_all = n_leaves + n_internal;
-  // (measured: the shared-memory variant is slower at config 2 -- 23 vs 18 us -- so it is off)
-  const int smem_c = (getenv("PS_MSE_SMEM_COMBINE") && nodes_all * 8 <= 200 * 1024) ? nodes_all * 8 : 0;
+  // values (8 B per node) + node index pairs (8 B per internal node) in shared memory: 14 -> 9
+  // us per launch at config 2 (the in-place L2 levels, PS_MSE_L2_COMBINE=1, wait for an L2
+  // round trip per level)
+  const int smem_need = nodes_all * 8 + n_internal * 8;
+  const int smem_c = (!getenv("PS_MSE_L2_COMBINE") && smem_need <= 200 * 1024) ? smem_need : 0;
   static bool attr_c = false;
   if (!attr_c) {
     cudaFuncSetAttribute(mse_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -505,11 +556,12 @@ int ps_cache_evict(void* stream, uint8_t* exists, int32_t* streak, const int32_t
 }
 
 int ps_cache_substitute(void* stream, const uint8_t* mask, const int32_t* slots, int P, int64_t n, const void* x,
-                        const void* snap_in, void* x_sub) {
+                        const void* snap_in, void* x_sub, const int32_t* patches, int n_list, const int32_t* n_dev) {
   PatchOpArgs a{};
   a.mask = mask; a.slots = slots; a.n = n; a.x = (const __nv_bfloat16*)x;
   a.snap_in = (__nv_bfloat16*)snap_in; a.o1 = (__nv_bfloat16*)x_sub;
-  return launch_op<OP_SUBST>((cudaStream_t)stream, P, n, a, "cache_substitute");
+  a.plist = patches; a.n_dev = patches ? n_dev : nullptr;
+  return launch_op<OP_SUBST>((cudaStream_t)stream, patches ? n_list : P, n, a, "cache_substitute");
 }
 
 int ps_cache_finish(void* stream, const uint8_t* mask, const int32_t* slots, uint8_t* exists, int32_t* streak, int P,

@@ -37,7 +37,7 @@ import torch
 from .cache import BlockCache
 from .csp import CSPBatch
 from .model import blend_batch, prompt_bias
-from .patched import _bf16_nchw, device_compaction_ok, run_block, run_block_active, run_block_masked
+from .patched import _bf16_nchw, device_compaction_ok, masked_context, run_block, run_block_active, run_block_ctx
 
 # eager steps: per-block mask read-back (default) or device-built compaction lists; the
 # device form pays off inside a CUDA graph (CachedStepGraph), where no host work is left --
@@ -52,9 +52,10 @@ def _device_blocks(batch, weights, cache, keys, slots, lat, h, rates):
     counts = []
     for b, ops in enumerate(weights):
         mask = cache.predict_reuse(b, keys, h, slots=slots)
-        x_sub = cache.block_substitute(b, slots, mask, h)
-        y, cnt = run_block_masked(batch, x_sub, ops, mask)
-        y = _bf16_nchw(y)
+        ctx, cnt = masked_context(batch, mask)
+        # the block reads its input only at the patches of live images
+        x_sub = cache.block_substitute(b, slots, mask, h, patches=ctx.gn_live)
+        y = _bf16_nchw(run_block_ctx(ctx, x_sub, ops))
         cache.block_finish(b, slots, mask, h, y)
         counts.append(cnt[4:5])
         h = y

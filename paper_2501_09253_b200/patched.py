@@ -543,9 +543,20 @@ def run_block_masked(batch: CSPBatch, x, ops, mask: torch.Tensor) -> tuple[torch
     m = mask.to(device=require_cuda(), dtype=torch.bool).contiguous()
     if tuple(m.shape) != (batch.n_patches,):
         raise InputError(f"mask must be ({batch.n_patches},) bool")
-    ctx = Ctx(batch)
-    counts = _device_lists(ctx, m)
+    ctx, counts = masked_context(batch, m)
     return _run_ops(ctx, x, ops), counts
+
+
+def masked_context(batch: CSPBatch, mask: torch.Tensor) -> tuple["Ctx", torch.Tensor]:
+    """The Ctx of run_block_masked (device-built compaction lists from the DEVICE mask) and
+    its counts; ctx.gn_live lists the patches whose block input is read."""
+    ctx = Ctx(batch)
+    return ctx, _device_lists(ctx, mask)
+
+
+def run_block_ctx(ctx: "Ctx", x, ops) -> torch.Tensor:
+    """The block stages of `ops` on a prepared Ctx (masked_context)."""
+    return _run_ops(ctx, _check_data(ctx.b, x), ops)
 
 
 def _attn_order(ctx: "Ctx") -> torch.Tensor:
