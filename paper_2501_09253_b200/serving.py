@@ -24,8 +24,11 @@ latency) are in B200 time.
 
 from __future__ import annotations
 
+import gc
 import heapq
 import json
+import os
+import sys
 from dataclasses import dataclass, field, replace
 from typing import Sequence
 
@@ -642,6 +645,10 @@ def measure_step_ms(model_cfg, weights, comps: Sequence[dict], patch_size: int =
         cache = BlockCache(model_cfg.n_blocks, PredictorConfig()) if use_cache else None
         n_runs = 12 if use_cache else reps + 1
         times = []
+        # host stalls (a Python GC pass, measured up to ~250 ms once in a long bench process)
+        # would land inside the event pair: no collection while a composition is timed
+        gc_was = gc.isenabled()
+        gc.disable()
         for rep in range(n_runs):
             t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             t0.record()
@@ -655,6 +662,14 @@ def measure_step_ms(model_cfg, weights, comps: Sequence[dict], patch_size: int =
             times.append(t0.elapsed_time(t1))
             if use_cache:
                 reqs = [(rid, lat[rid]) for rid, _ in reqs]
+        if gc_was:
+            gc.enable()
+        if os.environ.get("PS_CALIB_DEBUG"):
+            print("calibration", dict(comp), [round(t, 3) for t in times],
+                  f"reserved {torch.cuda.memory_reserved() / 2**30:.1f} GiB",
+                  f"allocated {torch.cuda.memory_allocated() / 2**30:.1f} GiB",
+                  f"alloc_retries {torch.cuda.memory_stats().get('num_alloc_retries', 0)}",
+                  f"cudaMalloc {torch.cuda.memory_stats().get('num_device_alloc', 0)}", file=sys.stderr, flush=True)
         if use_cache:
             cold, warm = float(np.mean(times[:4])), float(np.mean(times[4:]))
             k = min(4, steps)
@@ -671,7 +686,7 @@ CALIBRATION_COMPS = ({"low": 1}, {"med": 1}, {"high": 1}, {"low": 4, "med": 4, "
 
 def slo_run(model_cfg, weights, n_requests: int = 64, load: float = 0.9, steps: int = 50, seed: int = 0,
             use_cache: bool = True, policy: str = "slo_aware", max_active: int = 12, slo_scale: float = 3.0,
-            calib_reps: int = 3, rank: int = 0, world: int = 1, share=None, gather=None,
+            calib_reps: int = 5, rank: int = 0, world: int = 1, share=None, gather=None,
             adaptive: bool = True) -> dict:
     """SLO attainment of the B200 path in the wall plane.
 
