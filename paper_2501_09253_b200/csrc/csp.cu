@@ -333,59 +333,6 @@ __global__ void __launch_bounds__(256) blend_reassemble_kernel(const float* __re
   }
 }
 
-// blend + reassemble along image rows: one CTA per (request, patch row, CPB channels) writes
-// whole image rows (contiguous) from that patch row's patches
-__global__ void __launch_bounds__(256) blend_reassemble_rows_kernel(const float* __restrict__ lat,
-                                                                    const __nv_bfloat16* __restrict__ hh,
-                                                                    const float* __restrict__ rates,
-                                                                    const uint64_t* __restrict__ img_ptrs,
-                                                                    const int32_t* __restrict__ req_off,
-                                                                    const int32_t* __restrict__ sides, int n_req,
-                                                                    int C, int ps, int cpb) {
-  int pr = blockIdx.x, req = 0;
-  for (; req < n_req; ++req) {
-    const int sd = __ldg(sides + req);
-    if (pr < sd) break;
-    pr -= sd;
-  }
-  if (req >= n_req) return;
-  const int side = __ldg(sides + req), L = side * ps, p0 = __ldg(req_off + req) + pr * side;
-  float* img = reinterpret_cast<float*>(img_ptrs[req]);
-  const float rate = __ldg(rates + req);
-  const int c0 = blockIdx.y * cpb, nc = min(cpb, C - c0);
-  const int vrow = L / 4;
-  const int n = nc * ps * vrow;
-  for (int base = threadIdx.x; base < n; base += 256 * PM_UNR) {
-    float4 x[PM_UNR];
-    uint2 hv[PM_UNR];
-    int64_t io[PM_UNR];
-#pragma unroll
-    for (int u = 0; u < PM_UNR; ++u) {
-      const int i = base + u * 256;
-      io[u] = -1;
-      if (i < n) {
-        const int xv = i % vrow, y = (i / vrow) % ps, c = c0 + i / (vrow * ps);
-        const int xx = xv * 4, pc = xx / ps, xp = xx - pc * ps;
-        const int64_t po = (((int64_t)(p0 + pc) * C + c) * ps + y) * ps + xp;
-        x[u] = __ldg(reinterpret_cast<const float4*>(lat + po));
-        hv[u] = __ldg(reinterpret_cast<const uint2*>(hh + po));
-        io[u] = ((int64_t)c * L + (int64_t)pr * ps + y) * L + xx;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < PM_UNR; ++u)
-      if (io[u] >= 0) {
-        const __nv_bfloat162 h01 = *reinterpret_cast<const __nv_bfloat162*>(&hv[u].x);
-        const __nv_bfloat162 h23 = *reinterpret_cast<const __nv_bfloat162*>(&hv[u].y);
-        float4 o;
-        o.x = (1.f - rate) * x[u].x + rate * tanhf(__low2float(h01));
-        o.y = (1.f - rate) * x[u].y + rate * tanhf(__high2float(h01));
-        o.z = (1.f - rate) * x[u].z + rate * tanhf(__low2float(h23));
-        o.w = (1.f - rate) * x[u].w + rate * tanhf(__high2float(h23));
-        *reinterpret_cast<float4*>(img + io[u]) = o;
-      }
-  }
-}
 
 template <bool TO_PATCHES>
 static int csp_copy(cudaStream_t st, const uint64_t* ptrs, const int32_t* off, const int32_t* sides, int n_req,
@@ -529,14 +476,9 @@ int ps_blend_reassemble(void* stream, const float* latent, const void* h, const 
   if (n_patches == 0) return PS_OK;
   if (n_patches > 65535) return set_error(PS_ERR_INPUT, "blend_reassemble: too many patches");
   const int cpb = pm_cpb(C, ps_, 4);
-  if (!getenv("PS_BLEND_ROWS")) {  // row-wise variant measured slower (103 vs 95 us)
-    blend_reassemble_kernel<<<dim3(n_patches, (C + cpb - 1) / cpb), 256, 0, (cudaStream_t)stream>>>(
-        latent, (const __nv_bfloat16*)h, rates, dst_ptrs, request_offset, sides, n_req, C, ps_, cpb);
-  } else {
-    // one CTA per patch row (the grid is sized by P >= rows; surplus CTAs return)
-    blend_reassemble_rows_kernel<<<dim3(n_patches, (C + cpb - 1) / cpb), 256, 0, (cudaStream_t)stream>>>(
-        latent, (const __nv_bfloat16*)h, rates, dst_ptrs, request_offset, sides, n_req, C, ps_, cpb);
-  }
+  // (a row-wise variant -- one CTA per image row band -- measured 103 vs 95 us and was removed)
+  blend_reassemble_kernel<<<dim3(n_patches, (C + cpb - 1) / cpb), 256, 0, (cudaStream_t)stream>>>(
+      latent, (const __nv_bfloat16*)h, rates, dst_ptrs, request_offset, sides, n_req, C, ps_, cpb);
   count_launch();
   return check_launch("blend_reassemble");
 }

@@ -126,146 +126,13 @@ __global__ void __launch_bounds__(256, 4) gn_partials_kernel(const __nv_bfloat16
   }
 }
 
-// Persistent, software-pipelined partials: CTA b walks slices s = b, b + grid, ... (slice =
-// one (patch, group) run of cg*hw contiguous bf16, <= 256*V vectors); the next slice's
-// 16-byte loads are in flight while the current one is reduced (two-pass from registers).
-template <int V>
-__device__ __forceinline__ void gn_load(const __nv_bfloat16* base, int nv, uint4 (&r)[V]) {
-#pragma unroll
-  for (int i = 0; i < V; ++i) {
-    const int k = threadIdx.x + i * 256;
-    r[i] = k < nv ? __ldg(reinterpret_cast<const uint4*>(base) + k) : make_uint4(0, 0, 0, 0);
-  }
-}
-template <int V>
-__device__ __forceinline__ void gn_reduce(const uint4 (&r)[V], int nv, int64_t n, float* red, float* out) {
-  float s = 0.f;
-#pragma unroll
-  for (int i = 0; i < V; ++i) {
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r[i]);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) s += __low2float(h[k]) + __high2float(h[k]);
-  }
-  const float mean = block_sum(s, red) / (float)n;
-  float m2 = 0.f;
-#pragma unroll
-  for (int i = 0; i < V; ++i) {
-    if (threadIdx.x + i * 256 < nv) {
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r[i]);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float a = __low2float(h[k]) - mean, b = __high2float(h[k]) - mean;
-        m2 += a * a + b * b;
-      }
-    }
-  }
-  m2 = block_sum(m2, red + 32);
-  if (threadIdx.x == 0) {
-    out[0] = mean;
-    out[1] = m2;
-  }
-}
-template <int V>
-__global__ void __launch_bounds__(256, 2) gn_partials_pipe_kernel(const __nv_bfloat16* __restrict__ x, int C, int hw,
-                                                                  int G, const int32_t* __restrict__ plist,
-                                                                  int n_slices, float* __restrict__ partials) {
-  __shared__ float red[64];
-  const int cg = C / G;
-  const int64_t n = (int64_t)cg * hw;
-  const int nv = (int)(n / 8);
-  auto slice_base = [&](int sl, int& p, int& g) {
-    p = plist ? __ldg(plist + sl / G) : sl / G;
-    g = sl % G;
-    return x + ((int64_t)p * C + (int64_t)g * cg) * hw;
-  };
-  uint4 ra[V], rb[V];
-  int s = blockIdx.x;
-  int pa, ga, pb, gb;
-  if (s < n_slices) gn_load<V>(slice_base(s, pa, ga), nv, ra);
-  for (; s < n_slices; s += 2 * gridDim.x) {
-    const int s2 = s + gridDim.x;
-    if (s2 < n_slices) gn_load<V>(slice_base(s2, pb, gb), nv, rb);
-    gn_reduce<V>(ra, nv, n, red, partials + ((int64_t)pa * G + ga) * 2);
-    if (s2 >= n_slices) break;
-    const int s3 = s2 + gridDim.x;
-    if (s3 < n_slices) gn_load<V>(slice_base(s3, pa, ga), nv, ra);
-    gn_reduce<V>(rb, nv, n, red, partials + ((int64_t)pb * G + gb) * 2);
-  }
-}
-
-// Bulk-staged partials: the (patch, group) slice (contiguous cg*hw bf16) arrives in shared
-// memory through one TMA bulk copy, so a CTA keeps its whole slice in flight with no
-// register staging; mean and M2 are then two passes over shared memory.
-__global__ void __launch_bounds__(256) gn_partials_bulk_kernel(const __nv_bfloat16* __restrict__ x, int C, int hw,
-                                                               int G, const int32_t* __restrict__ plist,
-                                                               float* __restrict__ partials) {
-  extern __shared__ __align__(16) uint8_t gsm[];
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ float red[64];
-  const int p = plist ? __ldg(plist + blockIdx.x) : (int)blockIdx.x, g = blockIdx.y;
-  const int cg = C / G;
-  const int n = cg * hw;
-  const __nv_bfloat16* base = x + ((int64_t)p * C + (int64_t)g * cg) * hw;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    fence_mbar_init();
-    mbar_arrive_expect_tx(&bar, (uint32_t)n * 2);
-    bulk_load(gsm, base, (uint32_t)n * 2, &bar);
-  }
-  __syncthreads();
-  mbar_wait(&bar, 0);
-  const uint4* v4 = reinterpret_cast<const uint4*>(gsm);
-  const int nv = n / 8;
-  float s = 0.f;
-  for (int k = threadIdx.x; k < nv; k += 256) {
-    const uint4 r = v4[k];
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) s += __low2float(h[e]) + __high2float(h[e]);
-  }
-  const float mean = block_sum(s, red) / (float)n;
-  float m2 = 0.f;
-  for (int k = threadIdx.x; k < nv; k += 256) {
-    const uint4 r = v4[k];
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float a = __low2float(h[e]) - mean, b = __high2float(h[e]) - mean;
-      m2 += a * a + b * b;
-    }
-  }
-  m2 = block_sum(m2, red + 32);
-  if (threadIdx.x == 0) {
-    partials[((int64_t)p * G + g) * 2] = mean;
-    partials[((int64_t)p * G + g) * 2 + 1] = m2;
-  }
-}
-
-// host: pipelined kernel when a slice fits 256*8 vectors and is 16-byte aligned, else the simple one
+// host: one CTA per (patch, group) slice.  (Persistent software-pipelined and bulk-copy
+// staged variants measured 21-26 us against 20-21 us and were removed.)
 static void launch_gn_partials(cudaStream_t st, const void* x, int P, int C, int hw, int G, const int32_t* plist,
                                int n, float* partials, const int32_t* n_dev = nullptr) {
-  const int64_t elems = (int64_t)(C / G) * hw;
-  const int64_t nv = elems / 8;
-  const int n_slices = n * G;
-  int grid = 148 * 2;
-  if (grid > n_slices) grid = n_slices;
+  (void)P;
+  (void)C;
   const auto xb = (const __nv_bfloat16*)x;
-  const int64_t slice_bytes = elems * 2;
-  if (elems % 8 == 0 && slice_bytes <= 96 * 1024 && getenv_flag("PS_GN_BULK") && !n_dev) {  // measured 23 vs 21 us: opt-in
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(gn_partials_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-      attr = true;
-    }
-    gn_partials_bulk_kernel<<<dim3(n, G), 256, (size_t)slice_bytes, st>>>(xb, C, hw, G, plist, partials);
-    return;
-  }
-  if (elems % 8 == 0 && nv <= 256 * 6 && getenv_flag("PS_GN_PIPE") && !n_dev) {
-    if (nv <= 256 * 2) gn_partials_pipe_kernel<2><<<grid, 256, 0, st>>>(xb, C, hw, G, plist, n_slices, partials);
-    else if (nv <= 256 * 4) gn_partials_pipe_kernel<4><<<grid, 256, 0, st>>>(xb, C, hw, G, plist, n_slices, partials);
-    else gn_partials_pipe_kernel<6><<<grid, 256, 0, st>>>(xb, C, hw, G, plist, n_slices, partials);
-    return;
-  }
   gn_partials_kernel<<<dim3(n, G), 256, 0, st>>>(xb, C, hw, G, plist, n_dev, partials);
 }
 
@@ -645,7 +512,7 @@ __device__ __forceinline__ void frames_t8_unit(const __nv_bfloat16* __restrict__
 }
 
 template <bool FRAMES, bool PUSH>
-__global__ void __launch_bounds__(256, PUSH ? 3 : 4) frames_t8_kernel(const __nv_bfloat16* __restrict__ x, int C, int ps, int Cp,
+__global__ void __launch_bounds__(256, 3) frames_t8_kernel(const __nv_bfloat16* __restrict__ x, int C, int ps, int Cp,
                                                         int mode, const float* __restrict__ stats,
                                                         const int32_t* __restrict__ ri,
                                                         const int32_t* __restrict__ nbr, int G,
