@@ -52,6 +52,7 @@ template <int DP, int NV_>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
     attn2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                  const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
+  pdl_wait();
   using Cfg = Attn2Cfg<DP, NV_>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -345,7 +346,7 @@ static int launch2_nv(const CUtensorMap& q, const CUtensorMap& k, const CUtensor
     cudaFuncSetAttribute(attn2_kernel<DP, NV_>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr = true;
   }
-  attn2_kernel<DP, NV_><<<2 * p.n_tiles, A2_THREADS, Cfg::SMEM, st>>>(q, k, v, p);
+  launch_pdl(attn2_kernel<DP, NV_>, dim3(2 * p.n_tiles), dim3(A2_THREADS), Cfg::SMEM, st, q, k, v, p);
   count_launch();
   return check_launch("attention_2cta");
 }

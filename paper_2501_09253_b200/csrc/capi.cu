@@ -28,6 +28,11 @@ int set_error(int code, const char* fmt, ...) {
   va_end(ap);
   return code;
 }
+bool pdl_enabled() {
+  static const bool on = !getenv("PS_PDL") || atoi(getenv("PS_PDL")) != 0;
+  return on;
+}
+
 int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(PS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));

@@ -231,6 +231,9 @@ PS_DEV uint64_t sdesc_sw128(const void* smem_ptr) {
                "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]))
 // Keep uses of tcgen05.ld destination registers after the tcgen05.wait::ld that
 // makes them valid (the compiler sees no data dependence on the wait itself).
+// PDL: wait until the previous grid on the stream has completed and its writes are visible
+// (a no-op when the kernel was launched without the programmatic attribute)
+PS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 PS_DEV void reg_fence32(uint32_t (&r)[32]) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) asm volatile("" : "+r"(r[i]));

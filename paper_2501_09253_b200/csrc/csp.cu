@@ -245,6 +245,7 @@ __global__ void __launch_bounds__(256) csp_split_bias_rows_kernel(const uint64_t
                                                                   const float* __restrict__ prompts,
                                                                   float* __restrict__ patches,
                                                                   __nv_bfloat16* __restrict__ h) {
+  pdl_wait();
   int pr = blockIdx.x, req = 0;
   for (; req < n_req; ++req) {
     const int sd = __ldg(sides + req);
@@ -293,6 +294,7 @@ __global__ void __launch_bounds__(256) blend_reassemble_kernel(const float* __re
                                                                const int32_t* __restrict__ req_off,
                                                                const int32_t* __restrict__ sides, int n_req, int C,
                                                                int ps, int cpb) {
+  pdl_wait();
   const int p = blockIdx.x, c0 = blockIdx.y * cpb;
   int req, side, k;
   pm_locate(p, req_off, sides, n_req, req, side, k);
@@ -463,8 +465,8 @@ int ps_csp_split_bias(void* stream, const uint64_t* src_ptrs, const int32_t* req
   if (n_patches == 0) return PS_OK;
   if (n_patches > 65535) return set_error(PS_ERR_INPUT, "csp_split_bias: too many patches");
   const int cpb = pm_cpb(C, ps_, 4);
-  csp_split_bias_rows_kernel<<<dim3(n_patches, (C + cpb - 1) / cpb), 256, 0, (cudaStream_t)stream>>>(
-      src_ptrs, request_offset, sides, n_req, C, ps_, cpb, prompts, dst, (__nv_bfloat16*)h);
+  launch_pdl(csp_split_bias_rows_kernel, dim3(n_patches, (C + cpb - 1) / cpb), dim3(256), 0, (cudaStream_t)stream,
+             src_ptrs, request_offset, sides, n_req, C, ps_, cpb, prompts, dst, (__nv_bfloat16*)h);
   count_launch();
   return check_launch("csp_split_bias");
 }
@@ -477,8 +479,8 @@ int ps_blend_reassemble(void* stream, const float* latent, const void* h, const 
   if (n_patches > 65535) return set_error(PS_ERR_INPUT, "blend_reassemble: too many patches");
   const int cpb = pm_cpb(C, ps_, 4);
   // (a row-wise variant -- one CTA per image row band -- measured 103 vs 95 us and was removed)
-  blend_reassemble_kernel<<<dim3(n_patches, (C + cpb - 1) / cpb), 256, 0, (cudaStream_t)stream>>>(
-      latent, (const __nv_bfloat16*)h, rates, dst_ptrs, request_offset, sides, n_req, C, ps_, cpb);
+  launch_pdl(blend_reassemble_kernel, dim3(n_patches, (C + cpb - 1) / cpb), dim3(256), 0, (cudaStream_t)stream,
+             latent, (const __nv_bfloat16*)h, rates, dst_ptrs, request_offset, sides, n_req, C, ps_, cpb);
   count_launch();
   return check_launch("blend_reassemble");
 }

@@ -47,6 +47,7 @@ template <int CP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
     ff_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
                    const __grid_constant__ CUtensorMap tmW2, const FfParams p) {
+  pdl_wait();
   using Cfg = FfCfg<CP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -410,7 +411,7 @@ static int launch_ff(const CUtensorMap& x, const CUtensorMap& w1, const CUtensor
   const int units = (num_m + 1) / 2;
   if (units == 0) return PS_OK;
   const int grid = 2 * (units < sms / 2 ? units : sms / 2);
-  ff_pair_kernel<CP><<<grid, FF_THREADS, Cfg::SMEM, st>>>(x, w1, w2, p);
+  launch_pdl(ff_pair_kernel<CP>, dim3(grid), dim3(FF_THREADS), Cfg::SMEM, st, x, w1, w2, p);
   count_launch();
   return check_launch("ff_pair");
 }

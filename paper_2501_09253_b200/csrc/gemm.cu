@@ -88,6 +88,7 @@ template <int BN, bool PAIR>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
+  pdl_wait();
   using Cfg = GemmCfg<BN, PAIR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -534,20 +535,22 @@ static int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const CUtensorM
   const int max_units = num_sms() / per_unit;
   const int grid = (units < max_units ? units : max_units) * per_unit;
   if (!PAIR) {
-    gemm_tc_kernel<BN, false><<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(a, b, c, p);
+    launch_pdl(gemm_tc_kernel<BN, false>, dim3(grid), dim3(GEMM_THREADS), Cfg::SMEM, st, a, b, c, p);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(GEMM_THREADS);
     cfg.dynamicSmemBytes = Cfg::SMEM;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, true>, a, b, c, p);
   }
   count_launch();

@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(256, 4) gn_partials_kernel(const __nv_bfloat16
                                                           const int32_t* __restrict__ plist,
                                                           const int32_t* __restrict__ n_dev,
                                                           float* __restrict__ partials) {
+  pdl_wait();
   __shared__ float red[32];
   if (n_dev != nullptr && (int)blockIdx.x >= *n_dev) return;  // past the device list length
   const int p = plist ? __ldg(plist + blockIdx.x) : (int)blockIdx.x, g = blockIdx.y;
@@ -133,7 +134,7 @@ static void launch_gn_partials(cudaStream_t st, const void* x, int P, int C, int
   (void)P;
   (void)C;
   const auto xb = (const __nv_bfloat16*)x;
-  gn_partials_kernel<<<dim3(n, G), 256, 0, st>>>(xb, C, hw, G, plist, n_dev, partials);
+  launch_pdl(gn_partials_kernel, dim3(n, G), dim3(256), 0, st, xb, C, hw, G, plist, n_dev, partials);
 }
 
 // Chan-combine the equal-size partials of patches [p0, p1) for group g -> (mean, rstd).
@@ -159,6 +160,7 @@ __device__ __forceinline__ void gn_finalize_group(const float* partials, int p0,
 // grid R, block G (<=1024): Chan-combine the equal-size partials of each request.
 __global__ void gn_finalize_kernel(const float* __restrict__ partials, const int32_t* __restrict__ req_off, int G,
                                    int64_t n_each, float eps, float* __restrict__ stats) {
+  pdl_wait();
   const int r = blockIdx.x;
   for (int g = threadIdx.x; g < G; g += blockDim.x)
     gn_finalize_group<false>(partials, req_off[r], req_off[r + 1], G, g, n_each, eps, stats + ((int64_t)r * G + g) * 2);
@@ -521,6 +523,7 @@ __global__ void __launch_bounds__(256, 3) frames_t8_kernel(const __nv_bfloat16* 
                                                         const int32_t* __restrict__ plist,
                                                         const int32_t* __restrict__ n_dev,
                                                         __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
   extern __shared__ __align__(16) float sab[];  // [2][Cp] (mode 1)
   if (n_dev != nullptr && (int)blockIdx.y >= *n_dev) return;  // past the device list length
   const int p = plist ? __ldg(plist + blockIdx.y) : (int)blockIdx.y;
@@ -546,14 +549,14 @@ static int launch_frames_vec(cudaStream_t st, const void* x, int P, int C, int p
     const size_t sab_bytes = mode == 1 ? 2 * Cp * sizeof(float) : 0;  // <= 48 KB for Cp <= 6144
     if constexpr (FRAMES) {
       if (push) {
-        frames_t8_kernel<true, true><<<g2, 256, sab_bytes, st>>>((const __nv_bfloat16*)x, C, ps, Cp, mode, stats, ri, nbr, G,
-                                                         gamma, beta, plist, n_dev, (__nv_bfloat16*)out);
+        launch_pdl(frames_t8_kernel<true, true>, g2, dim3(256), sab_bytes, st, (const __nv_bfloat16*)x, C, ps, Cp,
+                   mode, stats, ri, nbr, G, gamma, beta, plist, n_dev, (__nv_bfloat16*)out);
         count_launch();
         return check_launch("frames_cl");
       }
     }
-    frames_t8_kernel<FRAMES, false><<<g2, 256, sab_bytes, st>>>((const __nv_bfloat16*)x, C, ps, Cp, mode, stats, ri, nbr, G,
-                                                          gamma, beta, plist, n_dev, (__nv_bfloat16*)out);
+    launch_pdl(frames_t8_kernel<FRAMES, false>, g2, dim3(256), sab_bytes, st, (const __nv_bfloat16*)x, C, ps, Cp,
+               mode, stats, ri, nbr, G, gamma, beta, plist, n_dev, (__nv_bfloat16*)out);
     count_launch();
     return check_launch(FRAMES ? "frames_cl" : "to_cl");
   }
@@ -643,8 +646,8 @@ int ps_gn_partials_sub(void* stream, const void* x, int P, int C, int ps_, int G
 int ps_gn_finalize(void* stream, const float* partials, const int32_t* request_offset, int R, int G, int cg_hw,
                    float eps, float* stats) {
   if (R == 0) return PS_OK;
-  gn_finalize_kernel<<<R, G < 1024 ? ((G + 31) / 32) * 32 : 1024, 0, (cudaStream_t)stream>>>(
-      partials, request_offset, G, cg_hw, eps, stats);
+  launch_pdl(gn_finalize_kernel, dim3(R), dim3(G < 1024 ? ((G + 31) / 32) * 32 : 1024), 0, (cudaStream_t)stream,
+             partials, request_offset, G, (int64_t)cg_hw, eps, stats);
   count_launch();
   return check_launch("gn_finalize");
 }

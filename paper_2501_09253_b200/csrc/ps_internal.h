@@ -57,6 +57,26 @@ int ff_launch(const CUtensorMap& x, const CUtensorMap& w1, const CUtensorMap& w2
 int set_error(int code, const char* fmt, ...);
 int check_launch(const char* what);
 void count_launch();
+
+// Programmatic dependent launch (PDL): the kernel may start while the previous kernel on the
+// stream drains; it must execute griddepcontrol.wait (pdl_wait) before touching memory that
+// kernel writes.  PS_PDL=0 launches normally.  Captured into CUDA graphs as programmatic edges.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, args...);
+}
 int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const GemmParams& p, int bn,
                 int pair, cudaStream_t st);
 int gemm_pick_bn(int n, int k, int epi);
