@@ -47,7 +47,6 @@ template <int CP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
     ff_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
                    const __grid_constant__ CUtensorMap tmW2, const FfParams p) {
-  pdl_wait();
   using Cfg = FfCfg<CP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -71,16 +70,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
-  const int num_m = p.m_map ? (p.m_count_dev ? *p.m_count_dev : p.m_count) : (p.M + FF_BM - 1) / FF_BM;
-  const int n_units = (num_m + 1) / 2;
-  const int unit0 = blockIdx.x >> 1, unit_step = gridDim.x >> 1;
-  const int m_oob = (p.M + FF_BM - 1) / FF_BM;
-  const int NC = p.hp / FF_HC;
-  auto my_m = [&](int u) {
-    const int lm = 2 * u + (int)rank;
-    return lm >= num_m ? -1 : p.m_map ? __ldg(p.m_map + lm) : lm;
-  };
-
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmX);
     tma_prefetch(&tmW1);
@@ -104,6 +93,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // PDL: the setup above overlaps the previous kernel's tail
+  const int num_m = p.m_map ? (p.m_count_dev ? *p.m_count_dev : p.m_count) : (p.M + FF_BM - 1) / FF_BM;
+  const int n_units = (num_m + 1) / 2;
+  const int unit0 = blockIdx.x >> 1, unit_step = gridDim.x >> 1;
+  const int m_oob = (p.M + FF_BM - 1) / FF_BM;
+  const int NC = p.hp / FF_HC;
+  auto my_m = [&](int u) {
+    const int lm = 2 * u + (int)rank;
+    return lm >= num_m ? -1 : p.m_map ? __ldg(p.m_map + lm) : lm;
+  };
+
   unsigned long long cnt[4] = {0, 0, 0, 0};
   const long long t_start = clock64();
   auto tw = [&](uint64_t* bar, uint32_t par, int k) {

@@ -88,7 +88,6 @@ template <int BN, bool PAIR>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
-  pdl_wait();
   using Cfg = GemmCfg<BN, PAIR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -101,21 +100,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int num_n = (p.N + BN - 1) / BN;
-  const int num_m = p.m_map ? (p.m_count_dev ? *p.m_count_dev : p.m_count) : (p.M + GEMM_BM - 1) / GEMM_BM;
-  // PAIR: a work item is (pair of m tiles, n tile); CTA `rank` takes m tile 2*mp + rank
-  const uint32_t rank = PAIR ? cluster_rank() : 0;
-  const bool leader = rank == 0;
-  const int unit0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int unit_step = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
-  const int num_mu = PAIR ? (num_m + 1) / 2 : num_m;
-  const int n_tiles = num_mu * num_n;
-  const int m_oob = (p.M + GEMM_BM - 1) / GEMM_BM;  // a physical tile past the end: TMA zero-fills it
-  // logical -> physical 128-row tile (active-patch compaction); -1 = no tile (odd pair tail)
-  auto phys_m = [&](int lm) { return lm >= num_m ? -1 : p.m_map ? __ldg(p.m_map + lm) : lm; };
-  auto my_m = [&](int t) { return phys_m(PAIR ? 2 * (t / num_n) + (int)rank : t / num_n); };
-  const int num_kb = p.K / GEMM_BK;
-
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
@@ -140,6 +124,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // PDL: barrier init, TMEM allocation and descriptor prefetch above overlap the previous
+  // kernel's tail; everything below may read what it wrote
+  pdl_wait();
+
+  const int num_n = (p.N + BN - 1) / BN;
+  const int num_m = p.m_map ? (p.m_count_dev ? *p.m_count_dev : p.m_count) : (p.M + GEMM_BM - 1) / GEMM_BM;
+  // PAIR: a work item is (pair of m tiles, n tile); CTA `rank` takes m tile 2*mp + rank
+  const uint32_t rank = PAIR ? cluster_rank() : 0;
+  const bool leader = rank == 0;
+  const int unit0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int unit_step = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int num_mu = PAIR ? (num_m + 1) / 2 : num_m;
+  const int n_tiles = num_mu * num_n;
+  const int m_oob = (p.M + GEMM_BM - 1) / GEMM_BM;  // a physical tile past the end: TMA zero-fills it
+  // logical -> physical 128-row tile (active-patch compaction); -1 = no tile (odd pair tail)
+  auto phys_m = [&](int lm) { return lm >= num_m ? -1 : p.m_map ? __ldg(p.m_map + lm) : lm; };
+  auto my_m = [&](int t) { return phys_m(PAIR ? 2 * (t / num_n) + (int)rank : t / num_n); };
+  const int num_kb = p.K / GEMM_BK;
+
 
   // profiling: cycles each role spends blocked on its barriers (p.dbg != null)
   unsigned long long t_wait = 0, t_wait2 = 0;
