@@ -51,7 +51,9 @@ struct Attn2Cfg {
 template <int DP, int NV_>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
     attn2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                 const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
+                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                 const AttnParams p) {
+  if (threadIdx.x == 0) { A2_TRACE(11, 0) }  // kernel entry (profiling)
   pdl_wait();
   using Cfg = Attn2Cfg<DP, NV_>;
   extern __shared__ uint8_t smem_raw[];
@@ -302,29 +304,77 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
     // epilogue: O / l -> bf16 channels-last
     mbar_wait(o_full, 0);
     tc_fence_after();
+    if (threadIdx.x == 128) { A2_TRACE(12, 0) }
     const int q = q0 + row;
     const bool ok = q < k_end;
     const float inv = 1.f / l_run;
-    __nv_bfloat16* dst = p.out + (size_t)q * p.Dp;
+    // up to EPI_G TMEM loads of 32 columns in flight per wait
+    constexpr int EPI_G = (DP / 32) % 5 == 0 ? 5 : (DP / 32) % 4 == 0 ? 4 : (DP / 32) % 3 == 0 ? 3 : (DP / 32) % 2 == 0 ? 2 : 1;
+    if (p.epi_tma && q0 + A2_BM <= k_end) {
+      // whole tile: stage O (bf16) in the Q buffer -- free once the last S MMA completed, and
+      // already laid out as the TMA boxes [64 columns][128 rows] with 128-byte swizzle -- and
+      // leave through TMA stores: per-thread 16-byte row stores (32 rows 640 B apart per
+      // warp instruction) made the epilogue ~8k cycles per tile
+      uint8_t* srow = sQ + row * 128;
 #pragma unroll 1
-    for (int c = 0; c < DP; c += 32) {
-      uint32_t o[32];
-      PS_TMEM_LD32(tmem + lane_base + Cfg::O_COL + c, o);
-      tmem_ld_wait();
-      if (ok) {
-        uint4* d4 = reinterpret_cast<uint4*>(dst + c);
+      for (int c0 = 0; c0 < DP; c0 += 32 * EPI_G) {
+        uint32_t o[EPI_G][32];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          uint4 w;
-          w.x = pack_bf16(__uint_as_float(o[8 * v + 0]) * inv, __uint_as_float(o[8 * v + 1]) * inv);
-          w.y = pack_bf16(__uint_as_float(o[8 * v + 2]) * inv, __uint_as_float(o[8 * v + 3]) * inv);
-          w.z = pack_bf16(__uint_as_float(o[8 * v + 4]) * inv, __uint_as_float(o[8 * v + 5]) * inv);
-          w.w = pack_bf16(__uint_as_float(o[8 * v + 6]) * inv, __uint_as_float(o[8 * v + 7]) * inv);
-          d4[v] = w;
+        for (int g = 0; g < EPI_G; ++g) PS_TMEM_LD32(tmem + lane_base + Cfg::O_COL + c0 + 32 * g, o[g]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int g = 0; g < EPI_G; ++g) {
+          reg_fence32(o[g]);
+          const int col = c0 + 32 * g;
+          uint8_t* box = srow + (col >> 6) * (A2_BM * 128);
+          const int j0 = (col & 63) >> 3;
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            uint4 w;
+            w.x = pack_bf16(__uint_as_float(o[g][8 * v + 0]) * inv, __uint_as_float(o[g][8 * v + 1]) * inv);
+            w.y = pack_bf16(__uint_as_float(o[g][8 * v + 2]) * inv, __uint_as_float(o[g][8 * v + 3]) * inv);
+            w.z = pack_bf16(__uint_as_float(o[g][8 * v + 4]) * inv, __uint_as_float(o[g][8 * v + 5]) * inv);
+            w.w = pack_bf16(__uint_as_float(o[g][8 * v + 6]) * inv, __uint_as_float(o[g][8 * v + 7]) * inv);
+            *reinterpret_cast<uint4*>(box + (((j0 + v) ^ (row & 7)) << 4)) = w;
+          }
+        }
+      }
+      fence_proxy_async();
+      named_bar_sync(1, 128);
+      if (threadIdx.x == 128) {
+        for (int kc = 0; kc < Cfg::KB; ++kc) tma_store_2d(&tmO, sQ + kc * A2_BM * 128, kc * 64, q0);
+        bulk_commit();
+        bulk_wait_read<0>();  // the Q buffer is read by the TMA engine before the CTA exits
+      }
+    } else {
+      __nv_bfloat16* dst = p.out + (size_t)q * p.Dp;
+#pragma unroll 1
+      for (int c0 = 0; c0 < DP; c0 += 32 * EPI_G) {
+        uint32_t o[EPI_G][32];
+#pragma unroll
+        for (int g = 0; g < EPI_G; ++g) PS_TMEM_LD32(tmem + lane_base + Cfg::O_COL + c0 + 32 * g, o[g]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int g = 0; g < EPI_G; ++g) reg_fence32(o[g]);
+        if (ok) {
+#pragma unroll
+          for (int g = 0; g < EPI_G; ++g) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst + c0 + 32 * g);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              uint4 w;
+              w.x = pack_bf16(__uint_as_float(o[g][8 * v + 0]) * inv, __uint_as_float(o[g][8 * v + 1]) * inv);
+              w.y = pack_bf16(__uint_as_float(o[g][8 * v + 2]) * inv, __uint_as_float(o[g][8 * v + 3]) * inv);
+              w.z = pack_bf16(__uint_as_float(o[g][8 * v + 4]) * inv, __uint_as_float(o[g][8 * v + 5]) * inv);
+              w.w = pack_bf16(__uint_as_float(o[g][8 * v + 6]) * inv, __uint_as_float(o[g][8 * v + 7]) * inv);
+              d4[v] = w;
+            }
+          }
         }
       }
     }
   }
+  if (threadIdx.x == 128) { A2_TRACE(13, 0) }  // epilogue stores issued
   if (p.dbg && lane == 0) {
     const unsigned long long tot = clock64() - t_start;
     if (warp == 1 && leader) { atomicAdd(p.dbg + 0, w_a); atomicAdd(p.dbg + 2, w_c); atomicAdd(p.dbg + 3, tot); }
@@ -338,35 +388,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
 }
 
 template <int DP, int NV_>
-static int launch2_nv(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const AttnParams& p,
-                      cudaStream_t st) {
+static int launch2_nv(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o,
+                      const AttnParams& p, cudaStream_t st) {
   using Cfg = Attn2Cfg<DP, NV_>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn2_kernel<DP, NV_>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr = true;
   }
-  launch_pdl(attn2_kernel<DP, NV_>, dim3(2 * p.n_tiles), dim3(A2_THREADS), Cfg::SMEM, st, q, k, v, p);
+  launch_pdl(attn2_kernel<DP, NV_>, dim3(2 * p.n_tiles), dim3(A2_THREADS), Cfg::SMEM, st, q, k, v, o, p);
   count_launch();
   return check_launch("attention_2cta");
 }
 
 template <int DP>
-static int launch2_dp(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const AttnParams& p,
-                      cudaStream_t st) {
+static int launch2_dp(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o,
+                      const AttnParams& p, cudaStream_t st) {
   // V ring depth (PS_ATTN2_NV=3|4): A/B switch for tools/attn_pair_check.py
   static const int nv = getenv("PS_ATTN2_NV") ? atoi(getenv("PS_ATTN2_NV")) : 4;
-  return nv == 3 ? launch2_nv<DP, 3>(q, k, v, p, st) : launch2_nv<DP, 4>(q, k, v, p, st);
+  return nv == 3 ? launch2_nv<DP, 3>(q, k, v, o, p, st) : launch2_nv<DP, 4>(q, k, v, o, p, st);
 }
 
-int attention2_launch(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& vt, const AttnParams& p, int dp,
+int attention2_launch(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& vt, const CUtensorMap& o,
+                      const AttnParams& p, int dp,
                       cudaStream_t st) {
   switch (dp) {
-    case 64: return launch2_dp<64>(q, k, vt, p, st);
-    case 128: return launch2_dp<128>(q, k, vt, p, st);
-    case 192: return launch2_dp<192>(q, k, vt, p, st);
-    case 256: return launch2_dp<256>(q, k, vt, p, st);
-    case 320: return launch2_dp<320>(q, k, vt, p, st);
+    case 64: return launch2_dp<64>(q, k, vt, o, p, st);
+    case 128: return launch2_dp<128>(q, k, vt, o, p, st);
+    case 192: return launch2_dp<192>(q, k, vt, o, p, st);
+    case 256: return launch2_dp<256>(q, k, vt, o, p, st);
+    case 320: return launch2_dp<320>(q, k, vt, o, p, st);
     default: return set_error(PS_ERR_INPUT, "attention: unsupported head dim %d", dp);
   }
 }

@@ -209,10 +209,11 @@ int ps_attention_pairs(void* stream, const void* qk, const void* vt, int ldv, in
   if (Dp % 64 || Dp < 64 || Dp > 320) return set_error(PS_ERR_INPUT, "attention: Dp %d unsupported", Dp);
   if (D < 1 || D > Dp) return set_error(PS_ERR_INPUT, "attention: bad D");
   if (n_pairs < 1) return PS_OK;
-  CUtensorMap tq, tk, tv;
+  CUtensorMap tq, tk, tv, to;
   int rc = make_tmap_2d(&tq, qk, T, Dp, 2 * (uint64_t)Dp, 128);
   if (!rc) rc = make_tmap_2d(&tk, (const __nv_bfloat16*)qk + Dp, T, Dp, 2 * (uint64_t)Dp, 64);
   if (!rc) rc = make_tmap_2d(&tv, vt, Dp, T, ldv, attention2_v_rows(Dp));
+  if (!rc) rc = make_tmap_2d(&to, out, T, Dp, Dp, 128);  // O tiles leave through TMA stores
   if (rc) return rc;
   AttnParams p{};
   p.T_total = T;
@@ -221,12 +222,14 @@ int ps_attention_pairs(void* stream, const void* qk, const void* vt, int ldv, in
   p.tile_q0 = pair_q0;
   p.tile_img = pair_img;
   p.n_dev = n_dev;
+  static const int epi_tma = getenv("PS_ATTN_EPI_TMA") ? atoi(getenv("PS_ATTN_EPI_TMA")) : 1;
+  p.epi_tma = epi_tma;
   p.img_tok0 = img_tok0;
   p.scale_log2 = 1.4426950408889634f / sqrtf((float)D);
   p.out = (__nv_bfloat16*)out;
   p.dbg = g_attn_dbg;
   p.trace = g_attn_trace;
-  return attention2_launch(tq, tk, tv, p, Dp, (cudaStream_t)stream);
+  return attention2_launch(tq, tk, tv, to, p, Dp, (cudaStream_t)stream);
 }
 
 // Profiling only: device counters [8] that later attention launches accumulate

@@ -109,14 +109,15 @@ struct AttnParams {
   // profiling (ps_attention_trace): clock64 stamps of the first CTA (pair leader), [event][block]
   long long* trace;
   const int* n_dev;      // optional DEVICE tile count (n_tiles is then an upper bound)
+  int epi_tma;           // pair kernel: O tiles staged in smem and TMA-stored (else row stores)
 };
 int attention_launch(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& vt, const AttnParams& p,
                      int dp, cudaStream_t st);
 int attention_combine_launch(const float* part_o, const float* part_ml, const int* q0s, const int* slot0,
                              const int* nsplit, const int* img_of, const int* img_tok0, int n, int Dp,
                              __nv_bfloat16* out, cudaStream_t st);
-int attention2_launch(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& vt, const AttnParams& p,
-                      int dp, cudaStream_t st);
+int attention2_launch(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& vt, const CUtensorMap& o,
+                      const AttnParams& p, int dp, cudaStream_t st);
 int attention2_v_rows(int dp);
 
 }  // namespace ps

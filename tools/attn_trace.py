@@ -15,12 +15,12 @@ x = b.data.to(torch.bfloat16)
 at = w[0][2][1]
 for _ in range(2):
     ps.patched_self_attention(b, x, at)
-tr = torch.zeros(11 * 64, dtype=torch.int64, device="cuda")
+tr = torch.zeros(14 * 64, dtype=torch.int64, device="cuda")
 _lib.load().ps_attention_trace(tr.data_ptr())
 ps.patched_self_attention(b, x, at)
 torch.cuda.synchronize()
 _lib.load().ps_attention_trace(None)
-t = tr.view(11, 64).cpu().numpy().astype(np.int64)
+t = tr.view(14, 64).cpu().numpy().astype(np.int64)
 names = ["S_iss0", "S_iss1", "PV_iss0", "PV_iss1", "sm_Srdy", "sm_Sld", "sm_exp", "sm_Pfree", "sm_Pst"]
 t0 = t[4, 8]
 print("block " + " ".join(f"{n:>8s}" for n in names) + "   (cycles relative to softmax S-ready of block 8)")
@@ -38,3 +38,6 @@ d = t[4, 9:41] - t[8, 8:40]
 print(f"{'P(j) stored->S(j+1) rdy':22s} mean {d.mean():7.0f}")
 print("S issuer k_full wait per block: mean %.0f   PV issuer v_full wait per block: mean %.0f" %
       (t[9, 8:40].mean(), t[10, 8:40].mean()))
+print("prologue (entry -> first S MMA issued): %d cycles; epilogue (O ready -> stores issued): %d cycles"
+      % (t[0, 0] - t[11, 0], t[13, 0] - t[12, 0]))
+print("last traced block PV issued -> O ready: see PV_iss1; tile blocks traced: %d" % int((t[4] != 0).sum()))
