@@ -62,8 +62,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
   uint8_t* sK = sQ + Cfg::Q_BYTES;
   uint8_t* sV = sK + Cfg::NK * Cfg::K_SLOT;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sV + Cfg::NV * Cfg::V_SLOT);
-  uint64_t* q_full = bars;                    // leader, one per 64-column chunk of Q
-  uint64_t* k_full = bars + Cfg::KB;          // leader
+  uint64_t* q_full = bars;                    // leader
+  uint64_t* k_full = bars + 1;                // leader
   uint64_t* k_empty = k_full + Cfg::NK;       // both (multicast commit)
   uint64_t* v_full = k_empty + Cfg::NK;       // leader
   uint64_t* v_empty = v_full + Cfg::NV;       // both
@@ -88,7 +88,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
     tma_prefetch(&tmQ);
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
-    for (int kc = 0; kc < Cfg::KB; ++kc) mbar_init(&q_full[kc], 1);
+    mbar_init(q_full, 1);
     for (int s = 0; s < Cfg::NK; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
@@ -124,12 +124,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
   if (warp == 0) {
     // -------------------------------------------------- producer (both CTAs)
     if (lane == 0) {
-      // Q per 64-column chunk: the first S MMAs start when chunk 0 (and K chunk 0) landed
-      // instead of after all 80 KB
-      for (int kc = 0; kc < Cfg::KB; ++kc) {
-        if (leader) mbar_arrive_expect_tx(&q_full[kc], 2 * A2_BM * 128);
-        tma_load_2d_2sm(sQ + kc * A2_BM * 128, &tmQ, mapa_shared(&q_full[kc], 0), kc * 64, q0);
-      }
+      const uint32_t lq = mapa_shared(q_full, 0);
+      if (leader) mbar_arrive_expect_tx(q_full, 2 * Cfg::Q_BYTES);
+      for (int kc = 0; kc < Cfg::KB; ++kc) tma_load_2d_2sm(sQ + kc * A2_BM * 128, &tmQ, lq, kc * 64, q0);
       int ks = 0, vs = 0;
       uint32_t kph = 0, vph = 0;
       auto load_k = [&](int j) {
@@ -166,6 +163,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
     if (leader) {
       constexpr uint32_t idesc_s = idesc_bf16_f32(2 * A2_BM, A2_BN);
       constexpr uint32_t idesc_o = idesc_bf16_f32(2 * A2_BM, Cfg::PV_N);
+      mbar_wait(q_full, 0);
       if (warp == 1) {
         int ks = 0;
         uint32_t kph = 0;
@@ -175,7 +173,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
           if (lane == 0) { A2_TRACE(0, j) }
           long long kw = 0;
           for (int kc = 0; kc < Cfg::KB; ++kc) {
-            if (j == 0) mbar_wait(&q_full[kc], 0);
             const long long tk0 = p.trace ? clock64() : 0;
             twait(&k_full[ks], kph, w_c);
             if (p.trace) kw += clock64() - tk0;
