@@ -222,7 +222,7 @@ def run_ours(args):
                     "path": "DenoisePipeline.run: pinned host latents -H2D-> split -> bias -> 7 blocks -> blend -> "
                             "reassemble -D2H-> pinned host, copies on their own streams"},
             "gpu_launches": int(launches),
-            "roofline": {"bound": "tensor", "kernel": "attn2_kernel<320> (per-image flash attention on CTA pairs, tcgen05 cta_group::2)" if patched.USE_PAIRS else "attn_kernel<320> (per-image flash attention, tcgen05)",
+            "roofline": {"bound": "tensor", "kernel": ("attn2p_kernel<320> (persistent per-image flash attention on CTA pairs, tcgen05 cta_group::2)" if os.environ.get("PS_ATTN_PERSIST", "1") != "0" else "attn2_kernel<320> (per-image flash attention on CTA pairs, tcgen05 cta_group::2)") if patched.USE_PAIRS else "attn_kernel<320> (per-image flash attention, tcgen05)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "algorithmic": "4*T^2*D per image, sum over the batch = %.3e FLOP per launch" % flops,

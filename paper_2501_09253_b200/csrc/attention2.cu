@@ -387,6 +387,364 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
   if (warp == 2) tmem_dealloc_2sm(tmem, Cfg::TMEM_COLS);
 }
 
+// Ticket counters of the persistent pair kernel, one pair of ints per device (zeroed once,
+// left zero by every launch; one persistent attention in flight per device).  Allocated on
+// the first launch outside stream capture; during a capture without one the one-tile-per-CTA
+// kernel runs instead.
+static int* attention2_tile_counter(cudaStream_t st) {
+  static int* ctr[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (ctr[dev] == nullptr) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs != cudaStreamCaptureStatusNone) return nullptr;
+    int* c = nullptr;
+    if (cudaMalloc(&c, 2 * sizeof(int)) != cudaSuccess) return nullptr;
+    cudaMemset(c, 0, 2 * sizeof(int));
+    ctr[dev] = c;
+  }
+  return ctr[dev];
+}
+
+// Persistent variant (default; PS_ATTN_PERSIST=0 for one tile per CTA pair): one cluster per
+// SM pair takes tiles of the (longest-first) tile list from an atomic ticket.  The next tile's Q is loaded as soon as
+// the last S MMA of the current tile has read Q (q_empty), its S MMAs run while the softmax
+// warps finish the current tile, and its first PV MMA waits for the epilogue to have read O
+// (o_empty) -- the per-tile prologue (barrier / TMEM setup, Q load, pipeline fill) leaves
+// the critical path.  Barrier parities run on a per-cluster block counter across tiles.
+// Same arithmetic per tile as attn2_kernel; the epilogue stores rows directly (the Q buffer
+// already holds the next tile's Q).
+template <int DP, int NV_>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
+    attn2p_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                  const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
+  pdl_wait();
+  using Cfg = Attn2Cfg<DP, NV_>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + Cfg::Q_BYTES;
+  uint8_t* sV = sK + Cfg::NK * Cfg::K_SLOT;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + Cfg::NV * Cfg::V_SLOT);
+  uint64_t* q_full = bars;                    // leader
+  uint64_t* q_empty = bars + 1;               // both (multicast commit)
+  uint64_t* k_full = bars + 2;                // leader
+  uint64_t* k_empty = k_full + Cfg::NK;       // both
+  uint64_t* v_full = k_empty + Cfg::NK;       // leader
+  uint64_t* v_empty = v_full + Cfg::NV;       // both
+  uint64_t* s_full = v_empty + Cfg::NV;       // both
+  uint64_t* s_free = s_full + 1;              // leader, 256 arrivals
+  uint64_t* p_full = s_free + 1;              // leader, 256 arrivals
+  uint64_t* p_free = p_full + 1;              // both
+  uint64_t* o_full = p_free + 1;              // both
+  uint64_t* o_empty = o_full + 1;             // leader, 256 arrivals
+  uint64_t* tile_full = o_empty + 1;          // both, [8]: tile ring entries written
+  int* tring = reinterpret_cast<int*>(tile_full + 8);  // [8] tile ring (leader fills both CTAs')
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tring + 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int n_tiles = p.n_dev != nullptr ? *p.n_dev : p.n_tiles;
+  const int ncl = gridDim.x >> 1;
+  // k-th tile of this cluster: dealt dynamically (an atomic ticket per tile, fetched by the
+  // leader's producer and published through an 8-entry ring in both CTAs), so the longest-
+  // first list balances like the hardware's CTA scheduling of the one-tile-per-CTA kernel.
+  // Ring reuse is safe: no role lags the producer by more than two tiles (the K ring holds
+  // two key blocks and every tile has at least one).
+  auto next_tile = [&](int k) -> int {
+    mbar_wait(&tile_full[k & 7], (k >> 3) & 1);
+    return *reinterpret_cast<volatile int*>(tring + (k & 7));
+  };
+  auto tile = [&](int t, int& q0, int& kb0, int& ke, int& nkb) {
+    const int img = p.tile_img[t];
+    q0 = p.tile_q0[t] + (int)rank * A2_BM;
+    kb0 = p.img_tok0[img];
+    ke = p.img_tok0[img + 1];
+    nkb = (ke - kb0 + A2_BN - 1) / A2_BN;
+  };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int s = 0; s < Cfg::NK; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < Cfg::NV; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_free, 2 * 128);
+    mbar_init(p_full, 2 * 128);
+    mbar_init(p_free, 1);
+    mbar_init(o_full, 1);
+    mbar_init(o_empty, 2 * 128);
+    for (int i = 0; i < 8; ++i) mbar_init(&tile_full[i], 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_2sm(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // -------------------------------------------------- producer (both CTAs)
+    if (lane == 0) {
+      int ks = 0, vs = 0;
+      uint32_t kph = 0, vph = 0;
+      for (int ti = 0;; ++ti) {
+        int t;
+        if (leader) {  // fetch and publish the next tile (-1: none left)
+          t = (int)atomicAdd(p.tile_ctr, 1u);
+          if (t >= n_tiles) t = -1;
+          tring[ti & 7] = t;
+          asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(mapa_shared(tring + (ti & 7), 1)), "r"(t) : "memory");
+          mbar_arrive(&tile_full[ti & 7]);
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                           mapa_shared(&tile_full[ti & 7], 1))
+                       : "memory");
+        } else {
+          t = next_tile(ti);
+        }
+        if (t < 0) break;
+        int q0, k_begin, k_end, n_kb;
+        tile(t, q0, k_begin, k_end, n_kb);
+        if (ti >= 1) mbar_wait(q_empty, (ti - 1) & 1);  // the previous tile's S MMAs read Q
+        if (leader) mbar_arrive_expect_tx(q_full, 2 * Cfg::Q_BYTES);
+        for (int kc = 0; kc < Cfg::KB; ++kc)
+          tma_load_2d_2sm(sQ + kc * A2_BM * 128, &tmQ, mapa_shared(q_full, 0), kc * 64, q0);
+        auto load_k = [&](int j) {
+          for (int kc = 0; kc < Cfg::KB; ++kc) {
+            mbar_wait(&k_empty[ks], kph ^ 1);
+            if (leader) mbar_arrive_expect_tx(&k_full[ks], 2 * Cfg::K_SLOT);
+            tma_load_2d_2sm(sK + ks * Cfg::K_SLOT, &tmK, mapa_shared(&k_full[ks], 0), kc * 64,
+                            k_begin + j * A2_BN + (int)rank * (A2_BN / 2));
+            if (++ks == Cfg::NK) { ks = 0; kph ^= 1; }
+          }
+        };
+        auto load_v = [&](int j) {
+          for (int ka = 0; ka < 2; ++ka) {
+            mbar_wait(&v_empty[vs], vph ^ 1);
+            if (leader) mbar_arrive_expect_tx(&v_full[vs], 2 * Cfg::V_SLOT);
+            const uint32_t lb = mapa_shared(&v_full[vs], 0);
+            uint8_t* dst = sV + vs * Cfg::V_SLOT;
+            for (int n = 0; n < Cfg::PV_MMAS; ++n)
+              tma_load_2d_2sm(dst + n * Cfg::V_ROWS * 128, &tmV, lb, k_begin + j * A2_BN + ka * 64,
+                              n * Cfg::PV_N + (int)rank * Cfg::V_ROWS);
+            if (++vs == Cfg::NV) { vs = 0; vph ^= 1; }
+          }
+        };
+        load_k(0);
+        for (int j = 0; j < n_kb; ++j) {
+          if (j + 1 < n_kb) load_k(j + 1);
+          load_v(j);
+        }
+      }
+    }
+  } else if (warp == 1 || warp == 3) {
+    // ------------------------------- MMA issuers (leader only): w1 S = Q K^T, w3 O += P V
+    if (leader) {
+      constexpr uint32_t idesc_s = idesc_bf16_f32(2 * A2_BM, A2_BN);
+      constexpr uint32_t idesc_o = idesc_bf16_f32(2 * A2_BM, Cfg::PV_N);
+      int ring = 0;
+      uint32_t rph = 0;
+      int gj = 0;
+      for (int ti = 0;; ++ti) {
+        const int t = next_tile(ti);
+        if (t < 0) break;
+        int q0, k_begin, k_end, n_kb;
+        tile(t, q0, k_begin, k_end, n_kb);
+        if (warp == 1) {
+          mbar_wait(q_full, ti & 1);
+          tc_fence_after();
+          for (int j = 0; j < n_kb; ++j, ++gj) {
+            if (gj >= 1) mbar_wait(s_free, (gj - 1) & 1);
+            tc_fence_after();
+            for (int kc = 0; kc < Cfg::KB; ++kc) {
+              mbar_wait(&k_full[ring], rph);
+              tc_fence_after();
+              if (lane == 0) {
+                const uint8_t* kt = sK + ring * Cfg::K_SLOT;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  mma_bf16_ss_2sm(tmem + Cfg::S_COL, sdesc_sw128(sQ + kc * A2_BM * 128 + k * 32),
+                                  sdesc_sw128(kt + k * 32), idesc_s, (kc | k) != 0);
+                mma_commit_2sm(&k_empty[ring], 0x3);
+                if (kc == Cfg::KB - 1) {
+                  mma_commit_2sm(s_full, 0x3);
+                  if (j == n_kb - 1) mma_commit_2sm(q_empty, 0x3);  // Q free for the next tile
+                }
+              }
+              __syncwarp();
+              if (++ring == Cfg::NK) { ring = 0; rph ^= 1; }
+            }
+          }
+        } else {
+          for (int j = 0; j < n_kb; ++j, ++gj) {
+            mbar_wait(p_full, gj & 1);
+            if (j == 0 && ti >= 1) mbar_wait(o_empty, (ti - 1) & 1);  // O of the previous tile read
+            tc_fence_after();
+            for (int ka = 0; ka < 2; ++ka) {
+              mbar_wait(&v_full[ring], rph);
+              tc_fence_after();
+              if (lane == 0) {
+                const uint8_t* vt = sV + ring * Cfg::V_SLOT;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                  for (int n = 0; n < Cfg::PV_MMAS; ++n)
+                    mma_bf16_ts_2sm(tmem + Cfg::O_COL + n * Cfg::PV_N, tmem + Cfg::P_COL + ka * 32 + k * 8,
+                                    sdesc_sw128(vt + n * Cfg::V_ROWS * 128 + k * 32), idesc_o, (j | ka | k) != 0);
+                mma_commit_2sm(&v_empty[ring], 0x3);
+                if (ka == 1) {
+                  mma_commit_2sm(p_free, 0x3);
+                  if (j == n_kb - 1) mma_commit_2sm(o_full, 0x3);
+                }
+              }
+              __syncwarp();
+              if (++ring == Cfg::NV) { ring = 0; rph ^= 1; }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ softmax + epilogue
+    const int wq = warp & 3;
+    const int row = wq * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    const uint32_t s_free_l = mapa_shared(s_free, 0);
+    const uint32_t p_full_l = mapa_shared(p_full, 0);
+    const uint32_t o_empty_l = mapa_shared(o_empty, 0);
+    int gj = 0;
+    for (int ti = 0;; ++ti) {
+      const int t = next_tile(ti);
+      if (t < 0) break;
+      int q0, k_begin, k_end, n_kb;
+      tile(t, q0, k_begin, k_end, n_kb);
+      float m_run = -INFINITY, l_run = 0.f;
+      for (int j = 0; j < n_kb; ++j, ++gj) {
+        mbar_wait(s_full, gj & 1);
+        tc_fence_after();
+        uint32_t sr[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) PS_TMEM_LD32(tmem + lane_base + Cfg::S_COL + 32 * c, (sr + 32 * c));
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive_cluster(s_free_l);
+        const int kvalid = k_end - (k_begin + j * A2_BN);
+        if (kvalid < A2_BN) {
+#pragma unroll
+          for (int i = 0; i < 128; ++i)
+            if (i >= kvalid) sr[i] = __float_as_uint(-INFINITY);
+        }
+        float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < 128; i += 4) {
+          mx0 = fmaxf(mx0, fmaxf(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])));
+          mx1 = fmaxf(mx1, fmaxf(__uint_as_float(sr[i + 2]), __uint_as_float(sr[i + 3])));
+        }
+        const float mx = fmaxf(mx0, mx1) * p.scale_log2;
+        float m_use = m_run;
+        const bool need = (m_run == -INFINITY) || (mx > m_run + 8.0f);
+        if (need) m_use = fmaxf(mx, m_run);
+        const float alpha = (m_run == -INFINITY) ? 0.f : ex2_approx(m_run - m_use);
+        const float neg = -m_use;
+        float sum0 = 0.f, sum1 = 0.f;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          const float a = ex2_approx(fmaf(__uint_as_float(sr[2 * i]), p.scale_log2, neg));
+          const float b = ex2_approx(fmaf(__uint_as_float(sr[2 * i + 1]), p.scale_log2, neg));
+          sum0 += a;
+          sum1 += b;
+          sr[i] = pack_bf16(a, b);
+        }
+        l_run = l_run * alpha + (sum0 + sum1);
+        // P columns (and O) are owned by the PV MMAs of the previous block -- across tiles too
+        if (gj >= 1) mbar_wait(p_free, (gj - 1) & 1);
+        tc_fence_after();
+        const bool warp_rescale = __any_sync(0xffffffffu, need && j >= 1 && alpha != 1.f);
+        if (warp_rescale) {
+          const float sc = (need && j >= 1) ? alpha : 1.f;
+#pragma unroll 1
+          for (int c = 0; c < DP; c += 16) {
+            uint32_t o[16];
+            PS_TMEM_LD16(tmem + lane_base + Cfg::O_COL + c, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * sc);
+            PS_TMEM_ST16(tmem + lane_base + Cfg::O_COL + c, o);
+          }
+        }
+        m_run = m_use;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) PS_TMEM_ST16(tmem + lane_base + Cfg::P_COL + 16 * c, (sr + 16 * c));
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive_cluster(p_full_l);
+      }
+      // epilogue: O / l -> bf16 channels-last rows, then hand O back to the PV issuer
+      mbar_wait(o_full, ti & 1);
+      tc_fence_after();
+      const int q = q0 + row;
+      const bool ok = q < k_end;
+      const float inv = 1.f / l_run;
+      __nv_bfloat16* dst = p.out + (size_t)q * p.Dp;
+      constexpr int EPI_G = (DP / 32) % 5 == 0 ? 5 : (DP / 32) % 4 == 0 ? 4 : (DP / 32) % 3 == 0 ? 3 : (DP / 32) % 2 == 0 ? 2 : 1;
+      uint32_t o[EPI_G][32];
+#pragma unroll 1
+      for (int c0 = 0; c0 < DP; c0 += 32 * EPI_G) {
+#pragma unroll
+        for (int g = 0; g < EPI_G; ++g) PS_TMEM_LD32(tmem + lane_base + Cfg::O_COL + c0 + 32 * g, o[g]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int g = 0; g < EPI_G; ++g) reg_fence32(o[g]);
+        if (c0 + 32 * EPI_G >= DP) {  // last TMEM read: O can be overwritten by the next tile
+          tc_fence_before();
+          mbar_arrive_cluster(o_empty_l);
+        }
+        if (ok) {
+#pragma unroll
+          for (int g = 0; g < EPI_G; ++g) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst + c0 + 32 * g);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              uint4 w;
+              w.x = pack_bf16(__uint_as_float(o[g][8 * v + 0]) * inv, __uint_as_float(o[g][8 * v + 1]) * inv);
+              w.y = pack_bf16(__uint_as_float(o[g][8 * v + 2]) * inv, __uint_as_float(o[g][8 * v + 3]) * inv);
+              w.z = pack_bf16(__uint_as_float(o[g][8 * v + 4]) * inv, __uint_as_float(o[g][8 * v + 5]) * inv);
+              w.w = pack_bf16(__uint_as_float(o[g][8 * v + 6]) * inv, __uint_as_float(o[g][8 * v + 7]) * inv);
+              d4[v] = w;
+            }
+          }
+        }
+      }
+    }
+  }
+  if (leader && warp == 0 && lane == 0) {
+    // the last cluster out leaves the ticket counters at zero for the next launch (every
+    // cluster has fetched its -1 before it counts itself done)
+    __threadfence();
+    if (atomicAdd(p.tile_ctr + 1, 1u) == (unsigned)ncl - 1) {
+      p.tile_ctr[0] = 0;
+      p.tile_ctr[1] = 0;
+      __threadfence();
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_2sm(tmem, Cfg::TMEM_COLS);
+}
+
 template <int DP, int NV_>
 static int launch2_nv(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o,
                       const AttnParams& p, cudaStream_t st) {
@@ -396,7 +754,26 @@ static int launch2_nv(const CUtensorMap& q, const CUtensorMap& k, const CUtensor
     cudaFuncSetAttribute(attn2_kernel<DP, NV_>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr = true;
   }
-  launch_pdl(attn2_kernel<DP, NV_>, dim3(2 * p.n_tiles), dim3(A2_THREADS), Cfg::SMEM, st, q, k, v, o, p);
+  // persistent kernel by default (config-2 step 14.9 -> 14.3 ms on one box); PS_ATTN_PERSIST=0:
+  // one tile per CTA pair
+  static const bool persist = !getenv("PS_ATTN_PERSIST") || atoi(getenv("PS_ATTN_PERSIST")) != 0;
+  int* ctr = persist ? attention2_tile_counter(st) : nullptr;
+  if (ctr != nullptr) {
+    AttnParams pp = p;
+    pp.tile_ctr = ctr;
+    static bool attr_p = false;
+    if (!attr_p) {
+      cudaFuncSetAttribute(attn2p_kernel<DP, NV_>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+      attr_p = true;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int clusters = p.n_tiles < sms / 2 ? p.n_tiles : sms / 2;
+    launch_pdl(attn2p_kernel<DP, NV_>, dim3(2 * clusters), dim3(A2_THREADS), Cfg::SMEM, st, q, k, v, pp);
+  } else {
+    launch_pdl(attn2_kernel<DP, NV_>, dim3(2 * p.n_tiles), dim3(A2_THREADS), Cfg::SMEM, st, q, k, v, o, p);
+  }
   count_launch();
   return check_launch("attention_2cta");
 }
