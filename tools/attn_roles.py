@@ -1,5 +1,6 @@
 """Per-role barrier-wait fractions of the attention kernel on the config-2 batch."""
 import os, sys
+os.environ.setdefault("PS_ATTN_PERSIST", "0")  # the trace / role counters live in the one-tile kernel
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import bench

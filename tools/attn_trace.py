@@ -1,5 +1,6 @@
 """Per-key-block timeline of the pair attention kernel's first CTA (ps_attention_trace)."""
 import os, sys
+os.environ.setdefault("PS_ATTN_PERSIST", "0")  # the trace / role counters live in the one-tile kernel
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
