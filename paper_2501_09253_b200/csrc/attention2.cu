@@ -14,6 +14,9 @@
 // what limited the single-CTA kernel (shared-memory bandwidth).
 #include <stdlib.h>
 
+#include <mutex>
+#include <unordered_map>
+
 #include "common.cuh"
 #include "ps_internal.h"
 
@@ -387,25 +390,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
   if (warp == 2) tmem_dealloc_2sm(tmem, Cfg::TMEM_COLS);
 }
 
-// Ticket counters of the persistent pair kernel, one pair of ints per device (zeroed once,
-// left zero by every launch; one persistent attention in flight per device).  Allocated on
-// the first launch outside stream capture; during a capture without one the one-tile-per-CTA
-// kernel runs instead.
+// Ticket counters of the persistent pair kernel: a pool of 64 pairs of ints per device
+// (zeroed once, left zero by every launch), one pair per stream that launches it -- two
+// persistent attentions in flight on different streams never share a counter (a stream
+// captured into a graph keeps its pair for the graph's replays).  The pool is allocated on
+// the first launch outside stream capture; a capture before that runs the one-tile kernel.
 static int* attention2_tile_counter(cudaStream_t st) {
-  static int* ctr[64] = {};
+  constexpr int kSlots = 64;
+  static std::mutex mu;
+  static int* pool[64] = {};
+  static std::unordered_map<cudaStream_t, int> slot_of[64];
+  static int next_slot[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return nullptr;
-  if (ctr[dev] == nullptr) {
+  std::lock_guard<std::mutex> lock(mu);
+  if (pool[dev] == nullptr) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(st, &cs);
     if (cs != cudaStreamCaptureStatusNone) return nullptr;
     int* c = nullptr;
-    if (cudaMalloc(&c, 2 * sizeof(int)) != cudaSuccess) return nullptr;
-    cudaMemset(c, 0, 2 * sizeof(int));
-    ctr[dev] = c;
+    if (cudaMalloc(&c, kSlots * 2 * sizeof(int)) != cudaSuccess) return nullptr;
+    cudaMemset(c, 0, kSlots * 2 * sizeof(int));
+    pool[dev] = c;
   }
-  return ctr[dev];
+  auto it = slot_of[dev].find(st);
+  int slot;
+  if (it != slot_of[dev].end()) {
+    slot = it->second;
+  } else {
+    if (next_slot[dev] >= kSlots) return nullptr;  // more streams than slots: one-tile kernel
+    slot = next_slot[dev]++;
+    slot_of[dev][st] = slot;
+  }
+  return pool[dev] + 2 * slot;
 }
 
 // Persistent variant (default; PS_ATTN_PERSIST=0 for one tile per CTA pair): one cluster per
