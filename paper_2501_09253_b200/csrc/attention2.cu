@@ -732,15 +732,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
         if (ok) {
 #pragma unroll
           for (int g = 0; g < EPI_G; ++g) {
-            uint4* d4 = reinterpret_cast<uint4*>(dst + c0 + 32 * g);
+            // 32-byte stores: one full sector per lane and half the store instructions
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              uint4 w;
-              w.x = pack_bf16(__uint_as_float(o[g][8 * v + 0]) * inv, __uint_as_float(o[g][8 * v + 1]) * inv);
-              w.y = pack_bf16(__uint_as_float(o[g][8 * v + 2]) * inv, __uint_as_float(o[g][8 * v + 3]) * inv);
-              w.z = pack_bf16(__uint_as_float(o[g][8 * v + 4]) * inv, __uint_as_float(o[g][8 * v + 5]) * inv);
-              w.w = pack_bf16(__uint_as_float(o[g][8 * v + 6]) * inv, __uint_as_float(o[g][8 * v + 7]) * inv);
-              d4[v] = w;
+            for (int v = 0; v < 2; ++v) {
+              uint32_t w[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                w[e] = pack_bf16(__uint_as_float(o[g][16 * v + 2 * e]) * inv,
+                                 __uint_as_float(o[g][16 * v + 2 * e + 1]) * inv);
+              st_global_v8(dst + c0 + 32 * g + 16 * v, w);
             }
           }
         }

@@ -233,6 +233,12 @@ PS_DEV uint64_t sdesc_sw128(const void* smem_ptr) {
 // makes them valid (the compiler sees no data dependence on the wait itself).
 // PDL: wait until the previous grid on the stream has completed and its writes are visible
 // (a no-op when the kernel was launched without the programmatic attribute)
+// 32-byte global store (STG.256, sm_100): p 32-byte aligned
+PS_DEV void st_global_v8(void* p, const uint32_t (&w)[8]) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+               "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+               : "memory");
+}
 PS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 PS_DEV void reg_fence32(uint32_t (&r)[32]) {
 #pragma unroll
