@@ -366,8 +366,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
             w0.z = pack_bf16(o[4], o[5]); w0.w = pack_bf16(o[6], o[7]);
             w1.x = pack_bf16(o[8], o[9]); w1.y = pack_bf16(o[10], o[11]);
             w1.z = pack_bf16(o[12], o[13]); w1.w = pack_bf16(o[14], o[15]);
-            reinterpret_cast<uint4*>(p.out + off)[0] = w0;
-            reinterpret_cast<uint4*>(p.out + off)[1] = w1;
+            const uint32_t w8[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            st_global_v8(p.out + off, w8);  // 32-byte aligned: pix_v is a multiple of 16
           }
           __syncwarp();
         }

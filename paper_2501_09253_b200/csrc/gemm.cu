@@ -80,8 +80,13 @@ __device__ __forceinline__ void store16_cl(__nv_bfloat16* dst, const float* v) {
   w1.y = pack_bf16(v[10], v[11]);
   w1.z = pack_bf16(v[12], v[13]);
   w1.w = pack_bf16(v[14], v[15]);
-  reinterpret_cast<uint4*>(dst)[0] = w0;
-  reinterpret_cast<uint4*>(dst)[1] = w1;
+  if ((reinterpret_cast<uintptr_t>(dst) & 31) == 0) {  // one 32-byte store (STG.256)
+    const uint32_t w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+    st_global_v8(dst, w);
+  } else {
+    reinterpret_cast<uint4*>(dst)[0] = w0;
+    reinterpret_cast<uint4*>(dst)[1] = w1;
+  }
 }
 
 template <int BN, bool PAIR>
