@@ -303,3 +303,35 @@ def test_fused_feed_forward_bit_identical_to_two_gemms(C, H, lat, compact, monke
         assert torch.equal(outs[0][act], outs[1][act])
     else:
         assert torch.equal(outs[0], outs[1])
+
+
+def test_persistent_attention_concurrent_streams_and_graph():
+    """The persistent pair attention deals tiles from per-stream ticket counters: launches on
+    two streams at once, and replays of a graph captured on a third stream, all give the
+    single-stream result bit for bit (a shared counter would drop or repeat tiles)."""
+    import paper_2501_09253_b200 as ps
+    torch.manual_seed(5)
+    cfg = ps.ModelConfig(arch="dit_like", channels=128, hidden=256, n_blocks=1, groups=8, seed=6)
+    at = ps.init_weights(cfg)[0][1][1]
+    b = ps.split([(f"r{i}", torch.randn(128, d, d)) for i, d in enumerate((64, 32, 96, 48, 64))], patch_size=16)
+    x = torch.randn(b.n_patches, 128, 16, 16, device="cuda").to(torch.bfloat16)
+    want = ps.patched_self_attention(b, x, at).clone()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    s1.wait_stream(torch.cuda.current_stream())
+    s2.wait_stream(torch.cuda.current_stream())
+    outs = []
+    for _ in range(4):
+        with torch.cuda.stream(s1):
+            outs.append(ps.patched_self_attention(b, x, at))
+        with torch.cuda.stream(s2):
+            outs.append(ps.patched_self_attention(b, x, at))
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o, want)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        got = ps.patched_self_attention(b, x, at)
+    for _ in range(3):
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(got, want)
