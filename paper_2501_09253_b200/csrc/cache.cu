@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(LEAVES_PER_CTA) mse_leaf_kernel(
     const __nv_bfloat16* __restrict__ x, int64_t n, const int32_t* __restrict__ slots,
     const __nv_bfloat16* __restrict__ snap, const uint8_t* __restrict__ exists, const int32_t* __restrict__ streak,
     int max_streak, const int32_t* __restrict__ leaves, int L, int stride_nodes, double* __restrict__ scratch) {
+  pdl_wait();
   extern __shared__ __align__(16) __nv_bfloat16 stage[];
   const int p = blockIdx.x;
   const int slot = slots[p];
@@ -122,6 +123,7 @@ __global__ void __launch_bounds__(256) mse_combine_kernel(
     const int32_t* __restrict__ streak, int max_streak, double sigma, int L, const int32_t* __restrict__ nodes,
     int I, const int32_t* __restrict__ level_off, int H, int stride_nodes, double* __restrict__ scratch,
     uint8_t* __restrict__ mask, int64_t* __restrict__ counters, int smem_nodes) {
+  pdl_wait();
   const int p = blockIdx.x;
   const int slot = slots[p];
   const bool live = entry_live(slot, exists, streak, max_streak);
@@ -288,6 +290,7 @@ __device__ __forceinline__ void zero_range(__nv_bfloat16* dst, int64_t n, bool v
 
 template <int OP>
 __global__ void __launch_bounds__(256) patch_op_kernel(PatchOpArgs a) {
+  pdl_wait();
   if (a.n_dev != nullptr && (int)blockIdx.x >= *a.n_dev) return;
   const int p = a.plist ? a.plist[blockIdx.x] : (int)blockIdx.x;
   const bool m = a.mask[p] != 0;
@@ -363,7 +366,7 @@ static int launch_op(cudaStream_t st, int P, int64_t n, const PatchOpArgs& a, co
   int chunks = (int)((vecs + 255) / 256);
   if (chunks > 16) chunks = 16;
   if (chunks < 1) chunks = 1;
-  patch_op_kernel<OP><<<dim3(P, chunks), 256, 0, st>>>(a);
+  launch_pdl(patch_op_kernel<OP>, dim3(P, chunks), dim3(256), 0, st, a);
   count_launch();
   return check_launch(name);
 }
@@ -412,6 +415,7 @@ __global__ void __launch_bounds__(1024) compact_lists_kernel(
     int32_t* __restrict__ live_patches,
     int32_t* __restrict__ aq_act, int32_t* __restrict__ ai_act, int32_t* __restrict__ aq_live,
     int32_t* __restrict__ ai_live, int32_t* __restrict__ counts) {
+  pdl_wait();
   __shared__ int warp_tot[32];
   __shared__ int total;
   for (int r = threadIdx.x; r < R; r += blockDim.x) live[r] = 0;
@@ -478,9 +482,9 @@ int ps_cache_predict(void* stream, const void* x, int P, int64_t n, const int32_
                          2 * (LEAVES_PER_CTA * 128 + 16) * 2);
     attr = true;
   }
-  mse_leaf_kernel<<<dim3(P, (n_leaves + LEAVES_PER_CTA - 1) / LEAVES_PER_CTA), LEAVES_PER_CTA, smem, st>>>(
-      (const __nv_bfloat16*)x, n, slots, (const __nv_bfloat16*)snap_in, exists, streak, max_streak, leaves, n_leaves,
-      stride, scratch);
+  launch_pdl(mse_leaf_kernel, dim3(P, (n_leaves + LEAVES_PER_CTA - 1) / LEAVES_PER_CTA), dim3(LEAVES_PER_CTA),
+             (size_t)smem, st, (const __nv_bfloat16*)x, n, slots, (const __nv_bfloat16*)snap_in, exists, streak,
+             max_streak, leaves, n_leaves, stride, scratch);
   count_launch();
   int rc = check_launch("mse_leaf");
   if (rc) return rc;
@@ -496,8 +500,8 @@ int ps_cache_predict(void* stream, const void* x, int P, int64_t n, const int32_
     cudaFuncSetAttribute(mse_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_c = true;
   }
-  mse_combine_kernel<<<P, 256, smem_c, st>>>(n, slots, exists, streak, max_streak, sigma, n_leaves, nodes, n_internal,
-                                        level_off, n_levels, stride, scratch, mask, counters, smem_c / 8);
+  launch_pdl(mse_combine_kernel, dim3(P), dim3(256), (size_t)smem_c, st, n, slots, exists, streak, max_streak, sigma,
+             n_leaves, nodes, n_internal, level_off, n_levels, stride, scratch, mask, counters, smem_c / 8);
   count_launch();
   return check_launch("mse_combine");
 }
@@ -507,10 +511,9 @@ int ps_compact_lists(void* stream, const uint8_t* mask, int P, const int32_t* re
                      int32_t* rows_live, int32_t* live_patches, int32_t* attn_q0_act, int32_t* attn_img_act,
                      int32_t* attn_q0_live, int32_t* attn_img_live, int32_t* counts) {
   if (P < 0 || R < 1 || tpp < 1 || qpp < 1) return set_error(PS_ERR_INPUT, "compact_lists: bad geometry");
-  ps::compact_lists_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(mask, P, request_index, R, order, tpp, qpp, tq, hw,
-                                                                live_scratch, rows_act, rows_live, live_patches,
-                                                                attn_q0_act,
-                                                                attn_img_act, attn_q0_live, attn_img_live, counts);
+  launch_pdl(ps::compact_lists_kernel, dim3(1), dim3(1024), 0, (cudaStream_t)stream, mask, P, request_index, R, order,
+             tpp, qpp, tq, hw, live_scratch, rows_act, rows_live, live_patches, attn_q0_act, attn_img_act,
+             attn_q0_live, attn_img_live, counts);
   count_launch();
   return check_launch("compact_lists");
 }
