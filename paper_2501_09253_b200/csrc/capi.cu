@@ -570,6 +570,8 @@ int ps_feed_forward(void* stream, const void* x, int M, int Cp, const void* w1, 
   p.dbg = g_ff_dbg;
   static const int ff_ts = getenv("PS_FF_TS") ? atoi(getenv("PS_FF_TS")) : 1;  // GELU(H) through TMEM (TS MMA) vs shared memory
   p.ts = ff_ts;
+  static const int ff_tail = getenv("PS_FF_TAIL_SPLIT") ? atoi(getenv("PS_FF_TAIL_SPLIT")) : 1;
+  p.tail_split = ff_tail;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -97,6 +97,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
   const int num_m = p.m_map ? (p.m_count_dev ? *p.m_count_dev : p.m_count) : (p.M + FF_BM - 1) / FF_BM;
   const int n_units = (num_m + 1) / 2;
   const int unit0 = blockIdx.x >> 1, unit_step = gridDim.x >> 1;
+  // tail split (p.tail_split): the units of the last, partial wave become two work items
+  // each, one per half of the output channels (each recomputes H; MMA2 and the epilogue do
+  // half the columns) -- a 0.27 wave of full units becomes 0.54 wave of ~0.75-cost items
+  const int tail = (p.tail_split && 2 * (n_units % unit_step) <= unit_step) ? n_units % unit_step : 0;
+  const int n_full = n_units - tail;
+  const int n_items = n_full + 2 * tail;
+  auto item = [&](int w, int& u, int& half) {
+    if (w < n_full) {
+      u = w;
+      half = -1;
+    } else {
+      u = n_full + ((w - n_full) >> 1);
+      half = (w - n_full) & 1;
+    }
+  };
   const int m_oob = (p.M + FF_BM - 1) / FF_BM;
   const int NC = p.hp / FF_HC;
   auto my_m = [&](int u) {
@@ -125,7 +140,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
       auto next = [&]() {
         if (++s == FF_NS) { s = 0; ph ^= 1; }
       };
-      for (int u = unit0; u < n_units; u += unit_step, ++li) {
+      for (int w = unit0; w < n_items; w += unit_step, ++li) {
+        int u, half;
+        item(w, u, half);
         const int mt0 = my_m(u);
         const int mt = mt0 < 0 ? m_oob : mt0;
         tw(x_empty, (li & 1) ^ 1, 1);
@@ -144,6 +161,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
         auto w2 = [&](int c) {
           for (int kk = 0; kk < 2; ++kk)
             for (int nn = 0; nn < 2; ++nn) {
+              if (half >= 0 && nn != half) continue;
               tw(&w_empty[s], ph ^ 1, 0);
               if (leader) mbar_arrive_expect_tx(&w_full[s], 2 * Cfg::W2_ROWS * 128);
               tma_load_2d_2sm(sW + s * FF_SLOT, &tmW2, mapa_shared(&w_full[s], 0), c * FF_HC + kk * 64,
@@ -168,14 +186,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
     if (leader) {
       constexpr uint32_t idesc1 = idesc_bf16_f32(2 * FF_BM, FF_HC);
       constexpr uint32_t idesc2 = idesc_bf16_f32(2 * FF_BM, Cfg::NHALF);
-      constexpr int PC = Cfg::KB + 4;  // weight pieces per chunk: KB of W1, 4 of W2
-      const int per_tile = PC * NC;
-      auto pos_w1 = [&](int c) { return c == 0 ? 0 : Cfg::KB + PC * (c - 1); };
-      auto pos_w2 = [&](int c) { return c < NC - 1 ? 2 * Cfg::KB + PC * c : Cfg::KB + PC * c; };
       int g = 0;  // global chunk counter
       int li = 0;
-      for (int u = unit0; u < n_units; u += unit_step, ++li) {
-        const long long base = (long long)li * per_tile;
+      long long base = 0;  // the item's first weight piece in the producer's sequence
+      for (int w = unit0; w < n_items; w += unit_step, ++li) {
+        int u, half;
+        item(w, u, half);
+        (void)u;
+        const int PC = Cfg::KB + (half < 0 ? 4 : 2);  // weight pieces per chunk: KB of W1, 4 (2) of W2
+        auto pos_w1 = [&](int c) { return c == 0 ? 0 : Cfg::KB + PC * (c - 1); };
+        auto pos_w2 = [&](int c) { return c < NC - 1 ? 2 * Cfg::KB + PC * c : Cfg::KB + PC * c; };
         if (warp == 1) {
           tw(x_full, li & 1, 3);
           tc_fence_after();
@@ -209,8 +229,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
             tc_fence_after();
             int piece = 0;
             for (int kk = 0; kk < 2; ++kk)
-              for (int nn = 0; nn < 2; ++nn, ++piece) {
+              for (int nn = 0; nn < 2; ++nn) {
+                if (half >= 0 && nn != half) continue;
                 const long long gi = base + pos_w2(c) + piece;
+                ++piece;
                 const int s = (int)(gi % FF_NS);
                 tw(&w_full[s], (uint32_t)((gi / FF_NS) & 1), 0);
                 tc_fence_after();
@@ -227,7 +249,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
                                       (c | kk | k) != 0);
                   }
                   mma_commit_2sm(&w_empty[s], 0x3);
-                  if (kk == 1 && nn == 1) {
+                  if (kk == 1 && (half >= 0 || nn == 1)) {  // the chunk's last W2 piece
                     mma_commit_2sm(hs_empty, 0x3);
                     if (c == NC - 1) mma_commit_2sm(o_full, 0x3);
                   }
@@ -236,6 +258,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
               }
           }
         }
+        base += (long long)PC * NC;
       }
     }
   } else if (warp >= 4) {
@@ -250,8 +273,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
     float* st = sStg + (warp - 4) * 512;          // [16][32] fp32 transpose tile of this warp
     const int ci = lane >> 1, seg = lane & 1;      // transposed role: column, 16-token half
     int g = 0, li = 0;
-    for (int u = unit0; u < n_units; u += unit_step, ++li) {
+    for (int w = unit0; w < n_items; w += unit_step, ++li) {
+      int u, half;
+      item(w, u, half);
       const int mt = my_m(u);
+      const int c_lo = half < 0 ? 0 : half * Cfg::NHALF, c_hi = half < 0 ? CP : c_lo + Cfg::NHALF;
       // ---- hidden chunks: H -> +b1 -> bf16 -> GELU -> MMA2's A operand (warpgroups 0, 1)
       for (int c = 0; c < NC; ++c, ++g) {
         if (wg >= 2) continue;
@@ -306,7 +332,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
       const int tok_v = (mt < 0 ? 0 : mt) * FF_BM + wq * 32 + seg * 16;
       const int pidx_v = tok_v / p.hw, pix_v = tok_v - pidx_v * p.hw;
       bool released = false;
-      for (int cc = wg * 32; cc < CP; cc += 96) {
+      for (int cc = c_lo + wg * 32; cc < c_hi; cc += 96) {
         // residual (2 pieces x 32 B per lane) in flight before the accumulator load
         uint4 rsd[4];
 #pragma unroll
@@ -323,7 +349,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
         PS_TMEM_LD32(tmem + lane_base + Cfg::O_COL + cc, r);
         tmem_ld_wait();
         reg_fence32(r);
-        if (cc + 96 >= CP) {
+        if (cc + 96 >= c_hi) {
           tc_fence_before();
           mbar_arrive_cluster(o_empty_l);
           released = true;

@@ -44,6 +44,7 @@ struct FfParams {
   const int* m_count_dev;      // optional DEVICE count (m_count is then an upper bound)
   int hp;                      // hidden units (multiple of 128)
   int ts;                      // MMA2 reads GELU(H) from TMEM (else from shared memory)
+  int tail_split;              // last partial wave split into output-channel halves
   const float* b1;             // [hp]
   const float* b2;             // [Cp]
   int c_real, hw;              // output channels, pixels per patch (NCHW output)
