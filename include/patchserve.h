@@ -65,12 +65,14 @@ int ps_csp_reassemble(void* stream, const void* src, const uint64_t* dst_ptrs, c
 /* Fused step ends for a fixed-composition step (pipeline.py): split + prompt bias writes the
  * CSP fp32 latents and h = bf16(latent + prompts[request]) (csp.py:161-167 + model.py:163);
  * blend + reassemble writes (1 - rate) x + rate tanh(h) straight into the per-request images
- * (model.py:129-131 + csp.py:196-214).  fp32 latents, ps % 4 == 0. */
+ * (model.py:129-131 + csp.py:196-214).  fp32 latents, ps % 4 == 0.  dst may be NULL (no CSP
+ * copy); blend then reads x from the input images src_ptrs (DEVICE [n_req]) instead of
+ * `latent` (which may be NULL). */
 int ps_csp_split_bias(void* stream, const uint64_t* src_ptrs, const int32_t* request_offset, const int32_t* sides,
                       int n_req, int C, int ps, float* dst, int n_patches, const float* prompts, void* h);
 int ps_blend_reassemble(void* stream, const float* latent, const void* h, const float* rates,
                         const int32_t* request_offset, const int32_t* sides, int n_req, int C, int ps,
-                        const uint64_t* dst_ptrs, int n_patches);
+                        const uint64_t* dst_ptrs, int n_patches, const uint64_t* src_ptrs);
 
 /* ----------------------------------------- patched operators (patched.py) */
 /* exchange_halos(): patched.py:57-89, NCHW frames (P, C, ps+2, ps+2). */

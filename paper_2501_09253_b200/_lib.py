@@ -47,7 +47,7 @@ _SIGS = {
     "ps_csp_build": ([C.c_int, p, i32] + [p] * 9, C.c_int),
     "ps_csp_split": ([p, p, p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, C.c_int], C.c_int),
     "ps_csp_split_bias": ([p, p, p, p, C.c_int, C.c_int, C.c_int, p, C.c_int, p, p], C.c_int),
-    "ps_blend_reassemble": ([p, p, p, p, p, p, C.c_int, C.c_int, C.c_int, p, C.c_int], C.c_int),
+    "ps_blend_reassemble": ([p, p, p, p, p, p, C.c_int, C.c_int, C.c_int, p, C.c_int, p], C.c_int),
     "ps_csp_reassemble": ([p, p, p, p, p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int], C.c_int),
     "ps_halo_frames_nchw": ([p, p, C.c_int, p, C.c_int, C.c_int, C.c_int, p], C.c_int),
     "ps_gn_partials": ([p, p, C.c_int, C.c_int, C.c_int, C.c_int, p], C.c_int),

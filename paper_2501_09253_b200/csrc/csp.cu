@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(256) csp_split_bias_rows_kernel(const uint64_t
 #pragma unroll
     for (int u = 0; u < PM_UNR; ++u)
       if (dst[u] >= 0) {
-        *reinterpret_cast<float4*>(patches + dst[u]) = v[u];
+        if (patches != nullptr) *reinterpret_cast<float4*>(patches + dst[u]) = v[u];
         uint2 o;
         o.x = pack_bf16(v[u].x + bb[u], v[u].y + bb[u]);
         o.y = pack_bf16(v[u].z + bb[u], v[u].w + bb[u]);
@@ -293,13 +293,17 @@ __global__ void __launch_bounds__(256) blend_reassemble_kernel(const float* __re
                                                                const uint64_t* __restrict__ img_ptrs,
                                                                const int32_t* __restrict__ req_off,
                                                                const int32_t* __restrict__ sides, int n_req, int C,
-                                                               int ps, int cpb) {
+                                                               int ps, int cpb,
+                                                               const uint64_t* __restrict__ src_ptrs) {
   pdl_wait();
   const int p = blockIdx.x, c0 = blockIdx.y * cpb;
   int req, side, k;
   pm_locate(p, req_off, sides, n_req, req, side, k);
   const int r = k / side, cc = k - r * side, L = side * ps;
   float* img = reinterpret_cast<float*>(img_ptrs[req]);
+  // x from the request's input image (same coordinates as the output) when given: the
+  // split then skips writing the fp32 CSP copy
+  const float* src = src_ptrs ? reinterpret_cast<const float*>(src_ptrs[req]) : nullptr;
   const float rate = __ldg(rates + req);
   const int vps = ps / 4;
   const int nc = min(cpb, C - c0);
@@ -315,9 +319,9 @@ __global__ void __launch_bounds__(256) blend_reassemble_kernel(const float* __re
       if (i < n) {
         const int xv = i % vps, y = (i / vps) % ps, c = c0 + i / (vps * ps);
         const int64_t po = (((int64_t)p * C + c) * ps + y) * ps + xv * 4;
-        x[u] = __ldg(reinterpret_cast<const float4*>(lat + po));
-        hv[u] = __ldg(reinterpret_cast<const uint2*>(hh + po));
         io[u] = ((int64_t)c * L + (int64_t)r * ps + y) * L + (int64_t)cc * ps + xv * 4;
+        x[u] = __ldg(reinterpret_cast<const float4*>(src ? src + io[u] : lat + po));
+        hv[u] = __ldg(reinterpret_cast<const uint2*>(hh + po));
       }
     }
 #pragma unroll
@@ -473,14 +477,15 @@ int ps_csp_split_bias(void* stream, const uint64_t* src_ptrs, const int32_t* req
 
 int ps_blend_reassemble(void* stream, const float* latent, const void* h, const float* rates,
                         const int32_t* request_offset, const int32_t* sides, int n_req, int C, int ps_,
-                        const uint64_t* dst_ptrs, int n_patches) {
+                        const uint64_t* dst_ptrs, int n_patches, const uint64_t* src_ptrs) {
   if (n_req < 1 || C < 1 || ps_ < 1 || ps_ % 4) return set_error(PS_ERR_INPUT, "blend_reassemble: bad sizes");
+  if (latent == nullptr && src_ptrs == nullptr) return set_error(PS_ERR_INPUT, "blend_reassemble: no latent source");
   if (n_patches == 0) return PS_OK;
   if (n_patches > 65535) return set_error(PS_ERR_INPUT, "blend_reassemble: too many patches");
   const int cpb = pm_cpb(C, ps_, 4);
   // (a row-wise variant -- one CTA per image row band -- measured 103 vs 95 us and was removed)
   launch_pdl(blend_reassemble_kernel, dim3(n_patches, (C + cpb - 1) / cpb), dim3(256), 0, (cudaStream_t)stream,
-             latent, (const __nv_bfloat16*)h, rates, dst_ptrs, request_offset, sides, n_req, C, ps_, cpb);
+             latent, (const __nv_bfloat16*)h, rates, dst_ptrs, request_offset, sides, n_req, C, ps_, cpb, src_ptrs);
   count_launch();
   return check_launch("blend_reassemble");
 }

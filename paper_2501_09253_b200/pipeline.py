@@ -70,15 +70,16 @@ class DenoisePipeline:
         st = torch.cuda.current_stream().cuda_stream
         # split + prompt bias in one pass over the input latents (csp.py:161-167, model.py:163)
         h = torch.empty(b.data.shape, dtype=torch.bfloat16, device=self.dev)
+        # (no fp32 CSP copy: the blend reads x back from the input images)
         _lib.call("ps_csp_split_bias", st, self._in_ptrs[k].data_ptr(), src_ptrs["request_offset"].data_ptr(),
-                  src_ptrs["sides"].data_ptr(), b.n_requests, self.C, self.ps, b.data.data_ptr(), b.n_patches,
+                  src_ptrs["sides"].data_ptr(), b.n_requests, self.C, self.ps, None, b.n_patches,
                   self.bias[k].data_ptr(), h.data_ptr())
         for ops in self.weights:
             h = run_block(b, h, ops)
         # blend straight into the per-request outputs (model.py:129-131, csp.py:196-214)
-        _lib.call("ps_blend_reassemble", st, b.data.data_ptr(), h.data_ptr(), self.rates[k].data_ptr(),
+        _lib.call("ps_blend_reassemble", st, None, h.data_ptr(), self.rates[k].data_ptr(),
                   src_ptrs["request_offset"].data_ptr(), src_ptrs["sides"].data_ptr(), b.n_requests, self.C,
-                  self.ps, self._out_ptrs[k].data_ptr(), b.n_patches)
+                  self.ps, self._out_ptrs[k].data_ptr(), b.n_patches, self._in_ptrs[k].data_ptr())
 
     def prepare(self) -> None:
         """Upload weights (eager warm-up) and capture one graph per buffer set."""
