@@ -243,6 +243,8 @@ def run_ours(args):
             line["slo"] = slo
         if args.cache_run:
             line["config3_cache"] = measure_cache(cfg, weights, reqs)
+        if args.hbm_table:
+            line["hbm_kernels"] = measure_hbm_kernels(pipe, _peaks().get("hbm_gbs", 6548.5))
         if args.cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline_sample(repeats=1)
         print(json.dumps(line), flush=True)
@@ -314,6 +316,81 @@ def measure_cache(cfg, weights, reqs, steps=12, sigma=0.1, max_streak=3):
                     "compaction lists -> compacted block on recomputed patches (kernels read their work counts "
                     "from device memory) -> fused splice/streak/snapshot; no host round trip inside the step, "
                     "one counter read-back after it"}
+
+
+def measure_hbm_kernels(pipe, peak_gbs):
+    """Per-kernel HBM roofline table (north star: >= 70% of HBM roofline on the patch kernels).
+
+    Every HBM-bound kernel of the config-2 step and of the patch-cache path is launched on its
+    config-2 operands with L2 flushed (a 256 MB write) before each launch and timed with CUDA
+    events on the launching stream (kernel_timer.KernelTimer); achieved = the kernel's
+    ALGORITHMIC bytes (compulsory reads + writes) / mean launch time, against
+    the measured HBM copy bandwidth (MEASURED_PEAKS.json hbm_gbs).
+      step kernels (one eager pipeline step, 7 blocks): split+bias, GN partials, GN apply +
+        halo frames (stitcher), blend+reassemble;
+      cache kernels (a BlockCache over the config-2 patch set): snapshot insert (all rows
+        fresh), reuse test (every entry live: the fp64 pairwise MSE reads both operands),
+        substitute and splice/finish at a 50% mask."""
+    import torch
+
+    import paper_2501_09253_b200 as ps
+    from paper_2501_09253_b200.kernel_timer import KernelTimer
+    b = pipe.batches[0]
+    P, Cc, pz = b.n_patches, pipe.C, pipe.ps
+    hw = pz * pz
+    cp = (Cc + 63) // 64 * 64
+    act = P * Cc * hw * 2  # one bf16 activation
+    step_bytes = {
+        "ps_csp_split_bias": P * Cc * hw * 4 + act,                      # fp32 latents in, bf16 h out
+        "ps_gn_partials": act,                                           # x in (partials: KB)
+        "ps_frames_cl": act + P * (pz + 2) ** 2 * cp * 2,                # x in, halo frames out
+        "ps_blend_reassemble": 2 * P * Cc * hw * 4 + act,                # x + h in, latents out
+    }
+    flush = 256 << 20
+    rows = []
+    with KernelTimer(step_bytes, flush_bytes=flush) as kt:
+        pipe._step(0)
+    t = kt.times_ms()
+    for name, nbytes in step_bytes.items():
+        if name in t:
+            rows.append((name, nbytes, float(np.mean(t[name])), len(t[name])))
+    # cache path on the same patch set (bf16 slab, n = C*ps*ps per patch)
+    n = Cc * hw
+    keys = [(f"k{i}", 0) for i in range(P)]
+    cache = ps.BlockCache(1, ps.PredictorConfig(0.1, 3), capacity=P)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn((P, Cc, pz, pz), device="cuda", generator=g).to(torch.bfloat16)
+    y = torch.randn((P, Cc, pz, pz), device="cuda", generator=g).to(torch.bfloat16)
+    none = torch.zeros(P, dtype=torch.bool, device="cuda")
+    half = torch.arange(P, device="cuda") % 2 == 0
+    m = int(half.sum())
+    with KernelTimer(["ps_cache_update"], flush_bytes=flush) as kt:
+        cache.batched_update(0, keys, none, x, y)
+    ins = kt.times_ms()["ps_cache_update"]
+    slots = cache.slots_for(keys, allocate=False)
+    with KernelTimer(["ps_cache_predict", "ps_cache_substitute", "ps_cache_finish"], flush_bytes=flush) as kt:
+        for _ in range(3):
+            cache.predict_reuse(0, keys, y, slots=slots)
+            cache.block_substitute(0, slots, half, y)
+        for _ in range(3):
+            cache.block_finish(0, slots, half, y, x)
+            cache._streak.zero_()
+    tc = kt.times_ms()
+    rows += [("ps_cache_update (insert, all rows)", 4 * n * 2 * P, float(np.mean(ins)), len(ins)),
+             ("ps_cache_predict (mse_leaf + mse_combine, all live)", 2 * n * 2 * P,
+              float(np.mean(tc["ps_cache_predict"])), len(tc["ps_cache_predict"])),
+             ("ps_cache_substitute (50% mask)", 2 * n * 2 * P, float(np.mean(tc["ps_cache_substitute"])),
+              len(tc["ps_cache_substitute"])),
+             ("ps_cache_finish (50% mask)", n * 2 * (2 * m + 4 * (P - m)), float(np.mean(tc["ps_cache_finish"])),
+              len(tc["ps_cache_finish"]))]
+    out = []
+    for name, nbytes, ms_, cnt in rows:
+        gbs = nbytes / (ms_ * 1e-3) / 1e9
+        out.append({"kernel": name, "bytes": int(nbytes), "us": round(ms_ * 1e3, 2), "gbs": round(gbs, 1),
+                    "frac": round(gbs / peak_gbs, 3), "launches": cnt})
+    return {"peak_gbs": peak_gbs, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, read+write bytes)",
+            "timing": "each launch alone, L2 flushed (256 MB write) before it, CUDA events on its stream",
+            "kernels": out}
 
 
 def _peaks():
@@ -388,6 +465,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-slo", dest="slo", action="store_false", help="skip the SLO-attainment serving run")
+    ap.add_argument("--no-hbm-table", dest="hbm_table", action="store_false",
+                    help="skip the per-kernel HBM roofline table")
     ap.add_argument("--no-cache-run", dest="cache_run", action="store_false",
                     help="skip the config-3 (patch cache in the loop) measurement")
     args = ap.parse_args()

@@ -36,6 +36,14 @@ extern "C" {
 
 #define PS_DTYPE_F32 0
 #define PS_DTYPE_BF16 1
+#define PS_DTYPE_F64 2
+
+/* ABI version: bumped on every signature change (2: ps_blend_reassemble gained src_ptrs and
+ * ps_csp_split_bias the nonfinite flag; 3: the cache entry points take the element dtype --
+ * bf16 on the hot path, fp32 / fp64 for the numpy-interface drop-in -- and the reuse test is one
+ * kernel with a per-patch ticket area at the end of its scratch).
+ * Callers check ps_abi_version() == PS_ABI_VERSION after loading the library. */
+#define PS_ABI_VERSION 3
 
 /* ------------------------------------------------------------ library */
 int ps_abi_version(void);
@@ -67,9 +75,12 @@ int ps_csp_reassemble(void* stream, const void* src, const uint64_t* dst_ptrs, c
  * blend + reassemble writes (1 - rate) x + rate tanh(h) straight into the per-request images
  * (model.py:129-131 + csp.py:196-214).  fp32 latents, ps % 4 == 0.  dst may be NULL (no CSP
  * copy); blend then reads x from the input images src_ptrs (DEVICE [n_req]) instead of
- * `latent` (which may be NULL). */
+ * `latent` (which may be NULL).  Image pointers are 32-byte aligned.  nonfinite (DEVICE int, may be
+ * NULL; ps in {16, 32, 64}): set to 1 when an input latent is not finite -- kernels.py:20-24
+ * rejects those; the caller reads the flag after the step and raises InputError. */
 int ps_csp_split_bias(void* stream, const uint64_t* src_ptrs, const int32_t* request_offset, const int32_t* sides,
-                      int n_req, int C, int ps, float* dst, int n_patches, const float* prompts, void* h);
+                      int n_req, int C, int ps, float* dst, int n_patches, const float* prompts, void* h,
+                      int* nonfinite);
 int ps_blend_reassemble(void* stream, const float* latent, const void* h, const float* rates,
                         const int32_t* request_offset, const int32_t* sides, int n_req, int C, int ps,
                         const uint64_t* dst_ptrs, int n_patches, const uint64_t* src_ptrs);
@@ -213,11 +224,15 @@ int ps_pairwise_plan(int64_t n, int32_t* n_leaves, int32_t* n_internal, int32_t*
                      int32_t* nodes, int32_t* level_off);
 /* predict_reuse(): cache.py:107-122 with _mse_predictor (cache.py:87-88):
  * mask[p] = exists[slot] && mse(x[p], snap_in[slot]) < sigma && streak[slot] < max_streak,
- * mse bit-exact to numpy (fp64, same pairwise tree).  x: (P, n) bf16 NCHW;
- * slots: DEVICE int32 [P] (-1 = no entry); scratch: fp64 [P, n_leaves + n_internal];
- * counters: int64 [2] += (reused, fresh). */
-int ps_cache_predict(void* stream, const void* x, int P, int64_t n, const int32_t* slots, const void* snap_in,
-                     const uint8_t* exists, const int32_t* streak, double sigma, int max_streak,
+ * mse bit-exact to numpy (fp64, same pairwise tree).  x, snap_in: (P, n) / (slots, n) of `dtype`
+ * (PS_DTYPE_BF16 / F32 / F64; each element is widened exactly to fp64 before the subtraction);
+ * slots: DEVICE int32 [P] (-1 = no entry); scratch: fp64 [P * (n_leaves + n_internal)] followed by
+ * P int32 tickets, i.e. P * (n_leaves + n_internal) + (P + 1) / 2 doubles (the tickets are zeroed
+ * on the stream by the call); scratch[p, n_leaves + n_internal - 1] holds patch p's sum of squares
+ * afterwards (scratch[p, 0] when the tree is a single leaf); counters: int64 [2] += (reused, fresh).
+ * One kernel: leaf sums per CTA, the last CTA of a patch evaluates its tree. */
+int ps_cache_predict(void* stream, const void* x, int dtype, int P, int64_t n, const int32_t* slots,
+                     const void* snap_in, const uint8_t* exists, const int32_t* streak, double sigma, int max_streak,
                      const int32_t* leaves, int n_leaves, const int32_t* nodes, int n_internal,
                      const int32_t* level_off, int n_levels, double* scratch, uint8_t* mask, int64_t* counters);
 /* Active-patch compaction (np.flatnonzero(~mask), ascending) + count. */
@@ -235,15 +250,16 @@ int ps_compact(void* stream, const uint8_t* mask, int P, int32_t* active, int32_
                int32_t* n_reused);
 /* gather(): cache.py:124-137 — cached (inputs, outputs) at masked rows, zeros elsewhere.
  * error_flag: int32, set to 1 when a masked patch has no entry (IntegrityError). */
+/* The data-moving cache entry points below take n elements of `dtype` per patch row. */
 int ps_cache_gather(void* stream, const uint8_t* mask, const int32_t* slots, const uint8_t* exists, int P,
-                    int64_t n, const void* snap_in, const void* snap_out, void* ins, void* outs, int32_t* error_flag);
+                    int64_t n, int dtype, const void* snap_in, const void* snap_out, void* ins, void* outs, int32_t* error_flag);
 /* batched_fill(): cache.py:139-151 — streak += 1 at masked rows; optional out copy. */
 int ps_cache_fill(void* stream, const uint8_t* mask, const int32_t* slots, const uint8_t* exists, int32_t* streak,
-                  int P, int64_t n, const void* snap_out, void* out, int32_t* error_flag);
+                  int P, int64_t n, int dtype, const void* snap_out, void* out, int32_t* error_flag);
 /* batched_update(): cache.py:153-169 — fresh snapshots, streak 0 at unmasked rows;
  * counters: int64 [2] += (refreshed, inserted). */
 int ps_cache_update(void* stream, const uint8_t* mask, const int32_t* slots, uint8_t* exists, int32_t* streak,
-                    int P, int64_t n, const void* x, const void* y, void* snap_in, void* snap_out,
+                    int P, int64_t n, int dtype, const void* x, const void* y, void* snap_in, void* snap_out,
                     int64_t* counters);
 /* evict_expired(): cache.py:171-181 — clear `exists` for listed slots. */
 int ps_cache_evict(void* stream, uint8_t* exists, int32_t* streak, const int32_t* slots, int n_slots);
@@ -253,12 +269,14 @@ int ps_cache_evict(void* stream, uint8_t* exists, int32_t* streak, const int32_t
  *             unmasked -> snap_in/out[slot] = x/y, streak = 0, exists = 1 (cache.py:165-169)
  * substitute with `patches` (DEVICE list, n_list entries or the DEVICE count n_dev) writes
  * those patches only (the live patches of a device-decided compaction). */
-int ps_cache_substitute(void* stream, const uint8_t* mask, const int32_t* slots, int P, int64_t n, const void* x,
-                        const void* snap_in, void* x_sub, const int32_t* patches, int n_list, const int32_t* n_dev);
+int ps_cache_substitute(void* stream, const uint8_t* mask, const int32_t* slots, int P, int64_t n, int dtype,
+                        const void* x, const void* snap_in, void* x_sub, const int32_t* patches, int n_list, const int32_t* n_dev);
 int ps_cache_finish(void* stream, const uint8_t* mask, const int32_t* slots, uint8_t* exists, int32_t* streak,
-                    int P, int64_t n, const void* x, void* y, void* snap_in, void* snap_out, int64_t* counters);
+                    int P, int64_t n, int dtype, const void* x, void* y, void* snap_in, void* snap_out,
+                    int64_t* counters);
 /* masked selection used by masked_block_forward (patched.py:241-246): out = mask ? a : b. */
-int ps_select_patches(void* stream, const uint8_t* mask, int P, int64_t n, const void* a, const void* b, void* out);
+int ps_select_patches(void* stream, const uint8_t* mask, int P, int64_t n, int dtype, const void* a, const void* b,
+                      void* out);
 
 /* ------------------------------------------------ step wrapper (model.py) */
 /* h = bf16(latent + prompt[request_index[p]])  (model.py:163, engine.py:131-132). */

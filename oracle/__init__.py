@@ -17,6 +17,6 @@ build container and records golden input/output vectors under `tests/golden/`;
 `tests/test_oracle_golden.py` checks this restatement against them (integer and
 copy results bit-exact, float results to 1e-12 or bit-exact where the reference
 itself is order-deterministic).  The numpy pairwise-summation dependency that
-makes cache masks bit-exact is restated in `pairwise.py` / `pairwise.c` and
-checked bitwise against `np.mean` (numpy 2.3.5).
+makes cache masks bit-exact is restated in `pairwise.py` and checked bitwise
+against `np.mean` (numpy 2.3.5).
 """

@@ -15,8 +15,9 @@ from .errors import InputError, IntegrityError
 LIB_PATH = os.environ.get("PS_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
                                                          "libpatchserve.so")  # override: experiments only
 
+ABI_VERSION = 3  # include/patchserve.h PS_ABI_VERSION
 PS_OK, PS_ERR_INPUT, PS_ERR_INTEGRITY, PS_ERR_CUDA = 0, 1, 2, 3
-DTYPE_F32, DTYPE_BF16 = 0, 1
+DTYPE_F32, DTYPE_BF16, DTYPE_F64 = 0, 1, 2
 
 p = C.c_void_p
 i32 = C.c_int32
@@ -46,7 +47,7 @@ _SIGS = {
     "ps_csp_count": ([C.c_int, p, i32, p, p], C.c_int),
     "ps_csp_build": ([C.c_int, p, i32] + [p] * 9, C.c_int),
     "ps_csp_split": ([p, p, p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, C.c_int], C.c_int),
-    "ps_csp_split_bias": ([p, p, p, p, C.c_int, C.c_int, C.c_int, p, C.c_int, p, p], C.c_int),
+    "ps_csp_split_bias": ([p, p, p, p, C.c_int, C.c_int, C.c_int, p, C.c_int, p, p, p], C.c_int),
     "ps_blend_reassemble": ([p, p, p, p, p, p, C.c_int, C.c_int, C.c_int, p, C.c_int, p], C.c_int),
     "ps_csp_reassemble": ([p, p, p, p, p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int], C.c_int),
     "ps_halo_frames_nchw": ([p, p, C.c_int, p, C.c_int, C.c_int, C.c_int, p], C.c_int),
@@ -75,17 +76,17 @@ _SIGS = {
     "ps_attention_trace": ([p], C.c_int),
     "ps_feed_forward_debug": ([p], C.c_int),
     "ps_pairwise_plan": ([i64, p, p, p, p, p, p], C.c_int),
-    "ps_cache_predict": ([p, p, C.c_int, i64, p, p, p, p, f64, C.c_int, p, C.c_int, p, C.c_int, p, C.c_int, p, p, p],
+    "ps_cache_predict": ([p, p, C.c_int, C.c_int, i64, p, p, p, p, f64, C.c_int, p, C.c_int, p, C.c_int, p, C.c_int, p, p, p],
                          C.c_int),
     "ps_compact": ([p, p, C.c_int, p, p, p, p], C.c_int),
     "ps_compact_lists": ([p, p, C.c_int, p, C.c_int, p, C.c_int, C.c_int, C.c_int, C.c_int] + [p] * 9, C.c_int),
-    "ps_cache_gather": ([p, p, p, p, C.c_int, i64, p, p, p, p, p], C.c_int),
-    "ps_cache_fill": ([p, p, p, p, p, C.c_int, i64, p, p, p], C.c_int),
-    "ps_cache_update": ([p, p, p, p, p, C.c_int, i64, p, p, p, p, p], C.c_int),
+    "ps_cache_gather": ([p, p, p, p, C.c_int, i64, C.c_int, p, p, p, p, p], C.c_int),
+    "ps_cache_fill": ([p, p, p, p, p, C.c_int, i64, C.c_int, p, p, p], C.c_int),
+    "ps_cache_update": ([p, p, p, p, p, C.c_int, i64, C.c_int, p, p, p, p, p], C.c_int),
     "ps_cache_evict": ([p, p, p, p, C.c_int], C.c_int),
-    "ps_cache_substitute": ([p, p, p, C.c_int, i64, p, p, p, p, C.c_int, p], C.c_int),
-    "ps_cache_finish": ([p, p, p, p, p, C.c_int, i64, p, p, p, p, p], C.c_int),
-    "ps_select_patches": ([p, p, C.c_int, i64, p, p, p], C.c_int),
+    "ps_cache_substitute": ([p, p, p, C.c_int, i64, C.c_int, p, p, p, p, C.c_int, p], C.c_int),
+    "ps_cache_finish": ([p, p, p, p, p, C.c_int, i64, C.c_int, p, p, p, p, p], C.c_int),
+    "ps_select_patches": ([p, p, C.c_int, i64, C.c_int, p, p, p], C.c_int),
     "ps_prompt_bias": ([p, p, p, p, C.c_int, C.c_int, C.c_int, p], C.c_int),
     "ps_blend": ([p, p, p, p, p, C.c_int, C.c_int, C.c_int, p], C.c_int),
     "ps_convert": ([p, p, C.c_int, p, C.c_int, i64], C.c_int),
@@ -107,6 +108,9 @@ def load():
             fn = getattr(lib, name)
             fn.argtypes = args
             fn.restype = res
+        if lib.ps_abi_version() != ABI_VERSION:
+            raise OSError(f"{LIB_PATH}: ABI version {lib.ps_abi_version()} != {ABI_VERSION} expected by the facade "
+                          "(stale build? run `make -C paper_2501_09253_b200/csrc`)")
         _lib = lib
     return _lib
 
@@ -122,7 +126,19 @@ def check(rc: int) -> None:
     raise RuntimeError(f"CUDA error in libpatchserve: {msg}")
 
 
+# measurement hook (bench.py / tools): when set to an object with .wants(name), .before(name)
+# and .after(name), calls of those entry points are bracketed by it (CUDA events on the
+# launching stream); None on the product path
+TIMER = None
+
+
 def call(name: str, *args) -> None:
+    t = TIMER
+    if t is not None and t.wants(name):
+        t.before(name)
+        check(getattr(load(), name)(*args))
+        t.after(name)
+        return
     check(getattr(load(), name)(*args))
 
 

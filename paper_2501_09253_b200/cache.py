@@ -90,30 +90,49 @@ class PairwisePlan:
         return p
 
 
-def _bf16_patches(x) -> torch.Tensor:
+_LIB_DTYPE = {torch.bfloat16: _lib.DTYPE_BF16, torch.float32: _lib.DTYPE_F32, torch.float64: _lib.DTYPE_F64}
+
+
+def _patches(x, dtype: torch.dtype) -> torch.Tensor:
+    """Device copy of x in the slab dtype (bf16 on the hot path: fp32 inputs are rounded the way
+    the block inputs are; fp32 / fp64 slabs keep numpy inputs exact)."""
     t = to_device(x)
-    if t.dtype != torch.bfloat16:
-        t = t.to(torch.float32).to(torch.bfloat16)
+    if t.dtype != dtype:
+        t = t.to(dtype)
     return t.contiguous()
 
 
+def scratch_doubles(P: int, plan: "PairwisePlan") -> int:
+    """fp64 scratch of ps_cache_predict: per-patch tree values + P int32 tickets."""
+    return P * (plan.L + plan.I) + (P + 1) // 2
+
+
 def mse(a, b) -> float:
-    """float(np.mean((a - b) ** 2)) (cache.py:54-55) on the device, bit-exact in fp64."""
-    ta, tb = _bf16_patches(a), _bf16_patches(b)
+    """float(np.mean((a - b) ** 2)) (cache.py:54-55) on the device, bit-exact in fp64.
+
+    The operands keep their precision: bf16 / fp32 tensors are widened exactly, anything else
+    (numpy float64 arrays, fp64 tensors) is evaluated in fp64 -- no rounding before the
+    subtraction, so the result equals numpy's for every input."""
+    ta, tb = to_device(a), to_device(b)
     if ta.shape != tb.shape:
         raise InputError("mse: shape mismatch")
+    dt = ta.dtype if (ta.dtype == tb.dtype and ta.dtype in _LIB_DTYPE) else torch.float64
+    ta, tb = _patches(ta, dt), _patches(tb, dt)
     n = ta.numel()
+    if n == 0:
+        return float("nan")  # np.mean of an empty array
     plan = PairwisePlan.get(n)
     dev = ta.device
     slots = torch.zeros(1, dtype=torch.int32, device=dev)
     exists = torch.ones(1, dtype=torch.uint8, device=dev)
     streak = torch.zeros(1, dtype=torch.int32, device=dev)
-    scratch = torch.empty(plan.L + plan.I, dtype=torch.float64, device=dev)
+    scratch = torch.empty(scratch_doubles(1, plan), dtype=torch.float64, device=dev)
     mask = torch.empty(1, dtype=torch.uint8, device=dev)
     # sigma = +inf makes the mask always true; the fp64 root is read from scratch
-    _lib.call("ps_cache_predict", stream(), ta.data_ptr(), 1, n, slots.data_ptr(), tb.data_ptr(), exists.data_ptr(),
-              streak.data_ptr(), float("inf"), 1, plan.leaves.data_ptr(), plan.L, plan.nodes.data_ptr(), plan.I,
-              plan.level_off.data_ptr(), plan.H, scratch.data_ptr(), mask.data_ptr(), None)
+    _lib.call("ps_cache_predict", stream(), ta.data_ptr(), _LIB_DTYPE[dt], 1, n, slots.data_ptr(), tb.data_ptr(),
+              exists.data_ptr(), streak.data_ptr(), float("inf"), 1, plan.leaves.data_ptr(), plan.L,
+              plan.nodes.data_ptr(), plan.I, plan.level_off.data_ptr(), plan.H, scratch.data_ptr(), mask.data_ptr(),
+              None)
     root = scratch[plan.L + plan.I - 1] if plan.I > 0 else scratch[0]
     return (0.0 + float(root)) / n
 
@@ -131,13 +150,19 @@ class BlockCache:
     """Per-block patch cache with batched predict / gather / fill / update / evict."""
 
     def __init__(self, n_blocks: int, cfg: PredictorConfig | None = None,
-                 predictor: Callable | None = None, capacity: int = 256):
+                 predictor: Callable | None = None, capacity: int = 256, dtype: torch.dtype = torch.bfloat16):
         if n_blocks < 1:
             raise InputError("n_blocks must be >= 1")
         self.cfg = cfg or PredictorConfig()
         self._predictor = predictor
         self._n_blocks = n_blocks
         self._dev = require_cuda()
+        if dtype not in _LIB_DTYPE:
+            raise InputError(f"cache dtype must be bf16, fp32 or fp64, got {dtype}")
+        # snapshot precision: bf16 on the hot path (the block inputs / outputs are bf16); fp64
+        # keeps numpy inputs exact for the numpy-interface drop-in (dropin.py)
+        self.dtype = dtype
+        self._dt = _LIB_DTYPE[dtype]
         self._slot_of: dict = {}
         self._free: list = []
         self._cap = 0
@@ -151,6 +176,9 @@ class BlockCache:
         self._err = torch.zeros(1, dtype=torch.int32, device=self._dev)
         self._evicted = 0
         self._want_cap = capacity
+        # storage generation: bumped whenever the slab tensors are replaced (_grow, restore), so
+        # holders of raw pointers into them (engine_step.CachedStepGraph) know to re-capture
+        self.storage_gen = 0
 
     # --------------------------------------------------------- storage
     @property
@@ -171,8 +199,8 @@ class BlockCache:
         if cap <= old:
             return
         dev = self._dev
-        ni = [torch.zeros((cap, self._n), dtype=torch.bfloat16, device=dev) for _ in range(self._n_blocks)]
-        no = [torch.zeros((cap, self._n), dtype=torch.bfloat16, device=dev) for _ in range(self._n_blocks)]
+        ni = [torch.zeros((cap, self._n), dtype=self.dtype, device=dev) for _ in range(self._n_blocks)]
+        no = [torch.zeros((cap, self._n), dtype=self.dtype, device=dev) for _ in range(self._n_blocks)]
         ex = torch.zeros((self._n_blocks, cap), dtype=torch.uint8, device=dev)
         st = torch.zeros((self._n_blocks, cap), dtype=torch.int32, device=dev)
         if old:
@@ -182,6 +210,7 @@ class BlockCache:
             ex[:, :old].copy_(self._exists)
             st[:, :old].copy_(self._streak)
         self._snap_in, self._snap_out, self._exists, self._streak = ni, no, ex, st
+        self.storage_gen += 1
         self._free.extend(range(cap - 1, old - 1, -1))
         self._cap = cap
 
@@ -238,7 +267,7 @@ class BlockCache:
     def predict_reuse(self, block_id: int, keys: Sequence[Key], inputs, slots: torch.Tensor | None = None):
         """Device bool mask: entry exists, mse < sigma, streak < R (cache.py:107-122)."""
         self._check_block(block_id)
-        x = _bf16_patches(inputs)
+        x = _patches(inputs, self.dtype)
         if len(keys) != x.shape[0]:
             raise InputError("keys and inputs length mismatch")
         P = x.shape[0]
@@ -251,8 +280,8 @@ class BlockCache:
             return self._predict_custom(block_id, keys, x)
         plan = PairwisePlan.get(self._n)
         mask = torch.empty(P, dtype=torch.bool, device=self._dev)
-        scratch = torch.empty((P, plan.L + plan.I), dtype=torch.float64, device=self._dev)
-        _lib.call("ps_cache_predict", stream(), x.data_ptr(), P, self._n, slots.data_ptr(),
+        scratch = torch.empty(scratch_doubles(P, plan), dtype=torch.float64, device=self._dev)
+        _lib.call("ps_cache_predict", stream(), x.data_ptr(), self._dt, P, self._n, slots.data_ptr(),
                   self._snap_in[block_id].data_ptr(), self._exists[block_id].data_ptr(),
                   self._streak[block_id].data_ptr(), float(self.cfg.mse_threshold), int(self.cfg.max_streak),
                   plan.leaves.data_ptr(), plan.L, plan.nodes.data_ptr(), plan.I, plan.level_off.data_ptr(), plan.H,
@@ -275,7 +304,7 @@ class BlockCache:
         self._check_block(block_id)
         P = len(keys)
         shape = tuple(int(s) for s in shape)
-        ins = torch.zeros((P,) + shape, dtype=torch.bfloat16, device=self._dev)
+        ins = torch.zeros((P,) + shape, dtype=self.dtype, device=self._dev)
         outs = torch.zeros_like(ins)
         m = self._mask_u8(mask, P)
         if P == 0:
@@ -287,7 +316,7 @@ class BlockCache:
         self._ensure_shape(shape)
         slots = self.slots_for(keys, allocate=False)
         _lib.call("ps_cache_gather", stream(), m.data_ptr(), slots.data_ptr(), self._exists[block_id].data_ptr(), P,
-                  self._n, self._snap_in[block_id].data_ptr(), self._snap_out[block_id].data_ptr(), ins.data_ptr(),
+                  self._n, self._dt, self._snap_in[block_id].data_ptr(), self._snap_out[block_id].data_ptr(), ins.data_ptr(),
                   outs.data_ptr(), self._err.data_ptr())
         self._raise_if_missing(block_id)
         return ins, outs
@@ -306,11 +335,11 @@ class BlockCache:
         slots = self.slots_for(keys, allocate=False)
         dst = None
         if out is not None:
-            dst = out if (isinstance(out, torch.Tensor) and out.is_cuda and out.dtype == torch.bfloat16
-                          and out.is_contiguous()) else torch.empty((P, self._n), dtype=torch.bfloat16,
+            dst = out if (isinstance(out, torch.Tensor) and out.is_cuda and out.dtype == self.dtype
+                          and out.is_contiguous()) else torch.empty((P, self._n), dtype=self.dtype,
                                                                     device=self._dev)
         _lib.call("ps_cache_fill", stream(), m.data_ptr(), slots.data_ptr(), self._exists[block_id].data_ptr(),
-                  self._streak[block_id].data_ptr(), P, self._n, self._snap_out[block_id].data_ptr(),
+                  self._streak[block_id].data_ptr(), P, self._n, self._dt, self._snap_out[block_id].data_ptr(),
                   None if dst is None else dst.data_ptr(), self._err.data_ptr())
         self._raise_if_missing(block_id)
         if out is not None and dst is not out:
@@ -319,14 +348,14 @@ class BlockCache:
             if isinstance(out, torch.Tensor):
                 out[mb] = src[mb].to(out.dtype).to(out.device)
             else:
-                out[mb] = src.float().cpu().numpy()[mb]
+                out[mb] = src.double().cpu().numpy()[mb]
         return out
 
     def batched_update(self, block_id: int, keys: Sequence[Key], mask, inputs, outputs,
                        slots: torch.Tensor | None = None) -> None:
         """Fresh snapshots with streak 0 for every unmasked row (cache.py:153-169)."""
         self._check_block(block_id)
-        x, y = _bf16_patches(inputs), _bf16_patches(outputs)
+        x, y = _patches(inputs, self.dtype), _patches(outputs, self.dtype)
         if not (len(keys) == x.shape[0] == y.shape[0]):
             raise InputError("keys/inputs/outputs length mismatch")
         P = len(keys)
@@ -337,7 +366,7 @@ class BlockCache:
         if slots is None:
             slots = self.slots_for(keys, allocate=True)
         _lib.call("ps_cache_update", stream(), m.data_ptr(), slots.data_ptr(), self._exists[block_id].data_ptr(),
-                  self._streak[block_id].data_ptr(), P, self._n, x.data_ptr(), y.data_ptr(),
+                  self._streak[block_id].data_ptr(), P, self._n, self._dt, x.data_ptr(), y.data_ptr(),
                   self._snap_in[block_id].data_ptr(), self._snap_out[block_id].data_ptr(),
                   self._ctr[block_id, 2:].data_ptr())
 
@@ -370,7 +399,7 @@ class BlockCache:
         out = torch.empty_like(x)
         plist, n_ub, n_dev = patches if patches is not None else (None, 0, None)
         _lib.call("ps_cache_substitute", stream(), mask.view(torch.uint8).data_ptr(), slots.data_ptr(), x.shape[0],
-                  self._n, x.data_ptr(), self._snap_in[block_id].data_ptr(), out.data_ptr(),
+                  self._n, self._dt, x.data_ptr(), self._snap_in[block_id].data_ptr(), out.data_ptr(),
                   None if plist is None else plist.data_ptr(), n_ub, None if n_dev is None else n_dev.data_ptr())
         return out
 
@@ -380,7 +409,7 @@ class BlockCache:
         snapshots for the rest (patched.py:246 + cache.py:139-169, fused)."""
         _lib.call("ps_cache_finish", stream(), mask.view(torch.uint8).data_ptr(), slots.data_ptr(),
                   self._exists[block_id].data_ptr(), self._streak[block_id].data_ptr(), x.shape[0], self._n,
-                  x.data_ptr(), y.data_ptr(), self._snap_in[block_id].data_ptr(),
+                  self._dt, x.data_ptr(), y.data_ptr(), self._snap_in[block_id].data_ptr(),
                   self._snap_out[block_id].data_ptr(), self._ctr[block_id, 2:].data_ptr())
 
     # ------------------------------------------------------ atomic steps
@@ -400,6 +429,7 @@ class BlockCache:
             self._slot_of, self._free = dict(snap["slots"]), list(snap["free"])
             if self._exists is not None:
                 self._exists.zero_()
+            self.storage_gen += 1
             return
         if len(snap["in"]) != self._n_blocks:
             raise IntegrityError("snapshot block count mismatch")
@@ -407,3 +437,4 @@ class BlockCache:
         self._exists, self._streak = snap["exists"].clone(), snap["streak"].clone()
         self._snap_in = [t.clone() for t in snap["in"]]
         self._snap_out = [t.clone() for t in snap["out"]]
+        self.storage_gen += 1

@@ -1,6 +1,7 @@
-// Per-image self-attention on CTA pairs (cta_group::2) — experimental (PS_ATTN_PAIRS=1).
-// Measured slower than the single-CTA kernel on config 2 (1.73 vs 1.53 ms): the pair's
-// softmax, not operand bandwidth, ends up on the critical path; kept for the record.
+// Per-image self-attention on CTA pairs (cta_group::2) -- the default attention path
+// (PS_ATTN_PAIRS=0 selects the single-CTA kernel in attention.cu).  attn2p_kernel (persistent,
+// tiles from an atomic ticket) is the production kernel; attn2_kernel (one tile per CTA pair,
+// PS_ATTN_PERSIST=0) is kept as the A/B baseline.
 //
 // Same math as attention.cu (reference patched.py:154-176 -> kernels.py:230-267,
 // one head, D = C, keys restricted to the query tile's image), but each cluster of
@@ -10,8 +11,8 @@
 //     [64r, 64r+64) of K and half of the V^T rows of each PV MMA;
 //   * the leader (rank 0) issues all MMAs; TMA loads of both CTAs complete on the
 //     leader's barriers; MMA completions are multicast to both CTAs.
-// Per SM this halves the K/V bytes loaded and read by the tensor core, which is
-// what limited the single-CTA kernel (shared-memory bandwidth).
+// Per SM this halves the K/V bytes loaded and read by the tensor core (shared-memory
+// operand bandwidth is what limits the single-CTA kernel).
 #include <stdlib.h>
 
 #include <mutex>
@@ -390,38 +391,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
   if (warp == 2) tmem_dealloc_2sm(tmem, Cfg::TMEM_COLS);
 }
 
-// Ticket counters of the persistent pair kernel: a pool of 64 pairs of ints per device
-// (zeroed once, left zero by every launch), one pair per stream that launches it -- two
-// persistent attentions in flight on different streams never share a counter (a stream
-// captured into a graph keeps its pair for the graph's replays).  The pool is allocated on
-// the first launch outside stream capture; a capture before that runs the one-tile kernel.
+// Ticket counters of the persistent pair kernel: a per-device pool of int pairs, zeroed once
+// (and synchronised) before first use; every launch leaves its pair at zero again (the last
+// cluster out resets it).  Eager launches take one pair per launching stream, so two
+// persistent attentions in flight on different streams never share a counter.  A launch
+// captured into a CUDA graph takes a pair of its own, never handed out again, so graphs
+// captured on the same stream can replay concurrently on different streams.  The pool is
+// allocated on the first launch outside stream capture; a capture before that, or after the
+// pool is exhausted, runs the one-tile kernel (same results).
 static int* attention2_tile_counter(cudaStream_t st) {
-  constexpr int kSlots = 64;
+  constexpr int kSlots = 16384;
+  constexpr int kMaxDev = 64;
   static std::mutex mu;
-  static int* pool[64] = {};
-  static std::unordered_map<cudaStream_t, int> slot_of[64];
-  static int next_slot[64] = {};
+  static int* pool[kMaxDev] = {};
+  static std::unordered_map<cudaStream_t, int> slot_of[kMaxDev];
+  static int next_slot[kMaxDev] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return nullptr;
+  if (dev < 0 || dev >= kMaxDev) return nullptr;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  const bool capturing = cs != cudaStreamCaptureStatusNone;
   std::lock_guard<std::mutex> lock(mu);
   if (pool[dev] == nullptr) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(st, &cs);
-    if (cs != cudaStreamCaptureStatusNone) return nullptr;
+    if (capturing) return nullptr;
     int* c = nullptr;
     if (cudaMalloc(&c, kSlots * 2 * sizeof(int)) != cudaSuccess) return nullptr;
-    cudaMemset(c, 0, kSlots * 2 * sizeof(int));
+    // zero on the launching stream, then wait: the pool is visible as zero to every stream
+    // (a plain cudaMemset runs on the legacy stream, unordered with non-blocking streams)
+    if (cudaMemsetAsync(c, 0, kSlots * 2 * sizeof(int), st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+      cudaFree(c);
+      return nullptr;
+    }
     pool[dev] = c;
   }
-  auto it = slot_of[dev].find(st);
   int slot;
-  if (it != slot_of[dev].end()) {
-    slot = it->second;
+  if (capturing) {
+    if (next_slot[dev] >= kSlots) return nullptr;
+    slot = next_slot[dev]++;  // owned by this captured launch for the graph's lifetime
   } else {
-    if (next_slot[dev] >= kSlots) return nullptr;  // more streams than slots: one-tile kernel
-    slot = next_slot[dev]++;
-    slot_of[dev][st] = slot;
+    auto it = slot_of[dev].find(st);
+    if (it != slot_of[dev].end()) {
+      slot = it->second;
+    } else {
+      if (next_slot[dev] >= kSlots) return nullptr;  // pool exhausted: one-tile kernel
+      slot = next_slot[dev]++;
+      slot_of[dev][st] = slot;
+    }
   }
   return pool[dev] + 2 * slot;
 }

@@ -20,16 +20,30 @@
 
 namespace ps {
 
-constexpr int LEAVES_PER_CTA = 128;
-
 __device__ __forceinline__ bool entry_live(int slot, const uint8_t* exists, const int32_t* streak, int max_streak) {
   return slot >= 0 && exists[slot] && streak[slot] < max_streak;
 }
 
-// numpy pairwise_sum leaf (n <= 128) over squared differences of bf16 pairs.
-__device__ __forceinline__ double leaf_sum(const __nv_bfloat16* a, const __nv_bfloat16* b, int n) {
+__device__ __forceinline__ double to_d(__nv_bfloat16 v) { return (double)__bfloat162float(v); }
+__device__ __forceinline__ double to_d(float v) { return (double)v; }
+__device__ __forceinline__ double to_d(double v) { return v; }
+
+// Leaves per CTA of the reuse test (one leaf per thread): both operands' spans of LPC
+// consecutive leaves (<= 128 elements each) are staged in shared memory.
+template <typename T>
+struct MseCfg {
+  static constexpr int LPC = sizeof(T) == 2 ? 128 : (sizeof(T) == 4 ? 64 : 32);
+  static constexpr int EPV = 16 / (int)sizeof(T);  // elements per 16-byte vector
+};
+
+// numpy pairwise_sum leaf (n <= 128, numpy/_core/src/umath/loops_utils.h.src) over the
+// squared differences (a - b)^2, fp64 with explicit round-to-nearest ops (no FMA contraction):
+// n < 8 sequential from -0.0; else 8 strided accumulators r[i % 8], combined
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the n % 8 tail.
+template <typename T>
+__device__ __forceinline__ double leaf_sum(const T* a, const T* b, int n) {
   auto sq = [&](int i) {
-    const double d = __dsub_rn((double)__bfloat162float(a[i]), (double)__bfloat162float(b[i]));
+    const double d = __dsub_rn(to_d(a[i]), to_d(b[i]));
     return __dmul_rn(d, d);
   };
   if (n < 8) {
@@ -37,62 +51,141 @@ __device__ __forceinline__ double leaf_sum(const __nv_bfloat16* a, const __nv_bf
     for (int i = 0; i < n; ++i) res = __dadd_rn(res, sq(i));
     return res;
   }
-  // 8 strided accumulators: element i goes to r[i % 8]; 16-byte smem loads deliver exactly one
-  // element per accumulator (leaf starts are multiples of 8 in numpy's tree)
-  auto sq8 = [&](int i, double* d8) {
-    const uint4 ua = *reinterpret_cast<const uint4*>(a + i);
-    const uint4 ub = *reinterpret_cast<const uint4*>(b + i);
-    const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&ua);
-    const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&ub);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const double d0 = __dsub_rn((double)__low2float(ha[k]), (double)__low2float(hb[k]));
-      const double d1 = __dsub_rn((double)__high2float(ha[k]), (double)__high2float(hb[k]));
-      d8[2 * k] = __dmul_rn(d0, d0);
-      d8[2 * k + 1] = __dmul_rn(d1, d1);
-    }
-  };
   double r[8];
-  sq8(0, r);
-  int i = 8;
-  const int stop = n - (n % 8);
-  for (; i < stop; i += 8) {
-    double d8[8];
-    sq8(i, d8);
+  if constexpr (sizeof(T) == 2) {
+    // bf16: one 16-byte smem load per operand delivers exactly one element per accumulator
+    // (leaf starts are multiples of 8 in numpy's tree)
+    auto sq8 = [&](int i, double* d8) {
+      const uint4 ua = *reinterpret_cast<const uint4*>(a + i);
+      const uint4 ub = *reinterpret_cast<const uint4*>(b + i);
+      const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&ua);
+      const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&ub);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], d8[j]);
+      for (int k = 0; k < 4; ++k) {
+        const double d0 = __dsub_rn((double)__low2float(ha[k]), (double)__low2float(hb[k]));
+        const double d1 = __dsub_rn((double)__high2float(ha[k]), (double)__high2float(hb[k]));
+        d8[2 * k] = __dmul_rn(d0, d0);
+        d8[2 * k + 1] = __dmul_rn(d1, d1);
+      }
+    };
+    sq8(0, r);
+    int i = 8;
+    const int stop = n - (n % 8);
+    for (; i < stop; i += 8) {
+      double d8[8];
+      sq8(i, d8);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], d8[j]);
+    }
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, sq(i));
+    return res;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = sq(j);
+    int i = 8;
+    const int stop = n - (n % 8);
+    for (; i < stop; i += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], sq(i + j));
+    }
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, sq(i));
+    return res;
   }
-  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-  for (; i < n; ++i) res = __dadd_rn(res, sq(i));
-  return res;
 }
 
-// grid (P, ceil(L / 128)): leaf sums of patch p into scratch[p, 0:L].
-__global__ void __launch_bounds__(LEAVES_PER_CTA) mse_leaf_kernel(
-    const __nv_bfloat16* __restrict__ x, int64_t n, const int32_t* __restrict__ slots,
-    const __nv_bfloat16* __restrict__ snap, const uint8_t* __restrict__ exists, const int32_t* __restrict__ streak,
-    int max_streak, const int32_t* __restrict__ leaves, int L, int stride_nodes, double* __restrict__ scratch) {
+// Internal nodes of patch p's tree, level by level (children from `nodes`, ids < L are
+// leaves), over the values w[0 .. L+I) -- in shared memory or in place in scratch -- then the
+// mask (mse < sigma, strict) and the reuse / fresh counters.  Called by the CTA that finished
+// the patch's last leaves (all CTA threads).
+__device__ __forceinline__ void mse_tree_and_mask(int p, double* w, bool w_in_smem, double* v_global, int64_t n, int L,
+                                                  const int32_t* __restrict__ nodes, int I,
+                                                  const int32_t* __restrict__ level_off, int H, double sigma,
+                                                  uint8_t* __restrict__ mask, int64_t* __restrict__ counters) {
+  for (int h = 0; h < H; ++h) {
+    const int e = __ldg(level_off + h + 1);
+    for (int i = __ldg(level_off + h) + threadIdx.x; i < e; i += blockDim.x) {
+      const int2 c = __ldg(reinterpret_cast<const int2*>(nodes) + i);
+      w[L + i] = __dadd_rn(w[c.x], w[c.y]);
+    }
+    if (!w_in_smem) __threadfence_block();
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double root = I > 0 ? w[L + I - 1] : w[0];
+    if (w_in_smem) v_global[I > 0 ? L + I - 1 : 0] = root;  // the root stays readable in scratch (ps.mse)
+    const double mse = __ddiv_rn(__dadd_rn(0.0, root), (double)n);
+    const bool m = mse < sigma;
+    mask[p] = m ? 1 : 0;
+    if (counters) atomicAdd(reinterpret_cast<unsigned long long*>(counters + (m ? 0 : 1)), 1ull);
+  }
+}
+
+// In-order pairwise reduction of n (a power of two) doubles in shared memory, ping-ponging
+// between buf and tmp: level by level w[i] = w[2i] + w[2i+1] -- numpy's tree when it is
+// perfect.  Returns the root (all CTA threads).
+__device__ __forceinline__ double smem_pairwise(double* buf, double* tmp, int n) {
+  double* src = buf;
+  double* dst = tmp;
+  for (int s = n >> 1; s >= 1; s >>= 1) {
+    for (int i = threadIdx.x; i < s; i += blockDim.x) dst[i] = __dadd_rn(src[2 * i], src[2 * i + 1]);
+    __syncthreads();
+    double* t = src;
+    src = dst;
+    dst = t;
+  }
+  return src[0];
+}
+
+// grid (ceil(L / LPC), P), LPC threads: the reuse test of patch p in one kernel.  Every CTA
+// sums its LPC leaves (both operands' spans staged in shared memory by two bulk copies);
+//  * perfect tree (depth >= 0: numpy's tree over n is a perfect binary tree, e.g. n = C ps^2
+//    with C = 4 or 320 and ps a power of two): the CTA reduces its leaves pairwise to its
+//    subtree root, and the patch's last CTA (per-patch ticket) reduces the CTA roots the
+//    same way -- the exact numpy tree, a few levels of shared-memory adds per CTA;
+//  * otherwise: the leaf sums go to scratch and the last CTA walks the plan's levels.
+// Then the mask (mse < sigma, strict) and the counters.  Patches with no live entry (absent /
+// streak exhausted) skip the MSE as the reference's short-circuit does (cache.py:87-88, 116-119).
+template <typename T>
+__global__ void __launch_bounds__(MseCfg<T>::LPC) mse_fused_kernel(
+    const T* __restrict__ x, int64_t n, const int32_t* __restrict__ slots, const T* __restrict__ snap,
+    const uint8_t* __restrict__ exists, const int32_t* __restrict__ streak, int max_streak, double sigma,
+    const int32_t* __restrict__ leaves, int L, const int32_t* __restrict__ nodes, int I,
+    const int32_t* __restrict__ level_off, int H, double* __restrict__ scratch, int* __restrict__ tickets,
+    uint8_t* __restrict__ mask, int64_t* __restrict__ counters, int tree_in_smem, int perfect) {
+  constexpr int LPC = MseCfg<T>::LPC, EPV = MseCfg<T>::EPV;
   pdl_wait();
-  extern __shared__ __align__(16) __nv_bfloat16 stage[];
-  const int p = blockIdx.x;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[2][LPC];
+  const int p = blockIdx.y;
   const int slot = slots[p];
-  if (!entry_live(slot, exists, streak, max_streak)) return;
-  const int l0 = blockIdx.y * LEAVES_PER_CTA;
-  const int l1 = min(L, l0 + LEAVES_PER_CTA);
+  if (!entry_live(slot, exists, streak, max_streak)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      mask[p] = 0;
+      if (counters) atomicAdd(reinterpret_cast<unsigned long long*>(counters + 1), 1ull);
+    }
+    return;
+  }
+  const int stride = L + I;
+  double* v = scratch + (int64_t)p * stride;
+  const int l0 = blockIdx.x * LPC;
+  const int l1 = min(L, l0 + LPC);
   const int64_t e0 = leaves[2 * l0];
   const int64_t e1 = (int64_t)leaves[2 * (l1 - 1)] + leaves[2 * (l1 - 1) + 1];
-  const __nv_bfloat16* xa = x + (int64_t)p * n;
-  const __nv_bfloat16* xb = snap + (int64_t)slot * n;
-  // stage [e0, e1) of both operands (16B vectors when aligned)
-  const int64_t v0 = e0 & ~int64_t(7), v1 = (e1 + 7) & ~int64_t(7);
-  __nv_bfloat16* sa = stage;
-  __nv_bfloat16* sb = stage + (v1 - v0);
-  const bool vec = (n % 8 == 0) && v1 <= n;
+  const T* xa = x + (int64_t)p * n;
+  const T* xb = snap + (int64_t)slot * n;
+  // stage [e0, e1) of both operands (16-byte vectors when aligned)
+  const int64_t v0 = e0 & ~int64_t(EPV - 1), v1 = (e1 + EPV - 1) & ~int64_t(EPV - 1);
+  T* sa = reinterpret_cast<T*>(smem_raw);
+  T* sb = sa + (v1 - v0);
+  const bool vec = (n % EPV == 0) && v1 <= n;
   __shared__ __align__(8) uint64_t bar;
+  __shared__ int last;
   if (vec) {
-    // two bulk copies (TMA engine, no register staging): the whole span is in flight at once
-    const uint32_t bytes = (uint32_t)((v1 - v0) * 2);
+    const uint32_t bytes = (uint32_t)((v1 - v0) * sizeof(T));
     if (threadIdx.x == 0) {
       mbar_init(&bar, 1);
       fence_mbar_init();
@@ -110,96 +203,64 @@ __global__ void __launch_bounds__(LEAVES_PER_CTA) mse_leaf_kernel(
   }
   __syncthreads();
   const int l = l0 + threadIdx.x;
+  double leaf = 0.0;
   if (l < l1) {
-    const int64_t s = leaves[2 * l];
-    const int len = leaves[2 * l + 1];
-    scratch[(int64_t)p * stride_nodes + l] = leaf_sum(sa + (s - v0), sb + (s - v0), len);
+    const int64_t st = leaves[2 * l];
+    leaf = leaf_sum<T>(sa + (st - v0), sb + (st - v0), leaves[2 * l + 1]);
   }
-}
-
-// grid P: evaluate internal nodes level by level, then the mask.
-__global__ void __launch_bounds__(256) mse_combine_kernel(
-    int64_t n, const int32_t* __restrict__ slots, const uint8_t* __restrict__ exists,
-    const int32_t* __restrict__ streak, int max_streak, double sigma, int L, const int32_t* __restrict__ nodes,
-    int I, const int32_t* __restrict__ level_off, int H, int stride_nodes, double* __restrict__ scratch,
-    uint8_t* __restrict__ mask, int64_t* __restrict__ counters, int smem_nodes) {
-  pdl_wait();
-  const int p = blockIdx.x;
-  const int slot = slots[p];
-  const bool live = entry_live(slot, exists, streak, max_streak);
-  double* v = scratch + (int64_t)p * stride_nodes;
-  extern __shared__ double sv[];  // leaf sums + internal nodes when they fit (else in place in scratch)
-  __shared__ double root_s;
-  const bool in_smem = smem_nodes >= L + I;
-  if (live) {
-    double* w = v;
-    if (in_smem) {
-      // the leaf sums (L2-resident, written by mse_leaf_kernel): 8 independent loads in
-      // flight per thread instead of one L2 round trip per loop trip
-      for (int base = 0; base < L; base += 8 * blockDim.x) {
-        double t[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int i = base + k * blockDim.x + threadIdx.x;
-          t[k] = i < L ? __ldcg(v + i) : 0.0;
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int i = base + k * blockDim.x + threadIdx.x;
-          if (i < L) sv[i] = t[k];
-        }
-      }
-      __syncthreads();
-      w = sv;
-    }
-    if (in_smem && smem_nodes >= L + I + I) {
-      // node index pairs staged next to the values (int2 per node): the levels then touch
-      // shared memory only -- no L2 round trip per level for the tree structure
-      int2* sn = reinterpret_cast<int2*>(sv + L + I);
-      for (int base = 0; base < I; base += 8 * blockDim.x) {
-        int2 t[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int i = base + k * blockDim.x + threadIdx.x;
-          t[k] = i < I ? __ldg(reinterpret_cast<const int2*>(nodes) + i) : make_int2(0, 0);
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int i = base + k * blockDim.x + threadIdx.x;
-          if (i < I) sn[i] = t[k];
-        }
-      }
-      __syncthreads();
-      for (int h = 0; h < H; ++h) {
-        const int e = __ldg(level_off + h + 1);
-        for (int i = __ldg(level_off + h) + threadIdx.x; i < e; i += blockDim.x) {
-          const int2 c = sn[i];
-          w[L + i] = __dadd_rn(w[c.x], w[c.y]);
-        }
-        __syncthreads();
-      }
-    } else {
-      for (int h = 0; h < H; ++h) {
-        for (int i = level_off[h] + threadIdx.x; i < level_off[h + 1]; i += blockDim.x)
-          w[L + i] = __dadd_rn(w[nodes[2 * i]], w[nodes[2 * i + 1]]);
-        __syncthreads();
-      }
-    }
+  if (perfect) {
+    red[0][threadIdx.x] = leaf;
+    __syncthreads();
+    const double root = smem_pairwise(red[0], red[1], l1 - l0);  // l1 - l0: a power of two
+    if (threadIdx.x == 0) v[blockIdx.x] = root;                   // CTA subtree root
+  } else if (l < l1) {
+    v[l] = leaf;
+  }
+  // ticket: the patch's last CTA finishes the tree
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(tickets + p, 1) == (int)gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (perfect) {
+    const int g = gridDim.x;  // a power of two
+    double* b0 = reinterpret_cast<double*>(smem_raw);
+    double* b1 = b0 + g;
+    for (int i = threadIdx.x; i < g; i += blockDim.x) b0[i] = __ldcg(v + i);
+    __syncthreads();
+    const double root = smem_pairwise(b0, b1, g);
     if (threadIdx.x == 0) {
-      root_s = I > 0 ? w[L + I - 1] : w[0];
-      if (in_smem && I > 0) v[L + I - 1] = root_s;  // the root stays readable in scratch (ps.mse)
-    }
-  }
-  if (threadIdx.x == 0) {
-    bool m = false;
-    if (live) {
-      const double root = root_s;
+      v[I > 0 ? L + I - 1 : 0] = root;  // readable in scratch (ps.mse)
       const double mse = __ddiv_rn(__dadd_rn(0.0, root), (double)n);
-      m = mse < sigma;
+      const bool m = mse < sigma;
+      mask[p] = m ? 1 : 0;
+      if (counters) atomicAdd(reinterpret_cast<unsigned long long*>(counters + (m ? 0 : 1)), 1ull);
+      tickets[p] = 0;
     }
-    mask[p] = m ? 1 : 0;
-    if (counters) atomicAdd(reinterpret_cast<unsigned long long*>(counters + (m ? 0 : 1)), 1ull);
+    return;
   }
+  double* w = v;
+  if (tree_in_smem) {
+    // all leaf sums of the patch (L2-resident) into shared memory, the staging space reused
+    w = reinterpret_cast<double*>(smem_raw);
+    for (int base = 0; base < L; base += 8 * (int)blockDim.x) {
+      double t[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int i = base + k * blockDim.x + threadIdx.x;
+        t[k] = i < L ? __ldcg(v + i) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int i = base + k * blockDim.x + threadIdx.x;
+        if (i < L) w[i] = t[k];
+      }
+    }
+    __syncthreads();
+  }
+  mse_tree_and_mask(p, w, tree_in_smem != 0, v, n, L, nodes, I, level_off, H, sigma, mask, counters);
+  if (threadIdx.x == 0) tickets[p] = 0;
 }
 
 // single CTA: ascending active (mask == 0) and reused (mask == 1) lists.
@@ -250,41 +311,43 @@ __global__ void __launch_bounds__(1024) compact_kernel(const uint8_t* __restrict
 
 enum PatchOp { OP_GATHER, OP_FILL, OP_UPDATE, OP_SUBST, OP_FINISH, OP_SELECT };
 
+// Pure data movement: rows are moved as bytes (n elements x esize), so one kernel serves the
+// bf16 hot-path slab and the fp32 / fp64 slabs of the numpy-interface drop-in.
 struct PatchOpArgs {
   const uint8_t* mask;
   const int32_t* slots;
   uint8_t* exists;
   int32_t* streak;
-  int64_t n;
-  const __nv_bfloat16* x;  // fresh input / select a
-  __nv_bfloat16* y;        // fresh output (finish: in/out) / select b
-  __nv_bfloat16* snap_in;
-  __nv_bfloat16* snap_out;
-  __nv_bfloat16* o1;  // gather ins / fill out / subst x_sub / select out
-  __nv_bfloat16* o2;  // gather outs
+  int64_t nb;             // bytes per patch row
+  const char* x;          // fresh input / select a
+  char* y;                // fresh output (finish: in/out) / select b
+  char* snap_in;
+  char* snap_out;
+  char* o1;  // gather ins / fill out / subst x_sub / select out
+  char* o2;  // gather outs
   int32_t* err;
   int64_t* counters;
   const int32_t* plist;  // optional patch list (grid.x walks it) ...
   const int32_t* n_dev;  // ... with its DEVICE length (grid.x is an upper bound)
 };
 
-__device__ __forceinline__ void copy_range(__nv_bfloat16* dst, const __nv_bfloat16* src, int64_t n, bool vec) {
-  if (vec) {
-    const int64_t nv = n / 8;
+__device__ __forceinline__ void copy_range(char* dst, const char* src, int64_t nb) {
+  if ((nb & 15) == 0) {
+    const int64_t nv = nb / 16;
     for (int64_t i = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.y * blockDim.x)
       reinterpret_cast<uint4*>(dst)[i] = __ldg(reinterpret_cast<const uint4*>(src) + i);
   } else {
-    for (int64_t i = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.y * blockDim.x)
+    for (int64_t i = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; i < nb; i += (int64_t)gridDim.y * blockDim.x)
       dst[i] = src[i];
   }
 }
-__device__ __forceinline__ void zero_range(__nv_bfloat16* dst, int64_t n, bool vec) {
-  if (vec) {
-    for (int64_t i = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; i < n / 8; i += (int64_t)gridDim.y * blockDim.x)
+__device__ __forceinline__ void zero_range(char* dst, int64_t nb) {
+  if ((nb & 15) == 0) {
+    for (int64_t i = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; i < nb / 16; i += (int64_t)gridDim.y * blockDim.x)
       reinterpret_cast<uint4*>(dst)[i] = make_uint4(0, 0, 0, 0);
   } else {
-    for (int64_t i = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.y * blockDim.x)
-      dst[i] = __float2bfloat16_rn(0.f);
+    for (int64_t i = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; i < nb; i += (int64_t)gridDim.y * blockDim.x)
+      dst[i] = 0;
   }
 }
 
@@ -295,17 +358,16 @@ __global__ void __launch_bounds__(256) patch_op_kernel(PatchOpArgs a) {
   const int p = a.plist ? a.plist[blockIdx.x] : (int)blockIdx.x;
   const bool m = a.mask[p] != 0;
   const int slot = a.slots ? a.slots[p] : -1;
-  const int64_t n = a.n;
-  const bool vec = (n % 8) == 0;
+  const int64_t nb = a.nb;
   const bool lead = blockIdx.y == 0 && threadIdx.x == 0;
-  const int64_t po = (int64_t)p * n, so = (int64_t)slot * n;
+  const int64_t po = (int64_t)p * nb, so = (int64_t)slot * nb;
   if constexpr (OP == OP_SELECT) {
-    copy_range(a.o1 + po, m ? a.x + po : a.y + po, n, vec);
+    copy_range(a.o1 + po, m ? a.x + po : a.y + po, nb);
     return;
   }
   if constexpr (OP == OP_SUBST) {
-    if (m && slot >= 0) copy_range(a.o1 + po, a.snap_in + so, n, vec);
-    else copy_range(a.o1 + po, a.x + po, n, vec);
+    if (m && slot >= 0) copy_range(a.o1 + po, a.snap_in + so, nb);
+    else copy_range(a.o1 + po, a.x + po, nb);
     return;
   }
   const bool have = slot >= 0 && a.exists[slot];
@@ -315,11 +377,11 @@ __global__ void __launch_bounds__(256) patch_op_kernel(PatchOpArgs a) {
       return;
     }
     if (m) {
-      copy_range(a.o1 + po, a.snap_in + so, n, vec);
-      copy_range(a.o2 + po, a.snap_out + so, n, vec);
+      copy_range(a.o1 + po, a.snap_in + so, nb);
+      copy_range(a.o2 + po, a.snap_out + so, nb);
     } else {
-      zero_range(a.o1 + po, n, vec);
-      zero_range(a.o2 + po, n, vec);
+      zero_range(a.o1 + po, nb);
+      zero_range(a.o2 + po, nb);
     }
     return;
   }
@@ -329,21 +391,21 @@ __global__ void __launch_bounds__(256) patch_op_kernel(PatchOpArgs a) {
       if (lead) atomicExch(a.err, 1);
       return;
     }
-    if (a.o1) copy_range(a.o1 + po, a.snap_out + so, n, vec);
+    if (a.o1) copy_range(a.o1 + po, a.snap_out + so, nb);
     if (lead) a.streak[slot] += 1;
     return;
   }
   if constexpr (OP == OP_UPDATE || OP == OP_FINISH) {
     if (m) {
       if constexpr (OP == OP_FINISH) {
-        copy_range(a.y + po, a.snap_out + so, n, vec);
+        copy_range(a.y + po, a.snap_out + so, nb);
         if (lead) a.streak[slot] += 1;
       }
       return;
     }
     if (slot < 0) return;
-    copy_range(a.snap_in + so, a.x + po, n, vec);
-    copy_range(a.snap_out + so, a.y + po, n, vec);
+    copy_range(a.snap_in + so, a.x + po, nb);
+    copy_range(a.snap_out + so, a.y + po, nb);
     if (lead) {
       if (a.counters) atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + (have ? 0 : 1)), 1ull);
       a.streak[slot] = 0;
@@ -359,10 +421,17 @@ __global__ void evict_kernel(uint8_t* exists, int32_t* streak, const int32_t* sl
   }
 }
 
+static int dtype_size(int dtype) {
+  return dtype == PS_DTYPE_BF16 ? 2 : dtype == PS_DTYPE_F32 ? 4 : dtype == PS_DTYPE_F64 ? 8 : 0;
+}
+
 template <int OP>
-static int launch_op(cudaStream_t st, int P, int64_t n, const PatchOpArgs& a, const char* name) {
+static int launch_op(cudaStream_t st, int P, int64_t n, int dtype, PatchOpArgs& a, const char* name) {
   if (P == 0) return PS_OK;
-  const int64_t vecs = (n % 8 == 0) ? n / 8 : n;
+  const int es = dtype_size(dtype);
+  if (es == 0) return set_error(PS_ERR_INPUT, "%s: unsupported dtype %d", name, dtype);
+  a.nb = n * es;
+  const int64_t vecs = (a.nb % 16 == 0) ? a.nb / 16 : a.nb;
   int chunks = (int)((vecs + 255) / 256);
   if (chunks > 16) chunks = 16;
   if (chunks < 1) chunks = 1;
@@ -465,45 +534,52 @@ __global__ void __launch_bounds__(1024) compact_lists_kernel(
 
 extern "C" {
 
-int ps_cache_predict(void* stream, const void* x, int P, int64_t n, const int32_t* slots, const void* snap_in,
-                     const uint8_t* exists, const int32_t* streak, double sigma, int max_streak,
+int ps_cache_predict(void* stream, const void* x, int dtype, int P, int64_t n, const int32_t* slots,
+                     const void* snap_in, const uint8_t* exists, const int32_t* streak, double sigma, int max_streak,
                      const int32_t* leaves, int n_leaves, const int32_t* nodes, int n_internal,
                      const int32_t* level_off, int n_levels, double* scratch, uint8_t* mask, int64_t* counters) {
   if (P == 0) return PS_OK;
   if (n < 1 || n_leaves < 1) return set_error(PS_ERR_INPUT, "cache_predict: empty patches");
+  if (P > 65535) return set_error(PS_ERR_INPUT, "cache_predict: too many patches");
   cudaStream_t st = (cudaStream_t)stream;
   const int stride = n_leaves + n_internal;
-  // shared staging of two operands: the widest span of LEAVES_PER_CTA consecutive leaves of
-  // this n's tree (+16 elements of vector alignment slack); smaller staging -> more CTAs per SM
-  const int smem = 2 * (int)(pairwise_max_span(n, LEAVES_PER_CTA) + 16) * 2;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(mse_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         2 * (LEAVES_PER_CTA * 128 + 16) * 2);
-    attr = true;
-  }
-  launch_pdl(mse_leaf_kernel, dim3(P, (n_leaves + LEAVES_PER_CTA - 1) / LEAVES_PER_CTA), dim3(LEAVES_PER_CTA),
-             (size_t)smem, st, (const __nv_bfloat16*)x, n, slots, (const __nv_bfloat16*)snap_in, exists, streak,
-             max_streak, leaves, n_leaves, stride, scratch);
-  count_launch();
-  int rc = check_launch("mse_leaf");
-  if (rc) return rc;
-  // the tree in shared memory when it fits (levels then cost smem latency, not L2 round trips)
-  const int nodes_all = n_leaves + n_internal;
-  // values (8 B per node) + node index pairs (8 B per internal node) in shared memory: 14 -> 9
-  // us per launch at config 2 (the in-place L2 levels, PS_MSE_L2_COMBINE=1, wait for an L2
-  // round trip per level)
-  const int smem_need = nodes_all * 8 + n_internal * 8;
-  const int smem_c = (!getenv("PS_MSE_L2_COMBINE") && smem_need <= 200 * 1024) ? smem_need : 0;
-  static bool attr_c = false;
-  if (!attr_c) {
-    cudaFuncSetAttribute(mse_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_c = true;
-  }
-  launch_pdl(mse_combine_kernel, dim3(P), dim3(256), (size_t)smem_c, st, n, slots, exists, streak, max_streak, sigma,
-             n_leaves, nodes, n_internal, level_off, n_levels, stride, scratch, mask, counters, smem_c / 8);
-  count_launch();
-  return check_launch("mse_combine");
+  int* tickets = reinterpret_cast<int*>(scratch + (int64_t)P * stride);
+  if (cudaMemsetAsync(tickets, 0, (size_t)P * sizeof(int), st) != cudaSuccess)
+    return check_launch("cache_predict tickets");
+  auto run = [&](auto tag) -> int {
+    using T = decltype(tag);
+    constexpr int LPC = MseCfg<T>::LPC;
+    // staging: the widest span of LPC consecutive leaves of this n's tree (+ vector slack), both
+    // operands; the tree values (L + I doubles) reuse it when they fit the budget
+    const int stage = 2 * (int)(pairwise_max_span(n, LPC) + 2 * MseCfg<T>::EPV) * (int)sizeof(T);
+    // perfect tree: every CTA holds LPC leaves (or all L < LPC) -> power-of-two groups
+    const int depth = pairwise_perfect_depth(n);
+    const int perfect = depth >= 0 && (n_leaves <= LPC || n_leaves % LPC == 0) ? 1 : 0;
+    const int g = (n_leaves + LPC - 1) / LPC;
+    int smem, tree_smem = 0;
+    if (perfect) {
+      smem = stage > 2 * g * 8 ? stage : 2 * g * 8;
+    } else {
+      const int tree = stride * 8;
+      tree_smem = tree <= 100 * 1024 ? 1 : 0;
+      smem = tree_smem ? (stage > tree ? stage : tree) : stage;
+    }
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(mse_fused_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    if (smem > 200 * 1024) return set_error(PS_ERR_INPUT, "cache_predict: leaf span too large");
+    launch_pdl(mse_fused_kernel<T>, dim3((n_leaves + LPC - 1) / LPC, P), dim3(LPC), (size_t)smem, st,
+               (const T*)x, n, slots, (const T*)snap_in, exists, streak, max_streak, sigma, leaves, n_leaves, nodes,
+               n_internal, level_off, n_levels, scratch, tickets, mask, counters, tree_smem, perfect);
+    count_launch();
+    return check_launch("mse_reuse_test");
+  };
+  if (dtype == PS_DTYPE_BF16) return run(__nv_bfloat16{});
+  if (dtype == PS_DTYPE_F32) return run(float{});
+  if (dtype == PS_DTYPE_F64) return run(double{});
+  return set_error(PS_ERR_INPUT, "cache_predict: unsupported dtype %d", dtype);
 }
 
 int ps_compact_lists(void* stream, const uint8_t* mask, int P, const int32_t* request_index, int R,
@@ -526,29 +602,30 @@ int ps_compact(void* stream, const uint8_t* mask, int P, int32_t* active, int32_
 }
 
 int ps_cache_gather(void* stream, const uint8_t* mask, const int32_t* slots, const uint8_t* exists, int P, int64_t n,
-                    const void* snap_in, const void* snap_out, void* ins, void* outs, int32_t* error_flag) {
+                    int dtype, const void* snap_in, const void* snap_out, void* ins, void* outs, int32_t* error_flag) {
   PatchOpArgs a{};
-  a.mask = mask; a.slots = slots; a.exists = const_cast<uint8_t*>(exists); a.n = n;
-  a.snap_in = (__nv_bfloat16*)snap_in; a.snap_out = (__nv_bfloat16*)snap_out;
-  a.o1 = (__nv_bfloat16*)ins; a.o2 = (__nv_bfloat16*)outs; a.err = error_flag;
-  return launch_op<OP_GATHER>((cudaStream_t)stream, P, n, a, "cache_gather");
+  a.mask = mask; a.slots = slots; a.exists = const_cast<uint8_t*>(exists);
+  a.snap_in = (char*)snap_in; a.snap_out = (char*)snap_out;
+  a.o1 = (char*)ins; a.o2 = (char*)outs; a.err = error_flag;
+  return launch_op<OP_GATHER>((cudaStream_t)stream, P, n, dtype, a, "cache_gather");
 }
 
 int ps_cache_fill(void* stream, const uint8_t* mask, const int32_t* slots, const uint8_t* exists, int32_t* streak,
-                  int P, int64_t n, const void* snap_out, void* out, int32_t* error_flag) {
+                  int P, int64_t n, int dtype, const void* snap_out, void* out, int32_t* error_flag) {
   PatchOpArgs a{};
-  a.mask = mask; a.slots = slots; a.exists = const_cast<uint8_t*>(exists); a.streak = streak; a.n = n;
-  a.snap_out = (__nv_bfloat16*)snap_out; a.o1 = (__nv_bfloat16*)out; a.err = error_flag;
-  return launch_op<OP_FILL>((cudaStream_t)stream, P, n, a, "cache_fill");
+  a.mask = mask; a.slots = slots; a.exists = const_cast<uint8_t*>(exists); a.streak = streak;
+  a.snap_out = (char*)snap_out; a.o1 = (char*)out; a.err = error_flag;
+  return launch_op<OP_FILL>((cudaStream_t)stream, P, n, dtype, a, "cache_fill");
 }
 
 int ps_cache_update(void* stream, const uint8_t* mask, const int32_t* slots, uint8_t* exists, int32_t* streak, int P,
-                    int64_t n, const void* x, const void* y, void* snap_in, void* snap_out, int64_t* counters) {
+                    int64_t n, int dtype, const void* x, const void* y, void* snap_in, void* snap_out,
+                    int64_t* counters) {
   PatchOpArgs a{};
-  a.mask = mask; a.slots = slots; a.exists = exists; a.streak = streak; a.n = n;
-  a.x = (const __nv_bfloat16*)x; a.y = (__nv_bfloat16*)y;
-  a.snap_in = (__nv_bfloat16*)snap_in; a.snap_out = (__nv_bfloat16*)snap_out; a.counters = counters;
-  return launch_op<OP_UPDATE>((cudaStream_t)stream, P, n, a, "cache_update");
+  a.mask = mask; a.slots = slots; a.exists = exists; a.streak = streak;
+  a.x = (const char*)x; a.y = (char*)y;
+  a.snap_in = (char*)snap_in; a.snap_out = (char*)snap_out; a.counters = counters;
+  return launch_op<OP_UPDATE>((cudaStream_t)stream, P, n, dtype, a, "cache_update");
 }
 
 int ps_cache_evict(void* stream, uint8_t* exists, int32_t* streak, const int32_t* slots, int n_slots) {
@@ -558,29 +635,30 @@ int ps_cache_evict(void* stream, uint8_t* exists, int32_t* streak, const int32_t
   return check_launch("cache_evict");
 }
 
-int ps_cache_substitute(void* stream, const uint8_t* mask, const int32_t* slots, int P, int64_t n, const void* x,
-                        const void* snap_in, void* x_sub, const int32_t* patches, int n_list, const int32_t* n_dev) {
+int ps_cache_substitute(void* stream, const uint8_t* mask, const int32_t* slots, int P, int64_t n, int dtype,
+                        const void* x, const void* snap_in, void* x_sub, const int32_t* patches, int n_list,
+                        const int32_t* n_dev) {
   PatchOpArgs a{};
-  a.mask = mask; a.slots = slots; a.n = n; a.x = (const __nv_bfloat16*)x;
-  a.snap_in = (__nv_bfloat16*)snap_in; a.o1 = (__nv_bfloat16*)x_sub;
+  a.mask = mask; a.slots = slots; a.x = (const char*)x;
+  a.snap_in = (char*)snap_in; a.o1 = (char*)x_sub;
   a.plist = patches; a.n_dev = patches ? n_dev : nullptr;
-  return launch_op<OP_SUBST>((cudaStream_t)stream, patches ? n_list : P, n, a, "cache_substitute");
+  return launch_op<OP_SUBST>((cudaStream_t)stream, patches ? n_list : P, n, dtype, a, "cache_substitute");
 }
 
 int ps_cache_finish(void* stream, const uint8_t* mask, const int32_t* slots, uint8_t* exists, int32_t* streak, int P,
-                    int64_t n, const void* x, void* y, void* snap_in, void* snap_out, int64_t* counters) {
+                    int64_t n, int dtype, const void* x, void* y, void* snap_in, void* snap_out, int64_t* counters) {
   PatchOpArgs a{};
-  a.mask = mask; a.slots = slots; a.exists = exists; a.streak = streak; a.n = n;
-  a.x = (const __nv_bfloat16*)x; a.y = (__nv_bfloat16*)y;
-  a.snap_in = (__nv_bfloat16*)snap_in; a.snap_out = (__nv_bfloat16*)snap_out; a.counters = counters;
-  return launch_op<OP_FINISH>((cudaStream_t)stream, P, n, a, "cache_finish");
+  a.mask = mask; a.slots = slots; a.exists = exists; a.streak = streak;
+  a.x = (const char*)x; a.y = (char*)y;
+  a.snap_in = (char*)snap_in; a.snap_out = (char*)snap_out; a.counters = counters;
+  return launch_op<OP_FINISH>((cudaStream_t)stream, P, n, dtype, a, "cache_finish");
 }
 
-int ps_select_patches(void* stream, const uint8_t* mask, int P, int64_t n, const void* a_, const void* b_,
+int ps_select_patches(void* stream, const uint8_t* mask, int P, int64_t n, int dtype, const void* a_, const void* b_,
                       void* out) {
   PatchOpArgs a{};
-  a.mask = mask; a.n = n; a.x = (const __nv_bfloat16*)a_; a.y = (__nv_bfloat16*)b_; a.o1 = (__nv_bfloat16*)out;
-  return launch_op<OP_SELECT>((cudaStream_t)stream, P, n, a, "select_patches");
+  a.mask = mask; a.x = (const char*)a_; a.y = (char*)b_; a.o1 = (char*)out;
+  return launch_op<OP_SELECT>((cudaStream_t)stream, P, n, dtype, a, "select_patches");
 }
 
 }  // extern "C"

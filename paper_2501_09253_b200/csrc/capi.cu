@@ -90,6 +90,28 @@ static void pairwise_leaves(int64_t lo, int64_t n, std::vector<std::pair<int64_t
   pairwise_leaves(lo + n2, n - n2, out);
 }
 
+// depth of numpy's pairwise tree over n elements when it is a perfect binary tree (every
+// internal node's two subtrees are perfect of equal depth), else -1: then the leaf sums
+// combine as adjacent pairs level by level, i.e. a plain in-order pairwise reduction.
+static int pairwise_depth(int64_t n) {
+  if (n <= 128) return 0;
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  const int a = pairwise_depth(n2), b = pairwise_depth(n - n2);
+  return (a < 0 || a != b) ? -1 : a + 1;
+}
+
+int pairwise_perfect_depth(int64_t n) {
+  static std::mutex mu;
+  static std::vector<std::pair<int64_t, int>> memo;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : memo)
+    if (e.first == n) return e.second;
+  const int d = pairwise_depth(n);
+  memo.push_back({n, d});
+  return d;
+}
+
 int64_t pairwise_max_span(int64_t n, int group) {
   static std::mutex mu;
   static std::vector<std::pair<std::pair<int64_t, int>, int64_t>> memo;
@@ -117,7 +139,7 @@ static unsigned long long* g_ff_dbg = nullptr;      // profiling hook (ps_feed_f
 
 extern "C" {
 
-int ps_abi_version(void) { return 1; }
+int ps_abi_version(void) { return PS_ABI_VERSION; }
 const char* ps_last_error(void) { return g_err; }
 uint64_t ps_launch_count(void) { return g_launches.load(); }
 

@@ -239,6 +239,18 @@ PS_DEV void st_global_v8(void* p, const uint32_t (&w)[8]) {
                "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
                : "memory");
 }
+// 32-byte read-only global load (LDG.256, sm_100): p 32-byte aligned, data read once (no L1 allocation)
+PS_DEV void ld_global_nc_v8(const void* p, uint32_t (&w)[8]) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+               : "l"(p));
+}
+// tanh(x) = 1 - 2 / (exp(2x) + 1) with the MUFU exp2 / reciprocal: absolute error ~1e-7 (fp32
+// rounding near 0), saturates to +-1 without NaNs (exp overflow -> 1, underflow -> -1)
+PS_DEV float tanh_exp(float x) {
+  const float e = exp2f(2.8853900817779268f * x);  // 2 / ln 2
+  return 1.f - __fdividef(2.f, e + 1.f);
+}
 PS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 PS_DEV void reg_fence32(uint32_t (&r)[32]) {
 #pragma unroll

@@ -173,10 +173,10 @@ __global__ void __launch_bounds__(256) blend_pm_kernel(const float* __restrict__
         const __nv_bfloat162 h01 = *reinterpret_cast<const __nv_bfloat162*>(&hv[u].x);
         const __nv_bfloat162 h23 = *reinterpret_cast<const __nv_bfloat162*>(&hv[u].y);
         float4 o;
-        o.x = (1.f - r) * x[u].x + r * tanhf(__low2float(h01));
-        o.y = (1.f - r) * x[u].y + r * tanhf(__high2float(h01));
-        o.z = (1.f - r) * x[u].z + r * tanhf(__low2float(h23));
-        o.w = (1.f - r) * x[u].w + r * tanhf(__high2float(h23));
+        o.x = (1.f - r) * x[u].x + r * tanh_exp(__low2float(h01));
+        o.y = (1.f - r) * x[u].y + r * tanh_exp(__high2float(h01));
+        o.z = (1.f - r) * x[u].z + r * tanh_exp(__low2float(h23));
+        o.w = (1.f - r) * x[u].w + r * tanh_exp(__high2float(h23));
         reinterpret_cast<float4*>(out)[off4 + i] = o;
       }
     }
@@ -330,13 +330,142 @@ __global__ void __launch_bounds__(256) blend_reassemble_kernel(const float* __re
         const __nv_bfloat162 h01 = *reinterpret_cast<const __nv_bfloat162*>(&hv[u].x);
         const __nv_bfloat162 h23 = *reinterpret_cast<const __nv_bfloat162*>(&hv[u].y);
         float4 o;
-        o.x = (1.f - rate) * x[u].x + rate * tanhf(__low2float(h01));
-        o.y = (1.f - rate) * x[u].y + rate * tanhf(__high2float(h01));
-        o.z = (1.f - rate) * x[u].z + rate * tanhf(__low2float(h23));
-        o.w = (1.f - rate) * x[u].w + rate * tanhf(__high2float(h23));
+        o.x = (1.f - rate) * x[u].x + rate * tanh_exp(__low2float(h01));
+        o.y = (1.f - rate) * x[u].y + rate * tanh_exp(__high2float(h01));
+        o.z = (1.f - rate) * x[u].z + rate * tanh_exp(__low2float(h23));
+        o.w = (1.f - rate) * x[u].w + rate * tanh_exp(__high2float(h23));
         *reinterpret_cast<float4*>(img + io[u]) = o;
       }
   }
+}
+
+
+// Step ends v2 (patch-major, one thread = 8 pixels of one patch row): the CTA owns
+// (patch, CPB channels); thread vector j of a channel covers patch row y = j / (PS/8), pixels
+// x = 8 (j % (PS/8)) .. +8, i.e. one 32-byte image read (two 16-byte halves of the same
+// 128-byte image row segment the neighbouring lanes read) and one 16-byte bf16 CSP write that
+// is contiguous with its lanes' -- no per-element division (PS is a template power of two), the
+// request is resolved once per CTA, every CTA has work, and each thread keeps U independent
+// 32-byte loads in flight.  `nonfinite` (optional): set to 1 when an input latent is not finite
+// (kernels.py:20-24 rejects those; the pipeline raises after the step).
+constexpr int SE_THREADS = 256;
+constexpr int SE_UNR = 4;
+
+template <int PS>
+__global__ void __launch_bounds__(SE_THREADS) split_bias_v2_kernel(const uint64_t* __restrict__ img_ptrs,
+                                                                   const int32_t* __restrict__ req_off,
+                                                                   const int32_t* __restrict__ sides, int n_req,
+                                                                   int C, int cpb, const float* __restrict__ prompts,
+                                                                   float* __restrict__ patches,
+                                                                   __nv_bfloat16* __restrict__ h,
+                                                                   int* __restrict__ nonfinite) {
+  constexpr int VPR = PS / 8;           // vectors per patch row
+  constexpr int VPC = PS * VPR;         // vectors per channel
+  pdl_wait();
+  const int p = blockIdx.x, c0 = blockIdx.y * cpb;
+  int req, side, k;
+  pm_locate(p, req_off, sides, n_req, req, side, k);
+  const int r = k / side, cc = k - r * side, L = side * PS;
+  const float* img = reinterpret_cast<const float*>(img_ptrs[req]) + (int64_t)r * PS * L + cc * PS;
+  const float* pb = prompts + (int64_t)req * C;
+  const int n = min(cpb, C - c0) * VPC;
+  const int64_t out0 = ((int64_t)p * C + c0) * PS * PS;
+  bool bad = false;
+  for (int base = threadIdx.x; base < n; base += SE_THREADS * SE_UNR) {
+    uint32_t v[SE_UNR][8];
+#pragma unroll
+    for (int u = 0; u < SE_UNR; ++u) {
+      const int j = base + u * SE_THREADS;
+      if (j < n) {
+        const int c = j / VPC, jj = j % VPC, y = jj / VPR, x = (jj % VPR) * 8;
+        ld_global_nc_v8(img + ((int64_t)(c0 + c) * L + y) * L + x, v[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < SE_UNR; ++u) {
+      const int j = base + u * SE_THREADS;
+      if (j < n) {
+        const float b = __ldg(pb + c0 + j / VPC);
+        float f[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          f[e] = __uint_as_float(v[u][e]);
+          bad |= !isfinite(f[e]);
+        }
+        if (patches != nullptr) st_global_v8(patches + out0 + (int64_t)j * 8, v[u]);
+        uint4 o;
+        o.x = pack_bf16(f[0] + b, f[1] + b);
+        o.y = pack_bf16(f[2] + b, f[3] + b);
+        o.z = pack_bf16(f[4] + b, f[5] + b);
+        o.w = pack_bf16(f[6] + b, f[7] + b);
+        *reinterpret_cast<uint4*>(h + out0 + (int64_t)j * 8) = o;
+      }
+    }
+  }
+  if (nonfinite != nullptr && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
+}
+
+template <int PS>
+__global__ void __launch_bounds__(SE_THREADS) blend_reassemble_v2_kernel(const float* __restrict__ lat,
+                                                                         const __nv_bfloat16* __restrict__ hh,
+                                                                         const float* __restrict__ rates,
+                                                                         const uint64_t* __restrict__ img_ptrs,
+                                                                         const int32_t* __restrict__ req_off,
+                                                                         const int32_t* __restrict__ sides, int n_req,
+                                                                         int C, int cpb,
+                                                                         const uint64_t* __restrict__ src_ptrs) {
+  constexpr int VPR = PS / 8;
+  constexpr int VPC = PS * VPR;
+  pdl_wait();
+  const int p = blockIdx.x, c0 = blockIdx.y * cpb;
+  int req, side, k;
+  pm_locate(p, req_off, sides, n_req, req, side, k);
+  const int r = k / side, cc = k - r * side, L = side * PS;
+  const int64_t img0 = (int64_t)r * PS * L + cc * PS;
+  float* dst = reinterpret_cast<float*>(img_ptrs[req]) + img0;
+  const float* src = src_ptrs ? reinterpret_cast<const float*>(src_ptrs[req]) + img0 : nullptr;
+  const float rate = __ldg(rates + req);
+  const int n = min(cpb, C - c0) * VPC;
+  const int64_t csp0 = ((int64_t)p * C + c0) * PS * PS;
+  for (int base = threadIdx.x; base < n; base += SE_THREADS * SE_UNR) {
+    uint32_t x[SE_UNR][8];
+    uint4 hv[SE_UNR];
+    int64_t io[SE_UNR];
+#pragma unroll
+    for (int u = 0; u < SE_UNR; ++u) {
+      const int j = base + u * SE_THREADS;
+      if (j < n) {
+        const int c = j / VPC, jj = j % VPC, y = jj / VPR, xo = (jj % VPR) * 8;
+        io[u] = ((int64_t)(c0 + c) * L + y) * L + xo;
+        ld_global_nc_v8(src ? src + io[u] : lat + csp0 + (int64_t)j * 8, x[u]);
+        hv[u] = __ldg(reinterpret_cast<const uint4*>(hh + csp0 + (int64_t)j * 8));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < SE_UNR; ++u) {
+      const int j = base + u * SE_THREADS;
+      if (j < n) {
+        const uint32_t hw4[4] = {hv[u].x, hv[u].y, hv[u].z, hv[u].w};
+        uint32_t o[8];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const __nv_bfloat162 h2 = *reinterpret_cast<const __nv_bfloat162*>(&hw4[e]);
+          o[2 * e] = __float_as_uint((1.f - rate) * __uint_as_float(x[u][2 * e]) + rate * tanh_exp(__low2float(h2)));
+          o[2 * e + 1] =
+              __float_as_uint((1.f - rate) * __uint_as_float(x[u][2 * e + 1]) + rate * tanh_exp(__high2float(h2)));
+        }
+        st_global_v8(dst + io[u], o);
+      }
+    }
+  }
+}
+
+// channels per CTA of the v2 step ends: ~8 KB of bf16 CSP output per CTA round
+static inline int se_cpb(int C, int ps) {
+  int cpb = (SE_THREADS * SE_UNR * 8) / (ps * ps);
+  if (cpb < 1) cpb = 1;
+  if (cpb > C) cpb = C;
+  return cpb;
 }
 
 
@@ -443,10 +572,10 @@ __global__ void blend_kernel(const float* __restrict__ lat, const __nv_bfloat16*
     const __nv_bfloat162 h01 = *reinterpret_cast<const __nv_bfloat162*>(&hv.x);
     const __nv_bfloat162 h23 = *reinterpret_cast<const __nv_bfloat162*>(&hv.y);
     float4 o;
-    o.x = (1.f - r) * x.x + r * tanhf(__low2float(h01));
-    o.y = (1.f - r) * x.y + r * tanhf(__high2float(h01));
-    o.z = (1.f - r) * x.z + r * tanhf(__low2float(h23));
-    o.w = (1.f - r) * x.w + r * tanhf(__high2float(h23));
+    o.x = (1.f - r) * x.x + r * tanh_exp(__low2float(h01));
+    o.y = (1.f - r) * x.y + r * tanh_exp(__high2float(h01));
+    o.z = (1.f - r) * x.z + r * tanh_exp(__low2float(h23));
+    o.w = (1.f - r) * x.w + r * tanh_exp(__high2float(h23));
     reinterpret_cast<float4*>(out)[i] = o;
   }
 }
@@ -464,13 +593,30 @@ using namespace ps;
 extern "C" {
 
 int ps_csp_split_bias(void* stream, const uint64_t* src_ptrs, const int32_t* request_offset, const int32_t* sides,
-                      int n_req, int C, int ps_, float* dst, int n_patches, const float* prompts, void* h) {
+                      int n_req, int C, int ps_, float* dst, int n_patches, const float* prompts, void* h,
+                      int* nonfinite) {
   if (n_req < 1 || C < 1 || ps_ < 1 || ps_ % 4) return set_error(PS_ERR_INPUT, "csp_split_bias: bad sizes");
   if (n_patches == 0) return PS_OK;
   if (n_patches > 65535) return set_error(PS_ERR_INPUT, "csp_split_bias: too many patches");
-  const int cpb = pm_cpb(C, ps_, 4);
-  launch_pdl(csp_split_bias_rows_kernel, dim3(n_patches, (C + cpb - 1) / cpb), dim3(256), 0, (cudaStream_t)stream,
-             src_ptrs, request_offset, sides, n_req, C, ps_, cpb, prompts, dst, (__nv_bfloat16*)h);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (ps_ == 16 || ps_ == 32 || ps_ == 64) {
+    const int cpb = se_cpb(C, ps_);
+    const dim3 grid(n_patches, (C + cpb - 1) / cpb);
+    if (ps_ == 16)
+      launch_pdl(split_bias_v2_kernel<16>, grid, dim3(SE_THREADS), 0, st, src_ptrs, request_offset, sides, n_req, C,
+                 cpb, prompts, dst, (__nv_bfloat16*)h, nonfinite);
+    else if (ps_ == 32)
+      launch_pdl(split_bias_v2_kernel<32>, grid, dim3(SE_THREADS), 0, st, src_ptrs, request_offset, sides, n_req, C,
+                 cpb, prompts, dst, (__nv_bfloat16*)h, nonfinite);
+    else
+      launch_pdl(split_bias_v2_kernel<64>, grid, dim3(SE_THREADS), 0, st, src_ptrs, request_offset, sides, n_req, C,
+                 cpb, prompts, dst, (__nv_bfloat16*)h, nonfinite);
+  } else {
+    if (nonfinite != nullptr) return set_error(PS_ERR_INPUT, "csp_split_bias: finiteness flag needs ps in {16,32,64}");
+    const int cpb = pm_cpb(C, ps_, 4);
+    launch_pdl(csp_split_bias_rows_kernel, dim3(n_patches, (C + cpb - 1) / cpb), dim3(256), 0, st, src_ptrs,
+               request_offset, sides, n_req, C, ps_, cpb, prompts, dst, (__nv_bfloat16*)h);
+  }
   count_launch();
   return check_launch("csp_split_bias");
 }
@@ -482,10 +628,25 @@ int ps_blend_reassemble(void* stream, const float* latent, const void* h, const 
   if (latent == nullptr && src_ptrs == nullptr) return set_error(PS_ERR_INPUT, "blend_reassemble: no latent source");
   if (n_patches == 0) return PS_OK;
   if (n_patches > 65535) return set_error(PS_ERR_INPUT, "blend_reassemble: too many patches");
-  const int cpb = pm_cpb(C, ps_, 4);
-  // (a row-wise variant -- one CTA per image row band -- measured 103 vs 95 us and was removed)
-  launch_pdl(blend_reassemble_kernel, dim3(n_patches, (C + cpb - 1) / cpb), dim3(256), 0, (cudaStream_t)stream,
-             latent, (const __nv_bfloat16*)h, rates, dst_ptrs, request_offset, sides, n_req, C, ps_, cpb, src_ptrs);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (ps_ == 16 || ps_ == 32 || ps_ == 64) {
+    const int cpb = se_cpb(C, ps_);
+    const dim3 grid(n_patches, (C + cpb - 1) / cpb);
+    const __nv_bfloat16* hb = (const __nv_bfloat16*)h;
+    if (ps_ == 16)
+      launch_pdl(blend_reassemble_v2_kernel<16>, grid, dim3(SE_THREADS), 0, st, latent, hb, rates, dst_ptrs,
+                 request_offset, sides, n_req, C, cpb, src_ptrs);
+    else if (ps_ == 32)
+      launch_pdl(blend_reassemble_v2_kernel<32>, grid, dim3(SE_THREADS), 0, st, latent, hb, rates, dst_ptrs,
+                 request_offset, sides, n_req, C, cpb, src_ptrs);
+    else
+      launch_pdl(blend_reassemble_v2_kernel<64>, grid, dim3(SE_THREADS), 0, st, latent, hb, rates, dst_ptrs,
+                 request_offset, sides, n_req, C, cpb, src_ptrs);
+  } else {
+    const int cpb = pm_cpb(C, ps_, 4);
+    launch_pdl(blend_reassemble_kernel, dim3(n_patches, (C + cpb - 1) / cpb), dim3(256), 0, st, latent,
+               (const __nv_bfloat16*)h, rates, dst_ptrs, request_offset, sides, n_req, C, ps_, cpb, src_ptrs);
+  }
   count_launch();
   return check_launch("blend_reassemble");
 }

@@ -83,6 +83,7 @@ int gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c
 int gemm_pick_bn(int n, int k, int epi);
 // widest element span of `group` consecutive leaves of numpy's pairwise tree over n elements
 int64_t pairwise_max_span(int64_t n, int group);
+int pairwise_perfect_depth(int64_t n);
 
 struct AttnParams {
   int T_total;   // tokens in the batch (rows of qk / columns of vt)

@@ -85,6 +85,7 @@ class CachedStepGraph:
         self.rates = None
         self.slots = None
         self.graph = None
+        self._gen = None  # cache.storage_gen the graph was captured against
         self._out = self._counts = None
 
     def _body(self):
@@ -103,7 +104,13 @@ class CachedStepGraph:
         else:
             self.bias.copy_(bias)
             self.rates.copy_(rates)
+            if self.graph is not None and self._gen != self.cache.storage_gen:
+                # the cache slab was re-allocated (grown by another batch, or restored): the graph's
+                # baked pointers are stale -- capture again against the current storage
+                self.graph = None
             if self.graph is None:
+                self.slots = self.cache.slots_for(self.keys, allocate=True)
+                self._gen = self.cache.storage_gen
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g):
                     self._out, self._counts = self._body()

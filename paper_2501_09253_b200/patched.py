@@ -857,7 +857,8 @@ def select_patches(mask: torch.Tensor, a: torch.Tensor, b: torch.Tensor) -> torc
     """out[p] = a[p] if mask[p] else b[p] (bf16 patch arrays)."""
     out = torch.empty_like(b)
     n = b[0].numel() if b.shape[0] else 0
-    _lib.call("ps_select_patches", stream(), mask.view(torch.uint8).data_ptr(), b.shape[0], n, a.data_ptr(),
+    _lib.call("ps_select_patches", stream(), mask.view(torch.uint8).data_ptr(), b.shape[0], n, _lib.DTYPE_BF16,
+              a.data_ptr(),
               b.data_ptr(), out.data_ptr())
     return out
 

@@ -28,6 +28,7 @@ import torch
 from . import _lib
 from ._dev import require_cuda
 from .csp import split
+from .errors import InputError
 from .model import ModelConfig, rate_schedule
 from .patched import run_block
 
@@ -62,6 +63,8 @@ class DenoisePipeline:
         self.ev_h2d = [torch.cuda.Event() for _ in range(n_sets)]
         self.ev_comp = [torch.cuda.Event() for _ in range(n_sets)]
         self.ev_d2h = [torch.cuda.Event() for _ in range(n_sets)]
+        # set by the split kernel when an input latent is not finite (kernels.py:20-24)
+        self.nonfinite = torch.zeros(1, dtype=torch.int32, device=self.dev)
 
     # ------------------------------------------------------------ step body
     def _step(self, k: int) -> None:
@@ -73,7 +76,7 @@ class DenoisePipeline:
         # (no fp32 CSP copy: the blend reads x back from the input images)
         _lib.call("ps_csp_split_bias", st, self._in_ptrs[k].data_ptr(), src_ptrs["request_offset"].data_ptr(),
                   src_ptrs["sides"].data_ptr(), b.n_requests, self.C, self.ps, None, b.n_patches,
-                  self.bias[k].data_ptr(), h.data_ptr())
+                  self.bias[k].data_ptr(), h.data_ptr(), self.nonfinite.data_ptr())
         for ops in self.weights:
             h = run_block(b, h, ops)
         # blend straight into the per-request outputs (model.py:129-131, csp.py:196-214)
@@ -124,14 +127,19 @@ class DenoisePipeline:
             self.bias[k].copy_(self.bias_host[k])
 
     def run(self, host_inputs: Sequence[Sequence[torch.Tensor]], step_idx: Sequence[Sequence[int]],
-            total_steps: Sequence[int], host_outputs: Sequence[Sequence[torch.Tensor]]) -> None:
+            total_steps: Sequence[int], host_outputs: Sequence[Sequence[torch.Tensor]],
+            check_finite: bool = True) -> None:
         """Denoise len(host_inputs) independent steps.
 
         host_inputs[i][r]: pinned (C, L_r, L_r) fp32 latents of request r for step i;
         step_idx[i][r] / total_steps[r]: schedule position (model.py:56-63);
         host_outputs[i][r]: pinned destination of the updated latents.
+        check_finite: after the last step, raise InputError if any input latent was not finite
+        (the split kernel flags it on the device; one 4-byte read-back per call).
         """
         comp = torch.cuda.current_stream()
+        if check_finite:
+            self.nonfinite.zero_()
         n = len(host_inputs)
         # per-step rates for all steps, uploaded once (storage-slot order)
         table = np.zeros((n, len(self.dims)), dtype=np.float32)
@@ -165,6 +173,8 @@ class DenoisePipeline:
                 self.ev_d2h[k].record(self.s_out)
         comp.wait_stream(self.s_out)
         comp.wait_stream(self.s_in)
+        if check_finite and int(self.nonfinite.item()):
+            raise InputError("non-finite values in input latents")
 
     def run_resident(self, n_steps: int) -> None:
         """Replay the step graph on device-resident inputs (no host copies)."""

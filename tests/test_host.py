@@ -38,7 +38,9 @@ def test_library_exports_every_declared_symbol():
     for name in decl:
         assert hasattr(lib, name), name
     assert sorted(L.EXPORTED) == decl
-    assert lib.ps_abi_version() == 1
+    assert lib.ps_abi_version() == L.ABI_VERSION
+    hdr = open(HEADER).read()
+    assert re.search(rf"#define PS_ABI_VERSION {L.ABI_VERSION}\b", hdr)
     out = subprocess.run(["nm", "-D", "--defined-only", L.LIB_PATH], capture_output=True, text=True).stdout
     for name in decl:
         assert re.search(rf"\bT {name}\b", out), name
