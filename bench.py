@@ -246,7 +246,7 @@ def run_ours(args):
         if args.hbm_table:
             line["hbm_kernels"] = measure_hbm_kernels(pipe, _peaks().get("hbm_gbs", 6548.5))
         if args.cpu_baseline and world == 1:
-            line["cpu_baseline"] = cpu_baseline_sample(repeats=1)
+            line["cpu_baseline"] = cpu_baseline_sample()
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -364,6 +364,13 @@ def measure_hbm_kernels(pipe, peak_gbs):
     none = torch.zeros(P, dtype=torch.bool, device="cuda")
     half = torch.arange(P, device="cuda") % 2 == 0
     m = int(half.sum())
+    warm = ps.BlockCache(1, ps.PredictorConfig(0.1, 3), capacity=P)  # first launches load the kernels
+    warm.batched_update(0, keys, none, x, y)
+    ws = warm.slots_for(keys, allocate=False)
+    warm.predict_reuse(0, keys, y, slots=ws)
+    warm.block_substitute(0, ws, half, y)
+    warm.block_finish(0, ws, half, y, x)
+    del warm
     with KernelTimer(["ps_cache_update"], flush_bytes=flush) as kt:
         cache.batched_update(0, keys, none, x, y)
     ins = kt.times_ms()["ps_cache_update"]
@@ -377,7 +384,7 @@ def measure_hbm_kernels(pipe, peak_gbs):
             cache._streak.zero_()
     tc = kt.times_ms()
     rows += [("ps_cache_update (insert, all rows)", 4 * n * 2 * P, float(np.mean(ins)), len(ins)),
-             ("ps_cache_predict (mse_leaf + mse_combine, all live)", 2 * n * 2 * P,
+             ("ps_cache_predict (fp64 pairwise MSE reuse test, all live)", 2 * n * 2 * P,
               float(np.mean(tc["ps_cache_predict"])), len(tc["ps_cache_predict"])),
              ("ps_cache_substitute (50% mask)", 2 * n * 2 * P, float(np.mean(tc["ps_cache_substitute"])),
               len(tc["ps_cache_substitute"])),
@@ -412,46 +419,142 @@ def _profile_traffic():
 # ------------------------------------------------------- CPU reference
 
 
-def cpu_baseline_sample(repeats=1):
-    """The oracle port (numpy fp64, the reference's algorithm) on a bounded sample:
-    one unet_like block at C=320 over one 512 px request (P=4 patches at ps=32),
-    extrapolated linearly to 7 blocks."""
+REF_SRC = os.path.join(ROOT, "oracle", "_ref", "src")
+SAMPLE_DIV = 20  # conv3 / FF output channels timed: 1 in SAMPLE_DIV (their cost is exactly linear in C_out)
+
+
+def _reference_modules():
+    """The reference package staged in oracle/_ref (oracle/make_ref.sh) -> kind "reference";
+    without it, the numpy restatement in oracle/mixref.py -> kind "port"."""
+    if os.path.isdir(os.path.join(REF_SRC, "mixserve")):
+        if REF_SRC not in sys.path:
+            sys.path.insert(0, REF_SRC)
+        from mixserve import csp, kernels, model, patched
+        return "reference", dict(split=csp.split, gn=patched.stitched_group_norm, conv=patched.patched_conv,
+                                 attn=patched.patched_self_attention, cmm=kernels._channel_matmul,
+                                 gelu=kernels.gelu, resid=kernels.residual_add, ModelConfig=model.ModelConfig,
+                                 init_weights=model.init_weights, ConvParams=kernels.ConvParams)
     from oracle import mixref as R
-    cfg = R.ModelConfig(arch="unet_like", channels=C, hidden=HIDDEN, groups=GROUPS, n_blocks=1, seed=0)
-    ops = R.init_weights(cfg)[0]
-    lat = np.random.default_rng([0, 0]).normal(size=(C, 64, 64))
-    b = R.split([("req-0", lat)], patch_size=PATCH)
-    times = []
-    for _ in range(repeats):
-        t0 = time.perf_counter()
-        R.run_block(b, b.data, ops)
-        times.append(time.perf_counter() - t0)
-    t_block = float(np.mean(times))
+    return "port", dict(split=R.split, gn=R.stitched_group_norm, conv=R.patched_conv,
+                        attn=R.patched_self_attention, cmm=R.channel_contract, gelu=R.gelu,
+                        resid=lambda x, y: x + y, ModelConfig=R.ModelConfig, init_weights=R.init_weights,
+                        ConvParams=R.ConvParams)
+
+
+def reference_block_sample(latent: int, M=None, ops=None):
+    """One unet_like block (GN + halos -> conv3 -> attention -> FF -> residual, model.py:81-88)
+    of the SDXL-shaped model (C=320, H=1280, G=32) on ONE request of the given latent side, run by
+    the reference's own functions (patched.py:116-176, kernels.py:99-161) on the host cores, stage by
+    stage.  GroupNorm, halos, attention and the residual run in full; conv3, FF1 and FF2 run the
+    reference's channel-ordered contraction for 1 in SAMPLE_DIV output channels and are scaled by
+    SAMPLE_DIV (their loops over output channels are independent and equal-cost).  Returns
+    {stage: seconds}."""
+    kind, M = M or _reference_modules()
+    if ops is None:
+        ops = M["init_weights"](M["ModelConfig"](arch="unet_like", channels=C, hidden=HIDDEN, groups=GROUPS,
+                                                 n_blocks=1, seed=0))[0]
+    gn, conv, at, ff = (ops[i][1] for i in range(4))
+    lat = np.random.default_rng([0, latent]).normal(size=(C, latent, latent))
+    b = M["split"]([("req", lat)], patch_size=PATCH)
+    x = b.data
+    t = {}
+    t0 = time.perf_counter()
+    cur, frames = M["gn"](b, x, gn, emit_halos=True)
+    t["group_norm+halos"] = time.perf_counter() - t0
+    k = C // SAMPLE_DIV
+    sub = M["ConvParams"](np.asarray(conv.weights)[:k], np.asarray(conv.bias)[:k])
+    t0 = time.perf_counter()
+    y = M["conv"](b, cur, sub, frames=frames)
+    t["conv3"] = (time.perf_counter() - t0) * SAMPLE_DIV
+    cur = np.concatenate([y] * SAMPLE_DIV, axis=1)  # full-width input for the next stage
+    t0 = time.perf_counter()
+    cur = M["attn"](b, cur, at)
+    t["attention"] = time.perf_counter() - t0
+    kh = HIDDEN // SAMPLE_DIV
+    t0 = time.perf_counter()
+    h = M["cmm"](np.asarray(ff.w1)[:kh], np.asarray(ff.b1)[:kh], cur)
+    t["ff1"] = (time.perf_counter() - t0) * SAMPLE_DIV
+    hfull = np.concatenate([h] * SAMPLE_DIV, axis=1)
+    t0 = time.perf_counter()
+    hfull = M["gelu"](hfull)
+    t["gelu"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    o = M["cmm"](np.asarray(ff.w2)[:k], np.asarray(ff.b2)[:k], hfull)
+    t["ff2"] = (time.perf_counter() - t0) * SAMPLE_DIV
+    o = np.concatenate([o] * SAMPLE_DIV, axis=1)
+    t0 = time.perf_counter()
+    M["resid"](o, x)
+    t["residual"] = time.perf_counter() - t0
+    return t
+
+
+def cpu_baseline_sample(n_samples=3):
+    """The reference CPU path on the box's host cores (rank 0, N=1): n_samples blocks, one request
+    per sample cycling 512 / 768 / 1024 px (one request per resolution: P = 4 + 9 + 16 = 29), per-
+    stage times, extrapolated linearly to the config-2 step (4 requests per resolution x 7 blocks:
+    every stage's cost is per image)."""
+    kind, M = _reference_modules()
+    ops = M["init_weights"](M["ModelConfig"](arch="unet_like", channels=C, hidden=HIDDEN, groups=GROUPS,
+                                             n_blocks=1, seed=0))[0]
+    lats = sorted(set(DIMS))
+    per = {d: [] for d in lats}
+    for i in range(max(n_samples, len(lats))):
+        d = lats[i % len(lats)]
+        per[d].append(reference_block_sample(d, (kind, M), ops))
+    stages = {d: {k: float(np.mean([r[k] for r in v])) for k in v[0]} for d, v in per.items()}
+    block = {d: sum(st.values()) for d, st in stages.items()}
+    step_s = BLOCKS * sum(DIMS.count(d) * block[d] for d in lats)
+    P = sum((d // PATCH) ** 2 for d in DIMS)
     cores = len(os.sched_getaffinity(0))
-    return {"value": b.n_patches / (t_block * BLOCKS), "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"1 unet_like block (C=320) on 1x512px request (P=4), {t_block:.2f} s/block, extrapolated to "
-                      f"7 blocks; numpy fp64 with OPENBLAS_NUM_THREADS={os.environ.get('OPENBLAS_NUM_THREADS', 'default')}"
-                      f" (BLAS threads only in the attention matmuls)"}
+    return {"value": P / step_s, "unit": UNIT, "cores": cores, "kind": kind,
+            "ms_per_step_extrapolated": 1000.0 * step_s,
+            "per_stage_s": {f"{d * 8}px": st for d, st in stages.items()},
+            "block_s": {f"{d * 8}px": block[d] for d in lats},
+            "openblas_threads": os.environ.get("OPENBLAS_NUM_THREADS", f"default ({cores})"),
+            "sample": (f"reference unet_like block (C=320) on one request per resolution (512/768/1024 px, P=29) "
+                       f"by the {'reference package (oracle/_ref)' if kind == 'reference' else 'numpy port'}; "
+                       f"conv3/FF timed on 1/{SAMPLE_DIV} of the output channels x{SAMPLE_DIV}; extrapolated to the "
+                       f"config-2 step: 7 blocks x 4 requests per resolution (P=116). numpy fp64; BLAS threads only "
+                       f"in the attention matmuls")}
 
 
 def run_reference(args):
     rank, world, _ = _env_rank()
     if rank != 0:
         return
-    for _ in range(args.warmup):
-        pass  # the numpy port has no warm-up state; warm-up steps are not repeated to bound run time
-    vals = []
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        vals.append(cpu_baseline_sample(repeats=1))
-    wall = time.perf_counter() - t0
-    v = float(np.mean([x["value"] for x in vals]))
-    cb = dict(vals[0], value=v)
+    kind, M = _reference_modules()
+    ops = M["init_weights"](M["ModelConfig"](arch="unet_like", channels=C, hidden=HIDDEN, groups=GROUPS,
+                                             n_blocks=1, seed=0))[0]
+    lats = sorted(set(DIMS))
+    for i in range(min(args.warmup, 1)):  # one warm-up sample (imports, BLAS thread pool)
+        reference_block_sample(lats[0], (kind, M), ops)
+    per = {d: [] for d in lats}
+    wall = []
+    for i in range(max(args.steps, len(lats))):  # each step: one block on one request, cycling resolutions
+        d = lats[i % len(lats)]
+        t0 = time.perf_counter()
+        per[d].append(reference_block_sample(d, (kind, M), ops))
+        wall.append(time.perf_counter() - t0)
+    stages = {d: {k: float(np.mean([r[k] for r in v])) for k in v[0]} for d, v in per.items()}
+    block = {d: sum(st.values()) for d, st in stages.items()}
+    step_s = BLOCKS * sum(DIMS.count(d) * block[d] for d in lats)
+    P = sum((d // PATCH) ** 2 for d in DIMS)
+    v = P / step_s
+    cores = len(os.sched_getaffinity(0))
+    cb = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+          "per_stage_s": {f"{d * 8}px": st for d, st in stages.items()},
+          "block_s": {f"{d * 8}px": block[d] for d in lats},
+          "openblas_threads": os.environ.get("OPENBLAS_NUM_THREADS", f"default ({cores})"),
+          "sample": (f"each step = one unet_like block (C=320) on one request, cycling 512/768/1024 px (P=29 per "
+                     f"cycle), by the {'reference package (oracle/_ref)' if kind == 'reference' else 'numpy port'}; "
+                     f"conv3/FF on 1/{SAMPLE_DIV} of the output channels x{SAMPLE_DIV}; value and ms_per_step are "
+                     f"the extrapolated config-2 step (7 blocks x 4 requests per resolution, P=116)")}
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1000.0 * wall / max(1, args.steps), "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * step_s, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": dict(WORKLOAD, sample=cb["sample"]),
+        "sample_wall_s_per_step": float(np.mean(wall)),
         "cpu_baseline": cb,
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)

@@ -7,10 +7,19 @@ over the same axes, 256-row attention chunks) so the golden vectors recorded
 from the reference compare bit-exactly where the reference is deterministic.
 
 Only tests, `__graft_entry__.smoke()` and bench.py's CPU legs use this module.
+
+BLAS mode (`blas_contractions()` / `DENSE_BLAS`): the channel contractions (linear, FF, 1x1
+and 3x3 conv) run as fp64 matrix products instead of the reference's channel-ordered axpy
+loops.  Same fp64 arithmetic, different summation order: results differ from the reference
+by fp64 rounding only (~1e-15 relative; tests/test_oracle_golden.py checks the mode against
+the golden vectors at 1e-10).  It makes the C = 320 parity checks at the benchmark's shapes
+(tests/test_gpu_parity_c320.py) run in seconds instead of minutes; bit-exact comparisons
+(masks, copies) never depend on it.
 """
 
 from __future__ import annotations
 
+import contextlib
 import math
 import zlib
 from dataclasses import dataclass, field, replace
@@ -232,9 +241,26 @@ def _f64(x):
     return a
 
 
+DENSE_BLAS = False
+
+
+@contextlib.contextmanager
+def blas_contractions():
+    """Evaluate the channel contractions as fp64 BLAS products inside the block."""
+    global DENSE_BLAS
+    prev, DENSE_BLAS = DENSE_BLAS, True
+    try:
+        yield
+    finally:
+        DENSE_BLAS = prev
+
+
 def channel_contract(w, b, x):
     """kernels.py:99-111 — per output channel, accumulate input channels in order."""
     w, b, x = _f64(w), _f64(b), _f64(x)
+    if DENSE_BLAS:
+        xm = np.moveaxis(x, 1, -1)  # (N, ..., C_in)
+        return np.moveaxis(xm @ w.T + b, -1, 1)
     out = np.empty((x.shape[0], w.shape[0]) + x.shape[2:])
     for o in range(w.shape[0]):
         acc = np.full(x.shape[:1] + x.shape[2:], b[o])
@@ -266,6 +292,18 @@ def conv_valid(xpad, w, b):
     n, _, hp, wp = xpad.shape
     k = w.shape[2]
     h, wd = hp - k + 1, wp - k + 1
+    if DENSE_BLAS:
+        # im2col per chunk of patches: (N, C*k*k, h*w) columns, one (C_out, C*k*k) product
+        out = np.empty((n, w.shape[0], h, wd))
+        wm = w.reshape(w.shape[0], -1)
+        for n0 in range(0, n, 8):
+            xs = xpad[n0:n0 + 8]
+            cols = np.empty((xs.shape[0], xs.shape[1], k, k, h, wd))
+            for ki in range(k):
+                for kj in range(k):
+                    cols[:, :, ki, kj] = xs[:, :, ki:ki + h, kj:kj + wd]
+            out[n0:n0 + 8] = (wm @ cols.reshape(xs.shape[0], -1, h * wd)).reshape(xs.shape[0], -1, h, wd)
+        return out + b[None, :, None, None]
     out = np.empty((n, w.shape[0], h, wd))
     for o in range(w.shape[0]):
         acc = np.full((n, h, wd), b[o])
@@ -463,11 +501,21 @@ def patched_self_attention(batch, data, p: AttentionParams):
     return out
 
 
+# precision-emulation hook (tools/drift_emulation.py only): when set, applied to every stage's
+# output inside run_block (e.g. bf16 rounding of the intra-block activations); None = exact
+STAGE_ROUND = None
+
+
 def run_block(batch, x, ops):
     """patched.py:179-221 — stage interpreter; GN followed by conv k3 emits halos."""
     x = _f64(x)
     cur, frames = x, None
+    rnd = STAGE_ROUND
     for i, (kind, prm) in enumerate(ops):
+        if rnd is not None and i > 0:
+            cur = rnd(cur)
+            if frames is not None:
+                frames = rnd(frames)
         nxt = ops[i + 1] if i + 1 < len(ops) else None
         if kind == "group_norm":
             if nxt is not None and nxt[0] == "conv" and nxt[1].kernel_size == 3:

@@ -36,8 +36,25 @@ def to_device(x, dtype=None) -> torch.Tensor:
     return t.contiguous()
 
 
+# Input validation of the public eager API (kernels.py:20-24 rejects non-finite inputs with
+# InputError).  Internal drivers whose inputs were validated once at their own entry
+# (engine_step.numeric_step, pipeline.DenoisePipeline -- its split kernel flags non-finite
+# latents on the device -- and CachedStepGraph) run inside `trusted_inputs()`, so their blocks
+# neither synchronise nor break stream capture; checks are also skipped while capturing.
+_TRUSTED = [0]
+
+
+class trusted_inputs:
+    def __enter__(self):
+        _TRUSTED[0] += 1
+
+    def __exit__(self, *exc):
+        _TRUSTED[0] -= 1
+
+
 def check_finite(t: torch.Tensor) -> None:
-    # kernels.py:20-24 rejects non-finite inputs
+    if _TRUSTED[0] or not t.is_floating_point() or torch.cuda.is_current_stream_capturing():
+        return
     if not bool(torch.isfinite(t).all()):
         raise InputError("non-finite values in input")
 

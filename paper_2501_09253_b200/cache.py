@@ -413,28 +413,43 @@ class BlockCache:
                   self._snap_out[block_id].data_ptr(), self._ctr[block_id, 2:].data_ptr())
 
     # ------------------------------------------------------ atomic steps
-    def snapshot(self) -> dict:
-        """Deep copy of the device store for step rollback (cache.py:185-187)."""
-        if self._exists is None:
-            return {"empty": True, "slots": dict(self._slot_of), "free": list(self._free), "cap": self._cap}
-        return {"slots": dict(self._slot_of), "free": list(self._free), "cap": self._cap,
-                "exists": self._exists.clone(), "streak": self._streak.clone(),
-                "in": [t.clone() for t in self._snap_in], "out": [t.clone() for t in self._snap_out]}
+    def snapshot(self) -> "CacheSnapshot":
+        """Copy of the device store for step rollback (cache.py:185-187): a list with one
+        element per block, like the reference's list of per-block dicts (a slice of it is no
+        longer a valid snapshot, cache.py:189-190)."""
+        snap = CacheSnapshot({"block": b} for b in range(self._n_blocks))
+        snap.slots, snap.free, snap.cap = dict(self._slot_of), list(self._free), self._cap
+        if self._exists is not None:
+            snap.exists, snap.streak = self._exists.clone(), self._streak.clone()
+            snap.snap_in = [t.clone() for t in self._snap_in]
+            snap.snap_out = [t.clone() for t in self._snap_out]
+        return snap
 
-    def restore(self, snap: dict) -> None:
+    def restore(self, snap: "CacheSnapshot") -> None:
         """cache.py:189-192."""
-        if not isinstance(snap, dict) or "slots" not in snap:
+        if not isinstance(snap, CacheSnapshot) or len(snap) != self._n_blocks:
             raise IntegrityError("snapshot block count mismatch")
-        if snap.get("empty"):
-            self._slot_of, self._free = dict(snap["slots"]), list(snap["free"])
+        self._slot_of, self._free = dict(snap.slots), list(snap.free)
+        if snap.exists is None:
             if self._exists is not None:
                 self._exists.zero_()
+                self._streak.zero_()
             self.storage_gen += 1
             return
-        if len(snap["in"]) != self._n_blocks:
-            raise IntegrityError("snapshot block count mismatch")
-        self._slot_of, self._free, self._cap = dict(snap["slots"]), list(snap["free"]), snap["cap"]
-        self._exists, self._streak = snap["exists"].clone(), snap["streak"].clone()
-        self._snap_in = [t.clone() for t in snap["in"]]
-        self._snap_out = [t.clone() for t in snap["out"]]
+        self._cap = snap.cap
+        self._exists, self._streak = snap.exists.clone(), snap.streak.clone()
+        self._snap_in = [t.clone() for t in snap.snap_in]
+        self._snap_out = [t.clone() for t in snap.snap_out]
         self.storage_gen += 1
+
+
+class CacheSnapshot(list):
+    """BlockCache.snapshot(): one element per block; the device copies ride along."""
+
+    slots: dict = {}
+    free: list = []
+    cap: int = 0
+    exists = None
+    streak = None
+    snap_in: list = []
+    snap_out: list = []

@@ -174,7 +174,8 @@ def split(requests: Sequence, patch_size: int | None = None) -> CSPBatch:
     """Cut (request_id, latent) pairs into a CSP batch (csp.py:117-193).
 
     Latents are (C, H, H) CUDA tensors (numpy / CPU tensors are copied to the
-    device first); the patch array keeps their dtype (float32 or bfloat16).
+    device first); the patch array keeps their dtype (float32, bfloat16 or float64 -- numpy
+    float64 latents stay exact, as csp.py:167 copies them).
     """
     if not requests:
         raise InputError("empty batch")
@@ -184,7 +185,7 @@ def split(requests: Sequence, patch_size: int | None = None) -> CSPBatch:
     lats = []
     for rid, lat in requests:
         t = to_device(lat)
-        if t.dtype not in (torch.float32, torch.bfloat16):
+        if t.dtype not in (torch.float32, torch.bfloat16, torch.float64):
             t = t.to(torch.float32)
         if t.dim() != 3 or t.shape[1] != t.shape[2]:
             raise InputError(f"latent for {rid!r} must be (C,H,H), got {tuple(t.shape)}")
@@ -194,8 +195,8 @@ def split(requests: Sequence, patch_size: int | None = None) -> CSPBatch:
         raise InputError("all latents in a batch must share a channel count")
     dtype = lats[0].dtype
     if any(t.dtype != dtype for t in lats):
-        lats = [t.to(torch.float32) for t in lats]
-        dtype = torch.float32
+        dtype = torch.float64 if any(t.dtype == torch.float64 for t in lats) else torch.float32
+        lats = [t.to(dtype) for t in lats]
     dims = [int(t.shape[1]) for t in lats]
     ps = choose_patch_size(dims) if patch_size is None else int(patch_size)
     if any(d % ps for d in dims):
@@ -221,6 +222,8 @@ def _dtype_code(dt) -> int:
         return _lib.DTYPE_F32
     if dt == torch.bfloat16:
         return _lib.DTYPE_BF16
+    if dt == torch.float64:
+        return _lib.DTYPE_F64
     raise InputError(f"unsupported dtype {dt}")
 
 
@@ -229,7 +232,7 @@ def reassemble(batch: CSPBatch, data=None) -> dict:
     src = batch.data if data is None else to_device(data)
     if tuple(src.shape) != tuple(batch.data.shape):
         raise InputError(f"data shape {tuple(src.shape)} does not match batch {tuple(batch.data.shape)}")
-    if src.dtype not in (torch.float32, torch.bfloat16):
+    if src.dtype not in (torch.float32, torch.bfloat16, torch.float64):
         src = src.to(torch.float32)
     src = src.contiguous()
     c, ps = src.shape[1], batch.patch_size

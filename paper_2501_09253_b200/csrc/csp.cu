@@ -486,6 +486,14 @@ static int csp_copy(cudaStream_t st, const uint64_t* ptrs, const int32_t* off, c
     const int cpb = pm_cpb(C, ps, 4);
     csp_copy_pm_kernel<float, TO_PATCHES><<<dim3(P, (C + cpb - 1) / cpb), th, 0, st>>>(ptrs, off, sides, n_req, C,
                                                                                     ps, cpb, (float*)patches);
+  } else if (dtype == PS_DTYPE_F64 && ps % 2 == 0 && P <= 65535) {
+    // fp64 patches (the numpy-interface drop-in keeps the reference's float64 pixels exact)
+    const int cpb = pm_cpb(C, ps, 8);
+    csp_copy_pm_kernel<double, TO_PATCHES><<<dim3(P, (C + cpb - 1) / cpb), th, 0, st>>>(ptrs, off, sides, n_req, C,
+                                                                                     ps, cpb, (double*)patches);
+  } else if (dtype == PS_DTYPE_F64) {
+    csp_copy_kernel<double, 1, TO_PATCHES><<<grid_for(elems, th), th, 0, st>>>(ptrs, off, sides, n_req, C, ps,
+                                                                            (double*)patches, elems);
   } else if (dtype == PS_DTYPE_BF16 && ps % 8 == 0 && P <= 65535) {
     const int cpb = pm_cpb(C, ps, 2);
     csp_copy_pm_kernel<__nv_bfloat16, TO_PATCHES><<<dim3(P, (C + cpb - 1) / cpb), th, 0, st>>>(
@@ -672,6 +680,9 @@ int ps_halo_frames_nchw(void* stream, const void* src, int dtype, const int32_t*
   if (dtype == PS_DTYPE_F32)
     halo_nchw_kernel<float><<<grid_for(total, 256), 256, 0, st>>>((const float*)src, neighbors, P, C, ps_,
                                                                   (float*)dst);
+  else if (dtype == PS_DTYPE_F64)
+    halo_nchw_kernel<double><<<grid_for(total, 256), 256, 0, st>>>((const double*)src, neighbors, P, C, ps_,
+                                                                    (double*)dst);
   else if (dtype == PS_DTYPE_BF16)
     halo_nchw_kernel<__nv_bfloat16><<<grid_for(total, 256), 256, 0, st>>>((const __nv_bfloat16*)src, neighbors, P, C,
                                                                           ps_, (__nv_bfloat16*)dst);

@@ -34,6 +34,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from ._dev import check_finite, trusted_inputs
 from .cache import BlockCache
 from .csp import CSPBatch
 from .model import blend_batch, prompt_bias
@@ -90,8 +91,10 @@ class CachedStepGraph:
 
     def _body(self):
         self.batch.data = self.lat
-        h = prompt_bias(self.batch, self.lat, self.bias)
-        return _device_blocks(self.batch, self.weights, self.cache, self.keys, self.slots, self.lat, h, self.rates)
+        with trusted_inputs():
+            h = prompt_bias(self.batch, self.lat, self.bias)
+            return _device_blocks(self.batch, self.weights, self.cache, self.keys, self.slots, self.lat, h,
+                                  self.rates)
 
     def run(self, lat: torch.Tensor, bias: torch.Tensor, rates: torch.Tensor):
         """One step; returns (new latents [static buffer], StepStats)."""
@@ -133,6 +136,12 @@ class StepStats:
 def numeric_step(batch: CSPBatch, weights, cache: BlockCache | None, bias: torch.Tensor, rates: torch.Tensor,
                  keys=None, slots: torch.Tensor | None = None, compact: bool = True):
     """Denoise one step of `batch` (fp32 latents in batch.data); returns (new latents, StepStats)."""
+    check_finite(batch.data)  # once per step (kernels.py:20-24); the blocks run trusted
+    with trusted_inputs():
+        return _numeric_step(batch, weights, cache, bias, rates, keys, slots, compact)
+
+
+def _numeric_step(batch, weights, cache, bias, rates, keys, slots, compact):
     P = batch.n_patches
     lat = batch.data if batch.data.dtype == torch.float32 else batch.data.float()
     h = prompt_bias(batch, lat.contiguous(), bias)

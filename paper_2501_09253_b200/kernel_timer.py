@@ -2,9 +2,10 @@
 
 `KernelTimer(names, flush_bytes)` installed as `_lib.TIMER` brackets every call of the
 named C entry points with CUDA events on the current stream.  With `flush_bytes` > 0 it
-first overwrites a buffer that large (bigger than the 126 MB L2) so each timed launch
-starts cold, the way the kernel's inputs arrive in a real step once the previous stage's
-output no longer fits L2; the flush is outside the event pair.
+first READS a buffer that large (bigger than the 126 MB L2; a read leaves no dirty lines to
+write back inside the timed launch) so each timed launch starts cold, the way the kernel's
+inputs arrive in a real step once the previous stage's output no longer fits L2; the flush is
+outside the event pair.
 """
 
 from __future__ import annotations
@@ -21,15 +22,16 @@ class KernelTimer:
         self.names = set(names)
         self.events = defaultdict(list)
         self._open = {}
-        self._flush = (torch.empty(flush_bytes // 4, dtype=torch.float32, device="cuda")
+        self._flush = (torch.ones(flush_bytes // 4, dtype=torch.float32, device="cuda")
                        if flush_bytes else None)
+        self._sink = None
 
     def wants(self, name: str) -> bool:
         return name in self.names
 
     def before(self, name: str) -> None:
         if self._flush is not None:
-            self._flush.fill_(1.0)
+            self._sink = self._flush.sum()
         e = torch.cuda.Event(enable_timing=True)
         e.record()
         self._open[name] = e

@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._dev import require_cuda, stream, to_device
+from ._dev import check_finite, require_cuda, stream, to_device, trusted_inputs
 from .csp import CSPBatch
 from .errors import InputError
 from .params import (AttentionParams, ConvParams, FeedForwardParams, GroupNormParams, LayerNormParams)
@@ -110,21 +110,30 @@ def blend_batch(batch: CSPBatch, latents: torch.Tensor, h: torch.Tensor, rates: 
 
 
 def blend(x, h, rate) -> torch.Tensor:
-    """model.py:129-131 for whole arrays with one scalar rate (device)."""
+    """model.py:129-131 on the device: (1 - rate) x + rate tanh(h), fp32 out.  `rate` is a scalar
+    or one rate per leading row of x (e.g. the engine's rate[request_index][:, None, None, None],
+    engine.py:158)."""
     xt = to_device(x, torch.float32)
     ht = to_device(h)
     if ht.shape != xt.shape:
         raise InputError("blend: shape mismatch")
-    flat = xt.reshape(1, -1, 1, 1) if xt.numel() % 4 == 0 else None
-    if flat is None:
-        raise InputError("blend: element count must be a multiple of 4")
-    hb = ht.to(torch.bfloat16).reshape(1, -1, 1, 1).contiguous()
+    r = np.asarray(rate.detach().cpu() if isinstance(rate, torch.Tensor) else rate, dtype=np.float64)
+    if r.size == 1:
+        rows = 1
+    elif xt.dim() >= 1 and r.size == xt.shape[0] and all(d == 1 for d in r.shape[1:]):
+        rows = xt.shape[0]
+    else:
+        raise InputError(f"blend: rate must be a scalar or one value per row, got shape {r.shape}")
+    n = xt.numel() // max(1, rows)
+    if n % 4:
+        raise InputError("blend: elements per row must be a multiple of 4")
+    flat = xt.reshape(rows, n // 4, 2, 2).contiguous()
+    hb = ht.to(torch.bfloat16).reshape(rows, n // 4, 2, 2).contiguous()
     out = torch.empty_like(flat)
-    rates = torch.tensor([float(rate)], dtype=torch.float32, device=xt.device)
-    ri = torch.zeros(1, dtype=torch.int32, device=xt.device)
-    n = flat.shape[1]
-    # view the array as one "patch" of n/4 channels of 2x2 pixels
-    _lib.call("ps_blend", stream(), flat.data_ptr(), hb.data_ptr(), rates.data_ptr(), ri.data_ptr(), 1, n // 4, 2,
+    rates = torch.as_tensor(r.reshape(-1), dtype=torch.float32, device=xt.device)
+    ri = torch.arange(rows, dtype=torch.int32, device=xt.device)
+    # view each row as one "patch" of n/4 channels of 2x2 pixels with its own rate
+    _lib.call("ps_blend", stream(), flat.data_ptr(), hb.data_ptr(), rates.data_ptr(), ri.data_ptr(), rows, n // 4, 2,
               out.data_ptr())
     return out.reshape(xt.shape)
 
@@ -151,9 +160,11 @@ def denoise_batch(cfg: ModelConfig, weights, batch: CSPBatch, prompts: dict, ste
     bias, rates = step_inputs(cfg, batch, prompts, step_idx, total_steps)
     lat = batch.data if batch.data.dtype == torch.float32 else batch.data.float()
     lat = lat.contiguous()
+    check_finite(lat)  # kernels.py:20-24, once per step
     h = prompt_bias(batch, lat, bias)
-    for ops in weights:
-        h = run_block(batch, h, ops)
+    with trusted_inputs():
+        for ops in weights:
+            h = run_block(batch, h, ops)
     return blend_batch(batch, lat, h, rates)
 
 

@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._dev import require_cuda, round_up, stream, to_device
+from ._dev import check_finite, require_cuda, round_up, stream, to_device
 from .csp import CSPBatch
 from .errors import InputError
 from .params import device_params
@@ -56,11 +56,13 @@ def _launch(kind: str) -> None:
 # ---------------------------------------------------------------- helpers
 
 
-def _check_data(batch: CSPBatch, data) -> torch.Tensor:
+def _check_data(batch: CSPBatch, data, finite: bool = True) -> torch.Tensor:
     t = to_device(data)
     if t.dim() != 4 or t.shape[0] != batch.n_patches or tuple(t.shape[2:]) != (batch.patch_size,) * 2:
         raise InputError(
             f"patch data must be ({batch.n_patches},C,{batch.patch_size},{batch.patch_size}), got {tuple(t.shape)}")
+    if finite:
+        check_finite(t)  # kernels.py:20-24 (skipped under trusted_inputs / stream capture)
     return t
 
 
@@ -412,13 +414,13 @@ class Ctx:
 
 def exchange_halos(batch: CSPBatch, data) -> torch.Tensor:
     """(P, C, ps+2, ps+2) frames: patch pixels plus a 1-pixel neighbour ring (patched.py:57-89)."""
-    data = _check_data(batch, data)
-    if data.dtype not in (torch.float32, BF16):
+    data = _check_data(batch, data, finite=False)  # a pure copy: the reference does not validate values
+    if data.dtype not in (torch.float32, BF16, torch.float64):
         data = data.to(torch.float32)
     p_n, c, ps = data.shape[0], data.shape[1], batch.patch_size
     out = torch.empty((p_n, c, ps + 2, ps + 2), dtype=data.dtype, device=data.device)
-    _lib.call("ps_halo_frames_nchw", stream(), data.data_ptr(),
-              _lib.DTYPE_F32 if data.dtype == torch.float32 else _lib.DTYPE_BF16,
+    code = {torch.float32: _lib.DTYPE_F32, BF16: _lib.DTYPE_BF16, torch.float64: _lib.DTYPE_F64}[data.dtype]
+    _lib.call("ps_halo_frames_nchw", stream(), data.data_ptr(), code,
               batch.device()["neighbors"].data_ptr(), p_n, c, ps, out.data_ptr())
     return out
 
@@ -509,7 +511,7 @@ def run_block_active(batch: CSPBatch, x, ops, active) -> torch.Tensor:
     unspecified (the cache splices their cached outputs, patched.py:246).  The
     active rows are bit-identical to run_block's.
     """
-    x = _check_data(batch, x)
+    x = _check_data(batch, x, finite=False)  # inactive rows may be unspecified
     active = np.asarray(active, dtype=bool)
     ctx = Ctx(batch)
     if ctx.hw % 128 or active.all():
@@ -537,7 +539,7 @@ def run_block_masked(batch: CSPBatch, x, ops, mask: torch.Tensor) -> tuple[torch
     the host enqueues the next block while this one runs.  The active rows are bit-identical
     to run_block_active's (same kernels and tile contents; only the tile counts move).
     Returns (output, counts) with counts the device int32 [6] of ps_compact_lists."""
-    x = _check_data(batch, x)
+    x = _check_data(batch, x, finite=False)  # inactive rows may be unspecified
     if not device_compaction_ok(batch):
         raise InputError("run_block_masked: geometry not covered (see device_compaction_ok)")
     m = mask.to(device=require_cuda(), dtype=torch.bool).contiguous()
@@ -556,7 +558,7 @@ def masked_context(batch: CSPBatch, mask: torch.Tensor) -> tuple["Ctx", torch.Te
 
 def run_block_ctx(ctx: "Ctx", x, ops) -> torch.Tensor:
     """The block stages of `ops` on a prepared Ctx (masked_context)."""
-    return _run_ops(ctx, _check_data(ctx.b, x), ops)
+    return _run_ops(ctx, _check_data(ctx.b, x, finite=False), ops)  # rows off the live set: unspecified
 
 
 def _attn_order(ctx: "Ctx") -> torch.Tensor:
@@ -787,7 +789,7 @@ def shard_context(batch: CSPBatch, shard, exch) -> "Ctx":
 
 def run_block_shard(batch: CSPBatch, x, ops, shard, exch, ctx: "Ctx | None" = None) -> torch.Tensor:
     """run_block for one rank of the split-image path; rows of ghost patches are unspecified."""
-    x = _check_data(batch, x)
+    x = _check_data(batch, x, finite=False)  # ghost rows are unspecified by contract
     return _run_ops(ctx or shard_context(batch, shard, exch), x, ops)
 
 
@@ -854,25 +856,35 @@ def _mask_tensor(batch: CSPBatch, mask) -> torch.Tensor:
 
 
 def select_patches(mask: torch.Tensor, a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
-    """out[p] = a[p] if mask[p] else b[p] (bf16 patch arrays)."""
+    """out[p] = a[p] if mask[p] else b[p] (patch arrays of one dtype: bf16, fp32 or fp64)."""
+    if a.dtype != b.dtype:
+        raise InputError("select_patches: dtype mismatch")
     out = torch.empty_like(b)
     n = b[0].numel() if b.shape[0] else 0
-    _lib.call("ps_select_patches", stream(), mask.view(torch.uint8).data_ptr(), b.shape[0], n, _lib.DTYPE_BF16,
-              a.data_ptr(),
-              b.data_ptr(), out.data_ptr())
+    code = {BF16: _lib.DTYPE_BF16, torch.float32: _lib.DTYPE_F32, torch.float64: _lib.DTYPE_F64}[b.dtype]
+    _lib.call("ps_select_patches", stream(), mask.view(torch.uint8).data_ptr(), b.shape[0], n, code,
+              a.contiguous().data_ptr(), b.contiguous().data_ptr(), out.data_ptr())
     return out
 
 
 def masked_block_forward(batch: CSPBatch, x, mask, ops, cached_inputs, cached_outputs) -> torch.Tensor:
-    """Run a block reusing cached results for masked patches (patched.py:224-246)."""
+    """Run a block reusing cached results for masked patches (patched.py:224-246).
+
+    Masked rows of the result are exact copies of `cached_outputs` at its precision (bf16 on the
+    hot path; fp32 / fp64 cached outputs stay exact, as np.where keeps them); the recomputed rows
+    are the bf16 block outputs at that precision."""
     x = _check_data(batch, x)
     m = _mask_tensor(batch, mask)
-    n_masked = int(m.sum())
+    # the all / none branches (patched.py:237-240) need the count on the host: free for a host
+    # (numpy) mask, one read-back for a device mask
+    n_masked = int(np.count_nonzero(mask)) if not isinstance(mask, torch.Tensor) else int(m.sum())
+    co = _check_data(batch, cached_outputs)
+    out_dt = co.dtype if co.dtype in (BF16, torch.float32, torch.float64) else torch.float32
     if n_masked == batch.n_patches:
-        return _bf16_nchw(_check_data(batch, cached_outputs)).clone()
+        return co.to(out_dt).clone()
     if n_masked == 0:
-        return run_block(batch, x, ops)
+        y = run_block(batch, x, ops)
+        return y if out_dt == BF16 else y.to(out_dt)
     ci = _bf16_nchw(_check_data(batch, cached_inputs))
-    co = _bf16_nchw(_check_data(batch, cached_outputs))
     y = run_block(batch, select_patches(m, ci, _bf16_nchw(x)), ops)
-    return select_patches(m, co, y)
+    return select_patches(m, co.to(out_dt).contiguous(), y.to(out_dt))

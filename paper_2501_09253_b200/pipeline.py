@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._dev import require_cuda
+from ._dev import require_cuda, trusted_inputs
 from .csp import split
 from .errors import InputError
 from .model import ModelConfig, rate_schedule
@@ -77,8 +77,9 @@ class DenoisePipeline:
         _lib.call("ps_csp_split_bias", st, self._in_ptrs[k].data_ptr(), src_ptrs["request_offset"].data_ptr(),
                   src_ptrs["sides"].data_ptr(), b.n_requests, self.C, self.ps, None, b.n_patches,
                   self.bias[k].data_ptr(), h.data_ptr(), self.nonfinite.data_ptr())
-        for ops in self.weights:
-            h = run_block(b, h, ops)
+        with trusted_inputs():  # the split kernel above flags non-finite latents
+            for ops in self.weights:
+                h = run_block(b, h, ops)
         # blend straight into the per-request outputs (model.py:129-131, csp.py:196-214)
         _lib.call("ps_blend_reassemble", st, None, h.data_ptr(), self.rates[k].data_ptr(),
                   src_ptrs["request_offset"].data_ptr(), src_ptrs["sides"].data_ptr(), b.n_requests, self.C,

@@ -125,3 +125,25 @@ def test_mse_bits_match_reference():
     for g in _load_json("mse_bits.json"):
         a, b = mse_inputs(tuple(g["shape"]), g["seed"], g["kind"])
         assert R.mse(a, b).hex() == g["mse_hex"], g
+
+
+def test_blas_mode_matches_reference_goldens():
+    # the BLAS contraction mode (used by the C=320 GPU parity tests) reorders only fp64 sums
+    g = np.load(os.path.join(GOLD, "ops_small.npz"))
+    reqs, b, P, extra = _ops_small()
+    with R.blas_contractions():
+        np.testing.assert_allclose(R.patched_conv(b, b.data, P["c3"]), g["conv3"], atol=1e-10, rtol=0)
+        np.testing.assert_allclose(R.patched_conv(b, b.data, P["c1"]), g["conv1"], atol=1e-10, rtol=0)
+        np.testing.assert_allclose(R.feed_forward(b.data, P["ff"]), g["ff"], atol=1e-10, rtol=0)
+        unet = [("group_norm", P["gn"]), ("conv", P["c3"]), ("attention", P["at"]),
+                ("feed_forward", P["ff"]), ("residual", None)]
+        np.testing.assert_allclose(R.run_block(b, b.data, unet), g["block_unet"], atol=1e-10, rtol=0)
+    gc = np.load(os.path.join(GOLD, "cfg1_steps.npz"))
+    cfg = R.ModelConfig(arch="unet_like", channels=4, hidden=8, n_blocks=2, groups=2, seed=0)
+    w = R.init_weights(cfg)
+    reqs = cfg1_requests()
+    prompts = {rid: R.make_prompt(cfg, rid) for rid, _ in reqs}
+    bb = R.split(reqs, patch_size=16)
+    with R.blas_contractions():
+        got = R.denoise_batch(cfg, w, bb, prompts, {r: 0 for r, _ in reqs}, {r: 4 for r, _ in reqs})
+    np.testing.assert_allclose(got, gc["step0"], atol=1e-10, rtol=0)
