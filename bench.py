@@ -253,10 +253,13 @@ def run_ours(args):
 
 
 def measure_slo(cfg, weights, rank, world, barrier):
-    """SLO-satisfaction % of the metric: a 128-request mixed trace (0.4/0.35/0.25 low/med/high,
-    50 steps, SLO = 3x standalone latency) served in the wall plane (serving.slo_run): every
-    denoising step runs on the GPU with the patch cache in the loop and the clock is its
-    measured device time; offered load = 0.9 x the fitted capacity of `world` GPUs."""
+    """SLO-satisfaction % of the metric, wall plane (serving.slo_run): every denoising step runs on
+    the GPU (resident CSP latents, the patch cache in the loop, one CUDA graph per composition)
+    and the clock is its measured device time.  The step-latency model is an MLP trained on 240
+    measured B200 compositions (200 train / 40 held out, error reported); SLO = 3x its standalone
+    latency (workload.py:74); offered load 0.9 x the capacity of `world` GPUs.
+      config2: 128-request mixed trace (0.4/0.35/0.25 low/med/high, 50 steps), max batch 12;
+      config4: the same trace shape with up to 64 requests in flight (max_active 64)."""
     from paper_2501_09253_b200.serving import slo_run
     share = gather = None
     if world > 1:
@@ -273,9 +276,14 @@ def measure_slo(cfg, weights, rank, world, barrier):
             return out
     barrier()
     r = slo_run(cfg, weights, n_requests=128, load=0.9, rank=rank, world=world, share=share, gather=gather)
-    r["plane"] = ("wall: step time = measured device time of each eager step (split, bias, 7 blocks with the "
-                  "cache, blend, reassemble); SLO budgets and admission on the cost model fitted to measured "
-                  "B200 step times")
+    barrier()
+    r4 = slo_run(cfg, weights, n_requests=128, load=0.9, rank=rank, world=world, share=share, gather=gather,
+                 max_active=64)
+    plane = ("wall: step time = measured device time of each step (resident CSP latents, bias, 7 blocks with "
+             "the cache as one CUDA graph per composition, blend); SLO budgets and admission on an MLP latency "
+             "model trained on measured B200 steps")
+    r["plane"] = r4["plane"] = plane
+    r["config4"] = r4
     return r
 
 
@@ -518,6 +526,34 @@ def cpu_baseline_sample(n_samples=3):
                        f"in the attention matmuls")}
 
 
+def reference_simulated_slo(load=0.9, n_requests=128, steps=50, seed=0):
+    """The reference's own SLO-satisfaction figure: its discrete-event Engine in the cost_only
+    plane (engine.py:162-169, 252-280), i.e. its analytic cost-model clock (latency.py:52-77),
+    the SLO-aware scheduler, a Poisson trace (workload.py:58-77) at `load` x the capacity of
+    full 12-request mixed batches under that cost model -- the same trace shape and relative load
+    as the GPU arm's wall-plane runs (max batch 12 = config 2, 64 = config 4)."""
+    if not os.path.isdir(os.path.join(REF_SRC, "mixserve")):
+        return None
+    if REF_SRC not in sys.path:
+        sys.path.insert(0, REF_SRC)
+    from mixserve.engine import Engine, EngineConfig
+    from mixserve.latency import DEFAULT_COST, step_latency
+    from mixserve.scheduler import SchedulerConfig
+    from mixserve.workload import WorkloadConfig, generate_trace
+    cap = 12 * 1000.0 / (steps * step_latency({"low": 4, "med": 4, "high": 4}, DEFAULT_COST))
+    trace = generate_trace(WorkloadConfig(seed=seed, qps=load * cap, n_requests=n_requests, steps=steps))
+    out = {}
+    for name, ma in (("config2", 12), ("config4", 64)):
+        res = Engine(EngineConfig(plane="cost_only", total_steps=steps,
+                                  scheduler=SchedulerConfig(policy="slo_aware", max_active=ma))).run(trace)
+        out[name] = {k: res.summary[k] for k in ("slo_attainment", "goodput_rps", "n_discarded", "mean_latency_ms",
+                                                 "p95_latency_ms")}
+        out[name]["max_active"] = ma
+    out.update(load=load, n_requests=n_requests, steps=steps,
+               plane="reference Engine, cost_only plane (simulated clock: the reference's analytic cost model)")
+    return out
+
+
 def run_reference(args):
     rank, world, _ = _env_rank()
     if rank != 0:
@@ -556,6 +592,7 @@ def run_reference(args):
         "config": dict(WORKLOAD, sample=cb["sample"]),
         "sample_wall_s_per_step": float(np.mean(wall)),
         "cpu_baseline": cb,
+        "slo": reference_simulated_slo(),
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 

@@ -46,6 +46,11 @@ STANDARD_CLASSES = {
     "low": ResolutionClass("low", 512),
     "med": ResolutionClass("med", 768),
     "high": ResolutionClass("high", 1024),
+    # beyond csp.py:42-46: the BASELINE configs' other sizes -- config 1's 256 / 384 px and config
+    # 5's 2048 px -- so those requests can enter the serving plane
+    "tiny": ResolutionClass("tiny", 256),
+    "small": ResolutionClass("small", 384),
+    "ultra": ResolutionClass("ultra", 2048),
 }
 
 

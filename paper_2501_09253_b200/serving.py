@@ -37,7 +37,7 @@ import numpy as np
 from .csp import STANDARD_CLASSES
 from .errors import InputError  # noqa: F401  (re-exported for callers)
 
-CLASS_ORDER = ("low", "med", "high")
+CLASS_ORDER = ("low", "med", "high", "tiny", "small", "ultra")
 
 # ------------------------------------------------------------ cost model
 
@@ -158,6 +158,134 @@ def fit_cost_model(samples: Sequence[tuple[dict, float]], base: CostModelParams 
                    c_attn_coeff=float(coef[3]))
 
 
+# ------------------------------------------------ learned latency model
+
+
+def composition_features(comp: dict, patch_size: int = 32) -> np.ndarray:
+    """Per-class request counts (CLASS_ORDER) plus the step's cost drivers on B200: distinct
+    resolutions, patches (the pixel-wise / conv work), sum of T^2 over images (attention work,
+    in units of 2^24) -- the reference's features (latency.py:78-91) plus the attention term."""
+    _validated(comp)
+    counts = [float(comp.get(c, 0)) for c in CLASS_ORDER]
+    lat = [STANDARD_CLASSES[c].latent for c in CLASS_ORDER]
+    n_res = float(sum(1 for v in counts if v > 0))
+    patches = sum(v * (d // patch_size) ** 2 for v, d in zip(counts, lat))
+    attn = sum(v * float(d * d) ** 2 for v, d in zip(counts, lat)) / 2.0 ** 24
+    return np.array(counts + [n_res, patches, attn], dtype=np.float64)
+
+
+class MlpLatencyModel:
+    """Step-latency predictor learned from measured B200 steps (the paper's MLP predictor,
+    latency.py:140-253, retrained on this hardware).
+
+    A 2 x 32 ReLU network on standardised composition features regresses log(step ms), full-batch
+    Adam.  With `residual` (default) the net learns log(measured / analytic) on top of the cost
+    model fitted to the same samples (fit_cost_model; exponent 2 = the T^2 attention work), so
+    the structure extrapolates and the net absorbs what the analytic form misses.
+    `fit` returns the training loss; `predict_step_latency(comp)` is the scheduler's predictor
+    interface (scheduler.py:126-128)."""
+
+    def __init__(self, hidden=(32, 32), lr: float = 1e-2, epochs: int = 1500, seed: int = 0, patch_size: int = 32,
+                 residual: bool = True):
+        self.hidden, self.lr, self.epochs, self.seed, self.patch_size = tuple(hidden), lr, epochs, seed, patch_size
+        self.residual = residual
+        self.base = None  # fitted CostModelParams (residual mode)
+        self.params: list = []
+        self.mu = self.sd = None
+
+    def _base_ms(self, comps) -> np.ndarray:
+        if self.base is None:
+            return np.ones(len(comps))
+        return np.array([step_latency(c, self.base) for c in comps])
+
+    def _feats(self, comps) -> np.ndarray:
+        return np.stack([composition_features(c, self.patch_size) for c in comps])
+
+    def _net(self, xn):
+        acts, h = [xn], xn
+        for i in range(0, len(self.params), 2):
+            h = h @ self.params[i] + self.params[i + 1]
+            if i + 2 < len(self.params):
+                h = np.maximum(h, 0.0)
+            acts.append(h)
+        return acts
+
+    def fit(self, comps, ms) -> float:
+        ms = np.asarray(ms, dtype=np.float64)
+        if np.any(~(ms > 0)):
+            raise InputError("step times must be positive")
+        self.base = None
+        if self.residual:
+            self.base = fit_cost_model(list(zip(comps, ms)), replace(DEFAULT_COST, attn_exponent=2.0,
+                                                                       patch_size=self.patch_size))
+        x, y = self._feats(comps), np.log(ms / self._base_ms(comps))[:, None]
+        self.mu, self.sd = x.mean(0), np.maximum(x.std(0), 1e-8)
+        xn = (x - self.mu) / self.sd
+        rng = np.random.default_rng(self.seed)
+        dims = [x.shape[1], *self.hidden, 1]
+        self.params = []
+        for a, b in zip(dims, dims[1:]):
+            self.params += [rng.normal(size=(a, b)) * np.sqrt(2.0 / a), np.zeros(b)]
+        m = [np.zeros_like(p) for p in self.params]
+        v = [np.zeros_like(p) for p in self.params]
+        loss = np.inf
+        for t in range(1, self.epochs + 1):
+            acts = self._net(xn)
+            err = acts[-1] - y
+            loss = float(np.mean(err ** 2))
+            g = 2.0 * err / len(xn)
+            grads = [None] * len(self.params)
+            for li in range(len(self.params) // 2 - 1, -1, -1):
+                grads[2 * li] = acts[li].T @ g
+                grads[2 * li + 1] = g.sum(0)
+                if li:
+                    g = (g @ self.params[2 * li].T) * (acts[li] > 0)
+            for j, (p, gr) in enumerate(zip(self.params, grads)):
+                m[j] = 0.9 * m[j] + 0.1 * gr
+                v[j] = 0.999 * v[j] + 0.001 * gr * gr
+                p -= self.lr * (m[j] / (1 - 0.9 ** t)) / (np.sqrt(v[j] / (1 - 0.999 ** t)) + 1e-8)
+        return loss
+
+    def predict(self, comps) -> np.ndarray:
+        if not self.params:
+            raise InputError("latency model is not trained")
+        return self._base_ms(comps) * np.exp(self._net((self._feats(comps) - self.mu) / self.sd)[-1][:, 0])
+
+    def predict_step_latency(self, comp: dict) -> float:
+        return float(self.predict([comp])[0])
+
+
+class LearnedPredictor:
+    """Scheduler predictor on the MLP, optionally following the measured pace: step time =
+    MLP(comp) x EWMA(measured / MLP) clamped <= 1 (the cache's speed-up, as AdaptivePredictor)."""
+
+    def __init__(self, model: MlpLatencyModel, alpha: float = 0.2, adaptive: bool = True):
+        self.model, self.alpha, self.adaptive, self.ratio = model, alpha, adaptive, 1.0
+
+    def predict_step_latency(self, comp: dict) -> float:
+        return self.ratio * self.model.predict_step_latency(comp)
+
+    def observe(self, comp: dict, measured_ms: float) -> None:
+        if self.adaptive:
+            r = measured_ms / self.model.predict_step_latency(comp)
+            self.ratio = min(1.0, (1.0 - self.alpha) * self.ratio + self.alpha * r)
+
+
+def random_compositions(n: int, seed: int = 0, max_batch: int = 12, classes=("low", "med", "high")) -> list:
+    """n distinct compositions of 1..max_batch requests over `classes` (latency.py:102-123)."""
+    rng = np.random.default_rng(seed)
+    seen, out = set(), []
+    while len(out) < n:
+        k = int(rng.integers(1, max_batch + 1))
+        counts = np.bincount(rng.integers(0, len(classes), size=k), minlength=len(classes))
+        key = tuple(int(c) for c in counts)
+        if key in seen:
+            continue
+        seen.add(key)
+        out.append({c: v for c, v in zip(classes, key) if v})
+    return out
+
+
 # ------------------------------------------------------------- workload
 
 DEFAULT_WEIGHTS = {"low": 0.4, "med": 0.35, "high": 0.25}
@@ -199,14 +327,19 @@ class TraceRow:
     slo_ms: float
 
 
-def generate_trace(cfg: WorkloadConfig, cost: CostModelParams = DEFAULT_COST) -> list[TraceRow]:
-    """workload.py:58-77: exponential gaps then weighted class picks from one seeded stream."""
+def generate_trace(cfg: WorkloadConfig, cost: CostModelParams = DEFAULT_COST, predictor=None) -> list[TraceRow]:
+    """workload.py:58-77: exponential gaps then weighted class picks from one seeded stream.
+    SLO budget = slo_scale x the standalone latency of the class: from `cost` (the reference's
+    semantics) or, when given, from `predictor`'s one-request step latency x steps."""
     rng = np.random.default_rng(cfg.seed)
     arrivals = np.cumsum(rng.exponential(scale=1000.0 / cfg.qps, size=cfg.n_requests))
     names = sorted(cfg.class_weights)
     w = np.asarray([cfg.class_weights[n] for n in names], dtype=np.float64)
     picks = rng.choice(len(names), size=cfg.n_requests, p=w / w.sum())
-    budget = {n: cfg.slo_scale * standalone_latency(n, cfg.steps, cost) for n in names}
+    if predictor is not None:
+        budget = {n: cfg.slo_scale * cfg.steps * predictor.predict_step_latency({n: 1}) for n in names}
+    else:
+        budget = {n: cfg.slo_scale * standalone_latency(n, cfg.steps, cost) for n in names}
     return [TraceRow(f"req-{i:05d}", float(arrivals[i]), names[int(k)], budget[names[int(k)]])
             for i, k in enumerate(picks)]
 
@@ -381,6 +514,7 @@ class EngineConfig:
     cost: CostModelParams = field(default_factory=CostModelParams)
     model: object = None            # model.ModelConfig (None -> the reference default)
     cache: object = None            # cache.PredictorConfig (None -> defaults)
+    graph_steps: bool = True        # GPU planes: a CUDA graph per batch composition (cached steps)
 
     def __post_init__(self):
         if self.plane not in PLANES:
@@ -410,6 +544,9 @@ class _Worker:
         self.prompts: dict = {}
         self.cache = None
         self.step_ms: list = []   # measured device time per step (wall plane)
+        self.batch = None         # resident CSP batch of the active set (GPU planes)
+        self.batch_ids = None
+        self.graph = None         # CachedStepGraph of that composition
 
 
 class Engine:
@@ -448,26 +585,51 @@ class Engine:
         w.latents[meta.request_id] = torch.as_tensor(lat, dtype=torch.float32, device=require_cuda())
         w.prompts[meta.request_id] = make_prompt(self.model_cfg, meta.request_id)
 
+    def _materialize(self, w: _Worker) -> None:
+        """Resident CSP batch -> per-request latents (on a composition change)."""
+        from .csp import reassemble
+        if w.batch is not None:
+            for rid, lat in reassemble(w.batch, w.batch.data).items():
+                w.latents[rid] = lat
+        w.batch, w.batch_ids, w.graph = None, None, None
+
     def _compute_step(self, w: _Worker) -> float:
-        """One denoising step of w's active batch on the GPU; returns its device time in ms."""
+        """One denoising step of w's active batch on the GPU; returns its device time in ms.
+
+        The batch's fp32 latents stay resident in CSP layout across steps and are re-split only
+        when the composition changes (an admission or a completion); while it is unchanged, the
+        cached step runs as one CUDA graph (engine_step.CachedStepGraph: the reuse test,
+        compaction and every block replay without the host) -- the reference re-splits and
+        reassembles every step (engine.py:129,159-160)."""
         import torch
 
         from ._dev import require_cuda
-        from .csp import reassemble, split
-        from .engine_step import numeric_step
+        from .csp import split
+        from .engine_step import CachedStepGraph, numeric_step
         from .model import rate_schedule
+        from .patched import device_compaction_ok
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record()
-        batch = split([(r.request_id, w.latents[r.request_id]) for r in w.active], patch_size=self.cfg.patch_size)
+        ids = tuple(r.request_id for r in w.active)
+        if w.batch_ids is None or set(w.batch_ids) != set(ids):
+            self._materialize(w)
+            w.batch = split([(rid, w.latents.pop(rid)) for rid in ids], patch_size=self.cfg.patch_size)
+            w.batch_ids = ids
+            if (self.cfg.use_cache and self.cfg.graph_steps and w.cache is not None
+                    and device_compaction_ok(w.batch)):
+                w.graph = CachedStepGraph(w.batch, self.weights, w.cache)
+        batch = w.batch
         order = [self._meta[e.request_id] for e in batch.requests]
         dev = require_cuda()
         bias = torch.as_tensor(np.stack([w.prompts[m.request_id] for m in order]), dtype=torch.float32, device=dev)
         rates = torch.as_tensor([rate_schedule(m.total_steps - m.remaining_steps, m.total_steps) for m in order],
                                 dtype=torch.float32, device=dev)
-        cache = w.cache if self.cfg.use_cache else None
-        new, st = numeric_step(batch, self.weights, cache, bias, rates)
-        for rid, lat in reassemble(batch, new).items():
-            w.latents[rid] = lat
+        if w.graph is not None:
+            new, st = w.graph.run(batch.data, bias, rates)
+        else:
+            cache = w.cache if self.cfg.use_cache else None
+            new, st = numeric_step(batch, self.weights, cache, bias, rates)
+        batch.data = new
         t1.record()
         t1.synchronize()
         self._skipped += st.skipped
@@ -503,7 +665,7 @@ class Engine:
             index[row.request_id] = i
             push(row.arrival_ms, "arrival", row.request_id)
 
-        unit = {c: step_latency({c: 1}, cfg.cost) for c in STANDARD_CLASSES}
+        unit = {c: step_latency({c: 1}, cfg.cost) for c in sorted({r.resolution_class for r in trace})}
 
         def backlog(w):  # engine.py:120-124
             return sum(r.remaining_steps * unit[r.cls] for r in w.active + w.waiting)
@@ -536,6 +698,8 @@ class Engine:
             for r in w.active:
                 r.remaining_steps -= 1
             done = [r for r in w.active if r.remaining_steps == 0]
+            if done and cfg.plane != "cost_only":
+                self._materialize(w)
             for r in done:
                 w.active.remove(r)
                 log(now, "complete", r.request_id, w.wid)
@@ -684,44 +848,66 @@ CALIBRATION_COMPS = ({"low": 1}, {"med": 1}, {"high": 1}, {"low": 4, "med": 4, "
                      {"low": 2, "high": 2}, {"med": 3}, {"low": 6}, {"high": 4}, {"low": 1, "med": 1, "high": 1})
 
 
+def calibrate_latency_model(model_cfg, weights, n_compositions: int = 240, n_train: int = 200,
+                            max_batch: int = 12, reps: int = 2, seed: int = 0, classes=("low", "med", "high"),
+                            patch_size: int = 32):
+    """Measure n_compositions distinct random batch compositions (1..max_batch requests) on the
+    GPU (measure_step_ms, uncached), train the MLP latency model on n_train of them (PAPER.md:
+    480-484: 200 compositions) and report its mean relative error on the held-out rest.
+    Returns (model, report)."""
+    comps = random_compositions(n_compositions, seed=seed, max_batch=max_batch, classes=classes)
+    np.random.default_rng(seed + 1).shuffle(comps)
+    samples = measure_step_ms(model_cfg, weights, comps, patch_size=patch_size, reps=reps)
+    ms = np.array([m for _, m in samples])
+    model = MlpLatencyModel(patch_size=patch_size)
+    loss = model.fit(comps[:n_train], ms[:n_train])
+    held = comps[n_train:]
+    pred = model.predict(held) if held else np.zeros(0)
+    rel = np.abs(pred - ms[n_train:]) / ms[n_train:] if held else np.zeros(0)
+    rel_train = np.abs(model.predict(comps[:n_train]) - ms[:n_train]) / ms[:n_train]
+    analytic = np.array([step_latency(c, model.base) for c in held]) if held else np.zeros(0)
+    return model, {
+        "n_measured": len(comps), "n_train": n_train, "n_heldout": len(held), "max_batch": max_batch,
+        "train_log_mse": loss, "train_mean_rel_err": float(rel_train.mean()),
+        "heldout_mean_rel_err": float(rel.mean()) if held else None,
+        "heldout_max_rel_err": float(rel.max()) if held else None,
+        "heldout_mean_rel_err_analytic_only": float((np.abs(analytic - ms[n_train:]) / ms[n_train:]).mean())
+        if held else None,
+        "step_ms_range": [float(ms.min()), float(ms.max())],
+        "analytic_base": {k: getattr(model.base, k) for k in ("c_step_fixed", "c_res_overhead", "c_patch",
+                                                               "c_attn_coeff", "attn_exponent")},
+    }
+
+
 def slo_run(model_cfg, weights, n_requests: int = 64, load: float = 0.9, steps: int = 50, seed: int = 0,
             use_cache: bool = True, policy: str = "slo_aware", max_active: int = 12, slo_scale: float = 3.0,
-            calib_reps: int = 5, rank: int = 0, world: int = 1, share=None, gather=None,
-            adaptive: bool = True) -> dict:
+            rank: int = 0, world: int = 1, share=None, gather=None, adaptive: bool = True,
+            latency_model=None, n_calib: int = 240, calib_report=None) -> dict:
     """SLO attainment of the B200 path in the wall plane.
 
-    1. measure one-step device times of CALIBRATION_COMPS and fit the cost model
-       (rank 0's fit is shared with every rank through `share`);
-    2. draw a trace whose SLO budgets are slo_scale x the fitted standalone
-       latency (workload.py:74) at `load` x the fitted capacity of `world` GPUs
-       serving full 12-request mixed batches without the cache;
-    3. dispatch requests to GPUs lowest-outstanding-work first (engine.py:228),
-       decided on the fitted model (a cost_only run with `world` workers, the
-       same on every rank), then each rank serves its requests with the
-       SLO-aware scheduler, every step run and timed on its device; completions
-       are pooled through `gather`.  With `adaptive` the scheduler's predictor
-       follows the measured pace (AdaptivePredictor); budgets stay on the fit.
-    """
-    # calibrated without the cache (the reference's cost-model semantics: SLO budgets and
-    # capacity in uncached step time; a cache-calibrated fit -- measure_step_ms(use_cache=True)
-    # -- makes budgets ~3x tighter than the mixed, churning batches can meet: FCFS 0.05 at 0.9)
-    samples = measure_step_ms(model_cfg, weights, CALIBRATION_COMPS, reps=calib_reps)
-    fit = fit_cost_model(samples)
-    # a transient on the box (seen once: one composition measured 6x its steady time) skews the
-    # whole fit; re-measure compositions the fit misses by > 50% once and refit
-    bad = [i for i, (c, ms) in enumerate(samples) if abs(step_latency(c, fit) - ms) > 0.5 * ms]
-    if bad:
-        again = measure_step_ms(model_cfg, weights, [samples[i][0] for i in bad], reps=calib_reps)
-        for i, (c, ms) in zip(bad, again):
-            samples[i] = (c, min(ms, samples[i][1]))
-        fit = fit_cost_model(samples)
+    1. the step-latency model: an MLP trained on >= 200 measured B200 compositions of up to
+       max_active requests (calibrate_latency_model; rank 0's model is shared through `share`;
+       pass `latency_model` to reuse one across runs);
+    2. a trace whose SLO budgets are slo_scale x the model's standalone latency (workload.py:74)
+       at `load` x the capacity of `world` GPUs serving full 12-request mixed batches without
+       the cache;
+    3. dispatch requests to GPUs lowest-outstanding-work first (engine.py:228) on the model's
+       analytic base (a cost_only run with `world` workers, the same on every rank), then each
+       rank serves its requests with `policy`, every step run and timed on its device (resident
+       CSP latents, one CUDA graph per composition); completions pooled through `gather`.  With
+       `adaptive` the scheduler's predictor follows the measured pace (LearnedPredictor)."""
+    model, report = latency_model, calib_report
+    if model is None:
+        model, report = calibrate_latency_model(model_cfg, weights, n_compositions=n_calib,
+                                                max_batch=max_active, seed=seed)
     if share is not None:
-        fit = share(fit)
+        model, report = share((model, report))
+    fit = model.base
     full = {"low": 4, "med": 4, "high": 4}
-    capacity_rps = world * 12 * 1000.0 / (steps * step_latency(full, fit))
+    capacity_rps = world * 12 * 1000.0 / (steps * model.predict_step_latency(full))
     qps = load * capacity_rps
     wc = WorkloadConfig(seed=seed, qps=qps, n_requests=n_requests, steps=steps, slo_scale=slo_scale)
-    trace = generate_trace(wc, fit)
+    trace = generate_trace(wc, fit, predictor=model)
     sched = SchedulerConfig(policy=policy, max_active=max_active, cost=fit)
     mine = trace
     if world > 1:
@@ -731,7 +917,7 @@ def slo_run(model_cfg, weights, n_requests: int = 64, load: float = 0.9, steps: 
         mine = [r for r in trace if owner[r.request_id] == rank]
     ec = EngineConfig(plane="wall", total_steps=steps, use_cache=use_cache, cost=fit, model=model_cfg,
                       scheduler=sched)
-    pred = AdaptivePredictor(fit) if adaptive else AnalyticPredictor(fit)
+    pred = LearnedPredictor(model, adaptive=adaptive)
     res = Engine(ec, predictor=pred, weights=weights).run(mine) if mine else None
     local = {"completions": res.completions if res else [], "steps_run": res.summary["steps_run"] if res else 0,
              "skipped": res.summary["skipped_patches"] if res else 0,
@@ -742,19 +928,16 @@ def slo_run(model_cfg, weights, n_requests: int = 64, load: float = 0.9, steps: 
     met = sum(1 for c in comp if c["met_slo"])
     fin = sorted(c["latency_ms"] for c in comp if not c["discarded"])
     horizon = max([c["finish_ms"] for c in comp] + [r.arrival_ms for r in trace])
-    rel = [abs(step_latency(c, fit) - ms) / ms for c, ms in samples]
     return {
         "slo_attainment": met / len(trace), "goodput_rps": 1000.0 * met / horizon, "qps": qps, "load": load,
         "n_gpus": world, "n_requests": n_requests, "steps": steps, "policy": policy, "max_active": max_active,
         "use_cache": use_cache, "slo_scale": slo_scale, "n_met_slo": met,
-        "predictor": "fitted analytic x EWMA(measured/predicted)" if adaptive else "fitted analytic",
+        "predictor": "MLP on measured B200 steps" + (" x EWMA(measured/predicted)" if adaptive else ""),
         "n_discarded": sum(1 for c in comp if c["discarded"]),
         "mean_latency_ms": float(np.mean(fin)) if fin else 0.0,
         "p95_latency_ms": fin[int(0.95 * (len(fin) - 1))] if fin else 0.0, "makespan_ms": horizon,
         "steps_run": sum(p["steps_run"] for p in parts),
         "device_step_ms_mean": float(np.mean([p["step_ms"] for p in parts if p["steps_run"]] or [0.0])),
         "skipped_patches": sum(p["skipped"] for p in parts), "computed_patches": sum(p["computed"] for p in parts),
-        "fitted_cost": {k: getattr(fit, k) for k in ("c_step_fixed", "c_res_overhead", "c_patch", "c_attn_coeff")},
-        "fit_mean_rel_err": float(np.mean(rel)),
-        "calibration": [{"comp": c, "ms": round(ms, 4)} for c, ms in samples],
+        "latency_model": report,
     }

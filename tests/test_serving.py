@@ -143,7 +143,7 @@ def test_slo_run_two_ranks_pool_completions():
     def run(rank):
         try:
             torch.cuda.set_device(0)
-            res[rank] = S.slo_run(mc, w, n_requests=8, load=0.5, steps=3, rank=rank, world=2, calib_reps=1,
+            res[rank] = S.slo_run(mc, w, n_requests=8, load=0.5, steps=3, rank=rank, world=2, n_calib=24,
                                   share=lambda o: share(o, rank), gather=lambda o: gather(o, rank))
         except BaseException as e:  # noqa: BLE001
             errs.append(e)
@@ -159,4 +159,42 @@ def test_slo_run_two_ranks_pool_completions():
     a, b = res[0], res[1]
     assert a["n_gpus"] == 2 and a["slo_attainment"] == b["slo_attainment"]
     assert a["n_met_slo"] + a["n_discarded"] <= 8
-    assert a["fitted_cost"] == b["fitted_cost"]
+    assert a["latency_model"] == b["latency_model"]
+
+
+def test_mlp_latency_model_generalises_on_synthetic_steps():
+    # the serving plane's predictor (MLP on measured compositions): trained on
+    # 200 compositions of a known T^2-attention cost law with 1% noise, held-out error < 5%
+    comps = S.random_compositions(260, seed=1)
+    assert len({tuple(sorted(c.items())) for c in comps}) == 260
+    np.random.default_rng(9).shuffle(comps)
+    true = S.CostModelParams(c_step_fixed=0.8, c_res_overhead=0.05, c_patch=0.008, c_attn_coeff=2.2e-9,
+                             attn_exponent=2.0)
+    y = np.array([S.step_latency(c, true) * (1 + 0.01 * np.random.default_rng(i).normal()) + 0.2 * sum(c.values()) ** 0.5
+                  for i, c in enumerate(comps)])
+    m = S.MlpLatencyModel()
+    m.fit(comps[:200], y[:200])
+    err = np.abs(m.predict(comps[200:]) - y[200:]) / y[200:]
+    assert err.mean() < 0.05, err.mean()
+    pred = S.LearnedPredictor(m)
+    assert pred.predict_step_latency({"low": 2}) == m.predict_step_latency({"low": 2})
+    pred.observe({"low": 2}, 0.5 * m.predict_step_latency({"low": 2}))
+    assert pred.ratio < 1.0
+
+
+def test_extended_resolution_classes_enter_the_serving_plane():
+    # configs 1 (256/384 px) and 5 (2048 px) through the engine
+    from paper_2501_09253_b200.csp import STANDARD_CLASSES
+    assert {c: STANDARD_CLASSES[c].latent for c in ("tiny", "small", "ultra")} == {"tiny": 32, "small": 48,
+                                                                                 "ultra": 256}
+    cost = S.CostModelParams(patch_size=16)
+    trace = S.generate_trace(S.WorkloadConfig(seed=1, qps=2.0, n_requests=12, steps=4,
+                                              class_weights={"tiny": 1, "small": 1, "low": 1}), cost)
+    res = S.Engine(S.EngineConfig(plane="cost_only", total_steps=4, patch_size=16, cost=cost,
+                                  scheduler=S.SchedulerConfig(cost=cost))).run(trace)
+    assert res.summary["n_completed"] + res.summary["n_discarded"] == 12
+    cost64 = S.CostModelParams(patch_size=64)
+    trace5 = [S.TraceRow("big", 0.0, "ultra", 1e9)] + [S.TraceRow(f"s{i}", 0.0, "low", 1e9) for i in range(8)]
+    res5 = S.Engine(S.EngineConfig(plane="cost_only", total_steps=2, patch_size=64, cost=cost64,
+                                   scheduler=S.SchedulerConfig(cost=cost64))).run(trace5)
+    assert res5.summary["n_completed"] == 9
