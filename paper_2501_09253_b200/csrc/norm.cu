@@ -127,8 +127,10 @@ __global__ void __launch_bounds__(256, 4) gn_partials_kernel(const __nv_bfloat16
   }
 }
 
-// host: one CTA per (patch, group) slice.  (Persistent software-pipelined and bulk-copy
-// staged variants measured 21-26 us against 20-21 us and were removed.)
+// host: one CTA per (patch, group) slice.  (Persistent software-pipelined and bulk-copy staged
+// variants measured 21-26 us against 20-21 us; a group-pair kernel -- one CTA per two adjacent
+// groups, all ten 16-byte loads per thread issued first, one shifted-sum block reduction --
+// measured 26.2 vs 21.6 us (ncu, round 2).  All removed.)
 static void launch_gn_partials(cudaStream_t st, const void* x, int P, int C, int hw, int G, const int32_t* plist,
                                int n, float* partials, const int32_t* n_dev = nullptr) {
   (void)P;

@@ -115,7 +115,9 @@ class CachedStepGraph:
                 self.slots = self.cache.slots_for(self.keys, allocate=True)
                 self._gen = self.cache.storage_gen
                 g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
+                # thread-local capture: another thread driving the same GPU (a second virtual rank,
+                # a copy stream) does not invalidate this capture
+                with torch.cuda.graph(g, capture_error_mode="thread_local"):
                     self._out, self._counts = self._body()
                 self.graph = g
             self.graph.replay()
