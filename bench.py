@@ -414,8 +414,9 @@ def run_split(args):
 
 def measure_slo(cfg, weights, rank, world, barrier):
     """SLO-satisfaction % of the metric, wall plane (serving.slo_run): every denoising step runs on
-    the GPU (resident CSP latents, the patch cache in the loop, one CUDA graph per composition)
-    and the clock is its measured device time.  The step-latency model is an MLP trained on 240
+    the GPU (resident CSP latents, the patch cache in the loop, eager steps: a per-composition
+    CUDA graph costs 10-100 ms of capture against a few steps of life) and the clock is its
+    measured device time.  The step-latency model is an MLP trained on 240
     measured B200 compositions of 1..64 requests (200 train / 40 held out, error reported); SLO =
     5x its standalone latency (the paper's protocol; the reference code's
     default is 3x, tools/slo_run.py sweeps both); offered load 0.9 x the capacity of `world` GPUs.
@@ -439,7 +440,7 @@ def measure_slo(cfg, weights, rank, world, barrier):
     barrier()
     t0 = time.perf_counter()
     # one latency model for both runs: 240 measured compositions of 1..64 requests
-    model, rep = calibrate_latency_model(cfg, weights, n_compositions=240, max_batch=64, reps=1)
+    model, rep = calibrate_latency_model(cfg, weights, n_compositions=240, max_batch=64, reps=2)
     t1 = time.perf_counter()
     kw = dict(n_requests=128, load=0.9, rank=rank, world=world, share=share, gather=gather, latency_model=model,
               calib_report=rep, slo_scale=5.0)
@@ -451,9 +452,9 @@ def measure_slo(cfg, weights, rank, world, barrier):
     print(f"bench: slo calibration {t1 - t0:.1f} s, config2 run {t2 - t1:.1f} s, config4 run {t3 - t2:.1f} s",
           file=sys.stderr, flush=True)
     r4.pop("latency_model", None)
-    plane = ("wall: step time = measured device time of each step (resident CSP latents, bias, 7 blocks with "
-             "the cache as one CUDA graph per composition, blend); SLO budgets and admission on an MLP latency "
-             "model trained on measured B200 steps")
+    plane = ("wall: step time = measured device time of each step incl. host gaps (resident CSP latents "
+             "re-split on composition changes, bias, 7 blocks with the patch cache in the loop, blend); SLO "
+             "budgets and admission on an MLP latency model trained on measured steady-state B200 steps")
     r["plane"] = r4["plane"] = plane
     r["config4"] = r4
     return r

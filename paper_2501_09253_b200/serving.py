@@ -135,8 +135,10 @@ class AdaptivePredictor(AnalyticPredictor):
 
 def fit_cost_model(samples: Sequence[tuple[dict, float]], base: CostModelParams = DEFAULT_COST) -> CostModelParams:
     """Least-squares fit of (c_step_fixed, c_res_overhead, c_patch, c_attn_coeff) to
-    measured (composition, step ms) pairs, keeping the exponent and block count.
-    Coefficients are clamped at zero (non-negative least squares by elimination)."""
+    measured (composition, step ms) pairs, keeping the exponent and block count.  The residuals
+    are relative (each row divided by its measured time), so 2 ms single-request steps weigh as
+    much as 20 ms full batches.  Coefficients are clamped at zero (non-negative least squares by
+    elimination)."""
     if len(samples) < 4:
         raise InputError("need at least 4 measured compositions to fit the cost model")
     rows, y = [], []
@@ -145,6 +147,7 @@ def fit_cost_model(samples: Sequence[tuple[dict, float]], base: CostModelParams 
         rows.append([1.0, n_res, base.blocks_per_step * patches, base.blocks_per_step * attn])
         y.append(float(ms))
     A, y = np.asarray(rows), np.asarray(y)
+    A, y = A / y[:, None], np.ones_like(y)
     active = list(range(4))
     while True:
         coef = np.zeros(4)
@@ -514,7 +517,11 @@ class EngineConfig:
     cost: CostModelParams = field(default_factory=CostModelParams)
     model: object = None            # model.ModelConfig (None -> the reference default)
     cache: object = None            # cache.PredictorConfig (None -> defaults)
-    graph_steps: bool = True        # GPU planes: a CUDA graph per batch composition (cached steps)
+    # GPU planes: capture the cached step of a composition as a CUDA graph once it has run this many
+    # eager steps unchanged (0 = never).  A capture costs 10-100 ms of host time on the clock
+    # (tools/serving_probe.py) against ~0.5 ms saved per replay, and a Poisson trace changes the
+    # composition every few steps, so the default serves eagerly.
+    graph_after_steps: int = 0
 
     def __post_init__(self):
         if self.plane not in PLANES:
@@ -547,6 +554,7 @@ class _Worker:
         self.batch = None         # resident CSP batch of the active set (GPU planes)
         self.batch_ids = None
         self.graph = None         # CachedStepGraph of that composition
+        self.comp_steps = 0       # steps run since the composition last changed
 
 
 class Engine:
@@ -592,6 +600,7 @@ class Engine:
             for rid, lat in reassemble(w.batch, w.batch.data).items():
                 w.latents[rid] = lat
         w.batch, w.batch_ids, w.graph = None, None, None
+        w.comp_steps = 0
 
     def _compute_step(self, w: _Worker) -> float:
         """One denoising step of w's active batch on the GPU; returns its device time in ms.
@@ -615,9 +624,9 @@ class Engine:
             self._materialize(w)
             w.batch = split([(rid, w.latents.pop(rid)) for rid in ids], patch_size=self.cfg.patch_size)
             w.batch_ids = ids
-            if (self.cfg.use_cache and self.cfg.graph_steps and w.cache is not None
-                    and device_compaction_ok(w.batch)):
-                w.graph = CachedStepGraph(w.batch, self.weights, w.cache)
+        if (w.graph is None and self.cfg.use_cache and self.cfg.graph_after_steps > 0 and w.cache is not None
+                and w.comp_steps >= self.cfg.graph_after_steps and device_compaction_ok(w.batch)):
+            w.graph = CachedStepGraph(w.batch, self.weights, w.cache)
         batch = w.batch
         order = [self._meta[e.request_id] for e in batch.requests]
         dev = require_cuda()
@@ -630,6 +639,7 @@ class Engine:
             cache = w.cache if self.cfg.use_cache else None
             new, st = numeric_step(batch, self.weights, cache, bias, rates)
         batch.data = new
+        w.comp_steps += 1
         t1.record()
         t1.synchronize()
         self._skipped += st.skipped
@@ -784,28 +794,35 @@ class Engine:
 
 def measure_step_ms(model_cfg, weights, comps: Sequence[dict], patch_size: int = 32, reps: int = 3,
                     use_cache: bool = False, seed: int = 0, steps: int = 50) -> list[tuple[dict, float]]:
-    """Measured device time (ms) of one denoising step for each composition, through the
-    same call the wall plane makes.
+    """Measured device time (ms) of one steady-state denoising step for each composition, through
+    the call the wall plane makes on a resident batch (numeric_step on the CSP latents; the split
+    happens once per composition, as in the wall plane).
 
-    Without the cache: median of `reps` steps after one warm-up.  With the cache: the
-    composition is denoised for 12 steps with a BlockCache in the loop (outputs fed back
-    as latents); the result is the lifetime-weighted mean of a request served for `steps`
-    steps -- the first 4 (cold cache) weighted 4/steps, the steady state the rest."""
+    Without the cache: median of `reps` steps after one warm-up step (the first step on a new
+    batch also builds its plans).  With the cache: the composition is denoised for 12 steps with
+    a BlockCache in the loop (outputs fed back as latents); the result is the lifetime-weighted
+    mean of a request served for `steps` steps -- the first 4 (cold cache) weighted 4/steps, the
+    steady state the rest."""
     import torch
 
     from ._dev import require_cuda
     from .cache import BlockCache, PredictorConfig
-    from .csp import reassemble, split
+    from .csp import split
     from .engine_step import numeric_step
     dev = require_cuda()
     out = []
     for comp in comps:
         reqs = []
+        # seeded N(0,1) latents drawn on the device (a host normal() of 64 x 320 x 128^2 doubles
+        # took seconds per composition); the step time does not depend on the values
+        gen = torch.Generator(device=dev).manual_seed(seed)
         for cls in CLASS_ORDER:
             for j in range(comp.get(cls, 0)):
                 d = STANDARD_CLASSES[cls].latent
-                x = np.random.default_rng([seed, len(reqs)]).normal(size=(model_cfg.channels, d, d))
-                reqs.append((f"{cls}{j}", torch.as_tensor(x, dtype=torch.float32, device=dev)))
+                reqs.append((f"{cls}{j}", torch.randn((model_cfg.channels, d, d), generator=gen, device=dev)))
+        b = split(reqs, patch_size=patch_size)
+        bias = torch.zeros((b.n_requests, model_cfg.channels), dtype=torch.float32, device=dev)
+        rates = torch.full((b.n_requests,), 0.1, dtype=torch.float32, device=dev)
         cache = BlockCache(model_cfg.n_blocks, PredictorConfig()) if use_cache else None
         n_runs = 12 if use_cache else reps + 1
         times = []
@@ -816,24 +833,18 @@ def measure_step_ms(model_cfg, weights, comps: Sequence[dict], patch_size: int =
         for rep in range(n_runs):
             t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             t0.record()
-            b = split(reqs, patch_size=patch_size)
-            bias = torch.zeros((b.n_requests, model_cfg.channels), dtype=torch.float32, device=dev)
-            rates = torch.full((b.n_requests,), 0.1, dtype=torch.float32, device=dev)
             new, _ = numeric_step(b, weights, cache, bias, rates)
-            lat = reassemble(b, new)
             t1.record()
             t1.synchronize()
             times.append(t0.elapsed_time(t1))
             if use_cache:
-                reqs = [(rid, lat[rid]) for rid, _ in reqs]
+                b.data = new
         if gc_was:
             gc.enable()
         if os.environ.get("PS_CALIB_DEBUG"):
             print("calibration", dict(comp), [round(t, 3) for t in times],
                   f"reserved {torch.cuda.memory_reserved() / 2**30:.1f} GiB",
-                  f"allocated {torch.cuda.memory_allocated() / 2**30:.1f} GiB",
-                  f"alloc_retries {torch.cuda.memory_stats().get('num_alloc_retries', 0)}",
-                  f"cudaMalloc {torch.cuda.memory_stats().get('num_device_alloc', 0)}", file=sys.stderr, flush=True)
+                  f"allocated {torch.cuda.memory_allocated() / 2**30:.1f} GiB", file=sys.stderr, flush=True)
         if use_cache:
             cold, warm = float(np.mean(times[:4])), float(np.mean(times[4:]))
             k = min(4, steps)
@@ -849,7 +860,7 @@ CALIBRATION_COMPS = ({"low": 1}, {"med": 1}, {"high": 1}, {"low": 4, "med": 4, "
 
 
 def calibrate_latency_model(model_cfg, weights, n_compositions: int = 240, n_train: int = 200,
-                            max_batch: int = 12, reps: int = 2, seed: int = 0, classes=("low", "med", "high"),
+                            max_batch: int = 12, reps: int = 3, seed: int = 0, classes=("low", "med", "high"),
                             patch_size: int = 32):
     """Measure n_compositions distinct random batch compositions (1..max_batch requests) on the
     GPU (measure_step_ms, uncached), train the MLP latency model on n_train of them (PAPER.md:
