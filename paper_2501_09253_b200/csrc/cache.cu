@@ -68,14 +68,50 @@ __device__ __forceinline__ double leaf_sum(const T* a, const T* b, int n) {
         d8[2 * k + 1] = __dmul_rn(d1, d1);
       }
     };
-    sq8(0, r);
+    // Fast form of the same arithmetic: d = a - b in fp32 is exact iff rounding down and up
+    // agree (both finite); then d has <= 24 significant bits, d^2 is exact in fp64, so
+    // fma(d, d, r) rounds the same exact sum r + d^2 once -- bit-identical to
+    // dadd(r, dmul(dsub(a, b), dsub(a, b))) with one F2F.F64.F32 per element instead of two and one
+    // DFMA instead of DSUB + DMUL + DADD.  A group with any inexact difference (exponent gap > 15,
+    // overflow, non-finite) takes the fp64 path.
+    auto d8f = [&](int i, float* d) {
+      const uint4 ua = *reinterpret_cast<const uint4*>(a + i);
+      const uint4 ub = *reinterpret_cast<const uint4*>(b + i);
+      const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&ua);
+      const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&ub);
+      bool ok = true;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float a0 = __low2float(ha[k]), b0 = __low2float(hb[k]);
+        const float a1 = __high2float(ha[k]), b1 = __high2float(hb[k]);
+        d[2 * k] = __fsub_rd(a0, b0);
+        d[2 * k + 1] = __fsub_rd(a1, b1);
+        ok &= (d[2 * k] == __fsub_ru(a0, b0)) & (d[2 * k + 1] == __fsub_ru(a1, b1));
+      }
+      return ok;
+    };
+    {
+      float d[8];
+      if (d8f(0, d)) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = __dmul_rn((double)d[j], (double)d[j]);
+      } else {
+        sq8(0, r);
+      }
+    }
     int i = 8;
     const int stop = n - (n % 8);
     for (; i < stop; i += 8) {
-      double d8[8];
-      sq8(i, d8);
+      float d[8];
+      if (d8f(i, d)) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], d8[j]);
+        for (int j = 0; j < 8; ++j) r[j] = __fma_rn((double)d[j], (double)d[j], r[j]);
+      } else {
+        double d8[8];
+        sq8(i, d8);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], d8[j]);
+      }
     }
     double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                            __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
@@ -261,6 +297,246 @@ __global__ void __launch_bounds__(MseCfg<T>::LPC) mse_fused_kernel(
   }
   mse_tree_and_mask(p, w, tree_in_smem != 0, v, n, L, nodes, I, level_off, H, sigma, mask, counters);
   if (threadIdx.x == 0) tickets[p] = 0;
+}
+
+// Persistent form of the perfect-tree reuse test (default when numpy's tree over n is perfect
+// and the operands are vector-aligned): two kernels, no cross-CTA tickets or fences.
+//
+// mse_ring_kernel: 2 CTAs per SM walk the (patch, chunk of LPC leaves) items with a stride of the
+// grid; each keeps S chunks of both operands in flight as 1-D bulk copies, so the loads of the
+// next chunks overlap the fp64 leaf sums of the current one.  A bf16 leaf is summed by MSE_TPL = 4
+// threads, each owning two of numpy's eight strided accumulators (r[2q], r[2q+1]); the leaf total
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) is formed with two shuffles in that order, then the n % 8
+// tail -- numpy's arithmetic, 4x the threads.  The chunk's leaves reduce pairwise (shuffles in
+// lane order, one barrier) to the chunk subtree root, written to scratch.
+// mse_root_kernel: per patch, the perfect tree over its chunk roots, the mask, the counters.
+// (One CTA per chunk with a ticket convoyed -- all resident CTAs of the GPU loaded, then all
+// computed with the HBM idle: 40% of DRAM peak, 47 us; a ring with one thread per leaf ran out of
+// warps (8 per SM) for the fp64 chains and waited on its MEMBAR.SC ticket fences: 84 us.)
+// Bit-identical to mse_fused_kernel.
+constexpr int MSE_MAX_STAGES = 4;
+template <typename T>
+struct MseRing {
+  static constexpr int TPL = sizeof(T) == 2 ? 2 : 1;  // threads per leaf
+  static constexpr int THREADS = MseCfg<T>::LPC * TPL;
+};
+
+// bf16 leaf over TPL = 2 adjacent lanes (h = lane % 2).  All lanes call it (shuffle); `on` masks
+// lanes without a leaf.  Returns the leaf sum on h == 0.
+__device__ __forceinline__ double leaf_sum_h2(const __nv_bfloat16* a, const __nv_bfloat16* b, int n, int h, bool on) {
+  auto sq = [&](int i) {
+    const double d = __dsub_rn((double)__bfloat162float(a[i]), (double)__bfloat162float(b[i]));
+    return __dmul_rn(d, d);
+  };
+  if (n < 8) {  // sequential from -0.0, one lane
+    double res = -0.0;
+    if (on && h == 0)
+      for (int i = 0; i < n; ++i) res = __dadd_rn(res, sq(i));
+    return res;
+  }
+  // Lane h owns numpy's accumulators r[4h .. 4h+3]: elements 4h .. 4h+3 of every 8-element
+  // group (one 8-byte load per operand).  A branch-free sweep takes the fp32 differences rounded
+  // down and up -- equal iff exact (see leaf_sum); the XOR of their bits is OR-accumulated (one
+  // LOP3), ignoring the sign bit, which only an exact zero (-0 vs +0) can flip -- and accumulates
+  // fma(d, d, r).  If any difference was inexact the lane redoes its sweep in fp64: both sweeps
+  // round the same exact values.
+  const int stop = n - (n % 8);
+  const uint2* pa = reinterpret_cast<const uint2*>(a + 4 * h);
+  const uint2* pb = reinterpret_cast<const uint2*>(b + 4 * h);
+  const int ng = stop / 8;
+  double r[4] = {0.0, 0.0, 0.0, 0.0};
+  if (on) {
+    uint32_t bad = 0;
+    auto diffs = [&](int k, float (&d)[4]) {
+      const uint2 ua = pa[2 * k], ub = pb[2 * k];
+      const float av[4] = {__uint_as_float(ua.x << 16), __uint_as_float(ua.x & 0xffff0000u),
+                           __uint_as_float(ua.y << 16), __uint_as_float(ua.y & 0xffff0000u)};
+      const float bv[4] = {__uint_as_float(ub.x << 16), __uint_as_float(ub.x & 0xffff0000u),
+                           __uint_as_float(ub.y << 16), __uint_as_float(ub.y & 0xffff0000u)};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        d[e] = __fsub_rd(av[e], bv[e]);
+        bad |= __float_as_uint(d[e]) ^ __float_as_uint(__fsub_ru(av[e], bv[e]));
+      }
+    };
+    {
+      float d[4];
+      diffs(0, d);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) r[e] = __dmul_rn((double)d[e], (double)d[e]);
+    }
+#pragma unroll 3
+    for (int k = 1; k < ng; ++k) {
+      float d[4];
+      diffs(k, d);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) r[e] = __fma_rn((double)d[e], (double)d[e], r[e]);
+    }
+    if (bad & 0x7fffffffu) {
+      for (int k = 0; k < ng; ++k) {
+        const uint2 ua = pa[2 * k], ub = pb[2 * k];
+        const uint32_t aw[4] = {ua.x << 16, ua.x & 0xffff0000u, ua.y << 16, ua.y & 0xffff0000u};
+        const uint32_t bw[4] = {ub.x << 16, ub.x & 0xffff0000u, ub.y << 16, ub.y & 0xffff0000u};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const double f = __dsub_rn((double)__uint_as_float(aw[e]), (double)__uint_as_float(bw[e]));
+          r[e] = k ? __dadd_rn(r[e], __dmul_rn(f, f)) : __dmul_rn(f, f);
+        }
+      }
+    }
+  }
+  const double t = __dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3]));  // h = 0: (r0+r1)+(r2+r3)
+  double res = __dadd_rn(t, __shfl_down_sync(0xffffffffu, t, 1));         // + ((r4+r5)+(r6+r7))
+  if (on && h == 0)
+    for (int i = stop; i < n; ++i) res = __dadd_rn(res, sq(i));
+  return res;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(MseRing<T>::THREADS + 32, 2) mse_ring_kernel(
+    const T* __restrict__ x, int64_t n, const int32_t* __restrict__ slots, const T* __restrict__ snap,
+    const uint8_t* __restrict__ exists, const int32_t* __restrict__ streak, int max_streak,
+    const int32_t* __restrict__ leaves, int L, int I, int CP, int P, int S, int stage_elems, int RW,
+    int leaf_len, int cp_shift, double* __restrict__ scratch) {
+  // leaf_len > 0: every leaf has that many elements (leaf l starts at l * leaf_len), so the item
+  // loop reads no plan table; CP = 1 << cp_shift chunks per patch.
+  // Warp-specialised: warps [0, NW) sum leaves; warp NW is the producer -- it resolves the
+  // entries (slot, exists, streak: three dependent loads) of its next 32 items at once, one item
+  // per lane, and issues the bulk copies as stages free up, so no compute warp waits on the
+  // dependent loads (on warp 0 they held the whole CTA at the next barrier: 22% of the stalls).
+  constexpr int LPC = MseCfg<T>::LPC, EPV = MseCfg<T>::EPV, TPL = MseRing<T>::TPL;
+  constexpr int CT = MseRing<T>::THREADS, NW = CT / 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[MSE_MAX_STAGES], empty[MSE_MAX_STAGES];
+  __shared__ int dead[MSE_MAX_STAGES];
+  pdl_wait();
+  const int n_items = P * CP;
+  if ((int)blockIdx.x >= n_items) return;
+  const int stride = L + I;
+  T* stages = reinterpret_cast<T*>(smem_raw);
+  double* red = reinterpret_cast<double*>(smem_raw + (size_t)S * 2 * stage_elems * sizeof(T));
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == NW) {  // ---------------------------------------------------------- producer
+    int live_w = 0, slot_w = -1;
+    int j = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++j) {
+      if ((j & 31) == 0) {  // entries of items j .. j+31, one per lane
+        const int itl = it + lane * (int)gridDim.x;
+        slot_w = -1;
+        live_w = 0;
+        if (itl < n_items) {
+          slot_w = slots[itl >> cp_shift];
+          live_w = entry_live(slot_w, exists, streak, max_streak) ? 1 : 0;
+        }
+      }
+      const int live = __shfl_sync(0xffffffffu, live_w, j & 31);
+      const int slot = __shfl_sync(0xffffffffu, slot_w, j & 31);
+      const int s = j % S;
+      if (lane == 0) {
+        if (j >= S) mbar_wait(&empty[s], (uint32_t)(((j / S) - 1) & 1));
+        dead[s] = live ? 0 : 1;
+        if (!live) {
+          mbar_arrive(&full[s]);
+        } else {
+          const int p = it >> cp_shift, c = it & (CP - 1);
+          const int l0 = c * LPC, l1 = min(L, l0 + LPC);
+          const int64_t e0 = leaf_len > 0 ? (int64_t)l0 * leaf_len : (int64_t)leaves[2 * l0];
+          const int64_t e1 = leaf_len > 0 ? (int64_t)l1 * leaf_len
+                                          : (int64_t)leaves[2 * (l1 - 1)] + leaves[2 * (l1 - 1) + 1];
+          const int64_t v0 = e0 & ~int64_t(EPV - 1), v1 = (e1 + EPV - 1) & ~int64_t(EPV - 1);
+          const uint32_t bytes = (uint32_t)((v1 - v0) * sizeof(T));
+          T* sa = stages + (size_t)s * 2 * stage_elems;
+          mbar_arrive_expect_tx(&full[s], 2 * bytes);
+          bulk_load(sa, x + (int64_t)p * n + v0, bytes, &full[s]);
+          bulk_load(sa + stage_elems, snap + (int64_t)slot * n + v0, bytes, &full[s]);
+        }
+      }
+      __syncwarp();
+    }
+    return;
+  }
+  // ------------------------------------------------------------------------ compute warps
+  const int lt = threadIdx.x / TPL, q = threadIdx.x % TPL;
+  int j = 0;
+  for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++j) {
+    const int s = j % S;
+    mbar_wait(&full[s], (uint32_t)((j / S) & 1));
+    const int p = it >> cp_shift, c = it & (CP - 1);
+    if (dead[s]) {  // no entry / streak exhausted: mse_root_kernel writes the mask
+      named_bar_sync(1, CT);  // every compute thread has read dead[s] before the stage is released
+      if (threadIdx.x == 0) mbar_arrive(&empty[s]);
+      continue;
+    }
+    const int l0 = c * LPC, l1 = min(L, l0 + LPC);
+    const int64_t v0 = (leaf_len > 0 ? (int64_t)l0 * leaf_len : (int64_t)leaves[2 * l0]) & ~int64_t(EPV - 1);
+    const T* sa = stages + (size_t)s * 2 * stage_elems;
+    const int l = l0 + lt;
+    const bool on = l < l1;
+    const int64_t st = on ? (leaf_len > 0 ? (int64_t)l * leaf_len : (int64_t)leaves[2 * l]) - v0 : 0;
+    const int ln = on ? (leaf_len > 0 ? leaf_len : leaves[2 * l + 1]) : 8;
+    double leaf;
+    if constexpr (TPL == 2) {
+      leaf = leaf_sum_h2(sa + st, sa + stage_elems + st, ln, q, on);
+    } else {
+      leaf = on ? leaf_sum<T>(sa + st, sa + stage_elems + st, ln) : 0.0;
+    }
+    // the chunk's perfect subtree over its (l1 - l0, a power of two) leaves: butterfly adds in
+    // lane order give each warp's subtree (left + right at every level), then warp 0 combines the
+    // warp roots the same way.  A chunk shorter than LPC (L < LPC) pads with +0.0 leaves on the
+    // right, whose subtrees are +0.0 and add exactly (a leaf sum is never -0.0).
+    double t = (q == 0 && on) ? leaf : 0.0;
+#pragma unroll
+    for (int off = TPL; off < 32; off <<= 1) t = __dadd_rn(t, __shfl_down_sync(0xffffffffu, t, off));
+    double* wr = red + (j & 1) * NW;  // double-buffered: the next item writes the other half
+    if (lane == 0) wr[warp] = t;
+    named_bar_sync(1, CT);  // the stage is consumed: the producer may refill it
+    if (threadIdx.x == 0) mbar_arrive(&empty[s]);
+    if (warp == 0) {
+      double w = lane < NW ? wr[lane] : 0.0;
+#pragma unroll
+      for (int off = 1; off < NW; off <<= 1) w = __dadd_rn(w, __shfl_down_sync(0xffffffffu, w, off));
+      if (lane == 0) scratch[(int64_t)p * stride + c] = w;  // chunk subtree root
+    }
+  }
+}
+
+// grid P, 32 threads: patch p's tree over its CP chunk roots (perfect, CP a power of two), then
+// the mask (mse < sigma, strict) and the counters; patches without a live entry get mask 0.
+__global__ void __launch_bounds__(32) mse_root_kernel(const int32_t* __restrict__ slots,
+                                                      const uint8_t* __restrict__ exists,
+                                                      const int32_t* __restrict__ streak, int max_streak,
+                                                      double sigma, int64_t n, int L, int I, int CP,
+                                                      double* __restrict__ scratch, uint8_t* __restrict__ mask,
+                                                      int64_t* __restrict__ counters) {
+  extern __shared__ double rr[];
+  pdl_wait();
+  const int p = blockIdx.x;
+  if (!entry_live(slots[p], exists, streak, max_streak)) {
+    if (threadIdx.x == 0) {
+      mask[p] = 0;
+      if (counters) atomicAdd(reinterpret_cast<unsigned long long*>(counters + 1), 1ull);
+    }
+    return;
+  }
+  double* v = scratch + (int64_t)p * (L + I);
+  for (int i = threadIdx.x; i < CP; i += blockDim.x) rr[i] = v[i];
+  __syncthreads();
+  const double r = smem_pairwise(rr, rr + CP, CP);
+  if (threadIdx.x == 0) {
+    v[I > 0 ? L + I - 1 : 0] = r;  // readable in scratch (ps.mse)
+    const double mse = __ddiv_rn(__dadd_rn(0.0, r), (double)n);
+    const bool m = mse < sigma;
+    mask[p] = m ? 1 : 0;
+    if (counters) atomicAdd(reinterpret_cast<unsigned long long*>(counters + (m ? 0 : 1)), 1ull);
+  }
 }
 
 // single CTA: ascending active (mask == 0) and reused (mask == 1) lists.
@@ -534,6 +810,17 @@ __global__ void __launch_bounds__(1024) compact_lists_kernel(
 
 extern "C" {
 
+static int ring_num_sms() {
+  static int nsm = 0;
+  if (nsm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  return nsm;
+}
+
 int ps_cache_predict(void* stream, const void* x, int dtype, int P, int64_t n, const int32_t* slots,
                      const void* snap_in, const uint8_t* exists, const int32_t* streak, double sigma, int max_streak,
                      const int32_t* leaves, int n_leaves, const int32_t* nodes, int n_internal,
@@ -567,7 +854,35 @@ int ps_cache_predict(void* stream, const void* x, int dtype, int P, int64_t n, c
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(mse_fused_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(mse_ring_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr = true;
+    }
+    static const bool ring_off = getenv("PS_MSE_RING_OFF") && atoi(getenv("PS_MSE_RING_OFF")) != 0;
+    if (!ring_off && perfect && n % MseCfg<T>::EPV == 0 && ((uintptr_t)x & 15) == 0 && ((uintptr_t)snap_in & 15) == 0) {
+      const int stage_elems = (int)(pairwise_max_span(n, LPC) + 2 * MseCfg<T>::EPV);
+      const int stage_bytes = 2 * stage_elems * (int)sizeof(T);
+      const int RW = 32;  // red: 2 x (warps per CTA <= 16) doubles
+      int S = (110 * 1024 - 2 * RW * 8) / stage_bytes;
+      if (S > MSE_MAX_STAGES) S = MSE_MAX_STAGES;
+      // equal leaves (the widest leaf is n / L): starts by arithmetic; g is a power of two
+      const int leaf_len = (n % n_leaves == 0 && pairwise_max_span(n, 1) == n / n_leaves) ? (int)(n / n_leaves) : 0;
+      int cp_shift = 0;
+      while ((1 << cp_shift) < g) ++cp_shift;
+      if (S >= 2 && (size_t)2 * g * 8 <= 48 * 1024 && (1 << cp_shift) == g) {
+        const size_t smem_r = (size_t)S * stage_bytes + 2 * RW * 8;
+        const int items = P * g;
+        const int grid = items < 2 * ring_num_sms() ? items : 2 * ring_num_sms();
+        launch_pdl(mse_ring_kernel<T>, dim3(grid), dim3(MseRing<T>::THREADS + 32), smem_r, st, (const T*)x, n, slots,
+                   (const T*)snap_in, exists, streak, max_streak, leaves, n_leaves, n_internal, g, P, S, stage_elems,
+                   RW, leaf_len, cp_shift, scratch);
+        count_launch();
+        const int rc = check_launch("mse_reuse_test");
+        if (rc != PS_OK) return rc;
+        launch_pdl(mse_root_kernel, dim3(P), dim3(32), (size_t)2 * g * 8, st, slots, exists, streak, max_streak,
+                   sigma, n, n_leaves, n_internal, g, scratch, mask, counters);
+        count_launch();
+        return check_launch("mse_reuse_roots");
+      }
     }
     if (smem > 200 * 1024) return set_error(PS_ERR_INPUT, "cache_predict: leaf span too large");
     launch_pdl(mse_fused_kernel<T>, dim3((n_leaves + LPC - 1) / LPC, P), dim3(LPC), (size_t)smem, st,

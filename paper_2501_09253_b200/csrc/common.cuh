@@ -251,6 +251,13 @@ PS_DEV float tanh_exp(float x) {
   const float e = exp2f(2.8853900817779268f * x);  // 2 / ln 2
   return 1.f - __fdividef(2.f, e + 1.f);
 }
+// device-scope release/acquire atomic add (a per-item ticket without a MEMBAR.SC.GPU fence)
+PS_DEV int atom_add_acq_rel_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+PS_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 PS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 PS_DEV void reg_fence32(uint32_t (&r)[32]) {
 #pragma unroll

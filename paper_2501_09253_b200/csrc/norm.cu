@@ -127,6 +127,89 @@ __global__ void __launch_bounds__(256, 4) gn_partials_kernel(const __nv_bfloat16
   }
 }
 
+// Warp-per-slice form (default): one warp streams a (patch, group) slice with 4 independent
+// 32-byte non-allocating loads (LDG.256) per lane in flight, accumulating shifted moments (shift
+// K = the slice's first element) in fp32: a single pass, no block reductions.
+// mean = K + S1/n, M2 = S2 - S1^2/n.  Two warps per CTA: 1856 small CTAs fill every SM evenly
+// in one wave (one-CTA-per-slice two-pass kernel: 6.3 waves of short CTAs, 22.6 us in ncu;
+// 8-warp CTAs: 464 CTAs left SMs with 4 vs 3 of them, 17.4 us; four warps per slice with the
+// quarters' sums added: 19.3 us; a persistent bulk-copy ring reduced by whole CTAs: 24 us).
+// (The parts machinery below adds GNW_PARTS warps' sums of one slice in a fixed order.)
+__device__ __forceinline__ void acc8(const uint4& r, float K, float& s1, float& s2) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+  float a = 0.f, b = 0.f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float d0 = __low2float(h[k]) - K, d1 = __high2float(h[k]) - K;
+    a += d0 + d1;
+    b = fmaf(d0, d0, fmaf(d1, d1, b));
+  }
+  s1 += a;
+  s2 += b;
+}
+constexpr int GNW_WARPS = 2, GNW_PARTS = 1, GNW_UNROLL = 4;
+constexpr int GNW_SLICES = GNW_WARPS / GNW_PARTS;  // slices per CTA
+__global__ void __launch_bounds__(GNW_WARPS * 32, 16) gn_partials_warp_kernel(
+    const __nv_bfloat16* __restrict__ x, int C, int hw, int G, const int32_t* __restrict__ plist,
+    const int32_t* __restrict__ n_dev, int n_host, float* __restrict__ partials) {
+  __shared__ float2 red[GNW_WARPS];
+  pdl_wait();
+  const int n_items = (n_dev != nullptr ? min(*n_dev, n_host) : n_host) * G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x * GNW_SLICES + warp / GNW_PARTS, part = warp % GNW_PARTS;
+  const bool live = item < n_items;
+  int p = 0, g = 0;
+  const int cg = C / G;
+  float t1 = 0.f, t2 = 0.f;
+  if (live) {
+    const int q = item / G;
+    g = item - q * G;
+    p = plist ? __ldg(plist + q) : q;
+    const __nv_bfloat16* base = x + ((int64_t)p * C + (int64_t)g * cg) * hw;
+    const int nv = cg * hw / 16;  // 32-byte vectors
+    const int per = (nv + GNW_PARTS - 1) / GNW_PARTS;
+    const int v0 = part * per, v1 = min(nv, v0 + per);
+    const float K = __bfloat162float(base[0]);  // the slice's shift, the same for its parts
+    float s1[2] = {0.f, 0.f}, s2[2] = {0.f, 0.f};
+    for (int k0 = v0; k0 < v1; k0 += 32 * GNW_UNROLL) {
+      uint4 r[GNW_UNROLL][2];
+#pragma unroll
+      for (int i = 0; i < GNW_UNROLL; ++i) {
+        const int k = k0 + i * 32 + lane;
+        if (k < v1) ld_global_nc_v8(base + (int64_t)k * 16, *reinterpret_cast<uint32_t(*)[8]>(&r[i][0]));
+      }
+#pragma unroll
+      for (int i = 0; i < GNW_UNROLL; ++i)
+        if (k0 + i * 32 + lane < v1) {
+          acc8(r[i][0], K, s1[0], s2[0]);
+          acc8(r[i][1], K, s1[1], s2[1]);
+        }
+    }
+    t1 = s1[0] + s1[1];
+    t2 = s2[0] + s2[1];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+      t2 += __shfl_xor_sync(0xffffffffu, t2, o);
+    }
+    if (lane == 0) red[warp] = make_float2(t1, t2);
+  }
+  __syncthreads();
+  if (live && part == 0 && lane == 0) {
+    // the parts share the shift, so their moments add (fixed order: deterministic)
+    float u1 = red[warp].x, u2 = red[warp].y;
+#pragma unroll
+    for (int k = 1; k < GNW_PARTS; ++k) {
+      u1 += red[warp + k].x;
+      u2 += red[warp + k].y;
+    }
+    const float n = (float)(cg * hw);
+    const float K = __bfloat162float(x[((int64_t)p * C + (int64_t)g * cg) * hw]);
+    partials[((int64_t)p * G + g) * 2] = K + u1 / n;
+    partials[((int64_t)p * G + g) * 2 + 1] = fmaxf(u2 - u1 * (u1 / n), 0.f);
+  }
+}
+
 // host: one CTA per (patch, group) slice.  (Persistent software-pipelined and bulk-copy staged
 // variants measured 21-26 us against 20-21 us; a group-pair kernel -- one CTA per two adjacent
 // groups, all ten 16-byte loads per thread issued first, one shifted-sum block reduction --
@@ -136,6 +219,14 @@ static void launch_gn_partials(cudaStream_t st, const void* x, int P, int C, int
   (void)P;
   (void)C;
   const auto xb = (const __nv_bfloat16*)x;
+  const int64_t slice = (int64_t)(C / G) * hw * 2;
+  static const bool warp_off = getenv_flag("PS_GN_WARP_OFF");
+  if (!warp_off && n > 0 && C % G == 0 && slice % 32 == 0 && ((uintptr_t)x & 31) == 0) {
+    const int items = n * G;
+    launch_pdl(gn_partials_warp_kernel, dim3((items + GNW_SLICES - 1) / GNW_SLICES), dim3(GNW_WARPS * 32), 0, st, xb,
+               C, hw, G, plist, n_dev, n, partials);
+    return;
+  }
   launch_pdl(gn_partials_kernel, dim3(n, G), dim3(256), 0, st, xb, C, hw, G, plist, n_dev, partials);
 }
 

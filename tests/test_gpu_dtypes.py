@@ -82,3 +82,39 @@ def test_pipeline_rejects_non_finite_latents():
     with pytest.raises(ps.InputError):
         pipe.run([bad], [[0, 0]], [4, 4], [out])
     pipe.run([ok], [[0, 0]], [4, 4], [out])  # the flag is per call
+
+
+def _bf16_adversarial(shape, seed):
+    """bf16 operands whose differences are inexact in fp32 in some 8-element groups: magnitudes
+    spread over 2^-60 .. 2^60, exact ties, zeros of both signs, values near the bf16 maximum (the
+    fp32 difference overflows) and subnormal bf16."""
+    rng = np.random.default_rng(seed)
+    n = int(np.prod(shape))
+    a = rng.normal(size=n) * np.exp2(rng.integers(-60, 61, size=n))
+    b = rng.normal(size=n) * np.exp2(rng.integers(-60, 61, size=n))
+    k = rng.choice(n, size=n // 16, replace=False)
+    b[k] = a[k]                                   # zero differences
+    z = rng.choice(n, size=n // 32, replace=False)
+    a[z] = np.where(rng.random(z.size) < 0.5, 0.0, -0.0)
+    big = rng.choice(n, size=max(2, n // 512), replace=False)
+    a[big], b[big[: big.size // 2]] = 3.3e38, -3.3e38
+    sub = rng.choice(n, size=max(2, n // 256), replace=False)
+    b[sub] = rng.normal(size=sub.size) * 1e-39    # bf16 subnormals
+    ta = torch.tensor(a, dtype=torch.float32).to(torch.bfloat16).reshape(shape)
+    tb = torch.tensor(b, dtype=torch.float32).to(torch.bfloat16).reshape(shape)
+    return ta, tb
+
+
+@pytest.mark.parametrize("shape,seed", [((320, 32, 32), 0), ((4, 16, 16), 1), ((64, 8, 8), 2), ((3, 5, 7), 3)])
+def test_mse_bf16_mixed_exponents_hex_equal(shape, seed):
+    """The bf16 leaf's fp32-difference fast path (exact iff round-down == round-up) and its fp64
+    fallback give numpy's fp64 pairwise mean bit for bit, on groups where both paths run."""
+    ta, tb = _bf16_adversarial(shape, seed)
+    a, b = ta.double().numpy(), tb.double().numpy()
+    want = float(np.mean((a - b) ** 2))
+    assert ps.mse(ta, tb).hex() == want.hex()
+    # the same on moderate values (the all-fast-path case)
+    rng = np.random.default_rng(seed + 100)
+    ua = torch.tensor(rng.normal(size=shape), dtype=torch.float32).to(torch.bfloat16)
+    ub = torch.tensor(rng.normal(size=shape), dtype=torch.float32).to(torch.bfloat16)
+    assert ps.mse(ua, ub).hex() == float(np.mean((ua.double().numpy() - ub.double().numpy()) ** 2)).hex()
