@@ -359,6 +359,7 @@ def run_split(args):
 
     e2e_step()
     barrier()
+    bytes0 = int(getattr(ex, "bytes_moved", 0))  # payload bytes this rank sent (eager steps count them)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
@@ -366,6 +367,7 @@ def run_split(args):
     e1.record()
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+    sent_per_step = (int(getattr(ex, "bytes_moved", 0)) - bytes0) // max(1, args.steps)
     P = sum((d // PATCH) ** 2 for d in DIMS)
     attn_ms = [a.elapsed_time(z) for a, z in attn_events]
     if args.slo:
@@ -396,7 +398,7 @@ def run_split(args):
                     "path": "per rank: pinned host latents -H2D-> split -> denoise_batch_shard (7 blocks, "
                             "exchanges over NCCL) -> D2H, eager"},
             "gpu_launches": launches if launches is not None else "graph-replayed (see smoke/tests for counts)",
-            "exchange_bytes_per_step_rank0": int(getattr(ex, "bytes_moved", 0)),
+            "exchange_bytes_sent_per_step_rank0": sent_per_step,
             "roofline": {"bound": "tensor", "kernel": "per-image flash attention over rank 0's owned queries "
                                                       "(CUDA events in the last eager warm-up step)",
                          "algorithmic": "4*T_img*D per owned query token = %.3e FLOP per launch" % flops0,

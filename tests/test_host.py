@@ -143,51 +143,3 @@ def test_pairwise_restatement_matches_numpy_and_differs_from_naive():
             naive_diff += (s / d.size) != float(np.mean((a - b) ** 2))
     assert naive_diff > 0  # the tree matters: sequential summation gives other bits
 
-
-def test_request_ownership_balanced_and_deterministic():
-    from paper_2501_09253_b200.shard import assign, step_flops
-    reqs = [(f"r{i}", d) for i, d in enumerate([64, 96, 128] * 4)]
-    cost = lambda d: step_flops(d, 320, 1280, 7)
-    for world in (1, 2, 4, 8):
-        own = assign(reqs, world, cost)
-        assert own == assign(reqs, world, cost)
-        assert set(own) <= set(range(world))
-        loads = [sum(cost(d) for (_, d), o in zip(reqs, own) if o == r) for r in range(world)]
-        assert max(loads) <= sum(loads) / world + cost(128) + 1
-
-
-def _gloo_worker(rank, world, port, q):
-    import torch
-    import torch.distributed as dist
-    from paper_2501_09253_b200.shard import local_requests, step_flops
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    reqs = [(f"r{i}", d) for i, d in enumerate([64, 96, 128] * 4 + [256])]
-    mine = local_requests(reqs, rank, world, lambda d: step_flops(d, 320, 1280, 7))
-    got = [None] * world
-    dist.all_gather_object(got, [r for r, _ in mine])
-    t = torch.tensor([float(rank + 1)])
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)  # bench.py times the job as the max over ranks
-    q.put((rank, got, float(t)))
-    dist.destroy_process_group()
-
-
-def test_two_rank_ownership_with_gloo():
-    import multiprocessing as mp
-    import socket
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    res = [q.get(timeout=120) for _ in procs]
-    for p in procs:
-        p.join(timeout=60)
-    (_, g0, t0), (_, g1, t1) = sorted(res)
-    assert g0 == g1 and t0 == t1 == 2.0
-    flat = [r for part in g0 for r in part]
-    assert sorted(flat) == sorted(f"r{i}" for i in range(13)) and len(set(flat)) == 13
