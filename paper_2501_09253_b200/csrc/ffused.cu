@@ -43,7 +43,9 @@ struct FfCfg {
   static_assert(CP + FF_HC + FF_HC / 2 <= 512, "TMEM");
 };
 
-template <int CP>
+// PROBE: the p.dbg build (role wait counters, epilogue phase clocks) -- a separate instantiation
+// so the production kernel carries no probe registers (the H epilogue sits at 128 registers)
+template <int CP, bool PROBE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
     ff_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
                    const __grid_constant__ CUtensorMap tmW2, const FfParams p) {
@@ -120,9 +122,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
   };
 
   unsigned long long cnt[4] = {0, 0, 0, 0};
-  const long long t_start = clock64();
+  // epilogue phase clocks (p.dbg, warp 4): [0] H TMEM load, [1] load + GELU, [2] Hb store + arrive,
+  // [3] chunks, [4] output drain per tile, [5] tiles
+  __shared__ unsigned long long ph[6];
+  if (threadIdx.x < 6) ph[threadIdx.x] = 0;
+  const long long t_start = PROBE ? clock64() : 0;
   auto tw = [&](uint64_t* bar, uint32_t par, int k) {
-    if (p.dbg) {
+    if (PROBE) {
       const long long t0 = clock64();
       mbar_wait(bar, par);
       cnt[k] += clock64() - t0;
@@ -287,16 +293,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 16; ++i) bq[i] = __ldg(b1 + i);
         tw(h_full, g & 1, 0);
+        const bool probe = PROBE && warp == 4 && lane == 0;
+        const long long ph0 = probe ? clock64() : 0;
         tc_fence_after();
         uint32_t r0[32], r1[32];
         PS_TMEM_LD32(tmem + lane_base + Cfg::H_COL + wg * 64, r0);
         PS_TMEM_LD32(tmem + lane_base + Cfg::H_COL + wg * 64 + 32, r1);
         tmem_ld_wait();
+        if (probe) ph[0] += clock64() - ph0;
         reg_fence32(r0);
         reg_fence32(r1);
         tc_fence_before();
         mbar_arrive_cluster(h_empty_l);
         uint32_t pk[32];
+        if (PROBE && p.dbg[31]) {  // timing experiment: the chunk epilogue without the GELU
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            pk[2 * i] = pack_bf16(__uint_as_float(r0[4 * i]) + bq[i].x, __uint_as_float(r0[4 * i + 1]) + bq[i].y);
+            pk[2 * i + 1] = pack_bf16(__uint_as_float(r0[4 * i + 2]) + bq[i].z, __uint_as_float(r0[4 * i + 3]) + bq[i].w);
+            pk[16 + 2 * i] = pack_bf16(__uint_as_float(r1[4 * i]) + bq[8 + i].x, __uint_as_float(r1[4 * i + 1]) + bq[8 + i].y);
+            pk[16 + 2 * i + 1] =
+                pack_bf16(__uint_as_float(r1[4 * i + 2]) + bq[8 + i].z, __uint_as_float(r1[4 * i + 3]) + bq[8 + i].w);
+          }
+        } else
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           pk[2 * i] = gelu_bf16x2(pack_bf16(__uint_as_float(r0[4 * i]) + bq[i].x,
@@ -308,13 +327,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
           pk[16 + 2 * i + 1] = gelu_bf16x2(pack_bf16(__uint_as_float(r1[4 * i + 2]) + bq[8 + i].z,
                                                      __uint_as_float(r1[4 * i + 3]) + bq[8 + i].w));
         }
+        if (probe) ph[1] += clock64() - ph0;  // load + release + GELU
         tw(hs_empty, (g & 1) ^ 1, 1);  // MMA2 of the previous chunk has read the buffer
         if (p.ts) {  // A operand in TMEM: 32 columns of bf16 pairs per warpgroup, no smem traffic
+          const long long ph2 = probe ? clock64() : 0;
           PS_TMEM_ST16(tmem + lane_base + Cfg::HB_COL + wg * 32, pk);
           PS_TMEM_ST16(tmem + lane_base + Cfg::HB_COL + wg * 32 + 16, (pk + 16));
           tmem_st_wait();
           tc_fence_before();
           mbar_arrive_cluster(hs_full_l);
+          if (probe) { ph[2] += clock64() - ph2; ph[3] += 1; }
           continue;
         }
         uint8_t* hrow = sH + wg * FF_BM * 128 + row * 128;
@@ -327,6 +349,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
       }
       // ---- output: O + b2 + residual -> NCHW (32-column chunks dealt to the 3 warpgroups)
       tw(o_full, li & 1, 2);
+      const long long po = (PROBE && warp == 4 && lane == 0) ? clock64() : 0;
       tc_fence_after();
       const bool ok = mt >= 0 && (mt + 1) * FF_BM <= p.M;
       const int tok_v = (mt < 0 ? 0 : mt) * FF_BM + wq * 32 + seg * 16;
@@ -402,9 +425,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
         tc_fence_before();
         mbar_arrive_cluster(o_empty_l);
       }
+      if (PROBE && warp == 4 && lane == 0) { ph[4] += clock64() - po; ph[5] += 1; }
     }
   }
-  if (p.dbg && lane == 0 && leader) {
+  if (PROBE && lane == 0 && leader) {
     const unsigned long long tot = clock64() - t_start;
     // [0-3] producer: w_empty, x_empty | [4-8] mma: w_full, h_empty, hs_full, o_empty, total
     // [9-12] epilogue (warp 4): h_full, hs_empty, o_full, total | [13] producer total
@@ -416,6 +440,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
     if (warp == 4) {
       for (int k = 0; k < 3; ++k) atomicAdd(p.dbg + 9 + k, cnt[k]);
       atomicAdd(p.dbg + 12, tot);
+      for (int k = 0; k < 6; ++k) atomicAdd(p.dbg + 16 + k, ph[k]);
     }
   }
   tc_fence_before();
@@ -430,14 +455,18 @@ static int launch_ff(const CUtensorMap& x, const CUtensorMap& w1, const CUtensor
   using Cfg = FfCfg<CP>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(ff_pair_kernel<CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    cudaFuncSetAttribute(ff_pair_kernel<CP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    cudaFuncSetAttribute(ff_pair_kernel<CP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr = true;
   }
   const int num_m = p.m_map ? p.m_count : (p.M + FF_BM - 1) / FF_BM;
   const int units = (num_m + 1) / 2;
   if (units == 0) return PS_OK;
   const int grid = 2 * (units < sms / 2 ? units : sms / 2);
-  launch_pdl(ff_pair_kernel<CP>, dim3(grid), dim3(FF_THREADS), Cfg::SMEM, st, x, w1, w2, p);
+  if (p.dbg)
+    launch_pdl(ff_pair_kernel<CP, true>, dim3(grid), dim3(FF_THREADS), Cfg::SMEM, st, x, w1, w2, p);
+  else
+    launch_pdl(ff_pair_kernel<CP, false>, dim3(grid), dim3(FF_THREADS), Cfg::SMEM, st, x, w1, w2, p);
   count_launch();
   return check_launch("ff_pair");
 }

@@ -32,7 +32,7 @@ for fused in (False, True, False, True):
 
 patched.FF_FUSED = True
 from paper_2501_09253_b200 import _lib
-dbg = torch.zeros(16, dtype=torch.int64, device="cuda")
+dbg = torch.zeros(32, dtype=torch.int64, device="cuda")
 _lib.load().ps_feed_forward_debug(dbg.data_ptr())
 ctx.feed_forward(a, ff, res)
 torch.cuda.synchronize()
@@ -42,3 +42,23 @@ f = lambda x, t: x / t if t else 0
 print(f"producer: w_empty {f(d[0], d[13]):.2f} x_empty {f(d[1], d[13]):.2f}")
 print(f"mma     : w_full {f(d[4], d[8]):.2f} h_empty {f(d[5], d[8]):.2f} hs_full {f(d[6], d[8]):.2f} o_empty {f(d[7], d[8]):.2f}")
 print(f"epilogue: h_full {f(d[9], d[12]):.2f} hs_empty {f(d[10], d[12]):.2f} o_full {f(d[11], d[12]):.2f}")
+print(f"epilogue phases per chunk (cycles): H load {f(d[16], d[19]):.0f}, load+GELU {f(d[17], d[19]):.0f}, "
+      f"Hb store+arrive {f(d[18], d[19]):.0f}; output drain per tile {f(d[20], d[21]):.0f}; "
+      f"chunk period {f(d[12], d[19]):.0f} (warp-4 total / chunks)")
+
+# timing experiment (probe build only): the same launch with the chunk epilogue's GELU skipped
+for nogelu in (0, 1):
+    dbg.zero_()
+    dbg[31] = nogelu
+    _lib.load().ps_feed_forward_debug(dbg.data_ptr())
+    for _ in range(2):
+        ctx.feed_forward(a, ff, res)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        ctx.feed_forward(a, ff, res)
+    e1.record()
+    torch.cuda.synchronize()
+    _lib.load().ps_feed_forward_debug(None)
+    print(f"probe build, gelu {'off' if nogelu else 'on'}: {e0.elapsed_time(e1) / 10 * 1e3:.1f} us")
