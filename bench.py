@@ -327,10 +327,17 @@ def run_split(args):
                     step()
             torch.cuda.current_stream().wait_stream(s_)
             graph = g
-            for _ in range(2):
-                graph.replay()
         except Exception as e:  # noqa: BLE001 -- the eager step is the fallback, reported in the line
             graph, graph_err = None, f"{type(e).__name__}: {e}"[:300]
+        # every rank replays a graph or none does (a capture records the NCCL calls without running
+        # them, so a rank whose capture failed has issued nothing the others wait for)
+        ok = torch.tensor([0 if graph is None else 1], dtype=torch.int32, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0 and graph is not None:
+            graph, graph_err = None, "another rank's capture failed"
+        if graph is not None:
+            for _ in range(2):  # warm replays (every rank has a graph: the collectives match)
+                graph.replay()
     barrier()
     launches0 = _lib.launches()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

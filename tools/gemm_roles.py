@@ -6,7 +6,7 @@ from paper_2501_09253_b200 import _lib
 from paper_2501_09253_b200._dev import stream
 
 T = 118784
-def run(name, M, N, K, epi, bn=0, out_tiled=0, a_tiled=0, resid=False):
+def run(name, M, N, K, epi, bn=0, out_tiled=0, a_tiled=0, resid=False, pair=0):
     a = torch.randn(M if not a_tiled else ((M + 127) // 128 * 128), K, device="cuda").to(torch.bfloat16)
     b = (torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
     bias = torch.zeros(N, device="cuda")
@@ -19,6 +19,7 @@ def run(name, M, N, K, epi, bn=0, out_tiled=0, a_tiled=0, resid=False):
     g.b, g.N, g.K, g.bias = b.data_ptr(), N, K, bias.data_ptr()
     g.epi, g.out, g.ldo, g.bn, g.out_tiled = epi, out.data_ptr(), N, bn, out_tiled
     g.P, g.ps = M // 1024, 32
+    g.cta_pair = pair
     if epi == 3:
         g.out2, g.ldo2, g.n_split, g.ldo = out2.data_ptr(), (M + 63) // 64 * 64, 2 * N // 3, 2 * N // 3
     if epi == 2:
@@ -46,6 +47,14 @@ run("ff1", T, 1280, 320, 1, out_tiled=1)
 run("ff2", T, 320, 1280, 2, a_tiled=1, resid=True)
 run("ff2-cl", T, 320, 1280, 0, a_tiled=1)
 run("plain256", T, 256, 1024, 0)
+if len(sys.argv) > 1 and sys.argv[1] == "pair":
+    run("conv-p320", T, 320, 2880, 0, bn=320, pair=2)
+    run("conv-p160", T, 320, 2880, 0, bn=160, pair=2)
+    run("conv-p256", T, 320, 2880, 0, bn=256, pair=2)
+    run("conv-s320", T, 320, 2880, 0, bn=320, pair=1)
+    run("conv-s160", T, 320, 2880, 0, bn=160, pair=1)
+    run("qkv-p", T, 960, 320, 3, pair=2)
+    run("oproj-p", T, 320, 320, 0, pair=2)
 if len(sys.argv) > 1 and sys.argv[1] == "bn":
     run("ff2-160", T, 320, 1280, 2, a_tiled=1, resid=True, bn=160)
     run("ff2-320", T, 320, 1280, 2, a_tiled=1, resid=True, bn=320)
