@@ -580,13 +580,41 @@ def measure_hbm_kernels(pipe, peak_gbs):
               len(tc["ps_cache_substitute"])),
              ("ps_cache_finish (50% mask)", n * 2 * (2 * m + 4 * (P - m)), float(np.mean(tc["ps_cache_finish"])),
               len(tc["ps_cache_finish"]))]
+    # read-only context: a plain read-reduction (torch.sum) of the same bytes, timed the same way
+    # -- read-only launches of these sizes stop well short of the copy bandwidth `peak_gbs` is
+    flushbuf = torch.ones(flush // 4, device="cuda")
+    sink = torch.zeros(1, device="cuda")
+
+    def read_floor(nbytes):
+        t = torch.ones(nbytes // 2, dtype=torch.bfloat16, device="cuda")
+        for _ in range(3):
+            t.sum(dtype=torch.float32)
+        ts = []
+        for _ in range(12):
+            sink.add_(flushbuf.sum())
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            t.sum(dtype=torch.float32)
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return float(np.median(ts))
+    floors = {act: read_floor(act), 2 * act: read_floor(2 * act)}
+    read_only = {"ps_gn_partials": act, "ps_cache_predict (fp64 pairwise MSE reuse test, all live)": 2 * act}
     out = []
     for name, nbytes, ms_, cnt in rows:
         gbs = nbytes / (ms_ * 1e-3) / 1e9
-        out.append({"kernel": name, "bytes": int(nbytes), "us": round(ms_ * 1e3, 2), "gbs": round(gbs, 1),
-                    "frac": round(gbs / peak_gbs, 3), "launches": cnt})
+        row = {"kernel": name, "bytes": int(nbytes), "us": round(ms_ * 1e3, 2), "gbs": round(gbs, 1),
+               "frac": round(gbs / peak_gbs, 3), "launches": cnt}
+        if name in read_only:
+            f = floors[read_only[name]]
+            row["read_floor_us"] = round(f * 1e3, 2)
+            row["vs_read_floor"] = round(f / ms_, 3)
+        out.append(row)
     return {"peak_gbs": peak_gbs, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, read+write bytes)",
             "timing": "each launch alone, L2 flushed (256 MB write) before it, CUDA events on its stream",
+            "read_floor": "read-only kernels: torch.sum over the same bytes timed the same way "
+                          "(vs_read_floor = its time / ours)",
             "kernels": out}
 
 

@@ -147,11 +147,11 @@ __device__ __forceinline__ void acc8(const uint4& r, float K, float& s1, float& 
   s1 += a;
   s2 += b;
 }
-constexpr int GNW_WARPS = 2, GNW_PARTS = 1, GNW_UNROLL = 4;
-constexpr int GNW_SLICES = GNW_WARPS / GNW_PARTS;  // slices per CTA
-__global__ void __launch_bounds__(GNW_WARPS * 32, 16) gn_partials_warp_kernel(
+template <int GNW_WARPS, int GNW_PARTS, int GNW_UNROLL>
+__global__ void __launch_bounds__(GNW_WARPS * 32) gn_partials_warp_kernel(
     const __nv_bfloat16* __restrict__ x, int C, int hw, int G, const int32_t* __restrict__ plist,
     const int32_t* __restrict__ n_dev, int n_host, float* __restrict__ partials) {
+  constexpr int GNW_SLICES = GNW_WARPS / GNW_PARTS;  // slices per CTA
   __shared__ float2 red[GNW_WARPS];
   pdl_wait();
   const int n_items = (n_dev != nullptr ? min(*n_dev, n_host) : n_host) * G;
@@ -223,8 +223,16 @@ static void launch_gn_partials(cudaStream_t st, const void* x, int P, int C, int
   static const bool warp_off = getenv_flag("PS_GN_WARP_OFF");
   if (!warp_off && n > 0 && C % G == 0 && slice % 32 == 0 && ((uintptr_t)x & 31) == 0) {
     const int items = n * G;
-    launch_pdl(gn_partials_warp_kernel, dim3((items + GNW_SLICES - 1) / GNW_SLICES), dim3(GNW_WARPS * 32), 0, st, xb,
-               C, hw, G, plist, n_dev, n, partials);
+    // (warps per CTA, warps per slice, 32-byte loads per lane in flight) = (2, 1, 4).  Round-2
+    // sweep (tools/gn_sweep.py, L2 flushed, CUDA events): (2,1,4) 18.4 us, (1,1,4) 18.5, (4,1,4)
+    // 18.4, (2,1,8) 21.9, (2,1,10) 20.5, (4,2,5) 20.5, (2,2,5) 20.5 -- a plain read-reduction of the
+    // same 76 MB (torch.sum) takes 24.6 us: read-only launches of this size stop well short of
+    // the copy bandwidth the roofline uses (profiles/r2_read_floor.jsonl).
+#define PS_GNW(W, PT, U)                                                                                      \
+  launch_pdl(gn_partials_warp_kernel<W, PT, U>, dim3((items + W / PT - 1) / (W / PT)), dim3(W * 32), 0, st, xb, C, \
+             hw, G, plist, n_dev, n, partials)
+    PS_GNW(2, 1, 4);
+#undef PS_GNW
     return;
   }
   launch_pdl(gn_partials_kernel, dim3(n, G), dim3(256), 0, st, xb, C, hw, G, plist, n_dev, partials);

@@ -335,3 +335,33 @@ def test_persistent_attention_concurrent_streams_and_graph():
         g.replay()
         torch.cuda.synchronize()
         assert torch.equal(got, want)
+
+
+def test_persistent_attention_two_graphs_replayed_concurrently():
+    """Two graphs captured the default way (torch.cuda.graph's shared capture stream) replayed at
+    the same time on two streams: each captured launch owns its tile-ticket pair, so neither
+    replay drops or repeats the other's tiles (a per-stream counter would be shared)."""
+    import paper_2501_09253_b200 as ps
+    torch.manual_seed(7)
+    cfg = ps.ModelConfig(arch="dit_like", channels=128, hidden=256, n_blocks=1, groups=8, seed=6)
+    at = ps.init_weights(cfg)[0][1][1]
+    b = ps.split([(f"r{i}", torch.randn(128, d, d)) for i, d in enumerate((64, 96, 64, 128))], patch_size=16)
+    x1 = torch.randn(b.n_patches, 128, 16, 16, device="cuda").to(torch.bfloat16)
+    x2 = torch.randn(b.n_patches, 128, 16, 16, device="cuda").to(torch.bfloat16)
+    want1 = ps.patched_self_attention(b, x1, at).clone()
+    want2 = ps.patched_self_attention(b, x2, at).clone()
+    g1, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g1):
+        o1 = ps.patched_self_attention(b, x1, at)
+    with torch.cuda.graph(g2):
+        o2 = ps.patched_self_attention(b, x2, at)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(8):
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s1):
+            g1.replay()
+        with torch.cuda.stream(s2):
+            g2.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(o1, want1)
+        assert torch.equal(o2, want2)
