@@ -26,6 +26,7 @@ constexpr int FF_HC = 128;      // hidden units per chunk (2 k-blocks of MMA2)
 constexpr int FF_NS = 8;        // weight ring slots
 constexpr int FF_SLOT = 10240;  // bytes per slot (max of a W1 piece 8 KB and a W2 piece <= 10 KB)
 constexpr int FF_THREADS = 512;
+constexpr int FF_ST_LD = 36;    // row pitch (floats) of the output epilogue's transpose tiles
 
 template <int CP>
 struct FfCfg {
@@ -35,7 +36,11 @@ struct FfCfg {
   static constexpr int NHALF = CP / 2;        // N of one MMA2
   static constexpr int W2_ROWS = NHALF / 2;   // this CTA's B rows of one MMA2
   static constexpr int W1_ROWS = FF_HC / 2;   // this CTA's B rows of one MMA1 (64)
-  static constexpr int STG = 12 * 2048;       // per-warp transpose tiles of the output epilogue
+  // per-warp [16][FF_ST_LD] fp32 transpose tiles of the output epilogue: rows padded 32 -> 36
+  // floats so the transposed float4 reads (16 lanes on 16 rows of one column range) spread over
+  // the banks -- with 32-float rows they were 16-way conflicts (77% of the kernel's shared-load
+  // wavefronts, ncu round 2)
+  static constexpr int STG = 12 * 16 * FF_ST_LD * 4;
   static constexpr int SMEM = X_BYTES + H_BYTES + FF_NS * FF_SLOT + STG + 1024 + 512;
   // TMEM: O (Cp fp32) | H chunk (128 fp32) | GELU(H) chunk as bf16 pairs (64), MMA2's A (p.ts)
   static constexpr int O_COL = 0, H_COL = CP, HB_COL = CP + FF_HC;
@@ -276,7 +281,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
     const uint32_t h_empty_l = mapa_shared(h_empty, 0);
     const uint32_t hs_full_l = mapa_shared(hs_full, 0);
     const uint32_t o_empty_l = mapa_shared(o_empty, 0);
-    float* st = sStg + (warp - 4) * 512;          // [16][32] fp32 transpose tile of this warp
+    float* st = sStg + (warp - 4) * 16 * FF_ST_LD;  // [16][FF_ST_LD] fp32 transpose tile of this warp
     const int ci = lane >> 1, seg = lane & 1;      // transposed role: column, 16-token half
     int g = 0, li = 0;
     for (int w = unit0; w < n_items; w += unit_step, ++li) {
@@ -389,12 +394,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
         for (int s16 = 0; s16 < 32; s16 += 16) {
           const int nv = cc + s16 + ci;
 #pragma unroll
-          for (int i = 0; i < 16; ++i) st[i * 32 + lane] = v[s16 + i];
+          for (int i = 0; i < 16; ++i) st[i * FF_ST_LD + lane] = v[s16 + i];
           __syncwarp();
           if (ok && nv < p.c_real) {
             const size_t off = ((size_t)pidx_v * p.c_real + nv) * p.hw + pix_v;
             const uint4 rs0 = rsd[s16 / 8], rs1 = rsd[s16 / 8 + 1];
-            const float4* src = reinterpret_cast<const float4*>(st + ci * 32 + seg * 16);
+            const float4* src = reinterpret_cast<const float4*>(st + ci * FF_ST_LD + seg * 16);
             float o[16];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {

@@ -428,16 +428,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               __syncwarp();
               st = reinterpret_cast<float*>(tma_stage + (warp - 4) * 4096 + (n_store & 1) * 2048);
             }
+            // per-warp [16][32] tile: 16-byte groups XOR-swizzled by row, so the transposed
+            // float4 reads (16 lanes on 16 rows of one column range) hit distinct banks -- plain
+            // [16][32] reads were 16-way bank conflicts; writes stay a permutation of each row
 #pragma unroll
-            for (int i = 0; i < 16; ++i) st[i * st_ld + st_row] = v[s16 + i];
+            for (int i = 0; i < 16; ++i) st[i * st_ld + (wst ? st_row ^ ((i & 7) << 2) : st_row)] = v[s16 + i];
             if (wst) __syncwarp();
             else named_bar_sync(bar_id, 128);
             if (tr_vt || nv < p.c_real) {
-              const float4* src = reinterpret_cast<const float4*>(st + ci * st_ld + seg * 16);
+              const float4* src = reinterpret_cast<const float4*>(st + ci * st_ld);
+              const int swz = wst ? (ci & 7) << 2 : 0;
               float o[16];
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
-                const float4 f = src[q];
+                const float4 f = src[((seg * 16 + 4 * q) ^ swz) >> 2];
                 o[4 * q] = f.x; o[4 * q + 1] = f.y; o[4 * q + 2] = f.z; o[4 * q + 3] = f.w;
               }
               const __nv_bfloat162* h0 = reinterpret_cast<const __nv_bfloat162*>(&rs0);
