@@ -56,7 +56,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
                    const __grid_constant__ CUtensorMap tmW2, const FfParams p) {
   using Cfg = FfCfg<CP>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned, derived from smem_raw by an integer offset so the compiler keeps the
+  // shared address space (uintptr_t arithmetic made every access through it a generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sX = smem;
   uint8_t* sH = sX + Cfg::X_BYTES;
   uint8_t* sW = sH + Cfg::H_BYTES;

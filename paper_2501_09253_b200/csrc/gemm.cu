@@ -95,7 +95,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                    const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
   using Cfg = GemmCfg<BN, PAIR>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned, derived from smem_raw by an integer offset so the compiler keeps the
+  // shared address space (uintptr_t arithmetic made every access through it a generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* epi_stage = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
   uint8_t* tma_stage = smem + Cfg::STAGES * Cfg::STAGE_BYTES + Cfg::STAGE_EPI;
   uint64_t* full = reinterpret_cast<uint64_t*>(tma_stage + Cfg::STAGE_TMA);
