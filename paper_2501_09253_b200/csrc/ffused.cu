@@ -131,8 +131,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
   unsigned long long cnt[4] = {0, 0, 0, 0};
   // epilogue phase clocks (p.dbg, warp 4): [0] H TMEM load, [1] load + GELU, [2] Hb store + arrive,
   // [3] chunks, [4] output drain per tile, [5] tiles
-  __shared__ unsigned long long ph[6];
-  if (threadIdx.x < 6) ph[threadIdx.x] = 0;
+  __shared__ unsigned long long ph[8];
+  __shared__ long long t_mma1;  // PROBE: clock when the issuer started the current chunk's MMA1
+  if (PROBE && threadIdx.x < 8) ph[threadIdx.x] = 0;
   const long long t_start = PROBE ? clock64() : 0;
   auto tw = [&](uint64_t* bar, uint32_t par, int k) {
     if (PROBE) {
@@ -216,6 +217,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
         for (int c = 0; c < NC; ++c, ++g) {
           if (warp == 1) {
             tw(h_empty, (g & 1) ^ 1, 1);  // the epilogue drained H(g - 1)
+            if (PROBE && lane == 0) t_mma1 = clock64();
             tc_fence_after();
             for (int kb = 0; kb < Cfg::KB; ++kb) {
               const long long gi = base + pos_w1(c) + kb;
@@ -302,6 +304,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
         tw(h_full, g & 1, 0);
         const bool probe = PROBE && warp == 4 && lane == 0;
         const long long ph0 = probe ? clock64() : 0;
+        if (probe) { ph[6] += ph0 - *(volatile long long*)&t_mma1; ph[7] += 1; }  // MMA1 issue -> H ready
         tc_fence_after();
         uint32_t r0[32], r1[32];
         PS_TMEM_LD32(tmem + lane_base + Cfg::H_COL + wg * 64, r0);
@@ -447,7 +450,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
     if (warp == 4) {
       for (int k = 0; k < 3; ++k) atomicAdd(p.dbg + 9 + k, cnt[k]);
       atomicAdd(p.dbg + 12, tot);
-      for (int k = 0; k < 6; ++k) atomicAdd(p.dbg + 16 + k, ph[k]);
+      for (int k = 0; k < 8; ++k) atomicAdd(p.dbg + 16 + k, ph[k]);
     }
   }
   tc_fence_before();

@@ -44,7 +44,7 @@ print(f"mma     : w_full {f(d[4], d[8]):.2f} h_empty {f(d[5], d[8]):.2f} hs_full
 print(f"epilogue: h_full {f(d[9], d[12]):.2f} hs_empty {f(d[10], d[12]):.2f} o_full {f(d[11], d[12]):.2f}")
 print(f"epilogue phases per chunk (cycles): H load {f(d[16], d[19]):.0f}, load+GELU {f(d[17], d[19]):.0f}, "
       f"Hb store+arrive {f(d[18], d[19]):.0f}; output drain per tile {f(d[20], d[21]):.0f}; "
-      f"chunk period {f(d[12], d[19]):.0f} (warp-4 total / chunks)")
+      f"chunk period {f(d[12], d[19]):.0f} (warp-4 total / chunks); MMA1 issue -> H ready {f(d[22], d[23]):.0f}")
 
 # timing experiment (probe build only): the same launch with the chunk epilogue's GELU skipped
 for nogelu in (0, 1):
