@@ -245,6 +245,8 @@ def run_ours(args):
             line["config3_cache"] = measure_cache(cfg, weights, reqs)
         if args.hbm_table:
             line["hbm_kernels"] = measure_hbm_kernels(pipe, _peaks().get("hbm_gbs", 6548.5))
+        if args.config5:
+            line["config5_single_gpu"] = measure_config5(cfg, weights)
         if args.cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline_sample()
         print(json.dumps(line), flush=True)
@@ -506,6 +508,46 @@ def measure_cache(cfg, weights, reqs, steps=12, sigma=0.1, max_streak=3):
                     "compaction lists -> compacted block on recomputed patches (kernels read their work counts "
                     "from device memory) -> fused splice/streak/snapshot; no host round trip inside the step, "
                     "one counter read-back after it"}
+
+
+def measure_config5(cfg, weights, steps=4):
+    """BASELINE config 5's batch (1x 2048 px + 8x 512 px, patch 64) on ONE B200 through the same
+    graph-captured pipeline: the T = 65,536-token attention and the ps = 64 geometry at speed
+    (config 5 itself is an 8-GPU configuration; its split path is tests/test_gpu_split.py and
+    tools/split_projection.py)."""
+    import torch
+
+    import paper_2501_09253_b200 as ps
+    from paper_2501_09253_b200 import patched
+    from paper_2501_09253_b200.pipeline import DenoisePipeline
+    dims, pz = [256] + [64] * 8, 64
+    ev = []
+    patched.ATTN_TIMER = ev
+    pipe = DenoisePipeline(cfg, weights, dims, pz)
+    pipe.set_prompts([ps.make_prompt(cfg, f"c5-{i}") for i in range(len(dims))])
+    g = torch.Generator(device="cuda").manual_seed(5)
+    for k in range(pipe.n_sets):
+        for x in pipe.lat_in[k]:
+            x.copy_(torch.randn(x.shape, generator=g, device="cuda"))
+        pipe.rates[k].fill_(0.1)
+    pipe.prepare()
+    patched.ATTN_TIMER = None
+    graph_attn = ev[-2 * BLOCKS:]
+    pipe.run_resident(2)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    pipe.run_resident(steps)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    P = sum((d // pz) ** 2 for d in dims)
+    attn_ms = float(np.mean([a.elapsed_time(b) for a, b in graph_attn]))
+    flops = attention_flops(dims, pz)
+    return {"workload": "config5 batch on 1 GPU: 1x 2048 px (T = 65,536) + 8x 512 px, patch 64, SDXL-shaped, 7 blocks",
+            "value": P / (ms * 1e-3), "unit": UNIT, "patches_per_step": P, "ms_per_step": ms, "steps": steps,
+            "attention_avg_launch_ms": attn_ms, "attention_tflops": flops / (attn_ms * 1e-3) / 1e12,
+            "attention_share_of_step": attn_ms * BLOCKS / ms}
 
 
 def measure_hbm_kernels(pipe, peak_gbs):
@@ -823,6 +865,8 @@ def main():
                     help="skip the per-kernel HBM roofline table")
     ap.add_argument("--no-cache-run", dest="cache_run", action="store_false",
                     help="skip the config-3 (patch cache in the loop) measurement")
+    ap.add_argument("--no-config5", dest="config5", action="store_false",
+                    help="skip the config-5 batch (2048 px + 8x 512 px, patch 64) on one GPU")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

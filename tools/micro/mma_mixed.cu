@@ -1,0 +1,83 @@
+// tcgen05.mma cta_group::2 throughput when the fused feed-forward's two MMA kinds share the
+// tensor pipe: SS M256 N128 (MMA1: X W1^T into 128 TMEM columns) interleaved with TS M256 N160
+// (MMA2: A = bf16 H from TMEM, accumulating into another 160 columns), operands resident (no
+// TMA traffic), issued from one thread or from two threads (one per kind, as in ff_pair_kernel).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o mma_mixed mma_mixed.cu
+#include <cstdio>
+#include "../../paper_2501_09253_b200/csrc/common.cuh"
+using namespace ps;
+
+// MODE 0: SS only (20 MMAs / iter), 1: TS only (16 / iter), 2: both, one issuer, 3: both, two issuers
+template <int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) mixed_kernel(int iters, unsigned long long* cycles) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sa = smem;           // 128 x 64 bf16 (16 KB): X k-block
+  uint8_t* sb1 = smem + 16384;  // 64 x 64 bf16 (8 KB): this CTA's half of W1 (N = 128)
+  uint8_t* sb2 = smem + 24576;  // 80 x 64 bf16 (10 KB): this CTA's half of W2 (N = 160)
+  __shared__ uint64_t bar[2];
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool leader = cluster_rank() == 0;
+  for (int i = threadIdx.x; i < 34816 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+  if (threadIdx.x == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); fence_mbar_init(); }
+  if (warp == 0) tmem_alloc_2sm(&tslot, 512);
+  fence_proxy_async();
+  tc_fence_before(); cluster_sync(); tc_fence_after();
+  const uint32_t tmem = tslot;
+  constexpr uint32_t id1 = idesc_bf16_f32(256, 128), id2 = idesc_bf16_f32(256, 160);
+  auto ss = [&](int k) { mma_bf16_ss_2sm(tmem, sdesc_sw128(sa + (k & 3) * 32), sdesc_sw128(sb1 + (k & 3) * 32), id1, 1); };
+  auto ts = [&](int k) { mma_bf16_ts_2sm(tmem + 128, tmem + 448 + (k & 7) * 8, sdesc_sw128(sb2 + (k & 3) * 32), id2, 1); };
+  long long t0 = clock64();
+  if (leader && lane == 0) {
+    if (MODE == 3) {
+      if (warp == 0) { for (int it = 0; it < iters; ++it) for (int k = 0; k < 20; ++k) ss(k); mma_commit_2sm(&bar[0], 0x3); }
+      if (warp == 1) { for (int it = 0; it < iters; ++it) for (int k = 0; k < 16; ++k) ts(k); mma_commit_2sm(&bar[1], 0x3); }
+    } else if (warp == 0) {
+      for (int it = 0; it < iters; ++it) {
+        if (MODE == 0 || MODE == 2) for (int k = 0; k < 20; ++k) ss(k);
+        if (MODE == 1 || MODE == 2) for (int k = 0; k < 16; ++k) ts(k);
+      }
+      mma_commit_2sm(&bar[0], 0x3);
+      if (MODE != 3) mma_commit_2sm(&bar[1], 0x3);
+    }
+  }
+  __syncwarp();
+  if (warp == 0) {
+    mbar_wait(&bar[0], 0);
+    mbar_wait(&bar[1], 0);
+    const long long t1 = clock64();
+    if (lane == 0 && blockIdx.x == 0) *cycles = t1 - t0;
+  }
+  tc_fence_before(); cluster_sync(); tc_fence_after();
+  if (warp == 0) tmem_dealloc_2sm(tmem, 512);
+}
+
+template <int MODE>
+void run(const char* name, int sms) {
+  const int iters = 4000;
+  unsigned long long* d;
+  cudaMalloc(&d, 8);
+  const int smem = 34816 + 2048;
+  cudaFuncSetAttribute(mixed_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  mixed_kernel<MODE><<<sms, 128, smem>>>(50, d);
+  cudaDeviceSynchronize();
+  mixed_kernel<MODE><<<sms, 128, smem>>>(iters, d);
+  cudaDeviceSynchronize();
+  unsigned long long cyc;
+  cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
+  // per SM per iteration: SS 20 x (128 x 128 x 16 x 2), TS 16 x (128 x 160 x 16 x 2)
+  const double ss = (MODE != 1) ? 20.0 * 128 * 128 * 16 * 2 : 0, tsf = (MODE != 0) ? 16.0 * 128 * 160 * 16 * 2 : 0;
+  printf("%-34s %6.0f FLOP/clk/SM (peak 8192)  %8.0f cycles/iter  err=%s\n", name, (ss + tsf) * iters / cyc,
+         (double)cyc / iters, cudaGetErrorString(cudaGetLastError()));
+}
+
+int main() {
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  run<0>("SS N128 only (MMA1)", sms);
+  run<1>("TS N160 only (MMA2)", sms);
+  run<2>("SS + TS, one issuer", sms);
+  run<3>("SS + TS, two issuers", sms);
+  return 0;
+}

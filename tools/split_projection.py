@@ -7,8 +7,6 @@ collectives replaced by no-ops (NullComm); its device time is measured with CUDA
 events.  The projected W-GPU step = max over ranks of (device time + bytes the
 rank exchanges / NVLink bandwidth), with the exchange NOT overlapped (upper bound).
 Bandwidth: 770 GB/s per direction (measured peer copy, B200_PROFILING.md).
-Also reports whole-request ownership (shard.py) for contrast: the 2048 px image
-cannot be split there, so its owner bounds the step.
 """
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
