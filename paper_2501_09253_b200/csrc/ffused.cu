@@ -129,6 +129,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
   };
 
   unsigned long long cnt[4] = {0, 0, 0, 0};
+  // PROBE timeline: clock64 stamps of CTA 0's first 40 chunks at dbg[64 + 8 g + k] (k: 0/1 MMA1
+  // issue start/end, 2/3 MMA2 issue start/end, 4 H ready seen, 5 H released, 6 GELU done,
+  // 7 Hb handed to MMA2)
+#define FF_STAMP(gg, k)                                                                 \
+  do {                                                                                  \
+    if (PROBE && blockIdx.x == 0 && (gg) < 40) p.dbg[64 + 8 * (gg) + (k)] = clock64(); \
+  } while (0)
   // epilogue phase clocks (p.dbg, warp 4): [0] H TMEM load, [1] load + GELU, [2] Hb store + arrive,
   // [3] chunks, [4] output drain per tile, [5] tiles
   __shared__ unsigned long long ph[8];
@@ -218,6 +225,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
           if (warp == 1) {
             tw(h_empty, (g & 1) ^ 1, 1);  // the epilogue drained H(g - 1)
             if (PROBE && lane == 0) t_mma1 = clock64();
+            if (lane == 0) FF_STAMP(g, 0);
             tc_fence_after();
             for (int kb = 0; kb < Cfg::KB; ++kb) {
               const long long gi = base + pos_w1(c) + kb;
@@ -234,6 +242,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
                 if (kb == Cfg::KB - 1) {
                   mma_commit_2sm(h_full, 0x3);
                   if (c == NC - 1) mma_commit_2sm(x_empty, 0x3);
+                  FF_STAMP(g, 1);
                 }
               }
               __syncwarp();
@@ -241,6 +250,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
           } else {
             tw(hs_full, g & 1, 2);  // H(c) written to shared memory
             if (c == 0) tw(o_empty, (li & 1) ^ 1, 3);  // O of the previous tile drained
+            if (lane == 0) FF_STAMP(g, 2);
             tc_fence_after();
             int piece = 0;
             for (int kk = 0; kk < 2; ++kk)
@@ -267,6 +277,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
                   if (kk == 1 && (half >= 0 || nn == 1)) {  // the chunk's last W2 piece
                     mma_commit_2sm(hs_empty, 0x3);
                     if (c == NC - 1) mma_commit_2sm(o_full, 0x3);
+                    FF_STAMP(g, 3);
                   }
                 }
                 __syncwarp();
@@ -304,6 +315,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
         tw(h_full, g & 1, 0);
         const bool probe = PROBE && warp == 4 && lane == 0;
         const long long ph0 = probe ? clock64() : 0;
+        if (probe) FF_STAMP(g, 4);
         if (probe) { ph[6] += ph0 - *(volatile long long*)&t_mma1; ph[7] += 1; }  // MMA1 issue -> H ready
         tc_fence_after();
         uint32_t r0[32], r1[32];
@@ -315,6 +327,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
         reg_fence32(r1);
         tc_fence_before();
         mbar_arrive_cluster(h_empty_l);
+        if (probe) FF_STAMP(g, 5);
         uint32_t pk[32];
         if (PROBE && p.dbg[31]) {  // timing experiment: the chunk epilogue without the GELU
 #pragma unroll
@@ -338,6 +351,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
                                                      __uint_as_float(r1[4 * i + 3]) + bq[8 + i].w));
         }
         if (probe) ph[1] += clock64() - ph0;  // load + release + GELU
+        if (probe) FF_STAMP(g, 6);
         tw(hs_empty, (g & 1) ^ 1, 1);  // MMA2 of the previous chunk has read the buffer
         if (p.ts) {  // A operand in TMEM: 32 columns of bf16 pairs per warpgroup, no smem traffic
           const long long ph2 = probe ? clock64() : 0;
@@ -346,7 +360,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
           tmem_st_wait();
           tc_fence_before();
           mbar_arrive_cluster(hs_full_l);
-          if (probe) { ph[2] += clock64() - ph2; ph[3] += 1; }
+          if (probe) { ph[2] += clock64() - ph2; ph[3] += 1; FF_STAMP(g, 7); }
           continue;
         }
         uint8_t* hrow = sH + wg * FF_BM * 128 + row * 128;

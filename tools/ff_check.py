@@ -32,13 +32,20 @@ for fused in (False, True, False, True):
 
 patched.FF_FUSED = True
 from paper_2501_09253_b200 import _lib
-dbg = torch.zeros(32, dtype=torch.int64, device="cuda")
+dbg = torch.zeros(64 + 40 * 8, dtype=torch.int64, device="cuda")
 _lib.load().ps_feed_forward_debug(dbg.data_ptr())
 ctx.feed_forward(a, ff, res)
 torch.cuda.synchronize()
 _lib.load().ps_feed_forward_debug(None)
 d = dbg.tolist()
 f = lambda x, t: x / t if t else 0
+tl = np.array(d[64:64 + 320]).reshape(40, 8)
+if tl[0, 4]:
+    t0 = tl[1:, :].min()
+    print("timeline of CTA 0, chunks 1..15 (cycles from the first stamp): MMA1 issue s/e, MMA2 issue s/e, H ready, "
+          "H released, GELU done, Hb handed")
+    for gc in range(1, 16):
+        print(gc, [int(v - t0) for v in tl[gc]])
 print(f"producer: w_empty {f(d[0], d[13]):.2f} x_empty {f(d[1], d[13]):.2f}")
 print(f"mma     : w_full {f(d[4], d[8]):.2f} h_empty {f(d[5], d[8]):.2f} hs_full {f(d[6], d[8]):.2f} o_empty {f(d[7], d[8]):.2f}")
 print(f"epilogue: h_full {f(d[9], d[12]):.2f} hs_empty {f(d[10], d[12]):.2f} o_full {f(d[11], d[12]):.2f}")
