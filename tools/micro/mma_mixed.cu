@@ -7,30 +7,61 @@
 #include "../../paper_2501_09253_b200/csrc/common.cuh"
 using namespace ps;
 
-// MODE 0: SS only (20 MMAs / iter), 1: TS only (16 / iter), 2: both, one issuer, 3: both, two issuers
-template <int MODE>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) mixed_kernel(int iters, unsigned long long* cycles) {
+// MODE 0: SS only (20 MMAs / iter), 1: TS only (16 / iter), 2: both, one issuer, 3: both, two issuers,
+// 4: 3 + eight warps streaming tcgen05.ld (64 columns) / tcgen05.st (32 columns) like the FF's H
+// epilogue, 5: 4 + a bulk-copy stream into another smem region (the weight ring's TMA writes)
+template <int MODE, bool STREAM>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1) mixed_kernel(int iters, unsigned long long* cycles,
+                                                                                 const uint8_t* gsrc) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sa = smem;           // 128 x 64 bf16 (16 KB): X k-block
-  uint8_t* sb1 = smem + 16384;  // 64 x 64 bf16 (8 KB): this CTA's half of W1 (N = 128)
-  uint8_t* sb2 = smem + 24576;  // 80 x 64 bf16 (10 KB): this CTA's half of W2 (N = 160)
-  __shared__ uint64_t bar[2];
+  // STREAM: operands laid out like the FF kernel's -- A = the X tile, 5 k-blocks of 16 KB (80 KB),
+  // B of MMA1 = 5 W1 pieces of 8 KB, B of MMA2 = 4 W2 pieces of 10 KB -- every MMA of an iteration
+  // reads different smem; else one 16 KB A block and one B piece reused by every MMA
+  uint8_t* sa = smem;            // [5][128 x 64] bf16
+  uint8_t* sb1 = smem + 81920;   // [5][64 x 64] bf16
+  uint8_t* sb2 = smem + 122880;  // [4][80 x 64] bf16
+  __shared__ uint64_t bar[2], cbar;
+  __shared__ volatile int done;
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool leader = cluster_rank() == 0;
-  for (int i = threadIdx.x; i < 34816 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
-  if (threadIdx.x == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); fence_mbar_init(); }
+  for (int i = threadIdx.x; i < 163840 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+  if (threadIdx.x == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); mbar_init(&cbar, 1); fence_mbar_init(); done = 0; }
   if (warp == 0) tmem_alloc_2sm(&tslot, 512);
   fence_proxy_async();
   tc_fence_before(); cluster_sync(); tc_fence_after();
   const uint32_t tmem = tslot;
   constexpr uint32_t id1 = idesc_bf16_f32(256, 128), id2 = idesc_bf16_f32(256, 160);
-  auto ss = [&](int k) { mma_bf16_ss_2sm(tmem, sdesc_sw128(sa + (k & 3) * 32), sdesc_sw128(sb1 + (k & 3) * 32), id1, 1); };
-  auto ts = [&](int k) { mma_bf16_ts_2sm(tmem + 128, tmem + 448 + (k & 7) * 8, sdesc_sw128(sb2 + (k & 3) * 32), id2, 1); };
+  auto ss = [&](int k) {
+    const int kb = STREAM ? k >> 2 : 0;
+    mma_bf16_ss_2sm(tmem, sdesc_sw128(sa + kb * 16384 + (k & 3) * 32), sdesc_sw128(sb1 + kb * 8192 + (k & 3) * 32), id1, 1);
+  };
+  auto ts = [&](int k) {
+    const int pc = STREAM ? k >> 2 : 0;
+    mma_bf16_ts_2sm(tmem + 128, tmem + 448 + (k & 7) * 8, sdesc_sw128(sb2 + pc * 10240 + (k & 3) * 32), id2, 1);
+  };
   long long t0 = clock64();
+  if (MODE >= 4 && warp >= 4) {  // side traffic until the MMAs are done
+    const uint32_t lb = (uint32_t)((warp & 3) * 32) << 16;
+    uint32_t r[32];
+    int ph = 0;
+    while (!done) {
+      if (MODE == 5 && warp == 4 && lane == 0) {
+        mbar_arrive_expect_tx(&cbar, 10240);
+        bulk_load(smem + 163840, gsrc + (blockIdx.x & 15) * 10240, 10240, &cbar);
+        mbar_wait(&cbar, ph);
+        ph ^= 1;
+      }
+      PS_TMEM_LD32(tmem + lb + 320 + (warp >= 8 ? 32 : 0), r);
+      tmem_ld_wait();
+      reg_fence32(r);
+      PS_TMEM_ST16(tmem + lb + 416 + (warp >= 8 ? 16 : 0), r);
+      tmem_st_wait();
+    }
+  }
   if (leader && lane == 0) {
-    if (MODE == 3) {
+    if (MODE >= 3) {
       if (warp == 0) { for (int it = 0; it < iters; ++it) for (int k = 0; k < 20; ++k) ss(k); mma_commit_2sm(&bar[0], 0x3); }
       if (warp == 1) { for (int it = 0; it < iters; ++it) for (int k = 0; k < 16; ++k) ts(k); mma_commit_2sm(&bar[1], 0x3); }
     } else if (warp == 0) {
@@ -48,21 +79,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) mixed_kernel
     mbar_wait(&bar[1], 0);
     const long long t1 = clock64();
     if (lane == 0 && blockIdx.x == 0) *cycles = t1 - t0;
+    if (lane == 0) done = 1;
   }
   tc_fence_before(); cluster_sync(); tc_fence_after();
   if (warp == 0) tmem_dealloc_2sm(tmem, 512);
 }
 
-template <int MODE>
+template <int MODE, bool STREAM = false>
 void run(const char* name, int sms) {
   const int iters = 4000;
   unsigned long long* d;
   cudaMalloc(&d, 8);
-  const int smem = 34816 + 2048;
-  cudaFuncSetAttribute(mixed_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  mixed_kernel<MODE><<<sms, 128, smem>>>(50, d);
+  const int smem = 163840 + 10240 + 2048;
+  uint8_t* g;
+  cudaMalloc(&g, 16 * 10240);
+  cudaFuncSetAttribute(mixed_kernel<MODE, STREAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  mixed_kernel<MODE, STREAM><<<sms, 384, smem>>>(50, d, g);
   cudaDeviceSynchronize();
-  mixed_kernel<MODE><<<sms, 128, smem>>>(iters, d);
+  mixed_kernel<MODE, STREAM><<<sms, 384, smem>>>(iters, d, g);
   cudaDeviceSynchronize();
   unsigned long long cyc;
   cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
@@ -70,6 +104,8 @@ void run(const char* name, int sms) {
   const double ss = (MODE != 1) ? 20.0 * 128 * 128 * 16 * 2 : 0, tsf = (MODE != 0) ? 16.0 * 128 * 160 * 16 * 2 : 0;
   printf("%-34s %6.0f FLOP/clk/SM (peak 8192)  %8.0f cycles/iter  err=%s\n", name, (ss + tsf) * iters / cyc,
          (double)cyc / iters, cudaGetErrorString(cudaGetLastError()));
+  fflush(stdout);
+  fflush(stdout);
 }
 
 int main() {
@@ -79,5 +115,11 @@ int main() {
   run<1>("TS N160 only (MMA2)", sms);
   run<2>("SS + TS, one issuer", sms);
   run<3>("SS + TS, two issuers", sms);
+  run<4>("  + TMEM ld/st by 8 warps", sms);
+  run<5>("  + bulk copies 10 KB (ring writes)", sms);
+  run<0, true>("STREAM SS only", sms);
+  run<1, true>("STREAM TS only", sms);
+  run<3, true>("STREAM SS + TS, two issuers", sms);
+  run<5, true>("STREAM + TMEM ld/st + bulk copies", sms);
   return 0;
 }
