@@ -65,3 +65,25 @@ def test_gn_partials_warp_kernel(tmp_path):
         mask[written] = True
         assert not r["sub"][mask].isnan().any() and r["sub"][~mask].isnan().all()
         assert torch.equal(r["sub"][mask], r["full"][mask])
+
+
+def test_gn_partials_offset_and_outlier_shift():
+    """Shifted single-pass moments stay accurate when the shift (the slice's first element) is an
+    outlier and the data sit on a large offset: mean 50, std 1, first element of every slice at
+    50 + 8 (M2 is then a difference of two sums ~65x larger than itself)."""
+    from paper_2501_09253_b200 import _lib
+    from paper_2501_09253_b200._dev import stream
+    P, C, ps_, G = 29, 320, 32, 32
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = (50.0 + torch.randn((P, C, ps_, ps_), device="cuda", generator=g))
+    xv = x.view(P, G, -1)
+    xv[:, :, 0] = 58.0
+    x = x.to(torch.bfloat16)
+    part = torch.empty((P, G, 2), device="cuda")
+    _lib.check(_lib.load().ps_gn_partials(stream(), x.data_ptr(), P, C, ps_, G, part.data_ptr()))
+    torch.cuda.synchronize()
+    ref = x.double().view(P, G, -1)
+    mean = ref.mean(-1)
+    m2 = ((ref - mean[..., None]) ** 2).sum(-1)
+    assert float((part[..., 0].double() - mean).abs().max()) <= 2e-4  # fp32 mean of ~50 (ulp 4e-6)
+    assert float(((part[..., 1].double() - m2).abs() / m2).max()) <= 1e-4
