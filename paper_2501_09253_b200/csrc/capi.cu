@@ -404,6 +404,8 @@ int ps_gemm(void* stream, const ps_gemm_args* a) {
   // per-warp epilogue stores (no cross-warp barriers): FF1 153 -> 128 us (tools/gemm_roles.py)
   static const int warp_store = getenv("PS_GEMM_WARP_STORE") ? atoi(getenv("PS_GEMM_WARP_STORE")) : 1;
   p.warp_store = warp_store;
+  static const int gemm_tail = getenv("PS_GEMM_TAIL_SPLIT") ? atoi(getenv("PS_GEMM_TAIL_SPLIT")) : 1;
+  p.tail_split = gemm_tail;
   CUtensorMap tc;
   memset(&tc, 0, sizeof(tc));
   p.store_tma = 0;

@@ -144,6 +144,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int unit_step = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const int num_mu = PAIR ? (num_m + 1) / 2 : num_m;
   const int n_tiles = num_mu * num_n;
+  // work items: tiles, except that with p.tail_split (BN = 320, one n tile) the tiles of the
+  // last partial wave become two items each, one per N = 160 column half -- a 0.27 wave of
+  // full tiles (conv3: 464 pair tiles on 74 pairs) becomes ~0.54 wave of ~0.6-cost items
+  const int tail = (GEMM_NWG > 2 && Cfg::N_MMA == 2 && num_n == 1 && p.tail_split &&
+                    2 * (n_tiles % unit_step) <= unit_step)
+                       ? n_tiles % unit_step : 0;
+  const int n_full = n_tiles - tail;
+  const int n_items = n_full + 2 * tail;
+  auto item = [&](int w, int& half) {  // item -> tile index; half = -1 (whole tile) or 0 / 1
+    if (w < n_full) {
+      half = -1;
+      return w;
+    }
+    half = (w - n_full) & 1;
+    return n_full + ((w - n_full) >> 1);
+  };
   const int m_oob = (p.M + GEMM_BM - 1) / GEMM_BM;  // a physical tile past the end: TMA zero-fills it
   // logical -> physical 128-row tile (active-patch compaction); -1 = no tile (odd pair tail)
   auto phys_m = [&](int lm) { return lm >= num_m ? -1 : p.m_map ? __ldg(p.m_map + lm) : lm; };
@@ -169,7 +185,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       const int kcb = p.conv_cp / GEMM_BK;
-      for (int t = unit0; t < n_tiles; t += unit_step) {
+      for (int w = unit0; w < n_items; w += unit_step) {
+        int half;
+        const int t = item(w, half);
         const int mt = my_m(t);
         const int m_tile = mt < 0 ? m_oob : mt, n0 = (t % num_n) * BN;
         int p0 = 0, y0 = 0;
@@ -193,7 +211,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (PAIR) {
             // both CTAs' bytes complete on the leader's barrier
             const uint32_t fb = mapa_shared(&full[stage], 0);
-            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+            if (leader)
+              mbar_arrive_expect_tx(&full[stage], 2 * (half < 0 ? Cfg::STAGE_BYTES : Cfg::A_BYTES + Cfg::B_ROWS * 128));
             if (p.a_mode == A_CONV3) {
               const int tap = kb / kcb, cb = kb % kcb;
               tma_load_4d_2sm(sa, &tmA, fb, cb * GEMM_BK, tap % 3, y0 + tap / 3, p0);
@@ -204,10 +223,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
 #pragma unroll
             for (int j = 0; j < Cfg::N_MMA; ++j)
-              tma_load_2d_2sm(sb + j * Cfg::B_ROWS * 128, &tmB, fb, kb * GEMM_BK,
-                              n0 + j * Cfg::MMA_N + (int)rank * Cfg::B_ROWS);
+              if (half < 0 || j == half)
+                tma_load_2d_2sm(sb + j * Cfg::B_ROWS * 128, &tmB, fb, kb * GEMM_BK,
+                                n0 + j * Cfg::MMA_N + (int)rank * Cfg::B_ROWS);
           } else {
-            mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+            mbar_arrive_expect_tx(&full[stage], half < 0 ? Cfg::STAGE_BYTES : Cfg::A_BYTES + Cfg::MMA_N * 128);
             if (p.a_mode == A_CONV3) {
               const int tap = kb / kcb, cb = kb % kcb;
               tma_load_4d(sa, &tmA, &full[stage], cb * GEMM_BK, tap % 3, y0 + tap / 3, p0);
@@ -219,7 +239,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
 #pragma unroll
             for (int j = 0; j < Cfg::N_MMA; ++j)
-              tma_load_2d(sb + j * Cfg::MMA_N * 128, &tmB, &full[stage], kb * GEMM_BK, n0 + j * Cfg::MMA_N);
+              if (half < 0 || j == half)
+                tma_load_2d(sb + j * Cfg::MMA_N * 128, &tmB, &full[stage], kb * GEMM_BK, n0 + j * Cfg::MMA_N);
           }
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -231,7 +252,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     int li = 0;
-    for (int t = unit0; t < n_tiles; t += unit_step, ++li) {
+    for (int w = unit0; w < n_items; w += unit_step, ++li) {
+      int half;
+      (void)item(w, half);
       const int buf = li % Cfg::NBUF;
       const int use = li / Cfg::NBUF;
       timed_wait(&acc_empty[buf], (use & 1) ^ 1, t_wait2);
@@ -247,6 +270,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int k = 0; k < GEMM_BK / 16; ++k)
 #pragma unroll
             for (int j = 0; j < Cfg::N_MMA; ++j) {
+              if (half >= 0 && j != half) continue;
               if (PAIR)
                 mma_bf16_ss_2sm(d + j * Cfg::MMA_N, sdesc_sw128(sa + k * 32),
                                 sdesc_sw128(sb + j * Cfg::B_ROWS * 128 + k * 32), idesc, (kb | k) != 0);
@@ -305,7 +329,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       if (PAIR) mbar_arrive_cluster(mapa_shared(&acc_empty[b], 0));
       else mbar_arrive(&acc_empty[b]);
     };
-    for (int t = unit0; t < n_tiles; t += unit_step, ++li) {
+    for (int w = unit0; w < n_items; w += unit_step, ++li) {
+      int half;
+      const int t = item(w, half);
       const int buf = li % Cfg::NBUF;
       const int use = li / Cfg::NBUF;
       if (!split && buf != wg) continue;
@@ -487,9 +513,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
       };
-      const int c_end = min(c_hi, p.N - n_tile * BN);  // columns of this tile for this warpgroup
+      int c_end = min(c_hi, p.N - n_tile * BN);  // columns of this tile for this warpgroup
+      int c_beg = c_lo;
+      if (half >= 0) {  // a tail item: only this column half of the accumulator was computed
+        c_beg = half * Cfg::MMA_N + (c_lo % Cfg::MMA_N);
+        c_end = min(c_end, (half + 1) * Cfg::MMA_N);
+        if (c_beg >= c_end) {
+          tc_fence_before();
+          release(buf);
+          continue;
+        }
+      }
 #pragma unroll 1
-      for (int c = c_lo; c < c_end; c += c_step) {
+      for (int c = c_beg; c < c_end; c += c_step) {
         uint32_t r[32];
         PS_TMEM_LD32(tmem + lane_base + buf * BN + c, r);
         float bv[32];

@@ -35,6 +35,8 @@ struct GemmParams {
   int epi_split;            // both epilogue warpgroups split each tile's columns (else alternate tiles)
   int no_prefetch;          // skip the L2 prefetch of residual rows
   int warp_store;           // channels-last TMA stores per warp (32x32 boxes) instead of per warpgroup
+  int tail_split;           // BN = 320 (two N = 160 MMAs): the last partial wave's tiles become one
+                            // work item per column half (A re-read, half the MMAs and epilogue)
 };
 
 struct FfParams {

@@ -87,3 +87,31 @@ def test_gn_partials_offset_and_outlier_shift():
     m2 = ((ref - mean[..., None]) ** 2).sum(-1)
     assert float((part[..., 0].double() - mean).abs().max()) <= 2e-4  # fp32 mean of ~50 (ulp 4e-6)
     assert float(((part[..., 1].double() - m2).abs() / m2).max()) <= 1e-4
+
+
+CONV_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2501_09253_b200 as ps
+cfg = ps.ModelConfig(arch="unet_like", channels=320, hidden=1280, n_blocks=1, groups=32, seed=2)
+conv = ps.init_weights(cfg)[0][1][1]
+g = torch.Generator().manual_seed(3)
+reqs = [(f"r{i}", torch.randn((320, d, d), generator=g)) for i, d in enumerate([64, 96, 128] * 4)]
+b = ps.split(reqs, patch_size=32)  # P = 116: 464 CTA-pair tiles on 74 pairs -> a 20-tile tail wave
+x = b.data.to(torch.bfloat16).cuda()
+y = ps.patched_conv(b, x, conv)
+torch.cuda.synchronize()
+torch.save(y.cpu(), sys.argv[2])
+"""
+
+
+def test_conv3_tail_split_bit_identical(tmp_path):
+    """conv3 (CTA-pair tiles, BN = 320) with the last partial wave split into column-half work
+    items equals the unsplit schedule bit for bit (every column keeps its k order)."""
+    outs = {}
+    for name, env in (("split", {}), ("whole", {"PS_GEMM_TAIL_SPLIT": "0"})):
+        out = tmp_path / f"{name}.pt"
+        subprocess.run([sys.executable, "-c", CONV_SCRIPT, ROOT, str(out)], check=True, timeout=300,
+                       env=dict(os.environ, **env))
+        outs[name] = torch.load(out)
+    assert torch.equal(outs["split"], outs["whole"])
