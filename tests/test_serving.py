@@ -198,3 +198,30 @@ def test_extended_resolution_classes_enter_the_serving_plane():
     res5 = S.Engine(S.EngineConfig(plane="cost_only", total_steps=2, patch_size=64, cost=cost64,
                                    scheduler=S.SchedulerConfig(cost=cost64))).run(trace5)
     assert res5.summary["n_completed"] == 9
+
+
+@pytest.mark.gpu
+def test_wall_and_numeric_planes_graph_opt_in_equals_eager():
+    """EngineConfig.graph_after_steps > 0 replays a composition's cached step as one CUDA graph
+    once it has run that many eager steps: the numeric plane's events and final latents equal
+    the all-eager run bit for bit (CachedStepGraph reproduces numeric_step exactly)."""
+    import torch
+
+    from paper_2501_09253_b200.model import ModelConfig
+    from paper_2501_09253_b200.patched import device_compaction_ok  # noqa: F401 -- the path exercised
+    mc = ModelConfig(arch="unet_like", channels=64, hidden=128, n_blocks=2, groups=8, seed=1)
+    wc = S.WorkloadConfig(seed=3, qps=5.0, n_requests=5, steps=12)
+    trace = S.generate_trace(wc)
+    runs = {}
+    for k in (0, 2):
+        ec = S.EngineConfig(plane="numeric", total_steps=12, model=mc, graph_after_steps=k)
+        runs[k] = S.Engine(ec).run(trace)
+    assert runs[0].events == runs[2].events
+    strip = lambda d: {k: v for k, v in d.items() if k != "device_step_ms_mean"}  # timing differs
+    assert strip(runs[0].summary) == strip(runs[2].summary)
+    for rid, lat in runs[0].latents.items():
+        assert torch.equal(lat, runs[2].latents[rid]), rid
+    # the wall plane runs with graphs on as well
+    ec = S.EngineConfig(plane="wall", total_steps=12, model=mc, graph_after_steps=2)
+    res = S.Engine(ec).run(trace)
+    assert res.summary["n_completed"] + res.summary["n_discarded"] == 5
