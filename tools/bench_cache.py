@@ -19,7 +19,7 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 import paper_2501_09253_b200 as ps  # noqa: E402
-from paper_2501_09253_b200.engine_step import numeric_step  # noqa: E402
+from paper_2501_09253_b200.engine_step import CachedStepGraph, numeric_step  # noqa: E402
 from paper_2501_09253_b200.model import step_inputs  # noqa: E402
 
 
@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--sigmas", default="0,0.001,0.01,0.05,0.1,0.5")
     ap.add_argument("--max-streak", type=int, default=3)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--graph", action="store_true",
+                    help="the cached step as one CUDA graph (engine_step.CachedStepGraph, as bench.py config 3)")
     args = ap.parse_args()
     cfg = ps.ModelConfig(arch="unet_like", channels=bench.C, hidden=bench.HIDDEN, groups=bench.GROUPS,
                          n_blocks=bench.BLOCKS, seed=0)
@@ -43,12 +45,17 @@ def main():
         keys = b.patch_keys()
         tot = dict(skipped=0, computed=0, rows_run=0)
         times = []
+        gstep = CachedStepGraph(b, w, cache, keys) if (args.graph and cache is not None) else None
         for s in range(args.steps):
             bias, rates = step_inputs(cfg, b, prompts, dict.fromkeys(prompts, s), dict.fromkeys(prompts, 50))
             b.data = data
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            data, st = numeric_step(b, w, cache, bias, rates, keys=keys)
+            if gstep is not None:
+                data, st = gstep.run(data, bias, rates)
+                data = data.clone()  # the graph's output buffer is overwritten by the next replay
+            else:
+                data, st = numeric_step(b, w, cache, bias, rates, keys=keys)
             e1.record()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
@@ -61,8 +68,9 @@ def main():
                 "ms_per_step_mean": float(np.mean(warm)), "ms_per_step_first": times[0],
                 "patches_per_s": b.n_patches / (float(np.mean(warm)) * 1e-3),
                 "cache": cache.stats.as_dict() if cache else None,
-                "note": "sigma=0: no cache (plain steps); timing with CUDA events per step, one mask read-back "
-                        "per block as in engine.py:143-144"}
+                "mode": "graph (CachedStepGraph: reuse decisions on the device)" if gstep is not None else
+                        "eager (one mask read-back per block as in engine.py:143-144)",
+                "note": "sigma=0: no cache (plain steps); timing with CUDA events per step, steps 2.. averaged"}
         print(json.dumps(line), flush=True)
         lines.append(line)
     if args.out:
