@@ -396,7 +396,7 @@ template <typename T>
 __global__ void __launch_bounds__(MseRing<T>::THREADS + 32, 2) mse_ring_kernel(
     const T* __restrict__ x, int64_t n, const int32_t* __restrict__ slots, const T* __restrict__ snap,
     const uint8_t* __restrict__ exists, const int32_t* __restrict__ streak, int max_streak,
-    const int32_t* __restrict__ leaves, int L, int I, int CP, int P, int S, int stage_elems, int RW,
+    const int32_t* __restrict__ leaves, int L, int I, int CP, int P, int S, int stage_elems,
     int leaf_len, int cp_shift, double* __restrict__ scratch) {
   // leaf_len > 0: every leaf has that many elements (leaf l starts at l * leaf_len), so the item
   // loop reads no plan table; CP = 1 << cp_shift chunks per patch.
@@ -874,7 +874,7 @@ int ps_cache_predict(void* stream, const void* x, int dtype, int P, int64_t n, c
         const int grid = items < 2 * ring_num_sms() ? items : 2 * ring_num_sms();
         launch_pdl(mse_ring_kernel<T>, dim3(grid), dim3(MseRing<T>::THREADS + 32), smem_r, st, (const T*)x, n, slots,
                    (const T*)snap_in, exists, streak, max_streak, leaves, n_leaves, n_internal, g, P, S, stage_elems,
-                   RW, leaf_len, cp_shift, scratch);
+                   leaf_len, cp_shift, scratch);
         count_launch();
         const int rc = check_launch("mse_reuse_test");
         if (rc != PS_OK) return rc;

@@ -143,3 +143,18 @@ def test_pairwise_restatement_matches_numpy_and_differs_from_naive():
             naive_diff += (s / d.size) != float(np.mean((a - b) ** 2))
     assert naive_diff > 0  # the tree matters: sequential summation gives other bits
 
+
+
+def test_integration_ctypes_stub_matches_header():
+    """INTEGRATION.md's ctypes stub for ps_cache_predict declares as many arguments as the C
+    prototype in include/patchserve.h and the facade's signature table."""
+    import re
+
+    from paper_2501_09253_b200 import _lib
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    stub = re.search(r"lib\.ps_cache_predict\.argtypes = \[(.*?)\]", doc, re.S).group(1)
+    n_stub = len([a for a in stub.split(",") if a.strip()])
+    hdr = open(os.path.join(ROOT, "include", "patchserve.h")).read()
+    proto = re.search(r"int ps_cache_predict\((.*?)\);", hdr, re.S).group(1)
+    n_hdr = len(proto.split(","))
+    assert n_stub == n_hdr == len(_lib._SIGS["ps_cache_predict"][0])
