@@ -181,11 +181,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
           tc_fence_after();
           if (lane == 0) { A2_TRACE(0, j) }
           long long kw = 0;
-          for (int kc = 0; kc < Cfg::KB; ++kc) {
+          {  // the block's K chunks first, then its MMAs back to back (as attn2p_kernel)
             const long long tk0 = p.trace ? clock64() : 0;
-            twait(&k_full[ks], kph, w_c);
+            int k2 = ks;
+            uint32_t p2 = kph;
+            for (int kc = 0; kc < Cfg::KB; ++kc) {
+              twait(&k_full[k2], p2, w_c);
+              if (++k2 == Cfg::NK) { k2 = 0; p2 ^= 1; }
+            }
             if (p.trace) kw += clock64() - tk0;
             tc_fence_after();
+          }
+          for (int kc = 0; kc < Cfg::KB; ++kc) {
             if (lane == 0) {
               const uint8_t* kt = sK + ks * Cfg::K_SLOT;
 #pragma unroll

@@ -42,7 +42,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1) mixed_kernel
     mma_bf16_ts_2sm(tmem + 128, tmem + 448 + (k & 7) * 8, sdesc_sw128(sb2 + pc * 10240 + (k & 3) * 32), id2, 1);
   };
   long long t0 = clock64();
-  if (MODE >= 4 && warp >= 4) {  // side traffic until the MMAs are done
+  if (MODE >= 4 && MODE <= 5 && warp >= 4) {  // side traffic until the MMAs are done
     const uint32_t lb = (uint32_t)((warp & 3) * 32) << 16;
     uint32_t r[32];
     int ph = 0;
@@ -60,7 +60,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1) mixed_kernel
       tmem_st_wait();
     }
   }
-  if (leader && lane == 0) {
+  if (MODE == 8 && warp >= 4 && warp < 8 && lane == 0) {  // heavy TMA-write side traffic
+    __shared__ uint64_t cb8[4];
+    const int wi = warp - 4;
+    mbar_init(&cb8[wi], 1);
+    fence_mbar_init();
+    int ph8 = 0;
+    while (!done) {
+      mbar_arrive_expect_tx(&cb8[wi], 10240);
+      bulk_load(smem + 163840 + 0 * 10240, gsrc + ((blockIdx.x + wi) & 15) * 10240, 10240, &cb8[wi]);
+      mbar_wait(&cb8[wi], ph8);
+      ph8 ^= 1;
+    }
+  }
+  if (MODE == 9 && warp >= 4 && warp < 8) {  // softmax-like ALU / MUFU load on every SMSP
+    float a0 = threadIdx.x * 1e-3f, a1 = a0 + 0.5f, a2 = a0 + 0.25f, a3 = a0 + 0.125f;
+    while (!done) {
+#pragma unroll 16
+      for (int i = 0; i < 64; ++i) {
+        a0 = exp2f(a0 * 0.999f) * 0.5f;
+        a1 = fmaf(a1, 0.999f, a0);
+        a2 = exp2f(a2 * 0.998f) * 0.5f;
+        a3 = fmaf(a3, 0.997f, a2);
+      }
+    }
+    if (a0 + a1 + a2 + a3 == 12345.f) cycles[1] = 1;  // keep the work
+  }
+  if (MODE >= 6) {  // SS only, with a multicast commit (to a spare barrier) after every 4 / 20 MMAs
+    if (leader && lane == 0 && warp == 0) {
+      for (int it = 0; it < iters; ++it)
+        for (int k = 0; k < 20; ++k) {
+          ss(k);
+          if ((MODE == 6 && (k & 3) == 3) || (MODE >= 7 && k == 19)) mma_commit_2sm(&cbar, 0x3);
+        }
+      mma_commit_2sm(&bar[0], 0x3);
+      mma_commit_2sm(&bar[1], 0x3);
+    }
+  } else if (leader && lane == 0) {
     if (MODE >= 3) {
       if (warp == 0) { for (int it = 0; it < iters; ++it) for (int k = 0; k < 20; ++k) ss(k); mma_commit_2sm(&bar[0], 0x3); }
       if (warp == 1) { for (int it = 0; it < iters; ++it) for (int k = 0; k < 16; ++k) ts(k); mma_commit_2sm(&bar[1], 0x3); }
@@ -89,7 +125,7 @@ template <int MODE, bool STREAM = false>
 void run(const char* name, int sms) {
   const int iters = 4000;
   unsigned long long* d;
-  cudaMalloc(&d, 8);
+  cudaMalloc(&d, 16);
   const int smem = 163840 + 10240 + 2048;
   uint8_t* g;
   cudaMalloc(&g, 16 * 10240);
@@ -101,7 +137,8 @@ void run(const char* name, int sms) {
   unsigned long long cyc;
   cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
   // per SM per iteration: SS 20 x (128 x 128 x 16 x 2), TS 16 x (128 x 160 x 16 x 2)
-  const double ss = (MODE != 1) ? 20.0 * 128 * 128 * 16 * 2 : 0, tsf = (MODE != 0) ? 16.0 * 128 * 160 * 16 * 2 : 0;
+  const double ss = (MODE != 1) ? 20.0 * 128 * 128 * 16 * 2 : 0,
+               tsf = (MODE != 0 && MODE < 6) ? 16.0 * 128 * 160 * 16 * 2 : 0;
   printf("%-34s %6.0f FLOP/clk/SM (peak 8192)  %8.0f cycles/iter  err=%s\n", name, (ss + tsf) * iters / cyc,
          (double)cyc / iters, cudaGetErrorString(cudaGetLastError()));
   fflush(stdout);
@@ -121,5 +158,9 @@ int main() {
   run<1, true>("STREAM TS only", sms);
   run<3, true>("STREAM SS + TS, two issuers", sms);
   run<5, true>("STREAM + TMEM ld/st + bulk copies", sms);
+  run<6, true>("STREAM SS, 2-CTA commit / 4 MMAs", sms);
+  run<7, true>("STREAM SS, 2-CTA commit / 20 MMAs", sms);
+  run<8, true>("STREAM SS + 4 bulk copies in flight", sms);
+  run<9, true>("STREAM SS + 4 ALU/MUFU warps", sms);
   return 0;
 }
