@@ -172,6 +172,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
     if (leader) {
       constexpr uint32_t idesc_s = idesc_bf16_f32(2 * A2_BM, A2_BN);
       constexpr uint32_t idesc_o = idesc_bf16_f32(2 * A2_BM, Cfg::PV_N);
+      // descriptor bases: the start-address field is (smem address >> 4) in the low bits, so an
+      // operand offset is a plain add (no carry: smem < 256 KB); fewer dependent ops per issue
+      const uint64_t dq0 = sdesc_sw128(sQ), dk0 = sdesc_sw128(sK), dv0 = sdesc_sw128(sV);
       mbar_wait(q_full, 0);
       if (warp == 1) {
         int ks = 0;
@@ -194,11 +197,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
           }
           for (int kc = 0; kc < Cfg::KB; ++kc) {
             if (lane == 0) {
-              const uint8_t* kt = sK + ks * Cfg::K_SLOT;
+              const uint64_t dq = dq0 + (uint64_t)((kc * A2_BM * 128) >> 4);
+              const uint64_t dk = dk0 + (uint64_t)((ks * Cfg::K_SLOT) >> 4);
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                mma_bf16_ss_2sm(tmem + Cfg::S_COL, sdesc_sw128(sQ + kc * A2_BM * 128 + k * 32),
-                                sdesc_sw128(kt + k * 32), idesc_s, (kc | k) != 0);
+                mma_bf16_ss_2sm(tmem + Cfg::S_COL, dq + (uint64_t)(k * 2), dk + (uint64_t)(k * 2), idesc_s,
+                                (kc | k) != 0);
               mma_commit_2sm(&k_empty[ks], 0x3);
               if (kc == Cfg::KB - 1) mma_commit_2sm(s_full, 0x3);
             }
@@ -222,13 +226,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
             if (p.trace) vw += clock64() - tv0;
             tc_fence_after();
             if (lane == 0) {
-              const uint8_t* vt = sV + vs * Cfg::V_SLOT;
+              const uint64_t dv = dv0 + (uint64_t)((vs * Cfg::V_SLOT) >> 4);
 #pragma unroll
               for (int k = 0; k < 4; ++k)
 #pragma unroll
                 for (int n = 0; n < Cfg::PV_MMAS; ++n)
                   mma_bf16_ts_2sm(tmem + Cfg::O_COL + n * Cfg::PV_N, tmem + Cfg::P_COL + ka * 32 + k * 8,
-                                  sdesc_sw128(vt + n * Cfg::V_ROWS * 128 + k * 32), idesc_o, (j | ka | k) != 0);
+                                  dv + (uint64_t)((n * Cfg::V_ROWS * 128 + k * 32) >> 4), idesc_o,
+                                  (j | ka | k) != 0);
               mma_commit_2sm(&v_empty[vs], 0x3);
               if (ka == 1) {
                 mma_commit_2sm(p_free, 0x3);
@@ -603,6 +608,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
     if (leader) {
       constexpr uint32_t idesc_s = idesc_bf16_f32(2 * A2_BM, A2_BN);
       constexpr uint32_t idesc_o = idesc_bf16_f32(2 * A2_BM, Cfg::PV_N);
+      const uint64_t dq0 = sdesc_sw128(sQ), dk0 = sdesc_sw128(sK), dv0 = sdesc_sw128(sV);
       int ring = 0;
       uint32_t rph = 0;
       int gj = 0;
@@ -631,11 +637,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
               tc_fence_after();
               for (int kc = kc0; kc < kc0 + A2_KWAIT && kc < Cfg::KB; ++kc) {
                 if (lane == 0) {
-                  const uint8_t* kt = sK + ring * Cfg::K_SLOT;
+                  // descriptors from hoisted bases: the start-address field is (smem address >> 4)
+                  // in the low bits, so an operand offset is a plain add (no carry: smem < 256 KB)
+                  const uint64_t dq = dq0 + (uint64_t)((kc * A2_BM * 128) >> 4);
+                  const uint64_t dk = dk0 + (uint64_t)((ring * Cfg::K_SLOT) >> 4);
 #pragma unroll
                   for (int k = 0; k < 4; ++k)
-                    mma_bf16_ss_2sm(tmem + Cfg::S_COL, sdesc_sw128(sQ + kc * A2_BM * 128 + k * 32),
-                                    sdesc_sw128(kt + k * 32), idesc_s, (kc | k) != 0);
+                    mma_bf16_ss_2sm(tmem + Cfg::S_COL, dq + (uint64_t)(k * 2), dk + (uint64_t)(k * 2), idesc_s,
+                                    (kc | k) != 0);
                   mma_commit_2sm(&k_empty[ring], 0x3);
                   if (kc == Cfg::KB - 1) {
                     mma_commit_2sm(s_full, 0x3);
@@ -656,13 +665,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
               mbar_wait(&v_full[ring], rph);
               tc_fence_after();
               if (lane == 0) {
-                const uint8_t* vt = sV + ring * Cfg::V_SLOT;
+                const uint64_t dv = dv0 + (uint64_t)((ring * Cfg::V_SLOT) >> 4);
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
 #pragma unroll
                   for (int n = 0; n < Cfg::PV_MMAS; ++n)
                     mma_bf16_ts_2sm(tmem + Cfg::O_COL + n * Cfg::PV_N, tmem + Cfg::P_COL + ka * 32 + k * 8,
-                                    sdesc_sw128(vt + n * Cfg::V_ROWS * 128 + k * 32), idesc_o, (j | ka | k) != 0);
+                                    dv + (uint64_t)((n * Cfg::V_ROWS * 128 + k * 32) >> 4), idesc_o,
+                                    (j | ka | k) != 0);
                 mma_commit_2sm(&v_empty[ring], 0x3);
                 if (ka == 1) {
                   mma_commit_2sm(p_free, 0x3);

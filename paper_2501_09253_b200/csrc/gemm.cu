@@ -264,19 +264,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         timed_wait(&full[stage], phase, t_wait);
         tc_fence_after();
         if (lane == 0) {
-          const uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
-          const uint8_t* sb = sa + Cfg::A_BYTES;
+          // descriptor = stage base + (byte offset >> 4): the start-address field is the low bits
+          const uint64_t da = sdesc_sw128(smem + stage * Cfg::STAGE_BYTES);
+          const uint64_t db = da + (uint64_t)(Cfg::A_BYTES >> 4);
 #pragma unroll
           for (int k = 0; k < GEMM_BK / 16; ++k)
 #pragma unroll
             for (int j = 0; j < Cfg::N_MMA; ++j) {
               if (half >= 0 && j != half) continue;
               if (PAIR)
-                mma_bf16_ss_2sm(d + j * Cfg::MMA_N, sdesc_sw128(sa + k * 32),
-                                sdesc_sw128(sb + j * Cfg::B_ROWS * 128 + k * 32), idesc, (kb | k) != 0);
+                mma_bf16_ss_2sm(d + j * Cfg::MMA_N, da + (uint64_t)(k * 2),
+                                db + (uint64_t)((j * Cfg::B_ROWS * 128 + k * 32) >> 4), idesc, (kb | k) != 0);
               else
-                mma_bf16_ss(d + j * Cfg::MMA_N, sdesc_sw128(sa + k * 32),
-                            sdesc_sw128(sb + j * Cfg::MMA_N * 128 + k * 32), idesc, (kb | k) != 0);
+                mma_bf16_ss(d + j * Cfg::MMA_N, da + (uint64_t)(k * 2),
+                            db + (uint64_t)((j * Cfg::MMA_N * 128 + k * 32) >> 4), idesc, (kb | k) != 0);
             }
           if (PAIR) {
             mma_commit_2sm(&empty[stage], 0x3);
