@@ -26,6 +26,9 @@ namespace ps {
 constexpr int A2_BM = 128;  // query rows per CTA (256 per pair)
 constexpr int A2_BN = 128;  // keys per block (64 per CTA)
 constexpr int A2_THREADS = 256;
+#ifndef A2_WARP_ISSUE  // MMA issue by the converged warp (elect.sync in the asm) instead of lane 0
+#define A2_WARP_ISSUE 1
+#endif
 #ifndef A2_KWAIT
 #define A2_KWAIT 5  // K chunks the persistent kernel's S issuer waits for before issuing their MMAs
 #endif
@@ -141,21 +144,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
       auto load_k = [&](int j) {
         for (int kc = 0; kc < Cfg::KB; ++kc) {
           mbar_wait(&k_empty[ks], kph ^ 1);
+#ifdef A2_NOLOAD  // profiling only: K slots keep stale data (no TMA traffic)
+          if (leader) mbar_arrive(&k_full[ks]);
+#else
           if (leader) mbar_arrive_expect_tx(&k_full[ks], 2 * Cfg::K_SLOT);
           tma_load_2d_2sm(sK + ks * Cfg::K_SLOT, &tmK, mapa_shared(&k_full[ks], 0), kc * 64,
                           k_begin + j * A2_BN + (int)rank * (A2_BN / 2));
+#endif
           if (++ks == Cfg::NK) { ks = 0; kph ^= 1; }
         }
       };
       auto load_v = [&](int j) {
         for (int ka = 0; ka < 2; ++ka) {
           mbar_wait(&v_empty[vs], vph ^ 1);
+#ifdef A2_NOLOAD
+          if (leader) mbar_arrive(&v_full[vs]);
+#else
           if (leader) mbar_arrive_expect_tx(&v_full[vs], 2 * Cfg::V_SLOT);
           const uint32_t lb = mapa_shared(&v_full[vs], 0);
           uint8_t* dst = sV + vs * Cfg::V_SLOT;
           for (int n = 0; n < Cfg::PV_MMAS; ++n)
             tma_load_2d_2sm(dst + n * Cfg::V_ROWS * 128, &tmV, lb, k_begin + j * A2_BN + ka * 64,
                             n * Cfg::PV_N + (int)rank * Cfg::V_ROWS);
+#endif
           if (++vs == Cfg::NV) { vs = 0; vph ^= 1; }
         }
       };
@@ -289,8 +300,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
       float sum0 = 0.f, sum1 = 0.f;
 #pragma unroll
       for (int i = 0; i < 64; ++i) {
+#ifdef A2_EXP_OFF  // profiling only: no exponentials
+        const float a = fmaf(__uint_as_float(sr[2 * i]), p.scale_log2, neg);
+        const float b = fmaf(__uint_as_float(sr[2 * i + 1]), p.scale_log2, neg);
+#else
         const float a = ex2_approx(fmaf(__uint_as_float(sr[2 * i]), p.scale_log2, neg));
         const float b = ex2_approx(fmaf(__uint_as_float(sr[2 * i + 1]), p.scale_log2, neg));
+#endif
         sum0 += a;
         sum1 += b;
         sr[i] = pack_bf16(a, b);  // packed P overwrites the consumed half of sr
@@ -636,11 +652,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
               }
               tc_fence_after();
               for (int kc = kc0; kc < kc0 + A2_KWAIT && kc < Cfg::KB; ++kc) {
+                // descriptors from hoisted bases: the start-address field is (smem address >> 4)
+                // in the low bits, so an operand offset is a plain add (no carry: smem < 256 KB)
+                const uint64_t dq = dq0 + (uint64_t)((kc * A2_BM * 128) >> 4);
+                const uint64_t dk = dk0 + (uint64_t)((ring * Cfg::K_SLOT) >> 4);
+#if A2_WARP_ISSUE
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  mma_bf16_ss_2sm_w(tmem + Cfg::S_COL, dq + (uint64_t)(k * 2), dk + (uint64_t)(k * 2), idesc_s,
+                                    (kc | k) != 0);
+                mma_commit_2sm_w(&k_empty[ring], 0x3);
+                if (kc == Cfg::KB - 1) {
+                  mma_commit_2sm_w(s_full, 0x3);
+                  if (j == n_kb - 1) mma_commit_2sm_w(q_empty, 0x3);  // Q free for the next tile
+                }
+#else
                 if (lane == 0) {
-                  // descriptors from hoisted bases: the start-address field is (smem address >> 4)
-                  // in the low bits, so an operand offset is a plain add (no carry: smem < 256 KB)
-                  const uint64_t dq = dq0 + (uint64_t)((kc * A2_BM * 128) >> 4);
-                  const uint64_t dk = dk0 + (uint64_t)((ring * Cfg::K_SLOT) >> 4);
 #pragma unroll
                   for (int k = 0; k < 4; ++k)
                     mma_bf16_ss_2sm(tmem + Cfg::S_COL, dq + (uint64_t)(k * 2), dk + (uint64_t)(k * 2), idesc_s,
@@ -652,6 +679,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
                   }
                 }
                 __syncwarp();
+#endif
                 if (++ring == Cfg::NK) { ring = 0; rph ^= 1; }
               }
             }
@@ -664,8 +692,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
             for (int ka = 0; ka < 2; ++ka) {
               mbar_wait(&v_full[ring], rph);
               tc_fence_after();
+              const uint64_t dv = dv0 + (uint64_t)((ring * Cfg::V_SLOT) >> 4);
+#if A2_WARP_ISSUE
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int n = 0; n < Cfg::PV_MMAS; ++n)
+                  mma_bf16_ts_2sm_w(tmem + Cfg::O_COL + n * Cfg::PV_N, tmem + Cfg::P_COL + ka * 32 + k * 8,
+                                    dv + (uint64_t)((n * Cfg::V_ROWS * 128 + k * 32) >> 4), idesc_o,
+                                    (j | ka | k) != 0);
+              mma_commit_2sm_w(&v_empty[ring], 0x3);
+              if (ka == 1) {
+                mma_commit_2sm_w(p_free, 0x3);
+                if (j == n_kb - 1) mma_commit_2sm_w(o_full, 0x3);
+              }
+#else
               if (lane == 0) {
-                const uint64_t dv = dv0 + (uint64_t)((ring * Cfg::V_SLOT) >> 4);
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
 #pragma unroll
@@ -680,6 +722,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
                 }
               }
               __syncwarp();
+#endif
               if (++ring == Cfg::NV) { ring = 0; rph ^= 1; }
             }
           }

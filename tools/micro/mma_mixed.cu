@@ -4,12 +4,15 @@
 // TMA traffic), issued from one thread or from two threads (one per kind, as in ff_pair_kernel).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o mma_mixed mma_mixed.cu
 #include <cstdio>
+#include <cstdlib>
 #include "../../paper_2501_09253_b200/csrc/common.cuh"
 using namespace ps;
 
 // MODE 0: SS only (20 MMAs / iter), 1: TS only (16 / iter), 2: both, one issuer, 3: both, two issuers,
 // 4: 3 + eight warps streaming tcgen05.ld (64 columns) / tcgen05.st (32 columns) like the FF's H
 // epilogue, 5: 4 + a bulk-copy stream into another smem region (the weight ring's TMA writes)
+__device__ int g_random;
+__device__ int g_delay;
 template <int MODE, bool STREAM>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1) mixed_kernel(int iters, unsigned long long* cycles,
                                                                                  const uint8_t* gsrc) {
@@ -26,7 +29,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1) mixed_kernel
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool leader = cluster_rank() == 0;
-  for (int i = threadIdx.x; i < 163840 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+  // operand data: constant 1.0 (low toggle) or pseudo-random bf16 in [-2, 2) (RANDOM)
+  for (int i = threadIdx.x; i < 163840 / 4; i += blockDim.x) {
+    uint32_t v = 0x3c003c00u;
+    if (g_random) {
+      uint32_t h = (uint32_t)i * 2654435761u + 0x9e3779b9u;
+      h ^= h >> 15; h *= 0x85ebca6bu; h ^= h >> 13;
+      v = (h & 0x807f807fu) | 0x3f803f80u;  // sign + 7 mantissa bits random, exponent 0x7f (|x| in [1, 2))
+    }
+    reinterpret_cast<uint32_t*>(smem)[i] = v;
+  }
   if (threadIdx.x == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); mbar_init(&cbar, 1); fence_mbar_init(); done = 0; }
   if (warp == 0) tmem_alloc_2sm(&tslot, 512);
   fence_proxy_async();
@@ -86,7 +98,70 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1) mixed_kernel
     }
     if (a0 + a1 + a2 + a3 == 12345.f) cycles[1] = 1;  // keep the work
   }
-  if (MODE >= 6) {  // SS only, with a multicast commit (to a spare barrier) after every 4 / 20 MMAs
+  if (MODE == 10) {  // SS only, g_delay dependent integer ops folded into every descriptor
+    if (leader && lane == 0 && warp == 0) {
+      uint32_t x = (uint32_t)clock();
+      const int dl = g_delay;
+      const uint32_t zmask = (uint32_t)g_random >> 8;  // 0 at run time, opaque to the compiler
+      for (int it = 0; it < iters; ++it)
+        for (int k = 0; k < 20; ++k) {
+          for (int d = 0; d < dl; ++d) x = x * 3u + 1u;
+          const int kb = k >> 2;
+          const uint64_t da = sdesc_sw128(sa + kb * 16384 + (k & 3) * 32) + (uint64_t)(x & zmask);
+          mma_bf16_ss_2sm(tmem, da, sdesc_sw128(sb1 + kb * 8192 + (k & 3) * 32), id1, 1);
+        }
+      mma_commit_2sm(&bar[0], 0x3);
+      mma_commit_2sm(&bar[1], 0x3);
+    }
+  } else if (MODE == 11) {  // whole warp runs the loop (uniform runtime descriptors), elect.sync issues
+    if (leader && warp == 0) {
+      const uint32_t zmask = (uint32_t)g_random >> 8;
+      const uint64_t a0 = sdesc_sw128(sa) + (uint64_t)zmask, b0 = sdesc_sw128(sb1) + (uint64_t)zmask;
+      for (int it = 0; it < iters; ++it)
+        for (int k = 0; k < 20; ++k) {
+          const int kb = k >> 2;
+          const uint64_t da = a0 + (uint64_t)((kb * 16384 + (k & 3) * 32) >> 4);
+          const uint64_t db = b0 + (uint64_t)((kb * 8192 + (k & 3) * 32) >> 4);
+          asm volatile(
+              "{\n\t.reg .pred e;\n\t"
+              "elect.sync _|e, 0xffffffff;\n\t"
+              "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, 1;\n}" ::"r"(tmem),
+              "l"(da), "l"(db), "r"(id1)
+              : "memory");
+        }
+      if (lane == 0) { mma_commit_2sm(&bar[0], 0x3); mma_commit_2sm(&bar[1], 0x3); }
+    }
+  } else if (MODE == 12) {  // lane 0 loop, runtime descriptor base hoisted, constant offsets per MMA
+    if (leader && lane == 0 && warp == 0) {
+      const uint32_t zmask = (uint32_t)g_random >> 8;
+      const uint64_t a0 = sdesc_sw128(sa) + (uint64_t)zmask, b0 = sdesc_sw128(sb1) + (uint64_t)zmask;
+      for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int k = 0; k < 20; ++k) {
+          const int kb = k >> 2;
+          mma_bf16_ss_2sm(tmem, a0 + (uint64_t)((kb * 16384 + (k & 3) * 32) >> 4),
+                          b0 + (uint64_t)((kb * 8192 + (k & 3) * 32) >> 4), id1, 1);
+        }
+      mma_commit_2sm(&bar[0], 0x3);
+      mma_commit_2sm(&bar[1], 0x3);
+    }
+  } else if (MODE == 13) {  // as 12 with a runtime ring slot per 4 MMAs (like the attention K ring)
+    if (leader && lane == 0 && warp == 0) {
+      const uint32_t zmask = (uint32_t)g_random >> 8;
+      const uint64_t a0 = sdesc_sw128(sa) + (uint64_t)zmask, b0 = sdesc_sw128(sb1) + (uint64_t)zmask;
+      int ring = 0;
+      for (int it = 0; it < iters; ++it)
+        for (int kb = 0; kb < 5; ++kb) {
+          const uint64_t da = a0 + (uint64_t)((kb * 16384) >> 4);
+          const uint64_t db = b0 + (uint64_t)((ring * 8192) >> 4);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) mma_bf16_ss_2sm(tmem, da + (uint64_t)(2 * k), db + (uint64_t)(2 * k), id1, 1);
+          if (++ring == 5) ring = 0;
+        }
+      mma_commit_2sm(&bar[0], 0x3);
+      mma_commit_2sm(&bar[1], 0x3);
+    }
+  } else if (MODE >= 6) {  // SS only, with a multicast commit (to a spare barrier) after every 4 / 20 MMAs
     if (leader && lane == 0 && warp == 0) {
       for (int it = 0; it < iters; ++it)
         for (int k = 0; k < 20; ++k) {
@@ -145,9 +220,24 @@ void run(const char* name, int sms) {
   fflush(stdout);
 }
 
-int main() {
+int main(int argc, char** argv) {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int rnd = argc > 1 ? atoi(argv[1]) : 0;
+  cudaMemcpyToSymbol(g_random, &rnd, sizeof(int));
+  printf("operands: %s\n", rnd ? "random bf16" : "constant 1.0");
+  if (argc > 2) {  // issue-latency sweep: dependent ops per MMA
+    for (int dl : {0, 4, 16, 64}) {
+      cudaMemcpyToSymbol(g_delay, &dl, sizeof(int));
+      char name[64];
+      snprintf(name, sizeof(name), "SS N128, %d dependent IMADs per MMA", dl);
+      run<10, true>(name, sms);
+    }
+    run<11, true>("SS N128, runtime desc, warp loop + elect", sms);
+    run<12, true>("SS N128, runtime base + const, lane 0", sms);
+    run<13, true>("SS N128, runtime ring slot, lane 0", sms);
+    return 0;
+  }
   run<0>("SS N128 only (MMA1)", sms);
   run<1>("TS N160 only (MMA2)", sms);
   run<2>("SS + TS, one issuer", sms);
