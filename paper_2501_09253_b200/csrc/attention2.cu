@@ -207,9 +207,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
             tc_fence_after();
           }
           for (int kc = 0; kc < Cfg::KB; ++kc) {
+            const uint64_t dq = dq0 + (uint64_t)((kc * A2_BM * 128) >> 4);
+            const uint64_t dk = dk0 + (uint64_t)((ks * Cfg::K_SLOT) >> 4);
+#if A2_WARP_ISSUE
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_bf16_ss_2sm_w(tmem + Cfg::S_COL, dq + (uint64_t)(k * 2), dk + (uint64_t)(k * 2), idesc_s,
+                                (kc | k) != 0);
+            mma_commit_2sm_w(&k_empty[ks], 0x3);
+            if (kc == Cfg::KB - 1) mma_commit_2sm_w(s_full, 0x3);
+#else
             if (lane == 0) {
-              const uint64_t dq = dq0 + (uint64_t)((kc * A2_BM * 128) >> 4);
-              const uint64_t dk = dk0 + (uint64_t)((ks * Cfg::K_SLOT) >> 4);
 #pragma unroll
               for (int k = 0; k < 4; ++k)
                 mma_bf16_ss_2sm(tmem + Cfg::S_COL, dq + (uint64_t)(k * 2), dk + (uint64_t)(k * 2), idesc_s,
@@ -218,6 +226,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
               if (kc == Cfg::KB - 1) mma_commit_2sm(s_full, 0x3);
             }
             __syncwarp();
+#endif
             if (++ks == Cfg::NK) { ks = 0; kph ^= 1; }
           }
           if (lane == 0) { A2_TRACE(1, j) }
@@ -236,8 +245,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
             twait(&v_full[vs], vph, w_c);
             if (p.trace) vw += clock64() - tv0;
             tc_fence_after();
+            const uint64_t dv = dv0 + (uint64_t)((vs * Cfg::V_SLOT) >> 4);
+#if A2_WARP_ISSUE
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+              for (int n = 0; n < Cfg::PV_MMAS; ++n)
+                mma_bf16_ts_2sm_w(tmem + Cfg::O_COL + n * Cfg::PV_N, tmem + Cfg::P_COL + ka * 32 + k * 8,
+                                  dv + (uint64_t)((n * Cfg::V_ROWS * 128 + k * 32) >> 4), idesc_o,
+                                  (j | ka | k) != 0);
+            mma_commit_2sm_w(&v_empty[vs], 0x3);
+            if (ka == 1) {
+              mma_commit_2sm_w(p_free, 0x3);
+              if (j == n_kb - 1) mma_commit_2sm_w(o_full, 0x3);
+            }
+#else
             if (lane == 0) {
-              const uint64_t dv = dv0 + (uint64_t)((vs * Cfg::V_SLOT) >> 4);
 #pragma unroll
               for (int k = 0; k < 4; ++k)
 #pragma unroll
@@ -252,6 +275,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
               }
             }
             __syncwarp();
+#endif
             if (++vs == Cfg::NV) { vs = 0; vph ^= 1; }
           }
           if (lane == 0) { A2_TRACE(3, j) }

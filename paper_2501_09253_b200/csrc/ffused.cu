@@ -19,6 +19,9 @@
 #include "common.cuh"
 #include "ps_internal.h"
 
+#ifndef FF_WARP_ISSUE  // MMA issue by the converged warp (elect.sync in the asm) instead of lane 0
+#define FF_WARP_ISSUE 0  // measured: fused FF 205 -> 210 us with it on
+#endif
 namespace ps {
 
 constexpr int FF_BM = 128;
@@ -232,6 +235,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
               const int s = (int)(gi % FF_NS);
               tw(&w_full[s], (uint32_t)((gi / FF_NS) & 1), 0);
               tc_fence_after();
+#if FF_WARP_ISSUE
+              {  // the converged warp issues (elect.sync in the asm): uniform-register descriptors
+                const uint64_t dx = sdesc_sw128(sX + kb * FF_BM * 128), dw = sdesc_sw128(sW + s * FF_SLOT);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  mma_bf16_ss_2sm_w(tmem + Cfg::H_COL, dx + (uint64_t)(k * 2), dw + (uint64_t)(k * 2), idesc1,
+                                    (kb | k) != 0);
+                mma_commit_2sm_w(&w_empty[s], 0x3);
+                if (kb == Cfg::KB - 1) {
+                  mma_commit_2sm_w(h_full, 0x3);
+                  if (c == NC - 1) mma_commit_2sm_w(x_empty, 0x3);
+                  if (lane == 0) FF_STAMP(g, 1);
+                }
+              }
+#else
               if (lane == 0) {
                 const uint8_t* wt = sW + s * FF_SLOT;
 #pragma unroll
@@ -246,6 +264,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
                 }
               }
               __syncwarp();
+#endif
             }
           } else {
             tw(hs_full, g & 1, 2);  // H(c) written to shared memory
@@ -261,6 +280,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
                 const int s = (int)(gi % FF_NS);
                 tw(&w_full[s], (uint32_t)((gi / FF_NS) & 1), 0);
                 tc_fence_after();
+#if FF_WARP_ISSUE
+                {
+                  const uint64_t dw = sdesc_sw128(sW + s * FF_SLOT), dh = sdesc_sw128(sH + kk * FF_BM * 128);
+#pragma unroll
+                  for (int k = 0; k < 4; ++k) {
+                    if (p.ts)
+                      mma_bf16_ts_2sm_w(tmem + Cfg::O_COL + nn * Cfg::NHALF, tmem + Cfg::HB_COL + kk * 32 + k * 8,
+                                        dw + (uint64_t)(k * 2), idesc2, (c | kk | k) != 0);
+                    else
+                      mma_bf16_ss_2sm_w(tmem + Cfg::O_COL + nn * Cfg::NHALF, dh + (uint64_t)(k * 2),
+                                        dw + (uint64_t)(k * 2), idesc2, (c | kk | k) != 0);
+                  }
+                  mma_commit_2sm_w(&w_empty[s], 0x3);
+                  if (kk == 1 && (half >= 0 || nn == 1)) {  // the chunk's last W2 piece
+                    mma_commit_2sm_w(hs_empty, 0x3);
+                    if (c == NC - 1) mma_commit_2sm_w(o_full, 0x3);
+                    if (lane == 0) FF_STAMP(g, 3);
+                  }
+                }
+#else
                 if (lane == 0) {
                   const uint8_t* wt = sW + s * FF_SLOT;
 #pragma unroll
@@ -281,6 +320,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
                   }
                 }
                 __syncwarp();
+#endif
               }
           }
         }

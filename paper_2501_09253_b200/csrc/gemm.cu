@@ -32,6 +32,9 @@
 #include "common.cuh"
 #include "ps_internal.h"
 
+#ifndef GEMM_WARP_ISSUE  // MMA issue by the converged warp (elect.sync in the asm) instead of lane 0
+#define GEMM_WARP_ISSUE 0  // measured: conv3 (pair, BN = 320) 192 -> 211 us with it on
+#endif
 namespace ps {
 
 constexpr int GEMM_BM = 128;
@@ -263,6 +266,31 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int kb = 0; kb < num_kb; ++kb) {
         timed_wait(&full[stage], phase, t_wait);
         tc_fence_after();
+#if GEMM_WARP_ISSUE
+        {  // the converged warp issues (elect.sync in the asm): uniform-register descriptors
+          const uint64_t da = sdesc_sw128(smem + stage * Cfg::STAGE_BYTES);
+          const uint64_t db = da + (uint64_t)(Cfg::A_BYTES >> 4);
+#pragma unroll
+          for (int k = 0; k < GEMM_BK / 16; ++k)
+#pragma unroll
+            for (int j = 0; j < Cfg::N_MMA; ++j) {
+              if (half >= 0 && j != half) continue;
+              if (PAIR)
+                mma_bf16_ss_2sm_w(d + j * Cfg::MMA_N, da + (uint64_t)(k * 2),
+                                  db + (uint64_t)((j * Cfg::B_ROWS * 128 + k * 32) >> 4), idesc, (kb | k) != 0);
+              else
+                mma_bf16_ss_w(d + j * Cfg::MMA_N, da + (uint64_t)(k * 2),
+                              db + (uint64_t)((j * Cfg::MMA_N * 128 + k * 32) >> 4), idesc, (kb | k) != 0);
+            }
+          if (PAIR) {
+            mma_commit_2sm_w(&empty[stage], 0x3);
+            if (kb == num_kb - 1) mma_commit_2sm_w(&acc_full[buf], 0x3);
+          } else {
+            mma_commit_w(&empty[stage]);
+            if (kb == num_kb - 1) mma_commit_w(&acc_full[buf]);
+          }
+        }
+#else
         if (lane == 0) {
           // descriptor = stage base + (byte offset >> 4): the start-address field is the low bits
           const uint64_t da = sdesc_sw128(smem + stage * Cfg::STAGE_BYTES);
@@ -288,6 +316,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
         __syncwarp();
+#endif
         if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
       }
     }
