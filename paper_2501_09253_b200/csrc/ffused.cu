@@ -20,7 +20,7 @@
 #include "ps_internal.h"
 
 #ifndef FF_WARP_ISSUE  // MMA issue by the converged warp (elect.sync in the asm) instead of lane 0
-#define FF_WARP_ISSUE 0  // measured: fused FF 205 -> 210 us with it on
+#define FF_WARP_ISSUE 1  // fused FF 207 -> 186 us (p.ts branch hoisted out of the MMA loop; with it inside, 205 -> 210)
 #endif
 namespace ps {
 
@@ -282,15 +282,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
                 tc_fence_after();
 #if FF_WARP_ISSUE
                 {
-                  const uint64_t dw = sdesc_sw128(sW + s * FF_SLOT), dh = sdesc_sw128(sH + kk * FF_BM * 128);
+                  const uint64_t dw = sdesc_sw128(sW + s * FF_SLOT);
+                  const uint32_t dcol = tmem + Cfg::O_COL + nn * Cfg::NHALF;
+                  if (p.ts) {  // one branch per piece: no runtime condition between the MMAs
+                    const uint32_t acol = tmem + Cfg::HB_COL + kk * 32;
 #pragma unroll
-                  for (int k = 0; k < 4; ++k) {
-                    if (p.ts)
-                      mma_bf16_ts_2sm_w(tmem + Cfg::O_COL + nn * Cfg::NHALF, tmem + Cfg::HB_COL + kk * 32 + k * 8,
-                                        dw + (uint64_t)(k * 2), idesc2, (c | kk | k) != 0);
-                    else
-                      mma_bf16_ss_2sm_w(tmem + Cfg::O_COL + nn * Cfg::NHALF, dh + (uint64_t)(k * 2),
-                                        dw + (uint64_t)(k * 2), idesc2, (c | kk | k) != 0);
+                    for (int k = 0; k < 4; ++k)
+                      mma_bf16_ts_2sm_w(dcol, acol + k * 8, dw + (uint64_t)(k * 2), idesc2, (c | kk | k) != 0);
+                  } else {
+                    const uint64_t dh = sdesc_sw128(sH + kk * FF_BM * 128);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                      mma_bf16_ss_2sm_w(dcol, dh + (uint64_t)(k * 2), dw + (uint64_t)(k * 2), idesc2,
+                                        (c | kk | k) != 0);
                   }
                   mma_commit_2sm_w(&w_empty[s], 0x3);
                   if (kk == 1 && (half >= 0 || nn == 1)) {  // the chunk's last W2 piece

@@ -33,7 +33,7 @@
 #include "ps_internal.h"
 
 #ifndef GEMM_WARP_ISSUE  // MMA issue by the converged warp (elect.sync in the asm) instead of lane 0
-#define GEMM_WARP_ISSUE 0  // measured: conv3 (pair, BN = 320) 192 -> 211 us with it on
+#define GEMM_WARP_ISSUE 1  // conv3 193 -> 180 us (per-MMA tail-split test hoisted; with it inside, 192 -> 211)
 #endif
 namespace ps {
 
@@ -270,18 +270,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         {  // the converged warp issues (elect.sync in the asm): uniform-register descriptors
           const uint64_t da = sdesc_sw128(smem + stage * Cfg::STAGE_BYTES);
           const uint64_t db = da + (uint64_t)(Cfg::A_BYTES >> 4);
+          auto issue = [&](int k, int j) {
+            if (PAIR)
+              mma_bf16_ss_2sm_w(d + j * Cfg::MMA_N, da + (uint64_t)(k * 2),
+                                db + (uint64_t)((j * Cfg::B_ROWS * 128 + k * 32) >> 4), idesc, (kb | k) != 0);
+            else
+              mma_bf16_ss_w(d + j * Cfg::MMA_N, da + (uint64_t)(k * 2),
+                            db + (uint64_t)((j * Cfg::MMA_N * 128 + k * 32) >> 4), idesc, (kb | k) != 0);
+          };
+          if (half < 0) {  // the common case: no per-MMA condition
 #pragma unroll
-          for (int k = 0; k < GEMM_BK / 16; ++k)
+            for (int k = 0; k < GEMM_BK / 16; ++k)
 #pragma unroll
-            for (int j = 0; j < Cfg::N_MMA; ++j) {
-              if (half >= 0 && j != half) continue;
-              if (PAIR)
-                mma_bf16_ss_2sm_w(d + j * Cfg::MMA_N, da + (uint64_t)(k * 2),
-                                  db + (uint64_t)((j * Cfg::B_ROWS * 128 + k * 32) >> 4), idesc, (kb | k) != 0);
-              else
-                mma_bf16_ss_w(d + j * Cfg::MMA_N, da + (uint64_t)(k * 2),
-                              db + (uint64_t)((j * Cfg::MMA_N * 128 + k * 32) >> 4), idesc, (kb | k) != 0);
-            }
+              for (int j = 0; j < Cfg::N_MMA; ++j) issue(k, j);
+          } else {
+#pragma unroll
+            for (int k = 0; k < GEMM_BK / 16; ++k) issue(k, half);
+          }
           if (PAIR) {
             mma_commit_2sm_w(&empty[stage], 0x3);
             if (kb == num_kb - 1) mma_commit_2sm_w(&acc_full[buf], 0x3);
@@ -295,18 +300,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           // descriptor = stage base + (byte offset >> 4): the start-address field is the low bits
           const uint64_t da = sdesc_sw128(smem + stage * Cfg::STAGE_BYTES);
           const uint64_t db = da + (uint64_t)(Cfg::A_BYTES >> 4);
+          auto issue = [&](int k, int j) {
+            if (PAIR)
+              mma_bf16_ss_2sm(d + j * Cfg::MMA_N, da + (uint64_t)(k * 2),
+                              db + (uint64_t)((j * Cfg::B_ROWS * 128 + k * 32) >> 4), idesc, (kb | k) != 0);
+            else
+              mma_bf16_ss(d + j * Cfg::MMA_N, da + (uint64_t)(k * 2),
+                          db + (uint64_t)((j * Cfg::MMA_N * 128 + k * 32) >> 4), idesc, (kb | k) != 0);
+          };
+          if (half < 0) {  // the common case: no per-MMA condition
 #pragma unroll
-          for (int k = 0; k < GEMM_BK / 16; ++k)
+            for (int k = 0; k < GEMM_BK / 16; ++k)
 #pragma unroll
-            for (int j = 0; j < Cfg::N_MMA; ++j) {
-              if (half >= 0 && j != half) continue;
-              if (PAIR)
-                mma_bf16_ss_2sm(d + j * Cfg::MMA_N, da + (uint64_t)(k * 2),
-                                db + (uint64_t)((j * Cfg::B_ROWS * 128 + k * 32) >> 4), idesc, (kb | k) != 0);
-              else
-                mma_bf16_ss(d + j * Cfg::MMA_N, da + (uint64_t)(k * 2),
-                            db + (uint64_t)((j * Cfg::MMA_N * 128 + k * 32) >> 4), idesc, (kb | k) != 0);
-            }
+              for (int j = 0; j < Cfg::N_MMA; ++j) issue(k, j);
+          } else {
+#pragma unroll
+            for (int k = 0; k < GEMM_BK / 16; ++k) issue(k, half);
+          }
           if (PAIR) {
             mma_commit_2sm(&empty[stage], 0x3);
             if (kb == num_kb - 1) mma_commit_2sm(&acc_full[buf], 0x3);
