@@ -61,6 +61,17 @@ PS_DEV void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint3
       : "memory");
 }
 
+// warp-wide variant (elect.sync in the asm), as mma_bf16_ts_2sm_w
+PS_DEV void mma_bf16_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 template <int DP>
 __global__ void __launch_bounds__(AT_THREADS, 1)
     attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -209,16 +220,14 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         for (int kc = 0; kc < Cfg::KB; ++kc) {
           twait(&k_full[ks], kph, w_c);
           tc_fence_after();
-          if (lane == 0) {
-            const uint8_t* kt = sK + ks * Cfg::K_SLOT;
+          {  // the converged warp issues (elect.sync in the asm; see attention2.cu)
+            const uint64_t dq = sdesc_sw128(sQ + kc * AT_BM * 128), dk = sdesc_sw128(sK + ks * Cfg::K_SLOT);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              mma_bf16_ss(tmem + Cfg::S_COL, sdesc_sw128(sQ + kc * AT_BM * 128 + k * 32), sdesc_sw128(kt + k * 32),
-                          idesc_s, (kc | k) != 0);
-            mma_commit(&k_empty[ks]);
-            if (kc == Cfg::KB - 1) mma_commit(s_full);
+              mma_bf16_ss_w(tmem + Cfg::S_COL, dq + (uint64_t)(k * 2), dk + (uint64_t)(k * 2), idesc_s, (kc | k) != 0);
+            mma_commit_w(&k_empty[ks]);
+            if (kc == Cfg::KB - 1) mma_commit_w(s_full);
           }
-          __syncwarp();
           if (++ks == Cfg::NK) { ks = 0; kph ^= 1; }
         }
       }
@@ -231,21 +240,20 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         for (int ka = 0; ka < 2; ++ka) {
           twait(&v_full[vs], vph, w_c);
           tc_fence_after();
-          if (lane == 0) {
-            const uint8_t* vt = sV + vs * Cfg::V_SLOT;
+          {
+            const uint64_t dv = sdesc_sw128(sV + vs * Cfg::V_SLOT);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
 #pragma unroll
               for (int n = 0; n < Cfg::PV_MMAS; ++n)
-                mma_bf16_ts(tmem + Cfg::O_COL + n * Cfg::PV_N, tmem + Cfg::P_COL + ka * 32 + k * 8,
-                            sdesc_sw128(vt + n * Cfg::PV_N * 128 + k * 32), idesc_o, (j | ka | k) != 0);
-            mma_commit(&v_empty[vs]);
+                mma_bf16_ts_w(tmem + Cfg::O_COL + n * Cfg::PV_N, tmem + Cfg::P_COL + ka * 32 + k * 8,
+                              dv + (uint64_t)((n * Cfg::PV_N * 128 + k * 32) >> 4), idesc_o, (j | ka | k) != 0);
+            mma_commit_w(&v_empty[vs]);
             if (ka == 1) {
-              mma_commit(p_free);
-              if (j == n_kb - 1) mma_commit(o_full);
+              mma_commit_w(p_free);
+              if (j == n_kb - 1) mma_commit_w(o_full);
             }
           }
-          __syncwarp();
           if (++vs == Cfg::NV) { vs = 0; vph ^= 1; }
         }
       }
