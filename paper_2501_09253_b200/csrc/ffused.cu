@@ -44,7 +44,8 @@ struct FfCfg {
   // the banks -- with 32-float rows they were 16-way conflicts (77% of the kernel's shared-load
   // wavefronts, ncu round 2)
   static constexpr int STG = 12 * 16 * FF_ST_LD * 4;
-  static constexpr int SMEM = X_BYTES + H_BYTES + FF_NS * FF_SLOT + STG + 1024 + 512;
+  static constexpr int B1_FLOATS = 1280;  // first-layer biases staged in shared memory (hp <= 1280)
+  static constexpr int SMEM = X_BYTES + H_BYTES + FF_NS * FF_SLOT + STG + (B1_FLOATS + CP) * 4 + 1024 + 512;
   // TMEM: O (Cp fp32) | H chunk (128 fp32) | GELU(H) chunk as bf16 pairs (64), MMA2's A (p.ts)
   static constexpr int O_COL = 0, H_COL = CP, HB_COL = CP + FF_HC;
   static_assert(CP % 64 == 0 && NHALF % 16 == 0 && W2_ROWS % 8 == 0 && W2_ROWS * 128 <= FF_SLOT, "Cp");
@@ -66,7 +67,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
   uint8_t* sH = sX + Cfg::X_BYTES;
   uint8_t* sW = sH + Cfg::H_BYTES;
   float* sStg = reinterpret_cast<float*>(sW + FF_NS * FF_SLOT);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sStg) + Cfg::STG);
+  float* sB1 = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(sStg) + Cfg::STG);
+  float* sB2 = sB1 + Cfg::B1_FLOATS;  // [CP] output biases
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB2 + CP);
   uint64_t* x_full = bars;
   uint64_t* x_empty = bars + 1;
   uint64_t* w_full = bars + 2;
@@ -101,6 +104,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc_2sm(tmem_slot, 512);
+  // first-layer biases -> shared memory (the chunk epilogue's per-chunk reads were L2 loads
+  // issued next to the H wait); weights are not written by the previous kernel, so this may
+  // run before the PDL wait
+  const bool b1_smem = p.hp <= Cfg::B1_FLOATS;
+  if (b1_smem && warp >= 4)
+    for (int i = threadIdx.x - 128; i < p.hp / 4; i += FF_THREADS - 128)
+      reinterpret_cast<float4*>(sB1)[i] = __ldg(reinterpret_cast<const float4*>(p.b1) + i);
+  if (warp >= 4)
+    for (int i = threadIdx.x - 128; i < CP / 4; i += FF_THREADS - 128)
+      reinterpret_cast<float4*>(sB2)[i] = __ldg(reinterpret_cast<const float4*>(p.b2) + i);
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
@@ -352,10 +365,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
       for (int c = 0; c < NC; ++c, ++g) {
         if (wg >= 2) continue;
         // the chunk's biases (64 per thread, warp-uniform addresses) load while MMA1 runs
-        const float4* b1 = reinterpret_cast<const float4*>(p.b1 + c * FF_HC + wg * 64);
         float4 bq[16];
+        if (b1_smem) {
+          const float4* b1 = reinterpret_cast<const float4*>(sB1 + c * FF_HC + wg * 64);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) bq[i] = __ldg(b1 + i);
+          for (int i = 0; i < 16; ++i) bq[i] = b1[i];
+        } else {
+          const float4* b1 = reinterpret_cast<const float4*>(p.b1 + c * FF_HC + wg * 64);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) bq[i] = __ldg(b1 + i);
+        }
         tw(h_full, g & 1, 0);
         const bool probe = PROBE && warp == 4 && lane == 0;
         const long long ph0 = probe ? clock64() : 0;
@@ -450,7 +469,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) + 0.f;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.b2 + cc) + q);
+          const float4 b4 = reinterpret_cast<const float4*>(sB2 + cc)[q];
           v[4 * q] += b4.x; v[4 * q + 1] += b4.y; v[4 * q + 2] += b4.z; v[4 * q + 3] += b4.w;
         }
 #pragma unroll
