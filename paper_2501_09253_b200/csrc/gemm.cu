@@ -61,14 +61,20 @@ struct GemmCfg {
   static constexpr int A_BYTES = GEMM_BM * 128;
   static constexpr int B_BYTES = N_MMA * B_ROWS * 128;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGE_BUDGET = 176 * 1024;
+  // BN = 320 (conv3): one epilogue staging buffer per warp instead of two, which pays for a
+  // fifth 36 KB operand stage (the MMA warp waited on TMA data 35% of the time with four)
+  static constexpr int TMA_BUFS = BN == 320 ? 1 : 2;
+  static constexpr int STAGE_EPI_ = GEMM_NWG > 2 ? 0 : GEMM_NWG * 16 * GEMM_BM * 4;
+  static constexpr int STAGE_TMA_ = GEMM_NWG * TMA_BUFS * GEMM_BM * 64;
+  static constexpr int STAGE_BUDGET = BN == 320 ? 227 * 1024 - STAGE_TMA_ - STAGE_EPI_ - 1280 : 176 * 1024;
   static constexpr int STAGES = STAGE_BUDGET / STAGE_BYTES > 8 ? 8 : STAGE_BUDGET / STAGE_BYTES;
   static constexpr int TMEM_COLS = NBUF * BN <= 128 ? 128 : NBUF * BN <= 256 ? 256 : 512;
   static constexpr int HALF = BN / 2;  // columns per epilogue warp
   static constexpr int STAGE_EPI = GEMM_NWG > 2 ? 0 : GEMM_NWG * 16 * GEMM_BM * 4;  // transposed-store staging
-  static constexpr int STAGE_TMA = GEMM_NWG * 2 * GEMM_BM * 64;  // per warpgroup: two 128x32 bf16 store boxes
+  static constexpr int STAGE_TMA = STAGE_TMA_;  // per warpgroup: TMA_BUFS 128x32 bf16 store boxes
   static constexpr int SMEM = STAGES * STAGE_BYTES + STAGE_EPI + STAGE_TMA + 1024 /*align*/ + 256 /*barriers*/;
   static_assert(MMA_N % 16 == 0 && MMA_N >= 64 && MMA_N <= 256, "invalid UMMA N");
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
   static_assert(B_ROWS % 8 == 0, "B half rows must be whole 128B-swizzle atoms");
   static_assert(BN % 32 == 0 && (BN / 2) % 32 == 0 || BN <= 256, "epilogue chunking");
 };
@@ -345,7 +351,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int bar_id = 1 + wg;
     const bool wg_leader = (warp & 3) == 0 && lane == 0;
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-    uint8_t* box_base = tma_stage + wg * 2 * (GEMM_BM * 64);  // two 8 KB boxes per warpgroup
+    uint8_t* box_base = tma_stage + wg * Cfg::TMA_BUFS * (GEMM_BM * 64);  // TMA_BUFS 8 KB boxes per warpgroup
     // transposed (NCHW / V^T) stores: a [16][128] fp32 tile per warpgroup, or with
     // warp_store a [16][32] tile per warp (its own 32 rows; only __syncwarp needed)
     const bool wst = GEMM_NWG > 2 || p.warp_store != 0;
@@ -429,8 +435,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
           if (p.warp_store) {
             // per-warp 32x32 box: no cross-warp barrier, lane 0 issues the TMA store
-            uint8_t* box = tma_stage + (warp - 4) * 4096 + (n_store & 1) * 2048;
-            if (lane == 0) bulk_wait_read<1>();
+            uint8_t* box = tma_stage + (warp - 4) * (Cfg::TMA_BUFS * 2048) + (n_store % Cfg::TMA_BUFS) * 2048;
+            if (lane == 0) bulk_wait_read<Cfg::TMA_BUFS - 1>();
             __syncwarp();
 #pragma unroll
             for (int q = 0; q < 4; ++q)
@@ -448,8 +454,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             ++n_store;
             return;
           }
-          uint8_t* box = box_base + (n_store & 1) * (GEMM_BM * 64);
-          if (wg_leader) bulk_wait_read<1>();  // the TMA store that last used this box has read it
+          uint8_t* box = box_base + (n_store % Cfg::TMA_BUFS) * (GEMM_BM * 64);
+          if (wg_leader) bulk_wait_read<Cfg::TMA_BUFS - 1>();  // the TMA store that last used this box has read it
           named_bar_sync(bar_id, 128);
 #pragma unroll
           for (int q = 0; q < 4; ++q)
@@ -492,9 +498,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               rs1 = __ldg(reinterpret_cast<const uint4*>(p.resid + off_v) + 1);
             }
             if constexpr (GEMM_NWG > 2) {
-              if (lane == 0 && p.store_tma) bulk_wait_read<1>();
+              if (lane == 0 && p.store_tma) bulk_wait_read<Cfg::TMA_BUFS - 1>();
               __syncwarp();
-              st = reinterpret_cast<float*>(tma_stage + (warp - 4) * 4096 + (n_store & 1) * 2048);
+              st = reinterpret_cast<float*>(tma_stage + (warp - 4) * (Cfg::TMA_BUFS * 2048) +
+                                            (n_store % Cfg::TMA_BUFS) * 2048);
             }
             // per-warp [16][32] tile: 16-byte groups XOR-swizzled by row, so the transposed
             // float4 reads (16 lanes on 16 rows of one column range) hit distinct banks -- plain
