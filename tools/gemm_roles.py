@@ -40,6 +40,12 @@ def run(name, M, N, K, epi, bn=0, out_tiled=0, a_tiled=0, resid=False, pair=0):
     f = lambda a, b: a / b if b else 0
     print(f"{name:8s} {ms*1e3:7.1f} us {2*M*N*K/ms/1e9:7.1f} TF | prod wait {f(d[0],d[1]):.2f} | mma wait-full {f(d[2],d[4]):.2f} wait-acc {f(d[3],d[4]):.2f} | epi wait-acc {f(d[5],d[6]):.2f}")
 
+ONLY = sys.argv[2:] if len(sys.argv) > 2 and sys.argv[1] == "only" else None  # e.g. only conv-ish (for ncu)
+_run = run
+def run(name, *a, **k):
+    if ONLY is None or name in ONLY:
+        _run(name, *a, **k)
+
 run("conv-ish", T, 320, 2880, 0)
 run("qkv", T, 960, 320, 3)
 run("oproj", T, 320, 320, 0)
