@@ -361,6 +361,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FF_THREADS, 1)
       item(w, u, half);
       const int mt = my_m(u);
       const int c_lo = half < 0 ? 0 : half * Cfg::NHALF, c_hi = half < 0 ? CP : c_lo + Cfg::NHALF;
+      // the idle third warpgroup pulls this tile's residual rows (one 256-byte NCHW segment per
+      // channel) into L2 while the chunks run, so the output drain's residual loads hit L2
+      if (wg == 2 && p.resid != nullptr && mt >= 0 && (mt + 1) * FF_BM <= p.M && p.hw % FF_BM == 0) {
+        const int pidx0 = mt * FF_BM / p.hw, pix0 = mt * FF_BM - pidx0 * p.hw;
+        for (int ch = c_lo + (threadIdx.x - 384); ch < min(c_hi, p.c_real); ch += 128)
+          l2_prefetch(p.resid + ((size_t)pidx0 * p.c_real + ch) * p.hw + pix0, FF_BM * 2);
+      }
       // ---- hidden chunks: H -> +b1 -> bf16 -> GELU -> MMA2's A operand (warpgroups 0, 1)
       for (int c = 0; c < NC; ++c, ++g) {
         if (wg >= 2) continue;
