@@ -334,10 +334,14 @@ int ps_gemm(void* stream, const ps_gemm_args* a) {
   const int mma_n = bn <= 256 ? bn : bn / 2;
   // CTA-pair tiles (cta_group::2) unless asked otherwise or the problem is too small to fill the SMs in pairs
   const int m_tiles = a->m_map ? a->m_count : (a->M + 127) / 128;
-  // auto: CTA pairs for the long-K 320-wide tiles (conv3: 219 -> 207 us, tools/gemm_pair_check.py),
-  // single-CTA tiles elsewhere (equal or faster); PS_GEMM_PAIR=1|2 forces single|pairs
+  // auto: CTA pairs for the long-K 320-wide tiles (conv3: 219 -> 207 us, tools/gemm_pair_check.py)
+  // and, since the warp-wide MMA issue, for every GEMM with at least two waves of pair tiles
+  // (O-projection 39 -> 35 us, QKV 90 -> 88 us, tools/gemm_roles.py pair); single-CTA tiles for
+  // small (compacted) problems; PS_GEMM_PAIR=1|2 forces single|pairs
   static const int env_pair = getenv("PS_GEMM_PAIR") ? atoi(getenv("PS_GEMM_PAIR")) : 0;
-  const int want = a->cta_pair ? a->cta_pair : env_pair ? env_pair : (bn == 320 && a->K >= 2048 ? 2 : 1);
+  const int want = a->cta_pair ? a->cta_pair
+                   : env_pair  ? env_pair
+                               : ((bn == 320 && a->K >= 2048) || m_tiles >= 4 * 148 ? 2 : 1);
   const int pair = want == 2 && m_tiles >= 2 ? 1 : 0;
   CUtensorMap ta, tb;
   GemmParams p{};

@@ -63,10 +63,12 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // BN = 320 (conv3): one epilogue staging buffer per warp instead of two, which pays for a
   // fifth 36 KB operand stage (the MMA warp waited on TMA data 35% of the time with four)
-  static constexpr int TMA_BUFS = BN == 320 ? 1 : 2;
+  // (BN = 160, the O-projection: 4 -> 5 stages, 39 -> 36 us single-CTA; the channels-last TMA-store
+  // epilogues -- QKV BN = 192 -- keep two boxes: one measured 90 -> 91.5 us)
+  static constexpr int TMA_BUFS = (BN == 320 || BN == 160) ? 1 : 2;
   static constexpr int STAGE_EPI_ = GEMM_NWG > 2 ? 0 : GEMM_NWG * 16 * GEMM_BM * 4;
   static constexpr int STAGE_TMA_ = GEMM_NWG * TMA_BUFS * GEMM_BM * 64;
-  static constexpr int STAGE_BUDGET = BN == 320 ? 227 * 1024 - STAGE_TMA_ - STAGE_EPI_ - 1280 : 176 * 1024;
+  static constexpr int STAGE_BUDGET = TMA_BUFS == 1 ? 227 * 1024 - STAGE_TMA_ - STAGE_EPI_ - 1280 : 176 * 1024;
   static constexpr int STAGES = STAGE_BUDGET / STAGE_BYTES > 8 ? 8 : STAGE_BUDGET / STAGE_BYTES;
   static constexpr int TMEM_COLS = NBUF * BN <= 128 ? 128 : NBUF * BN <= 256 ? 256 : 512;
   static constexpr int HALF = BN / 2;  // columns per epilogue warp
