@@ -59,6 +59,45 @@ void run(const char* name, int sms, int per_op) {
   cudaFree(c);
 }
 
+// the fused FF's chunk epilogue shape: 8 warps per SM (2 per SMSP), 32 independent bf16x2 GELUs
+// per thread per chunk (from fp32 pairs + bias, as ff_pair_kernel), cycles per chunk
+template <int NW, int NPAIR>
+__global__ void chunk_k(float* out, int iters, long long* cyc) {
+  float x[2 * NPAIR];
+  for (int i = 0; i < 2 * NPAIR; ++i) x[i] = 0.001f * (threadIdx.x + i);
+  uint32_t acc = 0;
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < NPAIR; ++i) {
+      const uint32_t g = gelu_bf16x2(pack_bf16(x[2 * i] + 0.5f, x[2 * i + 1] + 0.25f));
+      acc += g;
+      x[2 * i] += __uint_as_float(g & 0x8000u);  // keep a dependence across iterations
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = clock64() - t0;
+  out[blockIdx.x * blockDim.x + threadIdx.x] = (float)acc;
+}
+template <int NW, int NPAIR>
+void run_chunk(int sms) {
+  float* o;
+  long long* c;
+  cudaMalloc(&o, sms * NW * 32 * 4);
+  cudaMalloc(&c, 8);
+  const int iters = 200;
+  chunk_k<NW, NPAIR><<<sms, NW * 32>>>(o, 10, c);
+  chunk_k<NW, NPAIR><<<sms, NW * 32>>>(o, iters, c);
+  cudaDeviceSynchronize();
+  long long cyc;
+  cudaMemcpy(&cyc, c, 8, cudaMemcpyDeviceToHost);
+  printf("chunk GELU, %2d warps/SM, %2d pairs/thread: %6.0f cycles per chunk (%5.2f results/clk/SM)\n", NW, NPAIR,
+         (double)cyc / iters, 2.0 * NPAIR * NW * 32 * iters / cyc);
+  cudaFree(o);
+  cudaFree(c);
+}
+
 int main() {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -69,5 +108,9 @@ int main() {
   run<4>("ex2.approx.bf16x2", sms, 2);
   run<5>("rcp.approx.f32", sms, 1);
   run<6>("gelu_bf16x2 (common.cuh)", sms, 2);
+  run_chunk<8, 32>(sms);
+  run_chunk<12, 21>(sms);
+  run_chunk<16, 16>(sms);
+  run_chunk<8, 16>(sms);
   return 0;
 }
