@@ -512,7 +512,6 @@ template <int DP, int NV_>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
     attn2p_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
-  pdl_wait();
   using Cfg = Attn2Cfg<DP, NV_>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned, derived from smem_raw by an integer offset so the compiler keeps the
@@ -541,7 +540,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
-  const int n_tiles = p.n_dev != nullptr ? *p.n_dev : p.n_tiles;
   const int ncl = gridDim.x >> 1;
   // k-th tile of this cluster: dealt dynamically (an atomic ticket per tile, fetched by the
   // leader's producer and published through an 8-entry ring in both CTAs), so the longest-
@@ -588,6 +586,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // PDL: the setup above (barriers, TMEM, descriptor prefetch) overlaps the previous kernel's
+  // tail; Q/K/V, the device tile count and the ticket counters are read only after this
+  pdl_wait();
+  const int n_tiles = p.n_dev != nullptr ? *p.n_dev : p.n_tiles;
 
   if (warp == 0) {
     // -------------------------------------------------- producer (both CTAs)
