@@ -254,6 +254,41 @@ def test_gemm_cta_pair_tiles_bit_identical(M, N, K, bn):
     assert torch.equal(one, two)
 
 
+@pytest.mark.parametrize("epi", [2, 3])
+def test_gemm_cta_pair_epilogues_bit_identical(epi):
+    """The attention's GEMM epilogues on CTA-pair tiles (the default for >= 4 waves of tiles):
+    QKV's split epilogue (Q, K channels-last through TMA stores, V^T transposed) and the
+    O-projection's bias + residual -> NCHW epilogue equal the single-CTA tiles bit for bit,
+    including a ragged last m tile."""
+    torch.manual_seed(epi)
+    hw, ch = 1024, 320
+    M = 9 * hw + 512 if epi == 3 else 9 * hw  # NCHW epilogue: whole patches
+    N, K = (960, 320) if epi == 3 else (320, 320)
+    a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    b = (torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
+    bias = torch.randn(N, device="cuda")
+    res = torch.randn(M * N, device="cuda").to(torch.bfloat16)
+    outs = []
+    for pair in (1, 2):
+        out = torch.full((M * N + 1024,), float("nan"), dtype=torch.bfloat16, device="cuda")
+        out2 = torch.full((N * ((M + 63) // 64 * 64),), float("nan"), dtype=torch.bfloat16, device="cuda")
+        g = _lib.GemmArgs()
+        g.a, g.lda, g.M, g.a_mode = a.data_ptr(), K, M, 0
+        g.b, g.N, g.K, g.bias = b.data_ptr(), N, K, bias.data_ptr()
+        g.epi, g.out, g.ldo, g.bn = epi, out.data_ptr(), N, 0
+        g.P, g.ps = M // hw, 32
+        g.cta_pair = pair
+        if epi == 3:
+            g.out2, g.ldo2, g.n_split, g.ldo = out2.data_ptr(), (M + 63) // 64 * 64, 2 * N // 3, 2 * N // 3
+        else:
+            g.resid, g.c_real = res.data_ptr(), ch
+        _lib.check(_lib.load().ps_gemm(stream(), C.byref(g)))
+        torch.cuda.synchronize()
+        outs.append((out.clone(), out2.clone()))
+    assert torch.equal(outs[0][0].view(torch.int16), outs[1][0].view(torch.int16))
+    assert torch.equal(outs[0][1].view(torch.int16), outs[1][1].view(torch.int16))
+
+
 def test_attention_pair_kernel_bit_identical_to_single():
     """The default CTA-pair attention (attention2.cu) and the single-CTA kernel agree bit for
     bit on a mixed batch (same MMA accumulation order and softmax arithmetic)."""
