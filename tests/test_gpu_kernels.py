@@ -311,7 +311,8 @@ def test_attention_pair_kernel_bit_identical_to_single():
 
 
 @pytest.mark.parametrize("C,H,lat,compact", [(320, 1280, (64, 32, 96), False), (320, 1280, (64, 96), True),
-                                             (128, 256, (32, 64), False), (192, 384, (64,), False)])
+                                             (128, 256, (32, 64), False), (192, 384, (64,), False),
+                                             (320, 1280, (64, 96, 128) * 4, False)])  # config 2: P = 116
 def test_fused_feed_forward_bit_identical_to_two_gemms(C, H, lat, compact, monkeypatch):
     """ps_feed_forward (FF1 + GELU + FF2 + residual with the hidden kept on chip, CTA pairs)
     equals the two-GEMM path bit for bit, with and without a compaction tile map."""
