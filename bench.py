@@ -622,21 +622,27 @@ def measure_hbm_kernels(pipe, peak_gbs):
               len(tc["ps_cache_substitute"])),
              ("ps_cache_finish (50% mask)", n * 2 * (2 * m + 4 * (P - m)), float(np.mean(tc["ps_cache_finish"])),
               len(tc["ps_cache_finish"]))]
-    # read-only context: a plain read-reduction (torch.sum) of the same bytes, timed the same way
-    # -- read-only launches of these sizes stop well short of the copy bandwidth `peak_gbs` is
+    # read-only context: the pure streaming-read ceiling at the same size -- ps_checksum (an XOR
+    # fold: nothing but the loads; the fastest of the 14 read-kernel shapes tools/micro/read_bw.cu
+    # swept) over the same number of bytes, timed the same way.  Read-only launches of 76 / 152 MB
+    # stop short of the copy figure `peak_gbs` is (profiles/r2_read_bw.jsonl: 4.1 / 4.9 TB/s at
+    # 76 / 152 MB against 6.9 TB/s at 1 GB, L2 clean-flushed).
+    from paper_2501_09253_b200._dev import stream as _stream
+    from paper_2501_09253_b200._lib import call as _lib_call
     flushbuf = torch.ones(flush // 4, device="cuda")
     sink = torch.zeros(1, device="cuda")
+    word = torch.zeros(1, dtype=torch.int32, device="cuda")
 
     def read_floor(nbytes):
         t = torch.ones(nbytes // 2, dtype=torch.bfloat16, device="cuda")
         for _ in range(3):
-            t.sum(dtype=torch.float32)
+            _lib_call("ps_checksum", _stream(), t.data_ptr(), nbytes, word.data_ptr())
         ts = []
         for _ in range(12):
             sink.add_(flushbuf.sum())
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            t.sum(dtype=torch.float32)
+            _lib_call("ps_checksum", _stream(), t.data_ptr(), nbytes, word.data_ptr())
             e1.record()
             e1.synchronize()
             ts.append(e0.elapsed_time(e1))
@@ -652,11 +658,13 @@ def measure_hbm_kernels(pipe, peak_gbs):
             f = floors[read_only[name]]
             row["read_floor_us"] = round(f * 1e3, 2)
             row["vs_read_floor"] = round(f / ms_, 3)
+            row["read_peak_gbs"] = round(nbytes / (f * 1e-3) / 1e9, 1)
         out.append(row)
     return {"peak_gbs": peak_gbs, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, read+write bytes)",
             "timing": "each launch alone, L2 flushed (256 MB write) before it, CUDA events on its stream",
-            "read_floor": "read-only kernels: torch.sum over the same bytes timed the same way "
-                          "(vs_read_floor = its time / ours)",
+            "read_floor": "read-only kernels: the pure streaming-read ceiling at the same size (ps_checksum, "
+                          "LDG.256 XOR fold of the same bytes) timed the same way; vs_read_floor = its time / "
+                          "ours, read_frac = our bytes/s over its bytes/s",
             "kernels": out}
 
 

@@ -288,6 +288,11 @@ int ps_blend(void* stream, const float* latent, const void* h, const float* rate
              int P, int C, int ps, float* out);
 /* Dtype conversion helpers for the facade (f32 <-> bf16). */
 int ps_convert(void* stream, const void* src, int src_dtype, void* dst, int dst_dtype, int64_t n);
+/* *out ^= XOR fold of the buffer's 32-byte words (bytes % 32 == 0, data 32-byte aligned; the
+ * caller zeroes *out).  No reference counterpart: an integrity check for resident latents and
+ * cache snapshots, and the pure streaming-read ceiling bench.py measures the read-only kernels
+ * (ps_gn_partials, ps_cache_predict) against. */
+int ps_checksum(void* stream, const void* data, int64_t bytes, uint32_t* out);
 
 #ifdef __cplusplus
 }

@@ -65,3 +65,15 @@ def round_up(x: int, m: int) -> int:
 
 def i32(a, dev=None) -> torch.Tensor:
     return torch.as_tensor(np.asarray(a, dtype=np.int32), device=dev or require_cuda())
+
+
+def checksum(t: torch.Tensor) -> int:
+    """XOR fold of a CUDA tensor's 32-byte words (ps_checksum): an order-independent u32 over the
+    raw bytes, for checking resident latents / snapshots after a copy.  Needs a contiguous tensor
+    whose byte size is a multiple of 32 and whose storage is 32-byte aligned."""
+    from . import _lib
+    if t.device.type != "cuda" or not t.is_contiguous():
+        raise InputError("checksum: needs a contiguous CUDA tensor")
+    out = torch.zeros(1, dtype=torch.int32, device=t.device)
+    _lib.call("ps_checksum", stream(), t.data_ptr(), t.numel() * t.element_size(), out.data_ptr())
+    return int(out.item()) & 0xFFFFFFFF

@@ -90,6 +90,7 @@ _SIGS = {
     "ps_prompt_bias": ([p, p, p, p, C.c_int, C.c_int, C.c_int, p], C.c_int),
     "ps_blend": ([p, p, p, p, p, C.c_int, C.c_int, C.c_int, p], C.c_int),
     "ps_convert": ([p, p, C.c_int, p, C.c_int, i64], C.c_int),
+    "ps_checksum": ([p, p, i64, p], C.c_int),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -410,6 +410,7 @@ __global__ void __launch_bounds__(MseRing<T>::THREADS + 32, 2) mse_ring_kernel(
   __shared__ __align__(8) uint64_t full[MSE_MAX_STAGES], empty[MSE_MAX_STAGES];
   __shared__ int dead[MSE_MAX_STAGES];
   pdl_wait();
+  pdl_trigger();  // mse_root_kernel's CTAs become resident now and read their entries early
   const int n_items = P * CP;
   if ((int)blockIdx.x >= n_items) return;
   const int stride = L + I;
@@ -517,9 +518,12 @@ __global__ void __launch_bounds__(32) mse_root_kernel(const int32_t* __restrict_
                                                       double* __restrict__ scratch, uint8_t* __restrict__ mask,
                                                       int64_t* __restrict__ counters) {
   extern __shared__ double rr[];
-  pdl_wait();
   const int p = blockIdx.x;
-  if (!entry_live(slots[p], exists, streak, max_streak)) {
+  // the entry state was written before mse_ring_kernel started (which triggers this launch
+  // after its own pdl_wait), so it is read ahead of the wait for the chunk roots
+  const bool live = entry_live(slots[p], exists, streak, max_streak);
+  pdl_wait();
+  if (!live) {
     if (threadIdx.x == 0) {
       mask[p] = 0;
       if (counters) atomicAdd(reinterpret_cast<unsigned long long*>(counters + 1), 1ull);
@@ -806,6 +810,39 @@ __global__ void __launch_bounds__(1024) compact_lists_kernel(
   }
 }
 
+
+// XOR fold of a buffer's 32-byte words into one u32 (order-independent, so any streaming order
+// gives the same value): an integrity check for resident latents / snapshots after a copy, and the
+// pure-read ceiling the read-only patch kernels are measured against (bench.py hbm_kernels: a
+// streaming read of the same bytes, nothing but the loads -- tools/micro/read_bw.cu swept 14
+// read-kernel shapes; this is the fastest of them at 76 / 152 MB: LDG.256, two per thread in
+// flight, 8 CTAs of 256 threads per SM).
+__global__ void __launch_bounds__(256) checksum_kernel(const uint8_t* __restrict__ p, int64_t nv,
+                                                      uint32_t* __restrict__ out) {
+  pdl_wait();
+  uint32_t acc = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k0 < nv; k0 += 2 * stride) {
+    uint32_t r[2][8];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int64_t k = k0 + i * stride;
+      if (k < nv) {
+        ld_global_nc_v8(p + k * 32, r[i]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) r[i][e] = 0;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc ^= r[i][e];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc != 0) atomicXor(out, acc);
+}
 }  // namespace ps
 
 extern "C" {
@@ -831,8 +868,6 @@ int ps_cache_predict(void* stream, const void* x, int dtype, int P, int64_t n, c
   cudaStream_t st = (cudaStream_t)stream;
   const int stride = n_leaves + n_internal;
   int* tickets = reinterpret_cast<int*>(scratch + (int64_t)P * stride);
-  if (cudaMemsetAsync(tickets, 0, (size_t)P * sizeof(int), st) != cudaSuccess)
-    return check_launch("cache_predict tickets");
   auto run = [&](auto tag) -> int {
     using T = decltype(tag);
     constexpr int LPC = MseCfg<T>::LPC;
@@ -885,6 +920,9 @@ int ps_cache_predict(void* stream, const void* x, int dtype, int P, int64_t n, c
       }
     }
     if (smem > 200 * 1024) return set_error(PS_ERR_INPUT, "cache_predict: leaf span too large");
+    // per-patch tickets of the one-kernel form only (the ring path above has no cross-CTA tickets)
+    if (cudaMemsetAsync(tickets, 0, (size_t)P * sizeof(int), st) != cudaSuccess)
+      return check_launch("cache_predict tickets");
     launch_pdl(mse_fused_kernel<T>, dim3((n_leaves + LPC - 1) / LPC, P), dim3(LPC), (size_t)smem, st,
                (const T*)x, n, slots, (const T*)snap_in, exists, streak, max_streak, sigma, leaves, n_leaves, nodes,
                n_internal, level_off, n_levels, scratch, tickets, mask, counters, tree_smem, perfect);
@@ -974,6 +1012,19 @@ int ps_select_patches(void* stream, const uint8_t* mask, int P, int64_t n, int d
   PatchOpArgs a{};
   a.mask = mask; a.x = (const char*)a_; a.y = (char*)b_; a.o1 = (char*)out;
   return launch_op<OP_SELECT>((cudaStream_t)stream, P, n, dtype, a, "select_patches");
+}
+
+int ps_checksum(void* stream, const void* data, int64_t bytes, uint32_t* out) {
+  if (bytes < 0 || bytes % 32 != 0 || ((uintptr_t)data & 31) != 0 || out == nullptr)
+    return set_error(PS_ERR_INPUT, "checksum: needs 32-byte aligned data, a multiple of 32 bytes and an output word");
+  if (bytes == 0) return PS_OK;
+  const int64_t nv = bytes / 32;
+  int64_t grid = 8 * (int64_t)ring_num_sms();
+  const int64_t need = (nv + 511) / 512;  // two 32-byte loads per thread
+  if (need < grid) grid = need;
+  launch_pdl(checksum_kernel, dim3((unsigned)grid), dim3(256), 0, (cudaStream_t)stream, (const uint8_t*)data, nv, out);
+  count_launch();
+  return check_launch("checksum");
 }
 
 }  // extern "C"

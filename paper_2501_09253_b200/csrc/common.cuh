@@ -309,6 +309,9 @@ PS_DEV int atom_add_acq_rel_gpu(int* p, int v) {
 }
 PS_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 PS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// let the next PDL launch in the stream start its CTAs now (they still block in pdl_wait until
+// this grid has completed and flushed)
+PS_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 PS_DEV void reg_fence32(uint32_t (&r)[32]) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) asm volatile("" : "+r"(r[i]));

@@ -401,3 +401,19 @@ def test_persistent_attention_two_graphs_replayed_concurrently():
         torch.cuda.synchronize()
         assert torch.equal(o1, want1)
         assert torch.equal(o2, want2)
+
+
+@pytest.mark.parametrize("nbytes", [32, 1024, 32 * 777, 76021760])
+def test_checksum_xor_fold_bit_exact(nbytes):
+    """ps_checksum = XOR of every u32 word of the buffer (the 32-byte-word fold is order-free)."""
+    from paper_2501_09253_b200._dev import checksum
+    from paper_2501_09253_b200.errors import InputError
+    g = torch.Generator(device="cuda").manual_seed(nbytes)
+    t = torch.randint(-2 ** 31, 2 ** 31 - 1, (nbytes // 4,), dtype=torch.int32, device="cuda", generator=g)
+    want = int(np.bitwise_xor.reduce(t.cpu().numpy().view(np.uint32)))
+    assert checksum(t) == want
+    t[nbytes // 8] ^= 1 << 7  # one flipped bit changes it
+    assert checksum(t) == want ^ (1 << 7)
+    if nbytes >= 64:
+        with pytest.raises(InputError):
+            checksum(t[1:])  # 4 bytes off the 32-byte alignment

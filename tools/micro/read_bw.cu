@@ -147,10 +147,16 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
+  uint8_t* flush2;
+  CK(cudaMalloc(&flush2, 256ll << 20));
+  CK(cudaMemset(flush2, 0, 256ll << 20));
+  bool clean = false;
   auto timeit = [&](auto&& launch, int reps) {
     std::vector<float> t;
     for (int r = 0; r < reps; ++r) {
-      cudaMemsetAsync(flush, r, 256ll << 20);
+      cudaMemsetAsync(flush, r, 256ll << 20);  // L2 full of dirty lines ...
+      if (clean)  // ... written back by a 256 MB read of another buffer: L2 holds clean lines only
+        rd128<4><<<sms * 8, 256>>>((const uint4*)flush2, (256ll << 20) / 16, out);
       cudaEventRecord(e0);
       launch();
       cudaEventRecord(e1);
@@ -163,10 +169,12 @@ int main() {
     return t[t.size() / 2] * 1e3f;  // median us
   };
   const int64_t sizes[3] = {76021760ll, 152043520ll, 1ll << 30};
+  for (int mode = 0; mode < 2; ++mode)
   for (int64_t bytes : sizes) {
+    clean = mode == 1;
     auto rep = [&](const char* name, float us, double traffic) {
-      printf("{\"bytes\": %lld, \"variant\": \"%s\", \"us\": %.2f, \"gbs\": %.1f}\n", (long long)bytes, name, us,
-             traffic / us / 1e3);
+      printf("{\"flush\": \"%s\", \"bytes\": %lld, \"variant\": \"%s\", \"us\": %.2f, \"gbs\": %.1f}\n",
+             clean ? "clean" : "dirty", (long long)bytes, name, us, traffic / us / 1e3);
     };
     const int64_t nv16 = bytes / 16, nv32 = bytes / 32;
     for (int per_sm : {4, 8}) {
