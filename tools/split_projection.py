@@ -7,6 +7,7 @@ collectives replaced by no-ops (NullComm); its device time is measured with CUDA
 events.  The projected W-GPU step = max over ranks of (device time + bytes the
 rank exchanges / NVLink bandwidth), with the exchange NOT overlapped (upper bound).
 Bandwidth: 770 GB/s per direction (measured peer copy, B200_PROFILING.md).
+SPLIT_WORLDS=8 SPLIT_RANKS=0 SPLIT_GRAPH=0 times one rank of one world (for an ncu launch list).
 """
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -82,10 +83,14 @@ def main():
     cfg = ps.ModelConfig(arch="unet_like", channels=C, hidden=H, groups=G, n_blocks=NB, seed=0)
     w = ps.init_weights(cfg)
     out = []
-    for world in (1, 2, 4, 8):
+    worlds = [int(x) for x in os.environ.get("SPLIT_WORLDS", "1,2,4,8").split(",")]
+    only = os.environ.get("SPLIT_RANKS")  # e.g. "0": time only these ranks (ncu launch lists)
+    for world in worlds:
         plan = SplitPlan(REQS, PS, world, mode=MODE)
         ranks = []
         for r in range(world):
+            if only is not None and str(r) not in only.split(","):
+                continue
             ms, sent, owned = time_rank(cfg, w, plan, r)
             comm_ms = sent * (world - 1) / (NVLINK_GBS * 1e9) * 1e3 if world > 1 else 0.0
             ranks.append({"rank": r, "owned_patches": owned, "device_ms": ms, "sent_MB": sent / 1e6,
@@ -96,6 +101,8 @@ def main():
                 "step_ms_projected": step, "patches_per_s": 24 / (step * 1e-3), "ranks": ranks}
         out.append(line)
         print(json.dumps(line), flush=True)
+    if only is not None or worlds[0] != 1:
+        return
     base = out[0]["patches_per_s"]
     for l in out:
         print(f"W={l['world']}: {l['step_ms_projected']:.2f} ms/step projected, {l['patches_per_s']:.0f} patches/s, "
