@@ -128,6 +128,10 @@ int ps_halo_strips(void* stream, void* x, int C, int ps, int n, const int32_t* d
  * attention K rows / V^T columns (patched.py:164-176) into NCCL buffers and back. */
 int ps_copy_segments(void* stream, const void* src, void* dst, int n, const int64_t* src_off, const int64_t* dst_off,
                      int64_t seg_bytes);
+/* As ps_copy_segments with a byte count per segment (seg_bytes[i], even): the split-image K / V^T
+ * pack and unpack of every peer's token ranges in one launch.  No reference counterpart. */
+int ps_copy_segments_var(void* stream, const void* src, void* dst, int n, const int64_t* src_off,
+                         const int64_t* dst_off, const int64_t* seg_bytes);
 
 /* Dense contraction on tcgen05: D[M,N] = A[M,K] B[N,K]^T (+bias), bf16 in, fp32 accumulate.
  * a: CL tokens [M, lda] (a_mode 0), CL frames (a_mode 1: implicit conv3, K = 9*Cp,
@@ -192,6 +196,15 @@ int ps_attention_splitkv(void* stream, const void* qk, const void* vt, int ldv, 
                          const int32_t* img_tok0, const int32_t* tile_q0, const int32_t* tile_img,
                          const int32_t* tile_kb0, const int32_t* tile_nkb, const int32_t* tile_slot, int n_tiles,
                          float* part_o, float* part_ml, void* out);
+/* Split-KV on CTA pairs (the persistent pair kernel): pair tile t = 256 queries from pair_q0[t]
+ * of image pair_img[t] over key blocks [kb0[t], kb0[t] + nkb[t]) of 128 keys.  slot0[t] >= 0:
+ * the tile's two 128-row halves leave as fp32 partials (O unnormalised [slot][128][Dp], (m, l)
+ * [slot][128]) in slots slot0[t] / slot1[t] for ps_attention_combine; slot0[t] < 0: the tile
+ * covers all the image's keys and writes bf16 O to out.  Tiles are dealt in list order. */
+int ps_attention_pairs_splitkv(void* stream, const void* qk, const void* vt, int ldv, int T, int Dp, int D,
+                               const int32_t* img_tok0, const int32_t* pair_q0, const int32_t* pair_img,
+                               const int32_t* kb0, const int32_t* nkb, const int32_t* slot0, const int32_t* slot1,
+                               int n_pairs, float* part_o, float* part_ml, void* out);
 int ps_attention_combine(void* stream, const float* part_o, const float* part_ml, const int32_t* q0s,
                          const int32_t* slot0, const int32_t* nsplit, const int32_t* img_of,
                          const int32_t* img_tok0, int n, int Dp, void* out);

@@ -60,6 +60,7 @@ _SIGS = {
                           p], C.c_int),
     "ps_halo_strips": ([p, p, C.c_int, C.c_int, C.c_int, p, p, C.c_int], C.c_int),
     "ps_copy_segments": ([p, p, p, C.c_int, p, p, i64], C.c_int),
+    "ps_copy_segments_var": ([p, p, p, C.c_int, p, p, p], C.c_int),
     "ps_from_cl": ([p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, p], C.c_int),
     "ps_gemm": ([p, C.POINTER(GemmArgs)], C.c_int),
     "ps_feed_forward": ([p, p, C.c_int, C.c_int, p, p, p, p, C.c_int, C.c_int, C.c_int, p, p, p, C.c_int, p],
@@ -68,6 +69,8 @@ _SIGS = {
     "ps_attention_pairs": ([p, p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, C.c_int, p, p], C.c_int),
     "ps_attention_splitkv": ([p, p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, p, p, p, C.c_int, p, p, p],
                              C.c_int),
+    "ps_attention_pairs_splitkv": ([p, p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, p, p, p, p, C.c_int, p, p,
+                                    p], C.c_int),
     "ps_attention_combine": ([p, p, p, p, p, p, p, p, C.c_int, C.c_int, p], C.c_int),
     "ps_kv_peer_maps": ([p, C.c_int, p, p, p, p, C.c_int], C.c_int),
     "ps_attention_peer": ([p, p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, p, p, p, C.c_int, p, p, p, p, p, p],

@@ -556,6 +556,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
     kb0 = p.img_tok0[img];
     ke = p.img_tok0[img + 1];
     nkb = (ke - kb0 + A2_BN - 1) / A2_BN;
+    if (p.tile_kb0 != nullptr) {  // split-KV: key blocks [tile_kb0, +tile_nkb) of the image
+      kb0 += p.tile_kb0[t] * A2_BN;  // (ke stays the image end: interior ranges are whole blocks)
+      nkb = p.tile_nkb[t];
+    }
   };
 
   if (warp == 0 && lane == 0) {
@@ -837,6 +841,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
       const bool ok = q < k_end;
       const float inv = 1.f / l_run;
       __nv_bfloat16* dst = p.out + (size_t)q * p.Dp;
+      // split-KV: this CTA's 128 rows leave as an unnormalised fp32 partial (O, m, l) in slot
+      // tile_slot[t] (rank 0) / tile_slot1[t] (rank 1), merged by ps_attention_combine
+      const int slot = p.tile_slot != nullptr ? (rank == 0 ? p.tile_slot[t] : p.tile_slot1[t]) : -1;
+      float* po = slot >= 0 ? p.part_o + ((size_t)slot * A2_BM + row) * DP : nullptr;
+      if (slot >= 0) {
+        p.part_ml[((size_t)slot * A2_BM + row) * 2] = m_run;
+        p.part_ml[((size_t)slot * A2_BM + row) * 2 + 1] = l_run;
+      }
       constexpr int EPI_G = (DP / 32) % 5 == 0 ? 5 : (DP / 32) % 4 == 0 ? 4 : (DP / 32) % 3 == 0 ? 3 : (DP / 32) % 2 == 0 ? 2 : 1;
       uint32_t o[EPI_G][32];
 #pragma unroll 1
@@ -850,7 +862,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A2_THREADS, 1)
           tc_fence_before();
           mbar_arrive_cluster(o_empty_l);
         }
-        if (ok) {
+        if (slot >= 0) {
+#pragma unroll
+          for (int g = 0; g < EPI_G; ++g)
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+              st_global_v8(po + c0 + 32 * g + 8 * v, *reinterpret_cast<uint32_t(*)[8]>(&o[g][8 * v]));
+        } else if (ok) {
 #pragma unroll
           for (int g = 0; g < EPI_G; ++g) {
             // 32-byte stores: one full sector per lane and half the store instructions

@@ -225,9 +225,11 @@ int ps_csp_build(int n_req, const int32_t* dims, int32_t ps, int32_t* order, int
 // (sequential below 8, 8 strided accumulators otherwise); larger n splits at
 // n2 = n/2 - (n/2 % 8).  Nodes are numbered leaves first (in order), then
 // internal nodes grouped by height so a level can be evaluated in parallel.
-int ps_attention_pairs(void* stream, const void* qk, const void* vt, int ldv, int T, int Dp, int D,
-                       const int32_t* img_tok0, const int32_t* pair_q0, const int32_t* pair_img, int n_pairs,
-                       void* out, const int32_t* n_dev) {
+static int attention_pairs_impl(void* stream, const void* qk, const void* vt, int ldv, int T, int Dp, int D,
+                                const int32_t* img_tok0, const int32_t* pair_q0, const int32_t* pair_img,
+                                int n_pairs, void* out, const int32_t* n_dev, const int32_t* kb0,
+                                const int32_t* nkb, const int32_t* slot0, const int32_t* slot1, float* part_o,
+                                float* part_ml) {
   if (Dp % 64 || Dp < 64 || Dp > 320) return set_error(PS_ERR_INPUT, "attention: Dp %d unsupported", Dp);
   if (D < 1 || D > Dp) return set_error(PS_ERR_INPUT, "attention: bad D");
   if (n_pairs < 1) return PS_OK;
@@ -251,7 +253,35 @@ int ps_attention_pairs(void* stream, const void* qk, const void* vt, int ldv, in
   p.out = (__nv_bfloat16*)out;
   p.dbg = g_attn_dbg;
   p.trace = g_attn_trace;
+  p.tile_kb0 = kb0;
+  p.tile_nkb = nkb;
+  p.tile_slot = slot0;
+  p.tile_slot1 = slot1;
+  p.part_o = part_o;
+  p.part_ml = part_ml;
   return attention2_launch(tq, tk, tv, to, p, Dp, (cudaStream_t)stream);
+}
+
+int ps_attention_pairs(void* stream, const void* qk, const void* vt, int ldv, int T, int Dp, int D,
+                       const int32_t* img_tok0, const int32_t* pair_q0, const int32_t* pair_img, int n_pairs,
+                       void* out, const int32_t* n_dev) {
+  return attention_pairs_impl(stream, qk, vt, ldv, T, Dp, D, img_tok0, pair_q0, pair_img, n_pairs, out, n_dev,
+                              nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+}
+
+// Split-KV on CTA pairs: pair tile t (256 queries from pair_q0[t]) covers key blocks
+// [kb0[t], kb0[t] + nkb[t]) of its image; with slot0[t] >= 0 the first / second 128 rows
+// leave as fp32 partials in slots slot0[t] / slot1[t] (ps_attention_combine merges them),
+// with slot0[t] < 0 the tile covers all its keys and writes bf16 O directly.
+int ps_attention_pairs_splitkv(void* stream, const void* qk, const void* vt, int ldv, int T, int Dp, int D,
+                               const int32_t* img_tok0, const int32_t* pair_q0, const int32_t* pair_img,
+                               const int32_t* kb0, const int32_t* nkb, const int32_t* slot0, const int32_t* slot1,
+                               int n_pairs, float* part_o, float* part_ml, void* out) {
+  if (!kb0 || !nkb || !slot0 || !slot1) return set_error(PS_ERR_INPUT, "attention_pairs_splitkv: null tile arrays");
+  static const bool persist = !getenv("PS_ATTN_PERSIST") || atoi(getenv("PS_ATTN_PERSIST")) != 0;
+  if (!persist) return set_error(PS_ERR_INPUT, "attention_pairs_splitkv: needs the persistent pair kernel");
+  return attention_pairs_impl(stream, qk, vt, ldv, T, Dp, D, img_tok0, pair_q0, pair_img, n_pairs, out, nullptr,
+                              kb0, nkb, slot0, slot1, part_o, part_ml);
 }
 
 // Profiling only: device counters [8] that later attention launches accumulate

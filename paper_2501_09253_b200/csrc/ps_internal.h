@@ -115,6 +115,7 @@ struct AttnParams {
   const int* n_dev;      // optional DEVICE tile count (n_tiles is then an upper bound)
   int epi_tma;           // pair kernel: O tiles staged in smem and TMA-stored (else row stores)
   int* tile_ctr;         // persistent pair kernel: [next tile, clusters done], zero between launches
+  const int* tile_slot1; // split-KV pair tiles: partial slot of the second CTA's 128 rows
 };
 int attention_launch(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& vt, const AttnParams& p,
                      int dp, cudaStream_t st);

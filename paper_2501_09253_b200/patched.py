@@ -166,6 +166,19 @@ class Ctx:
             _SKV_CACHE[key] = splitkv_plan(q0_host, img_host, tok0, sm_count(), self.device)
         return _SKV_CACHE[key]
 
+    def _splitkv_pairs(self, q0_host, img_host, min_base: int = 0):
+        """Pair split-KV plan over the 256-query pair tiles of these 128-query tiles (every
+        other one: a patch's 128-query tiles are consecutive and hw % 256 == 0)."""
+        tok0 = self.b.request_offset * self.hw
+        pq0, pimg = np.asarray(q0_host)[0::2], np.asarray(img_host)[0::2]
+        key = ("pairs", pq0.tobytes(), pimg.tobytes(), np.asarray(tok0).tobytes(), sm_count(), SPLITKV_MIN_BLOCKS,
+               min_base, str(self.device))
+        if key not in _SKV_CACHE:
+            if len(_SKV_CACHE) > 64:
+                _SKV_CACHE.clear()
+            _SKV_CACHE[key] = splitkv_plan_pairs(pq0, pimg, tok0, sm_count(), self.device, min_base)
+        return _SKV_CACHE[key]
+
     def empty_cl(self, cp: int) -> torch.Tensor:
         return torch.empty((self.T, cp), dtype=BF16, device=self.device)
 
@@ -368,8 +381,28 @@ class Ctx:
         # split-KV on the split-image path (few long query tiles per GPU); single-GPU batches keep
         # the one-pass kernels so compacted and full runs stay bit-identical
         use_skv = SPLITKV and (self.owned is not None or SPLITKV_ALL)
-        skv = None if host is None or not use_skv else self._splitkv(*host)
-        if finish is not None:
+        skv = pskv = None
+        if host is not None and host[0] is None:
+            host = None  # device-decided tile lists (no host copy): one-pass kernels
+        if host is not None and SPLITKV and pairs and SPLITKV_PAIRS and not peer and finish is None:
+            # single-GPU batches: only long attentions (SPLITKV_SINGLE_MIN_BLOCKS)
+            min_base = 0 if use_skv else SPLITKV_SINGLE_MIN_BLOCKS
+            pskv = self._splitkv_pairs(host[0], host[1], min_base=min_base)
+        elif host is not None and use_skv:
+            skv = self._splitkv(host[0], host[1])
+        if pskv is not None:
+            # few long pair tiles for the SM pairs: keys split over several pairs, partials merged
+            kb0, nkb, s0, s1, n_rows, cq0, cslot0, cns, cimg, n_q, pq0, pimg, n_slots = pskv
+            part_o = torch.empty((n_slots, 128, dpp), dtype=torch.float32, device=self.device)
+            part_ml = torch.empty((n_slots, 128, 2), dtype=torch.float32, device=self.device)
+            _lib.call("ps_attention_pairs_splitkv", stream(), qk.data_ptr(), vt.data_ptr(), ldv, self.T, dpp, d,
+                      self.dev["img_tok0"].data_ptr(), pq0.data_ptr(), pimg.data_ptr(), kb0.data_ptr(),
+                      nkb.data_ptr(), s0.data_ptr(), s1.data_ptr(), n_rows, part_o.data_ptr(), part_ml.data_ptr(),
+                      o.data_ptr())
+            _lib.call("ps_attention_combine", stream(), part_o.data_ptr(), part_ml.data_ptr(), cq0.data_ptr(),
+                      cslot0.data_ptr(), cns.data_ptr(), cimg.data_ptr(), self.dev["img_tok0"].data_ptr(), n_q, dpp,
+                      o.data_ptr())
+        elif finish is not None:
             self._attention_overlapped(qk, vt, ldv, dpp, d, host, finish, o)
         elif peer and skv is None:
             # one-pass kernel over 128-query tiles, remote key blocks read from their owners
@@ -618,6 +651,15 @@ SPLITKV_ALL = os.environ.get("PS_SPLITKV_ALL", "0") == "1"  # also outside the s
 OVERLAP_KV = os.environ.get("PS_OVERLAP_KV", "0") == "1"
 _SKV_CACHE: dict = {}
 SPLITKV_MIN_BLOCKS = 8  # key blocks (of 128) per split
+# split-KV on the persistent CTA-pair kernel when the query tiles pair up (PS_SPLITKV_PAIRS=0: the
+# single-CTA split-KV kernel)
+SPLITKV_PAIRS = os.environ.get("PS_SPLITKV_PAIRS", "1") != "0"
+# single-GPU batches (no split images) use the pair split-KV only when the longest-first makespan
+# of the unsplit pair tiles is at least this many key blocks: long attentions (config 5's 2048 px
+# image: 4 waves of 512-block tiles, 29.8 -> ~27.5 ms/step) gain more from a balanced last wave
+# than the partials cost; short ones (config 2, every test shape) keep the one-pass kernel, so
+# their compacted and full runs stay bit-identical
+SPLITKV_SINGLE_MIN_BLOCKS = int(os.environ.get("PS_SPLITKV_SINGLE_MIN_BLOCKS", "1536"))
 
 
 def _lpt_makespan(pieces, sms: int) -> int:
@@ -680,6 +722,65 @@ def splitkv_plan(q0_host, img_host, img_tok0_host, sms: int, device):
     cols = list(zip(*rows))
     return (t(cols[2]), t(cols[3]), t(cols[4]), len(rows), t(cq0), t(cs0), t(cns), t(cimg), len(cq0),
             t(cols[0]), t(cols[1]))
+
+
+def splitkv_plan_pairs(q0_host, img_host, img_tok0_host, sms: int, device, min_base: int = 0):
+    """splitkv_plan for the persistent CTA-pair kernel (ps_attention_pairs_splitkv): units are
+    256-query pair tiles (q0_host / img_host) on sms // 2 SM pairs.  A pair tile whose keys are
+    not split writes bf16 O directly (slots -1); a split one writes its two 128-row halves to
+    slots [base, base + ns) and [base + ns, base + 2 ns), merged by ps_attention_combine over
+    128-query tiles.  Returns None when no split helps; else device arrays (kb0, nkb, slot0,
+    slot1 per pair tile, longest first), the number of pair tiles, the combine lists (q0, first
+    slot, splits, image per 128-query tile), their count, the pair tiles' (q0, image), and the
+    number of partial slots."""
+    n = len(q0_host)
+    if n == 0:
+        return None
+    pairs = max(1, sms // 2)
+    nkb_img = [(int(img_tok0_host[i + 1] - img_tok0_host[i]) + 127) // 128 for i in range(len(img_tok0_host) - 1)]
+    units = [nkb_img[int(i)] for i in img_host]
+    base = _lpt_makespan(units, pairs)
+    if base < min_base:
+        return None
+    best, best_cost = None, base
+    for k in range(2, 17):
+        target = max(SPLITKV_MIN_BLOCKS, -(-max(units) // k))
+        pieces, n_part = [], 0
+        for nb in units:
+            ns = -(-nb // target) if nb > target else 1
+            q, r = divmod(nb, ns)
+            pieces.extend([q + 1] * r + [q] * (ns - r))
+            n_part += ns if ns > 1 else 0
+        # a pair partial: two fp32 halves written + read by the combine ~ 4 key blocks of pair time
+        cost = _lpt_makespan(pieces, pairs) + 4.0 * n_part / pairs
+        if cost < 0.97 * best_cost:
+            best, best_cost = target, cost
+    if best is None:
+        return None
+    rows = []  # (q0, img, kb0, nkb, slot0, slot1)
+    cq0, cs0, cns, cimg = [], [], [], []
+    slot = 0
+    for q0, img, nb in zip(q0_host, img_host, units):
+        ns = -(-nb // best) if nb > best else 1
+        if ns == 1:
+            rows.append((int(q0), int(img), 0, nb, -1, -1))
+            continue
+        q, r = divmod(nb, ns)
+        for h in range(2):
+            cq0.append(int(q0) + 128 * h); cs0.append(slot + h * ns); cns.append(ns); cimg.append(int(img))
+        k = 0
+        for s_ in range(ns):
+            m = q + (1 if s_ < r else 0)
+            rows.append((int(q0), int(img), k, m, slot + s_, slot + ns + s_))
+            k += m
+        slot += 2 * ns
+    if not cq0:
+        return None
+    rows.sort(key=lambda r_: -r_[3])  # longest ranges first
+    t = lambda v: torch.as_tensor(np.asarray(v, dtype=np.int32), device=device)
+    cols = list(zip(*rows))
+    return (t(cols[2]), t(cols[3]), t(cols[4]), t(cols[5]), len(rows), t(cq0), t(cs0), t(cns), t(cimg), len(cq0),
+            t(cols[0]), t(cols[1]), slot)
 
 
 def overlap_plan(q0_host, img_host, req_off, hw: int, owned, sms: int, device):

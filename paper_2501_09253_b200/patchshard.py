@@ -356,8 +356,11 @@ def kv_plan(sh: LocalShard, dpp: int, ldv: int) -> dict:
             ku_dst.extend((t0 + i) * qk_row + kb for i in range(ntok))
             vu_jobs.append(([base + vpos + d * ntok * 2 for d in range(dpp)],
                             [d * ldv * 2 + t0 * 2 for d in range(dpp)], ntok * 2))
+    def merged(jobs):  # one variable-length segment list per direction (ps_copy_segments_var)
+        return ([o for js, _, _ in jobs for o in js], [o for _, jd, _ in jobs for o in jd],
+                [nb for js, _, nb in jobs for _ in js])
     return dict(k_pack=(k_src, k_dst, kb), v_pack=v_jobs, k_unpack=(ku_src, ku_dst, kb), v_unpack=vu_jobs,
-                buf_bytes=maxb)
+                v_pack_var=merged(v_jobs), v_unpack_var=merged(vu_jobs), buf_bytes=maxb)
 
 
 class VirtualGroup:
@@ -521,6 +524,18 @@ class ShardExchange:
         _lib.call("ps_copy_segments", stream(), src.data_ptr(), dst.data_ptr(), n, so.data_ptr(), do.data_ptr(),
                   int(seg_bytes))
 
+    def _copy_var(self, src, dst, key, segs):
+        from . import _lib
+        from ._dev import stream
+        src_off, dst_off, nbytes = segs
+        if not src_off:
+            return
+        so = self._dev_i64(key + ("s",), src_off)
+        do = self._dev_i64(key + ("d",), dst_off)
+        nb = self._dev_i64(key + ("n",), nbytes)
+        _lib.call("ps_copy_segments_var", stream(), src.data_ptr(), dst.data_ptr(), len(src_off), so.data_ptr(),
+                  do.data_ptr(), nb.data_ptr())
+
     # 1. GroupNorm partials ----------------------------------------------
     def gn(self, partials, G: int) -> None:
         import torch
@@ -581,8 +596,7 @@ class ShardExchange:
         send = torch.empty(pl["buf_bytes"], dtype=torch.uint8, device=qk.device)
         ks, kd, kb = pl["k_pack"]
         self._copy(qk, send, key + ("kp",), ks, kd, kb)
-        for i, (vs, vd, nb) in enumerate(pl["v_pack"]):
-            self._copy(vt, send, key + ("vp", i), vs, vd, nb)
+        self._copy_var(vt, send, key + ("vp",), pl["v_pack_var"])
         self.bytes_moved += send.numel()
         if hasattr(self.comm, "all_gather_async"):
             got, wait = self.comm.all_gather_async(self.rank, send)
@@ -593,8 +607,7 @@ class ShardExchange:
             wait()
             ks_, kd_, kb_ = pl["k_unpack"]
             self._copy(got, qk, key + ("ku",), ks_, kd_, kb_)
-            for i, (vs_, vd_, nb_) in enumerate(pl["v_unpack"]):
-                self._copy(got, vt, key + ("vu", i), vs_, vd_, nb_)
+            self._copy_var(got, vt, key + ("vu",), pl["v_unpack_var"])
         return finish
 
     def kv(self, qk, vt, ldv: int, dpp: int) -> None:
@@ -609,13 +622,11 @@ class ShardExchange:
         send = torch.empty(pl["buf_bytes"], dtype=torch.uint8, device=qk.device)
         ks, kd, kb = pl["k_pack"]
         self._copy(qk, send, key + ("kp",), ks, kd, kb)
-        for i, (vs, vd, nb) in enumerate(pl["v_pack"]):
-            self._copy(vt, send, key + ("vp", i), vs, vd, nb)
+        self._copy_var(vt, send, key + ("vp",), pl["v_pack_var"])
         got = self.comm.all_gather(self.rank, send)
         ks, kd, kb = pl["k_unpack"]
         self._copy(got, qk, key + ("ku",), ks, kd, kb)
-        for i, (vs, vd, nb) in enumerate(pl["v_unpack"]):
-            self._copy(got, vt, key + ("vu", i), vs, vd, nb)
+        self._copy_var(got, vt, key + ("vu",), pl["v_unpack_var"])
         self.bytes_moved += send.numel()
 
     # 3'. attention K / V read in place from the owners (peer_kv) ----------

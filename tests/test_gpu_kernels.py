@@ -203,10 +203,13 @@ def test_frames_cl_register_transpose_matches_smem_kernel(C, ps, mode, monkeypat
         assert torch.equal(inner, x)
 
 
+@pytest.mark.parametrize("pairs_kv", [True, False])
 @pytest.mark.parametrize("world", [4, 8])
-def test_splitkv_attention_matches_single_pass(world, monkeypatch):
+def test_splitkv_attention_matches_single_pass(world, pairs_kv, monkeypatch):
     """Split-KV attention (few query tiles: a rank of a split 2048 px image) against the
-    one-pass kernel on the same QKV: the merged partials agree to bf16 rounding."""
+    one-pass kernel on the same QKV: the merged partials agree to bf16 rounding.  pairs_kv:
+    the persistent CTA-pair kernel's split-KV (ps_attention_pairs_splitkv, the default for
+    pair-able tiles) or the single-CTA one."""
     import paper_2501_09253_b200 as ps_
     from paper_2501_09253_b200 import patched
     from paper_2501_09253_b200.patchshard import SplitPlan
@@ -228,11 +231,17 @@ def test_splitkv_attention_matches_single_pass(world, monkeypatch):
     patched._SKV_CACHE.clear()
     monkeypatch.setattr(patched, "SPLITKV_MIN_BLOCKS", 1)
     monkeypatch.setattr(patched, "sm_count", lambda: 1000)   # more SMs than tiles: forces splits
+    monkeypatch.setattr(patched, "SPLITKV_PAIRS", pairs_kv)
     b._dev.clear()
     ctx2 = patched.Ctx(b)
     ctx2.attn_tiles = patched._attn_tiles(ctx2, owned)
-    plan = ctx2._splitkv(*ctx2.attn_tiles[4:])
-    assert plan is not None and plan[3] > plan[8], "expected split tiles"
+    if pairs_kv:
+        assert ctx2.attn_tiles[3], "patch 32: pair tiles"
+        plan = ctx2._splitkv_pairs(*ctx2.attn_tiles[4:])
+        assert plan is not None and plan[9] > 0 and plan[4] > plan[9] // 2, "expected split pair tiles"
+    else:
+        plan = ctx2._splitkv(*ctx2.attn_tiles[4:])
+        assert plan is not None and plan[3] > plan[8], "expected split tiles"
     got = ctx2.as_nchw(ctx2.attention(patched.Act("nchw", x, 64), at, None)).float()
     torch.cuda.synchronize()
     d = (got[owned] - ref[owned]).abs().max().item()

@@ -224,16 +224,18 @@ def test_kv_exchange_simulated(case):
         send = np.zeros(pl["buf_bytes"], np.uint8)
         ks, kd, kb = pl["k_pack"]
         _copy_segments(qk.view(np.uint8).reshape(-1), send, ks, kd, kb)
-        for vs, vd, nb in pl["v_pack"]:
-            _copy_segments(vt.view(np.uint8).reshape(-1), send, vs, vd, nb)
+        vs, vd, vn = pl["v_pack_var"]  # the merged variable-length list the GPU path launches
+        for a, b_, n in zip(vs, vd, vn):
+            _copy_segments(vt.view(np.uint8).reshape(-1), send, [a], [b_], n)
         st.append((sh, qk, vt, pl, send))
     got = np.stack([s[4] for s in st]).reshape(-1)
     split = set(plan.split_requests())
     for sh, qk, vt, pl, _ in st:
         ks, kd, kb = pl["k_unpack"]
         _copy_segments(got, qk.view(np.uint8).reshape(-1), ks, kd, kb)
-        for vs, vd, nb in pl["v_unpack"]:
-            _copy_segments(got, vt.view(np.uint8).reshape(-1), vs, vd, nb)
+        vs, vd, vn = pl["v_unpack_var"]
+        for a, b_, n in zip(vs, vd, vn):
+            _copy_segments(got, vt.view(np.uint8).reshape(-1), [a], [b_], n)
         for k in sh.slots:
             if k not in split:
                 continue
@@ -283,3 +285,54 @@ def test_dist_comm_gloo_ws2():
         g, x = res[r]
         assert g == [[0.0] * 3, [1.0] * 3]
         assert x == [10.0 * ((r - 1) % 2) + i for i in range(4)]
+
+
+@pytest.mark.parametrize("sms,min_base", [(148, 0), (600, 0), (148, 10 ** 6)])
+def test_splitkv_plan_pairs_layout(sms, min_base):
+    """Pair split-KV plan (ps_attention_pairs_splitkv + ps_attention_combine): every pair tile's
+    key blocks are covered exactly once by its pieces; a split tile's two 128-row halves own
+    contiguous slot ranges [s0, s0 + ns) / [s0 + ns, s0 + 2 ns) listed in the combine tables;
+    unsplit tiles write directly (slots -1); pieces are dealt longest first; a makespan under
+    min_base gives no plan."""
+    from paper_2501_09253_b200.patched import splitkv_plan_pairs
+    hw = 64 * 64
+    sizes = [16, 1, 1, 1, 1, 1, 1, 1, 1]  # config 5: one 2048 px image (16 patches) + 8x 512 px
+    tok0 = np.concatenate([[0], np.cumsum(sizes)]) * hw
+    pq0, pimg = [], []
+    for r, n in enumerate(sizes):
+        for q in range(int(tok0[r]), int(tok0[r + 1]), 256):
+            pq0.append(q)
+            pimg.append(r)
+    plan = splitkv_plan_pairs(np.asarray(pq0), np.asarray(pimg), tok0, sms, "cpu", min_base)
+    if min_base:
+        assert plan is None
+        return
+    assert plan is not None
+    kb0, nkb, s0, s1, n_rows, cq0, cs0, cns, cimg, n_q, rq0, rimg, n_slots = plan
+    kb0, nkb, s0, s1 = (t.numpy() for t in (kb0, nkb, s0, s1))
+    rq0, rimg = rq0.numpy(), rimg.numpy()
+    assert len(kb0) == n_rows and list(nkb) == sorted(nkb, reverse=True)
+    cover = {}
+    for q, img, k0, n, a, b in zip(rq0, rimg, kb0, nkb, s0, s1):
+        cover.setdefault(int(q), []).append((int(k0), int(n), int(a), int(b), int(img)))
+    comb = {int(q): (int(s), int(n)) for q, s, n in zip(cq0.numpy(), cs0.numpy(), cns.numpy())}
+    assert len(comb) == n_q
+    used = []
+    for q, img in zip(pq0, pimg):
+        pieces = sorted(cover[q])
+        total = (int(tok0[img + 1] - tok0[img]) + 127) // 128
+        pos = 0
+        for k0, n, a, b, im in pieces:
+            assert k0 == pos and im == img
+            pos += n
+        assert pos == total
+        if len(pieces) == 1:
+            assert pieces[0][2] == pieces[0][3] == -1 and q not in comb
+            continue
+        ns = len(pieces)
+        base, n0 = comb[q]
+        assert n0 == ns and comb[q + 128] == (base + ns, ns)
+        assert sorted(p[2] for p in pieces) == list(range(base, base + ns))
+        assert sorted(p[3] for p in pieces) == list(range(base + ns, base + 2 * ns))
+        used += list(range(base, base + 2 * ns))
+    assert sorted(used) == list(range(n_slots))
