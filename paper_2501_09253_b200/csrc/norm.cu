@@ -231,7 +231,14 @@ static void launch_gn_partials(cudaStream_t st, const void* x, int P, int C, int
 #define PS_GNW(W, PT, U)                                                                                      \
   launch_pdl(gn_partials_warp_kernel<W, PT, U>, dim3((items + W / PT - 1) / (W / PT)), dim3(W * 32), 0, st, xb, C, \
              hw, G, plist, n_dev, n, partials)
-    PS_GNW(2, 1, 4);
+    // ps = 64 slices (C/G * 4096 bf16 = 80 KB at C = 320): four warps per slice, their shifted
+    // sums added in a fixed order -- a warp streaming 80 KB alone is 20 dependent round trips, and
+    // a rank of a split image has only ~100 slices (config 5, 8 ranks: 19.6 us for 8 MB).  Chosen by
+    // slice size only, so a split-image rank and the single-GPU batch round identically.
+    if (slice >= 64 * 1024)
+      PS_GNW(8, 4, 4);
+    else
+      PS_GNW(2, 1, 4);
 #undef PS_GNW
     return;
   }

@@ -67,13 +67,15 @@ def test_gn_partials_warp_kernel(tmp_path):
         assert torch.equal(r["sub"][mask], r["full"][mask])
 
 
-def test_gn_partials_offset_and_outlier_shift():
+@pytest.mark.parametrize("P,ps_", [(29, 32), (6, 64)])
+def test_gn_partials_offset_and_outlier_shift(P, ps_):
     """Shifted single-pass moments stay accurate when the shift (the slice's first element) is an
     outlier and the data sit on a large offset: mean 50, std 1, first element of every slice at
-    50 + 8 (M2 is then a difference of two sums ~65x larger than itself)."""
+    50 + 8 (M2 is then a difference of two sums ~65x larger than itself).  ps = 64: 80 KB slices,
+    four warps per slice whose sums share the shift."""
     from paper_2501_09253_b200 import _lib
     from paper_2501_09253_b200._dev import stream
-    P, C, ps_, G = 29, 320, 32, 32
+    C, G = 320, 32
     g = torch.Generator(device="cuda").manual_seed(11)
     x = (50.0 + torch.randn((P, C, ps_, ps_), device="cuda", generator=g))
     xv = x.view(P, G, -1)
