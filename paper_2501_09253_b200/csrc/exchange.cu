@@ -35,17 +35,16 @@ __global__ void __launch_bounds__(256) copy_segments_kernel(const uint8_t* __res
   }
 }
 
-// Variable-length form: warp per segment (grid-stride), segment s moves seg_bytes[s] bytes.  The
+// Variable-length form: CTA per segment (grid-stride), segment s moves seg_bytes[s] bytes.  The
 // K / V^T pack and unpack of every peer's token ranges go out as one launch each instead of one
-// per (peer, token-run length).
+// per (peer, token-run length).  The segments are V^T rows (ntok x 2 bytes: 24-64 KB at config
+// 5), so a whole CTA streams each one (a warp per segment left 40 CTAs: 34 us for 21 MB).
 __global__ void __launch_bounds__(256) copy_segments_var_kernel(const uint8_t* __restrict__ src,
                                                                 uint8_t* __restrict__ dst, int n,
                                                                 const int64_t* __restrict__ src_off,
                                                                 const int64_t* __restrict__ dst_off,
                                                                 const int64_t* __restrict__ seg_bytes) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t s = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < n; s += nw) {
+  for (int64_t s = blockIdx.x; s < n; s += gridDim.x) {
     const uint8_t* a = src + __ldg(src_off + s);
     uint8_t* b = dst + __ldg(dst_off + s);
     const int64_t len = __ldg(seg_bytes + s);
@@ -53,17 +52,16 @@ __global__ void __launch_bounds__(256) copy_segments_var_kernel(const uint8_t* _
       const uint4* a4 = reinterpret_cast<const uint4*>(a);
       uint4* b4 = reinterpret_cast<uint4*>(b);
       const int64_t nv = len / 16;
-      int64_t k = lane;
-      for (; k + 96 < nv; k += 128) {  // four 16-byte loads in flight per lane
-        const uint4 r0 = __ldg(a4 + k), r1 = __ldg(a4 + k + 32), r2 = __ldg(a4 + k + 64), r3 = __ldg(a4 + k + 96);
+      const int T = blockDim.x;
+      int64_t k = threadIdx.x;
+      for (; k + T < nv; k += 2 * T) {  // two 16-byte loads in flight per thread
+        const uint4 r0 = __ldg(a4 + k), r1 = __ldg(a4 + k + T);
         b4[k] = r0;
-        b4[k + 32] = r1;
-        b4[k + 64] = r2;
-        b4[k + 96] = r3;
+        b4[k + T] = r1;
       }
-      for (; k < nv; k += 32) b4[k] = __ldg(a4 + k);
+      for (; k < nv; k += T) b4[k] = __ldg(a4 + k);
     } else {
-      for (int64_t k = lane; k < len / 2; k += 32)
+      for (int64_t k = threadIdx.x; k < len / 2; k += blockDim.x)
         reinterpret_cast<uint16_t*>(b)[k] = __ldg(reinterpret_cast<const uint16_t*>(a) + k);
     }
   }
@@ -111,8 +109,7 @@ int ps_copy_segments_var(void* stream, const void* src, void* dst, int n, const 
                          const int64_t* dst_off, const int64_t* seg_bytes) {
   if (n < 0) return set_error(PS_ERR_INPUT, "copy_segments_var: n=%d", n);
   if (n == 0) return PS_OK;
-  int64_t blocks = (n + 7) / 8;
-  if (blocks > 148 * 8) blocks = 148 * 8;
+  const int64_t blocks = n < 148 * 8 ? n : 148 * 8;
   copy_segments_var_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
       (const uint8_t*)src, (uint8_t*)dst, n, src_off, dst_off, seg_bytes);
   count_launch();
