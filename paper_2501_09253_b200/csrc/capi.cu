@@ -278,6 +278,7 @@ int ps_attention_pairs_splitkv(void* stream, const void* qk, const void* vt, int
                                const int32_t* kb0, const int32_t* nkb, const int32_t* slot0, const int32_t* slot1,
                                int n_pairs, float* part_o, float* part_ml, void* out) {
   if (!kb0 || !nkb || !slot0 || !slot1) return set_error(PS_ERR_INPUT, "attention_pairs_splitkv: null tile arrays");
+  if (!part_o || !part_ml) return set_error(PS_ERR_INPUT, "attention_pairs_splitkv: null partial buffers");
   static const bool persist = !getenv("PS_ATTN_PERSIST") || atoi(getenv("PS_ATTN_PERSIST")) != 0;
   if (!persist) return set_error(PS_ERR_INPUT, "attention_pairs_splitkv: needs the persistent pair kernel");
   return attention_pairs_impl(stream, qk, vt, ldv, T, Dp, D, img_tok0, pair_q0, pair_img, n_pairs, out, nullptr,
