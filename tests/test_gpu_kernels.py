@@ -426,3 +426,29 @@ def test_checksum_xor_fold_bit_exact(nbytes):
     if nbytes >= 64:
         with pytest.raises(InputError):
             checksum(t[1:])  # 4 bytes off the 32-byte alignment
+
+
+def test_copy_segments_var_bit_exact():
+    """ps_copy_segments_var: per-segment byte counts, 16-byte aligned segments (vector path) and
+    2-byte aligned ones (u16 path) mixed in one launch, against a host copy."""
+    rng = np.random.default_rng(5)
+    src = torch.randint(0, 255, (1 << 20,), dtype=torch.uint8, device="cuda")
+    dst = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda")
+    so, do, nb = [], [], []
+    pos = 0
+    for i in range(300):
+        n = int(rng.integers(1, 3000)) * (16 if i % 3 else 2)
+        a = int(rng.integers(0, (1 << 20) - n)) & ~(15 if i % 3 else 1)
+        so.append(a); do.append(pos); nb.append(n)
+        pos += n + (16 if i % 2 else 2)
+        if pos >= (1 << 20) - 50000:
+            break
+    so_d, do_d, nb_d = (torch.as_tensor(np.asarray(v, np.int64), device="cuda") for v in (so, do, nb))
+    _lib.check(_lib.load().ps_copy_segments_var(stream(), src.data_ptr(), dst.data_ptr(), len(so), so_d.data_ptr(),
+                                                  do_d.data_ptr(), nb_d.data_ptr()))
+    torch.cuda.synchronize()
+    want = np.zeros(1 << 20, np.uint8)
+    s_np = src.cpu().numpy()
+    for a, b_, n in zip(so, do, nb):
+        want[b_:b_ + n] = s_np[a:a + n]
+    assert np.array_equal(dst.cpu().numpy(), want)
